@@ -1,0 +1,244 @@
+// ref_shim.cpp — extern "C" wrappers around the UNMODIFIED reference library.
+// TEST INFRASTRUCTURE ONLY: compiled by oracle/Makefile together with the
+// reference's own sources (/root/reference/proj/src/{graph,metrics,
+// placement,topology}.cpp) into oracle/_ref/libqvref.so. Used to pin the C
+// restatement (oracle.c), to generate tests/golden fixtures, and as the
+// timed CPU baseline (bench.py cpu_baseline kind "reference").
+// Nothing here re-implements reference logic; it only marshals arguments.
+#include <chrono>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <span>
+#include <string>
+#include <vector>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "qv/error.hpp"
+#include "qv/graph.hpp"
+#include "qv/metrics.hpp"
+#include "qv/placement.hpp"
+#include "qv/topology.hpp"
+#include "../include/qvb.h"
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const qv::PlacementError& e) {
+    g_err = e.what();
+    return QVB_ERR_PLACEMENT;
+  } catch (const qv::ValidationError& e) {
+    g_err = e.what();
+    return QVB_ERR_VALIDATION;
+  } catch (const qv::ParseError& e) {
+    g_err = e.what();
+    return QVB_ERR_VALIDATION;
+  } catch (const qv::ConfigError& e) {
+    g_err = e.what();
+    return QVB_ERR_VALIDATION;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return QVB_ERR_GENERIC;
+  }
+}
+
+qv::Graph make_graph(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col,
+                     const double* w) {
+  qv::Graph g;
+  g.node_count = n;
+  g.edge_count = e;
+  g.row_offsets.assign(ro, ro + n + 1);
+  g.col_indices.assign(col, col + e);
+  if (w) g.edge_weights.assign(w, w + e);
+  else g.edge_weights.assign(e, 1.0);
+  return g;
+}
+
+qv::ClusterTopology make_topo(const qvb_topology* t) {
+  qv::ClusterTopology c;
+  c.servers = t->servers;
+  c.numa_per_server = t->numa_per_server;
+  c.gpus_per_server = t->gpus_per_server;
+  c.gpu_feature_capacity = t->gpu_feature_capacity;
+  c.host_feature_capacity = t->host_feature_capacity;
+  c.disk_feature_capacity = t->disk_feature_capacity;
+  c.nvlink_within_numa = t->nvlink_within_numa != 0;
+  c.infiniband = t->infiniband != 0;
+  for (std::size_t i = 0; i < qv::kLinkClassCount; ++i) {
+    c.links[i].latency_s = t->link_latency_s[i];
+    c.links[i].bandwidth_Bps = t->link_bandwidth_Bps[i];
+  }
+  c.tlb_miss_penalty_s = t->tlb_miss_penalty_s;
+  if (t->gpu_replicated_capacity != 0)
+    throw qv::ValidationError("reference has no gpu_replicated_capacity extension");
+  return c;
+}
+
+qv::PlacementPlan make_plan(const uint64_t* lo, const int64_t* ids, uint64_t n,
+                            const qv::ClusterTopology& topo) {
+  qv::PlacementPlan p;
+  p.feature_count = n;
+  p.locations.resize(n);
+  for (uint64_t f = 0; f < n; ++f) {
+    for (uint64_t k = lo[f]; k < lo[f + 1]; ++k) {
+      qv::Location l = qv::decode_location(topo, ids[k]);
+      l.replica = k > lo[f];
+      p.locations[f].push_back(l);
+    }
+  }
+  return p;
+}
+}  // namespace
+
+extern "C" {
+
+const char* qvr_last_error(void) { return g_err.c_str(); }
+
+int qvr_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+void qvr_set_threads(int t) {
+#ifdef _OPENMP
+  if (t > 0) omp_set_num_threads(t);
+#else
+  (void)t;
+#endif
+}
+
+void qvr_topology_defaults(qvb_topology* t) {
+  qv::ClusterTopology c = qv::ClusterTopology::with_defaults();
+  std::memset(t, 0, sizeof *t);
+  t->servers = c.servers;
+  t->numa_per_server = c.numa_per_server;
+  t->gpus_per_server = c.gpus_per_server;
+  t->gpu_feature_capacity = c.gpu_feature_capacity;
+  t->host_feature_capacity = c.host_feature_capacity;
+  t->disk_feature_capacity = c.disk_feature_capacity;
+  t->nvlink_within_numa = c.nvlink_within_numa;
+  t->infiniband = c.infiniband;
+  for (std::size_t i = 0; i < qv::kLinkClassCount; ++i) {
+    t->link_latency_s[i] = c.links[i].latency_s;
+    t->link_bandwidth_Bps[i] = c.links[i].bandwidth_Bps;
+  }
+  t->tlb_miss_penalty_s = c.tlb_miss_penalty_s;
+}
+
+// qv::compute_access_prob_ie / qv::serial::compute_access_prob_ie; ms_out
+// (nullable) receives the wall time of the call alone (graph marshalling
+// excluded).
+int qvr_access_prob(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col,
+                    const double* w, uint32_t layers, int parallel, double* out, double* ms_out) {
+  return guard([&] {
+    qv::Graph g = make_graph(n, e, ro, col, w);
+    qv::TransitionView t = qv::transition_view(g);
+    auto t0 = std::chrono::steady_clock::now();
+    qv::AccessProbTable a = parallel ? qv::compute_access_prob_ie(g, t, layers)
+                                     : qv::serial::compute_access_prob_ie(g, t, layers);
+    auto t1 = std::chrono::steady_clock::now();
+    if (ms_out) *ms_out = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    std::memcpy(out, a.values.data(), n * sizeof(double));
+  });
+}
+
+int qvr_in_adjacency(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col,
+                     const double* w, uint64_t* tro, uint64_t* tcol, double* tw) {
+  return guard([&] {
+    qv::Graph g = make_graph(n, e, ro, col, w);
+    qv::Graph t = qv::in_adjacency(g);
+    std::memcpy(tro, t.row_offsets.data(), (n + 1) * sizeof(uint64_t));
+    std::memcpy(tcol, t.col_indices.data(), e * sizeof(uint64_t));
+    std::memcpy(tw, t.edge_weights.data(), e * sizeof(double));
+  });
+}
+
+int qvr_row_sums(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col, const double* w,
+                 double* rs) {
+  return guard([&] {
+    qv::Graph g = make_graph(n, e, ro, col, w);
+    qv::TransitionView t = qv::transition_view(g);
+    std::memcpy(rs, t.row_sums.data(), n * sizeof(double));
+  });
+}
+
+int qvr_plan_placement(const double* v, uint64_t n, const qvb_topology* topo,
+                       uint64_t* loc_offsets, int64_t* loc_ids, uint64_t cap, uint64_t* copies,
+                       double* ms_out) {
+  return guard([&] {
+    qv::ClusterTopology t = make_topo(topo);
+    qv::FapTable fap;
+    fap.values.assign(v, v + n);
+    auto t0 = std::chrono::steady_clock::now();
+    qv::PlacementPlan p = qv::plan_placement(fap, t);
+    auto t1 = std::chrono::steady_clock::now();
+    if (ms_out) *ms_out = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    uint64_t total = 0;
+    for (const auto& l : p.locations) total += l.size();
+    *copies = total;
+    if (total > cap) throw qv::ValidationError("loc_capacity too small");
+    uint64_t at = 0;
+    for (uint64_t f = 0; f < n; ++f) {
+      loc_offsets[f] = at;
+      for (const auto& l : p.locations[f])
+        loc_ids[at++] = qv::encode_location(t, l.server, l.tier, l.device);
+    }
+    loc_offsets[n] = at;
+  });
+}
+
+int qvr_build_lookup_table(const uint64_t* lo, const int64_t* ids, uint64_t n,
+                           const qvb_topology* topo, uint32_t home, int64_t* location_ids,
+                           uint64_t* offsets, double* ms_out) {
+  return guard([&] {
+    qv::ClusterTopology t = make_topo(topo);
+    qv::PlacementPlan p = make_plan(lo, ids, n, t);
+    auto t0 = std::chrono::steady_clock::now();
+    qv::FeatureLookupTable lut = qv::build_lookup_table(p, t, home);
+    auto t1 = std::chrono::steady_clock::now();
+    if (ms_out) *ms_out = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    std::memcpy(location_ids, lut.location_ids.data(), n * sizeof(int64_t));
+    std::memcpy(offsets, lut.offsets.data(), n * sizeof(uint64_t));
+  });
+}
+
+int qvr_page_transitions(const uint64_t* o, uint64_t count, uint64_t page, uint64_t* out) {
+  return guard([&] { *out = qv::page_transitions(std::span<const uint64_t>(o, count), page); });
+}
+
+int qvr_plan_reads(const int64_t* location_ids, const uint64_t* offsets, uint64_t table_n,
+                   const uint64_t* ids, uint64_t b, uint64_t page, int64_t* group_loc,
+                   uint64_t* group_count, uint64_t* group_transitions, uint64_t* n_groups,
+                   uint64_t* offsets_out, double* ms_out) {
+  return guard([&] {
+    qv::FeatureLookupTable lut;
+    lut.location_ids.assign(location_ids, location_ids + table_n);
+    lut.offsets.assign(offsets, offsets + table_n);
+    auto t0 = std::chrono::steady_clock::now();
+    qv::ReadPlan rp = qv::plan_reads(lut, std::span<const qv::NodeId>(ids, b), page);
+    auto t1 = std::chrono::steady_clock::now();
+    if (ms_out) *ms_out = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    uint64_t g = 0, at = 0;
+    for (const auto& lr : rp.per_location) {
+      group_loc[g] = lr.location_id;
+      group_count[g] = lr.offsets.size();
+      group_transitions[g] = lr.page_transitions;
+      ++g;
+      for (uint64_t o : lr.offsets) offsets_out[at++] = o;
+    }
+    *n_groups = g;
+  });
+}
+
+}  // extern "C"
