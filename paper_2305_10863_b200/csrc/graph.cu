@@ -1,0 +1,549 @@
+// graph.cu — device in-CSR build (replaces in_adjacency, graph.cpp:260-281,
+// and transition_view's row sums, graph.cpp:292-318) and the device-side
+// synthetic generator (tools/bench.cpp:22-34).
+//
+// Pipeline (all on device, one-time per graph):
+//   validate + row sums      thread per out-row; sequential sum in CSR order
+//                            (bit-exact with graph.cpp:305); unit weights are
+//                            exact integer counts, no loop
+//   source of every edge     marks at row starts + inclusive scan
+//   transpose                stable radix sort by destination with the edge
+//                            index as payload => inside a destination the
+//                            edges keep out-CSR order = ascending source, and
+//                            parallel edges keep their CSR order (exactly the
+//                            counting-sort order of graph.cpp:271-279)
+//   coalesce                 runs of equal (dst, src) -> one factor edge; the
+//                            run's weights summed left to right
+//                            (metrics.cpp:157-164); R = w_sum / row_sum(s)
+//   layout                   compact (u32 col + per-source y) when almost
+//                            every R equals 1/row_sum(s) bitwise, else
+//                            weighted (u32 col + f64 R per edge)
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "graph.cuh"
+
+qvb_graph::~qvb_graph() {
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaDeviceSynchronize();
+  cudaFree(uptr);
+  cudaFree(col);
+  cudaFree(R);
+  cudaFree(exc_src);
+  cudaFree(exc_R);
+  cudaFree(inv);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(p[i]);
+    cudaFree(y[i]);
+  }
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
+namespace qvb {
+namespace {
+
+constexpr unsigned kBlock = 256;
+constexpr unsigned long long kNone = ~0ull;
+
+__global__ void k_check_ro(const uint64_t* __restrict__ ro, uint64_t n,
+                           unsigned long long* bad_mono) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (ro[i + 1] < ro[i]) atomicMin(bad_mono, (unsigned long long)i);
+}
+
+// col u64 -> u32 with the range check of graph.cpp:78-81 (edge-level code 1).
+__global__ void k_col_to_u32(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
+                             uint64_t count, uint64_t base, uint64_t n,
+                             unsigned long long* bad_edge) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t v = in[i];
+    if (v >= n) {
+      atomicMin(bad_edge, (unsigned long long)(((base + i) << 2) | 1));
+      v = 0;
+    }
+    out[i] = static_cast<uint32_t>(v);
+  }
+}
+
+// graph.cpp:82-85 (edge-level code 2).
+__global__ void k_check_weights(const double* __restrict__ w, uint64_t e,
+                                unsigned long long* bad_edge) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < e;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    double x = w[i];
+    if (!(x >= 0.0)) atomicMin(bad_edge, (unsigned long long)((i << 2) | 2));
+  }
+}
+
+// transition_view row sums (graph.cpp:301-316) + the all-zero-weights row
+// check (graph.cpp:76,86-91).
+__global__ void k_row_sums(const uint64_t* __restrict__ ro, const double* __restrict__ w,
+                           uint64_t n, double* __restrict__ rs, double* __restrict__ inv,
+                           unsigned long long* bad_zero) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = ro[i], b = ro[i + 1];
+    double sum;
+    if (w) {
+      sum = 0.0;
+      bool any_positive = a == b;
+      for (uint64_t k = a; k < b; ++k) {
+        double x = w[k];
+        sum = __dadd_rn(sum, x);
+        any_positive |= x > 0.0;
+      }
+      if (!any_positive) atomicMin(bad_zero, (unsigned long long)i);
+    } else {
+      sum = static_cast<double>(b - a);  // sum of (b-a) ones, exact
+    }
+    rs[i] = sum;
+    inv[i] = sum > 0.0 ? __ddiv_rn(1.0, sum) : 0.0;
+  }
+}
+
+__global__ void k_row_marks(const uint64_t* __restrict__ ro, uint64_t n, uint64_t e,
+                            uint32_t* __restrict__ marks) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t a = ro[i];
+    if (a < e && ro[i + 1] > a) atomicAdd(&marks[a], 1u);
+  }
+}
+
+// marks[p] = 1 where a non-empty row starts; the inclusive scan then gives
+// 1 + the rank of each edge's row among non-empty rows (row_of_rank maps it
+// back to the row id).
+__global__ void k_src_from_rank(const uint32_t* __restrict__ incl, const uint32_t* __restrict__ row_of_rank,
+                                uint64_t e, uint32_t* __restrict__ src) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < e;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    src[k] = row_of_rank[incl[k] - 1];
+}
+
+__global__ void k_rank_rows(const uint64_t* __restrict__ ro, uint64_t n, const uint32_t* __restrict__ incl,
+                            uint64_t e, uint32_t* __restrict__ row_of_rank) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t a = ro[i];
+    if (a < e && ro[i + 1] > a) row_of_rank[incl[a] - 1] = static_cast<uint32_t>(i);
+  }
+}
+
+__global__ void k_iota(uint32_t* __restrict__ v, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    v[i] = static_cast<uint32_t>(i);
+}
+
+// For every transposed position k: its source and whether it starts a run
+// of equal (destination, source).
+__global__ void k_runs(const uint32_t* __restrict__ sdst, const uint32_t* __restrict__ seid,
+                       const uint32_t* __restrict__ src, uint64_t e, uint32_t* __restrict__ ssrc,
+                       uint8_t* __restrict__ head) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < e;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t s = src[seid[k]];
+    bool h = k == 0;
+    if (!h) h = sdst[k] != sdst[k - 1] || s != src[seid[k - 1]];
+    ssrc[k] = s;
+    head[k] = h ? 1 : 0;
+  }
+}
+
+// One thread per run head: coalesce the run (metrics.cpp:157-164), form
+// R = w_sum / row_sum(s) and flag it when it differs bitwise from
+// 1/row_sum(s); also writes the in-row pointers of every destination whose
+// first edge this is (and of the empty rows before it).
+__global__ void k_coalesce(const uint32_t* __restrict__ sdst, const uint32_t* __restrict__ seid,
+                           const uint32_t* __restrict__ ssrc, const uint8_t* __restrict__ head,
+                           const uint32_t* __restrict__ uidx, const double* __restrict__ w,
+                           const double* __restrict__ rs, const double* __restrict__ inv,
+                           uint64_t e, uint64_t n, uint64_t eu, uint32_t* __restrict__ ucol,
+                           double* __restrict__ uR, uint8_t* __restrict__ uexc,
+                           uint64_t* __restrict__ uptr) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < e;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    if (k == e - 1) {  // tail rows after the last destination
+      for (uint64_t d = (uint64_t)sdst[k] + 1; d <= n; ++d) uptr[d] = eu;
+    }
+    if (!head[k]) continue;
+    const uint32_t s = ssrc[k];
+    const uint32_t u = uidx[k];
+    double W;
+    uint64_t k2 = k + 1;
+    if (w) {
+      W = w[seid[k]];
+      while (k2 < e && !head[k2]) {
+        W = __dadd_rn(W, w[seid[k2]]);
+        ++k2;
+      }
+    } else {
+      while (k2 < e && !head[k2]) ++k2;
+      W = static_cast<double>(k2 - k);  // sum of ones, exact
+    }
+    const double R = __ddiv_rn(W, rs[s]);
+    ucol[u] = s;
+    uR[u] = R;
+    uexc[u] = __double_as_longlong(R) != __double_as_longlong(inv[s]) ? 1 : 0;
+    const uint32_t d = sdst[k];
+    if (k == 0 || sdst[k - 1] != d) {
+      const uint64_t d0 = k == 0 ? 0 : (uint64_t)sdst[k - 1] + 1;
+      for (uint64_t dd = d0; dd <= d; ++dd) uptr[dd] = u;
+    }
+  }
+}
+
+__global__ void k_compact(const uint32_t* __restrict__ ucol, const double* __restrict__ uR,
+                          const uint8_t* __restrict__ uexc, const uint32_t* __restrict__ xidx,
+                          uint64_t eu, uint32_t* __restrict__ col, uint32_t* __restrict__ exc_src,
+                          double* __restrict__ exc_R) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < eu;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = ucol[u];
+    if (uexc[u]) {
+      const uint32_t x = xidx[u];
+      col[u] = kExcFlag | x;
+      exc_src[x] = s;
+      exc_R[x] = uR[u];
+    } else {
+      col[u] = s;
+    }
+  }
+}
+
+// tools/bench.cpp:22-34 on the device: edge i consumes draws 3i, 3i+1, 3i+2
+// of derive_stream(seed, 0xBE9C4).
+__global__ void k_gen_edges(uint64_t n, uint64_t e, uint64_t state, int weighted, int transposed,
+                            uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                            double* __restrict__ w) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < e;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double u = to_uniform(stream_draw(state, 3 * i));
+    uint64_t s = __double2ull_rz(__dmul_rn(__dmul_rn(u, u), static_cast<double>(n)));
+    uint64_t d = to_below(stream_draw(state, 3 * i + 1), n);
+    if (s > n - 1) s = n - 1;
+    if (transposed) {
+      uint64_t t = s;
+      s = d;
+      d = t;
+    }
+    src[i] = static_cast<uint32_t>(s);
+    dst[i] = static_cast<uint32_t>(d);
+    if (w) w[i] = weighted ? __dadd_rn(1.0, to_uniform(stream_draw(state, 3 * i + 2))) : 1.0;
+  }
+}
+
+// Row offsets from sorted row keys: ro[r] = first position with key >= r.
+__global__ void k_offsets_from_sorted(const uint32_t* __restrict__ keys, uint64_t e, uint64_t n,
+                                      uint64_t* __restrict__ ro) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < e;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t d = keys[k];
+    const uint64_t d0 = k == 0 ? 0 : (uint64_t)keys[k - 1] + 1;
+    if (k == 0 || keys[k - 1] != keys[k])
+      for (uint64_t dd = d0; dd <= d; ++dd) ro[dd] = k;
+    if (k == e - 1)
+      for (uint64_t dd = d + 1; dd <= n; ++dd) ro[dd] = e;
+  }
+}
+
+template <typename T>
+__global__ void k_gather_by(const T* __restrict__ in, const uint32_t* __restrict__ idx, uint64_t e,
+                            T* __restrict__ out) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < e;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    out[k] = in[idx[k]];
+}
+
+template <typename T>
+T* persist(DevBuf<T>& b) {
+  return b.release_ownership();
+}
+
+}  // namespace
+
+void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, const double* d_w,
+                  const uint32_t* d_src, cudaStream_t s) {
+  const uint64_t n = g.n, e = g.e;
+  DevBuf<double> rs(n, s), inv(n, s);
+  DevBuf<unsigned long long> flags(1, s);
+  QVB_CUDA(cudaMemsetAsync(flags.p, 0xFF, sizeof(unsigned long long), s));
+  k_row_sums<<<grid_for(n, kBlock), kBlock, 0, s>>>(d_ro, d_w, n, rs.p, inv.p, flags.p);
+  QVB_LAUNCH_CHECK();
+  unsigned long long bad_zero = read_scalar(flags.p, s);
+  if (bad_zero != kNone)
+    fail(QVB_ERR_VALIDATION, "node " + std::to_string(bad_zero) +
+                                 " has out-edges but all weights are zero");
+
+  DevBuf<uint64_t> uptr(n + 1, s);
+  if (e == 0) {
+    QVB_CUDA(cudaMemsetAsync(uptr.p, 0, (n + 1) * sizeof(uint64_t), s));
+    g.eu = 0;
+    g.nexc = 0;
+    g.layout = 0;
+    g.uptr = persist(uptr);
+    g.inv = persist(inv);
+    g.bytes = (n + 1) * 8 + n * 8;
+    return;
+  }
+
+  // Source of every out-CSR edge.
+  DevBuf<uint32_t> src_buf;
+  if (!d_src) {
+    src_buf.alloc(e, s);
+    DevBuf<uint32_t> marks(e, s), incl(e, s);
+    QVB_CUDA(cudaMemsetAsync(marks.p, 0, e * sizeof(uint32_t), s));
+    k_row_marks<<<grid_for(n, kBlock), kBlock, 0, s>>>(d_ro, n, e, marks.p);
+    QVB_LAUNCH_CHECK();
+    inclusive_sum_u32_u32(marks.p, incl.p, e, s);
+    DevBuf<uint32_t> row_of_rank(n, s);
+    k_rank_rows<<<grid_for(n, kBlock), kBlock, 0, s>>>(d_ro, n, incl.p, e, row_of_rank.p);
+    QVB_LAUNCH_CHECK();
+    k_src_from_rank<<<grid_for(e, kBlock), kBlock, 0, s>>>(incl.p, row_of_rank.p, e, src_buf.p);
+    QVB_LAUNCH_CHECK();
+    d_src = src_buf.p;
+  }
+
+  // Transpose: stable sort by destination, payload = out-CSR edge index.
+  DevBuf<uint32_t> sdst(e, s), seid(e, s);
+  {
+    DevBuf<uint32_t> iota(e, s);
+    k_iota<<<grid_for(e, kBlock), kBlock, 0, s>>>(iota.p, e);
+    QVB_LAUNCH_CHECK();
+    sort_pairs_u32_u32(d_col, sdst.p, iota.p, seid.p, e, 0, bits_for(n - 1), s);
+  }
+  DevBuf<uint32_t> ssrc(e, s);
+  DevBuf<uint8_t> head(e, s);
+  k_runs<<<grid_for(e, kBlock), kBlock, 0, s>>>(sdst.p, seid.p, d_src, e, ssrc.p, head.p);
+  QVB_LAUNCH_CHECK();
+  src_buf.release();
+  DevBuf<uint32_t> uidx(e, s);
+  exclusive_sum_u8_u32(head.p, uidx.p, e, s);
+  uint32_t last_idx = read_scalar(uidx.p + (e - 1), s);
+  uint8_t last_head = read_scalar(head.p + (e - 1), s);
+  const uint64_t eu = (uint64_t)last_idx + last_head;
+
+  DevBuf<uint32_t> ucol(eu, s);
+  DevBuf<double> uR(eu, s);
+  DevBuf<uint8_t> uexc(eu, s);
+  k_coalesce<<<grid_for(e, kBlock), kBlock, 0, s>>>(sdst.p, seid.p, ssrc.p, head.p, uidx.p, d_w,
+                                                    rs.p, inv.p, e, n, eu, ucol.p, uR.p, uexc.p,
+                                                    uptr.p);
+  QVB_LAUNCH_CHECK();
+  sdst.release();
+  seid.release();
+  ssrc.release();
+  head.release();
+  uidx.release();
+
+  DevBuf<uint64_t> cnt(1, s);
+  sum_u8_u64(uexc.p, cnt.p, eu, s);
+  const uint64_t nexc = read_scalar(cnt.p, s);
+  g.eu = eu;
+  g.nexc = nexc;
+  if (nexc * 16 <= eu) {  // compact layout
+    g.layout = 0;
+    DevBuf<uint32_t> xidx(eu, s), col(eu, s), xsrc(nexc ? nexc : 1, s);
+    DevBuf<double> xR(nexc ? nexc : 1, s);
+    exclusive_sum_u8_u32(uexc.p, xidx.p, eu, s);
+    k_compact<<<grid_for(eu, kBlock), kBlock, 0, s>>>(ucol.p, uR.p, uexc.p, xidx.p, eu, col.p,
+                                                      xsrc.p, xR.p);
+    QVB_LAUNCH_CHECK();
+    g.col = persist(col);
+    g.exc_src = persist(xsrc);
+    g.exc_R = persist(xR);
+    g.bytes = eu * 4 + (nexc ? nexc : 1) * 12;
+  } else {
+    g.layout = 1;
+    g.col = persist(ucol);
+    g.R = persist(uR);
+    g.bytes = eu * 12;
+  }
+  g.uptr = persist(uptr);
+  g.inv = persist(inv);
+  g.bytes += (n + 1) * 8 + n * 8;
+  QVB_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace qvb
+
+using namespace qvb;
+
+namespace {
+
+void finish_build(qvb_graph* g, cudaEvent_t a, cudaEvent_t b, cudaStream_t s) {
+  QVB_CUDA(cudaEventRecord(b, s));
+  QVB_CUDA(cudaEventSynchronize(b));
+  float ms = 0;
+  QVB_CUDA(cudaEventElapsedTime(&ms, a, b));
+  g->build_ms = ms;
+}
+
+}  // namespace
+
+extern "C" int qvb_graph_upload(int device, uint64_t n, uint64_t e, const uint64_t* row_offsets,
+                                const uint64_t* col, const double* weights, void* stream,
+                                qvb_graph** out) {
+  return guarded([&] {
+    if (!out) fail(QVB_ERR_VALIDATION, "out is null");
+    *out = nullptr;
+    // Graph::validate order (graph.cpp:58-93).
+    if (n == 0) fail(QVB_ERR_VALIDATION, "empty graph: node count is zero");
+    if (!row_offsets || (e && !col)) fail(QVB_ERR_VALIDATION, "null graph arrays");
+    if (n > kMaxNodes || e > kMaxEdges)
+      fail(QVB_ERR_UNSUPPORTED, "graph exceeds the device path limits (n < 2^31, e < 2^32)");
+    if (row_offsets[0] != 0 || row_offsets[n] != e)
+      fail(QVB_ERR_VALIDATION, "row_offsets endpoints invalid");
+    DeviceGuard dg(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto g = std::make_unique<qvb_graph>();
+    g->device = device;
+    g->n = n;
+    g->e = e;
+    cudaEvent_t ea, eb;
+    QVB_CUDA(cudaEventCreate(&ea));
+    QVB_CUDA(cudaEventCreate(&eb));
+    QVB_CUDA(cudaEventRecord(ea, s));
+
+    DevBuf<uint64_t> ro(n + 1, s);
+    QVB_CUDA(cudaMemcpyAsync(ro.p, row_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
+    DevBuf<unsigned long long> flags(2, s);
+    QVB_CUDA(cudaMemsetAsync(flags.p, 0xFF, 2 * sizeof(unsigned long long), s));
+    k_check_ro<<<grid_for(n, kBlock), kBlock, 0, s>>>(ro.p, n, flags.p);
+    QVB_LAUNCH_CHECK();
+    unsigned long long bad_mono = read_scalar(flags.p, s);
+    if (bad_mono != kNone)
+      fail(QVB_ERR_VALIDATION, "row_offsets not non-decreasing at node " + std::to_string(bad_mono));
+
+    DevBuf<uint32_t> dcol(e, s);
+    DevBuf<double> dw;
+    if (e) {
+      const uint64_t chunk = 1ull << 25;  // 256 MiB of u64 per staging round
+      DevBuf<uint64_t> stage(std::min(e, chunk), s);
+      for (uint64_t base = 0; base < e; base += chunk) {
+        const uint64_t c = std::min(chunk, e - base);
+        QVB_CUDA(cudaMemcpyAsync(stage.p, col + base, c * 8, cudaMemcpyHostToDevice, s));
+        k_col_to_u32<<<grid_for(c, kBlock), kBlock, 0, s>>>(stage.p, dcol.p + base, c, base, n,
+                                                            flags.p + 1);
+        QVB_LAUNCH_CHECK();
+      }
+      if (weights) {
+        dw.alloc(e, s);
+        QVB_CUDA(cudaMemcpyAsync(dw.p, weights, e * 8, cudaMemcpyHostToDevice, s));
+        k_check_weights<<<grid_for(e, kBlock), kBlock, 0, s>>>(dw.p, e, flags.p + 1);
+        QVB_LAUNCH_CHECK();
+      }
+    }
+    unsigned long long bad_edge = read_scalar(flags.p + 1, s);
+    if (bad_edge != kNone) {
+      // The first failing edge names its row (graph.cpp:75-91 walks rows in
+      // order; a zero-weight row before it would be reported first).
+      const uint64_t ei = bad_edge >> 2;
+      const uint64_t row =
+          static_cast<uint64_t>(std::upper_bound(row_offsets, row_offsets + n + 1, ei) - row_offsets) - 1;
+      // Rows before `row` may still fail the all-zero check: run it on them.
+      bool zero_before = false;
+      uint64_t zrow = 0;
+      if (weights) {
+        for (uint64_t i = 0; i < row && !zero_before; ++i) {
+          bool anyp = row_offsets[i] == row_offsets[i + 1];
+          for (uint64_t k = row_offsets[i]; k < row_offsets[i + 1]; ++k) anyp |= weights[k] > 0.0;
+          if (!anyp) {
+            zero_before = true;
+            zrow = i;
+          }
+        }
+      }
+      if (zero_before)
+        fail(QVB_ERR_VALIDATION,
+             "node " + std::to_string(zrow) + " has out-edges but all weights are zero");
+      if ((bad_edge & 3) == 1)
+        fail(QVB_ERR_VALIDATION, "column index out of range at node " + std::to_string(row));
+      fail(QVB_ERR_VALIDATION, "negative or NaN edge weight at node " + std::to_string(row));
+    }
+    build_in_csr(*g, ro.p, dcol.p, dw.p, nullptr, s);
+    finish_build(g.get(), ea, eb, s);
+    cudaEventDestroy(ea);
+    cudaEventDestroy(eb);
+    *out = g.release();
+  });
+}
+
+extern "C" int qvb_graph_synthetic(int device, uint64_t n, uint64_t e, uint64_t seed, int weighted,
+                                   int transposed, void* stream, qvb_graph** out) {
+  return guarded([&] {
+    if (!out) fail(QVB_ERR_VALIDATION, "out is null");
+    *out = nullptr;
+    if (n == 0) fail(QVB_ERR_VALIDATION, "empty graph: node count is zero");
+    if (n > kMaxNodes || e > kMaxEdges)
+      fail(QVB_ERR_UNSUPPORTED, "graph exceeds the device path limits (n < 2^31, e < 2^32)");
+    DeviceGuard dg(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto g = std::make_unique<qvb_graph>();
+    g->device = device;
+    g->n = n;
+    g->e = e;
+    cudaEvent_t ea, eb;
+    QVB_CUDA(cudaEventCreate(&ea));
+    QVB_CUDA(cudaEventCreate(&eb));
+    QVB_CUDA(cudaEventRecord(ea, s));
+    DevBuf<uint64_t> ro(n + 1, s);
+    DevBuf<uint32_t> col(e, s), ssrc(e, s);
+    DevBuf<double> w;
+    if (e) {
+      DevBuf<uint32_t> src(e, s), dst(e, s), iota(e, s), perm(e, s);
+      DevBuf<double> w_in;
+      if (weighted) w_in.alloc(e, s);
+      const uint64_t state = derive_state(seed, 0xBE9C4ULL);
+      k_gen_edges<<<grid_for(e, kBlock), kBlock, 0, s>>>(n, e, state, weighted, transposed, src.p,
+                                                        dst.p, w_in.p);
+      QVB_LAUNCH_CHECK();
+      // Graph::from_edges / build_csr (graph.cpp:16-47): stable by source.
+      k_iota<<<grid_for(e, kBlock), kBlock, 0, s>>>(iota.p, e);
+      QVB_LAUNCH_CHECK();
+      sort_pairs_u32_u32(src.p, ssrc.p, iota.p, perm.p, e, 0, bits_for(n - 1), s);
+      k_gather_by<uint32_t><<<grid_for(e, kBlock), kBlock, 0, s>>>(dst.p, perm.p, e, col.p);
+      QVB_LAUNCH_CHECK();
+      if (weighted) {
+        w.alloc(e, s);
+        k_gather_by<double><<<grid_for(e, kBlock), kBlock, 0, s>>>(w_in.p, perm.p, e, w.p);
+        QVB_LAUNCH_CHECK();
+      }
+      k_offsets_from_sorted<<<grid_for(e, kBlock), kBlock, 0, s>>>(ssrc.p, e, n, ro.p);
+      QVB_LAUNCH_CHECK();
+    } else {
+      QVB_CUDA(cudaMemsetAsync(ro.p, 0, (n + 1) * 8, s));
+    }
+    build_in_csr(*g, ro.p, col.p, w.p, ssrc.p, s);
+    finish_build(g.get(), ea, eb, s);
+    cudaEventDestroy(ea);
+    cudaEventDestroy(eb);
+    *out = g.release();
+  });
+}
+
+extern "C" int qvb_graph_info_get(const qvb_graph* g, qvb_graph_info* info) {
+  return guarded([&] {
+    if (!g || !info) fail(QVB_ERR_VALIDATION, "null argument");
+    std::memset(info, 0, sizeof *info);
+    info->node_count = g->n;
+    info->edge_count = g->e;
+    info->unique_edge_count = g->eu;
+    info->exception_count = g->nexc;
+    info->layout = g->layout;
+    info->device = static_cast<uint32_t>(g->device);
+    info->device_bytes = g->bytes;
+    info->build_ms = g->build_ms;
+  });
+}
+
+extern "C" int qvb_graph_destroy(qvb_graph* g) {
+  return guarded([&] { delete g; });
+}

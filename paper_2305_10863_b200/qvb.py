@@ -1,0 +1,305 @@
+"""Python mirror of the reference's hot-path interface over the qvb C-ABI.
+
+The reference is the C++ library ``qv`` (/root/reference/proj). This module
+exposes the same operations under the same names and argument meanings —
+``compute_access_prob_ie``, ``plan_placement``, ``build_lookup_table``,
+``plan_reads``, ``page_transitions``, ``encode_location`` — plus the real
+feature gather (``FeatureStore.gather``) that the reference only models with
+``fetch_cost``. Errors raise the same exception family as the reference
+(include/qv/error.hpp:10-32): ``ValidationError``, ``PlacementError`` …
+
+Everything runs through ``libqvb.so`` (include/qvb.h). There is no CPU
+fallback: importing this module without the built library, or calling a
+compute function without a usable CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqvb.so")
+
+LINK_LOCAL, LINK_NVLINK, LINK_PCIE, LINK_UPI, LINK_INFINIBAND, LINK_ETHERNET, LINK_DISK = range(7)
+TIER_GPU, TIER_HOST, TIER_DISK = 0, 1, 2
+
+
+# ---- errors (include/qv/error.hpp:10-32) ------------------------------------
+class Error(RuntimeError):
+    """qv::Error"""
+
+
+class ValidationError(Error):
+    """qv::ValidationError (also ParseError/ConfigError at this boundary)."""
+
+
+class PlacementError(Error):
+    """qv::PlacementError"""
+
+
+class CudaError(Error):
+    """CUDA failure or no usable device (the library has no CPU fallback)."""
+
+
+class UnsupportedError(Error):
+    """Valid input outside the device path's limits."""
+
+
+_CODES = {1: Error, 2: ValidationError, 3: PlacementError, 10: CudaError, 11: UnsupportedError}
+
+
+class Topology(C.Structure):
+    """qvb_topology == qv::ClusterTopology (topology.hpp:32-54) + extension."""
+
+    _fields_ = [
+        ("servers", C.c_uint32),
+        ("numa_per_server", C.c_uint32),
+        ("gpus_per_server", C.c_uint32),
+        ("nvlink_within_numa", C.c_uint32),
+        ("infiniband", C.c_uint32),
+        ("_pad0", C.c_uint32),
+        ("gpu_feature_capacity", C.c_uint64),
+        ("host_feature_capacity", C.c_uint64),
+        ("disk_feature_capacity", C.c_uint64),
+        ("link_latency_s", C.c_double * 7),
+        ("link_bandwidth_Bps", C.c_double * 7),
+        ("tlb_miss_penalty_s", C.c_double),
+        ("gpu_replicated_capacity", C.c_uint64),
+    ]
+
+    @staticmethod
+    def with_defaults(**kw) -> "Topology":
+        """ClusterTopology::with_defaults (topology.cpp:27-40) + overrides."""
+        t = Topology()
+        _lib().qvb_topology_defaults(C.byref(t))
+        for k, v in kw.items():
+            setattr(t, k, v)
+        return t
+
+    def validate(self) -> None:
+        _check(_lib().qvb_topology_validate(C.byref(self)))
+
+    def gpus_per_numa(self) -> int:
+        return self.gpus_per_server // self.numa_per_server
+
+
+class GraphInfo(C.Structure):
+    _fields_ = [
+        ("node_count", C.c_uint64),
+        ("edge_count", C.c_uint64),
+        ("unique_edge_count", C.c_uint64),
+        ("exception_count", C.c_uint64),
+        ("layout", C.c_uint32),
+        ("device", C.c_uint32),
+        ("device_bytes", C.c_uint64),
+        ("build_ms", C.c_double),
+    ]
+
+
+class StoreInfo(C.Structure):
+    _fields_ = [
+        ("feature_count", C.c_uint64),
+        ("dim", C.c_uint32),
+        ("reader_device", C.c_uint32),
+        ("row_stride_bytes", C.c_uint64),
+        ("local_rows", C.c_uint64),
+        ("host_rows", C.c_uint64),
+        ("lut_bytes", C.c_uint64),
+        ("location_count", C.c_uint32),
+        ("_pad", C.c_uint32),
+    ]
+
+
+_LIB = None
+vp = C.c_void_p
+u64 = C.c_uint64
+u32 = C.c_uint32
+i32 = C.c_int
+P = C.POINTER
+
+_SIGNATURES = {
+    "qvb_last_error": (C.c_char_p, []),
+    "qvb_version": (C.c_char_p, []),
+    "qvb_device_count": (i32, [P(i32)]),
+    "qvb_topology_defaults": (None, [P(Topology)]),
+    "qvb_topology_validate": (i32, [P(Topology)]),
+    "qvb_encode_location": (C.c_int64, [P(Topology), u32, u32, u32]),
+    "qvb_decode_location": (i32, [P(Topology), C.c_int64, P(u32), P(u32), P(u32)]),
+    "qvb_graph_upload": (i32, [i32, u64, u64, vp, vp, vp, vp, P(vp)]),
+    "qvb_graph_synthetic": (i32, [i32, u64, u64, u64, i32, i32, vp, P(vp)]),
+    "qvb_graph_info_get": (i32, [vp, P(GraphInfo)]),
+    "qvb_graph_destroy": (i32, [vp]),
+    "qvb_access_prob": (i32, [vp, u32, vp, i32, vp]),
+    "qvb_compute_access_prob_ie": (i32, [i32, u64, u64, vp, vp, vp, u32, vp, vp]),
+    "qvb_rank_desc": (i32, [i32, vp, u64, vp, i32, vp]),
+    "qvb_plan_placement": (i32, [i32, vp, u64, P(Topology), vp, vp, u64, P(u64)]),
+    "qvb_build_lookup_table": (i32, [i32, vp, vp, u64, P(Topology), u32, u32, vp, vp]),
+    "qvb_page_transitions": (i32, [vp, u64, u64, P(u64)]),
+    "qvb_plan_reads": (i32, [i32, vp, vp, u64, vp, u64, u64, vp, vp, vp, P(u64), vp]),
+    "qvb_store_create": (i32, [i32, vp, vp, u64, u32, P(Topology), u32, vp, P(vp)]),
+    "qvb_store_info_get": (i32, [vp, P(StoreInfo)]),
+    "qvb_store_export_handle": (i32, [vp, vp]),
+    "qvb_store_attach_peer": (i32, [vp, u32, vp]),
+    "qvb_store_destroy": (i32, [vp]),
+    "qvb_gather": (i32, [vp, vp, u64, vp, vp]),
+    "qvb_gather_planned": (i32, [vp, vp, u64, vp, vp]),
+    "qvb_gather_host": (i32, [vp, vp, u64, vp, vp]),
+    "qvb_store_check_error": (i32, [vp]),
+    "qvb_request_ids_synthetic": (i32, [i32, u64, u64, u64, vp, u64, vp]),
+}
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2305_10863_b200.build` "
+                "(the qvb path has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGNATURES.items():
+            f = getattr(L, name, None)
+            if f is None:  # tests/test_boundary.py requires every symbol to exist
+                continue
+            f.restype = res
+            f.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def exported_symbols():
+    return list(_SIGNATURES)
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = _lib().qvb_last_error().decode()
+        raise _CODES.get(rc, Error)(msg)
+
+
+def _ptr(a) -> int | None:
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):  # torch tensor (device or host)
+        return a.data_ptr()
+    return int(a)
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def device_count() -> int:
+    c = C.c_int(0)
+    _check(_lib().qvb_device_count(C.byref(c)))
+    return c.value
+
+
+def version() -> str:
+    return _lib().qvb_version().decode()
+
+
+# ---- locations (placement.cpp:25-51) ------------------------------------------
+def encode_location(topo: Topology, server: int, tier: int, device: int) -> int:
+    return _lib().qvb_encode_location(C.byref(topo), server, tier, device)
+
+
+def decode_location(topo: Topology, loc: int):
+    s, t, d = u32(), u32(), u32()
+    _check(_lib().qvb_decode_location(C.byref(topo), loc, C.byref(s), C.byref(t), C.byref(d)))
+    return s.value, t.value, d.value
+
+
+# ---- graph + K1 ----------------------------------------------------------------
+class DeviceGraph:
+    """Device-resident in-CSR (qvb_graph): in_adjacency + transition_view once."""
+
+    def __init__(self, handle: int):
+        self._h = handle
+
+    @classmethod
+    def upload(cls, row_offsets, col, weights=None, device: int = 0, stream=None):
+        ro = np.ascontiguousarray(row_offsets, np.uint64)
+        c = np.ascontiguousarray(col, np.uint64)
+        w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+        h = vp()
+        _check(_lib().qvb_graph_upload(device, len(ro) - 1, len(c), _ptr(ro), _ptr(c) if len(c) else None,
+                                       _ptr(w) if w is not None and len(w) else None,
+                                       _stream_ptr(stream), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def synthetic(cls, n: int, e: int, seed: int = 7, weighted: bool = False,
+                  transposed: bool = False, device: int = 0, stream=None):
+        """tools/bench.cpp:22-34 generator, directly on the device."""
+        h = vp()
+        _check(_lib().qvb_graph_synthetic(device, n, e, seed, int(weighted), int(transposed),
+                                          _stream_ptr(stream), C.byref(h)))
+        return cls(h.value)
+
+    def info(self) -> GraphInfo:
+        i = GraphInfo()
+        _check(_lib().qvb_graph_info_get(self._h, C.byref(i)))
+        return i
+
+    def access_prob(self, layers: int, out=None, stream=None):
+        """P(n, layers) for every node. ``out``: a host numpy array (default)
+        or a device tensor of n float64."""
+        n = self.info().node_count
+        if out is None:
+            out = np.zeros(n, np.float64)
+        on_dev = 0 if isinstance(out, np.ndarray) else 1
+        _check(_lib().qvb_access_prob(self._h, layers, _ptr(out), on_dev, _stream_ptr(stream)))
+        return out
+
+    def close(self):
+        if self._h:
+            _lib().qvb_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+@dataclass
+class AccessProbTable:
+    """qv::AccessProbTable (metrics.hpp:38-45)."""
+
+    values: np.ndarray
+    layers: int
+
+
+def compute_access_prob_ie(row_offsets, col, weights, layers: int, device: int = 0,
+                           timings: list | None = None) -> AccessProbTable:
+    """qv::compute_access_prob_ie(g, transition_view(g), layers) (metrics.hpp:53-54)
+    from a host out-CSR, end to end on the GPU."""
+    ro = np.ascontiguousarray(row_offsets, np.uint64)
+    c = np.ascontiguousarray(col, np.uint64)
+    w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+    n = len(ro) - 1
+    out = np.zeros(max(n, 1), np.float64)
+    ms = (C.c_double * 3)()
+    _check(_lib().qvb_compute_access_prob_ie(device, n, len(c), _ptr(ro), _ptr(c) if len(c) else None,
+                                             _ptr(w) if w is not None and len(w) else None, layers,
+                                             _ptr(out), ms))
+    if timings is not None:
+        timings[:] = list(ms)
+    return AccessProbTable(out[:n], layers)

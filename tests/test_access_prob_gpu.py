@@ -1,0 +1,146 @@
+"""K1 parity: the device P(n,j) against the CPU oracle, bit for bit.
+
+Mirrors the reference's own P(n,j) tests (tests/test_metrics.cpp:136-235,
+acceptance.cpp:156-173) and adds the BASELINE configs. The bar is
+bit-identical fp64 (north_star allows 1e-9 relative; SURVEY §0 shows only a
+bit-exact P keeps the placement/LUT exact, so that is what we test).
+"""
+import numpy as np
+import pytest
+
+from tests.util import CONFIGS, bits, derive_stream, fig8_edges, random_edges
+
+pytestmark = pytest.mark.gpu
+
+GOLD_FIG8 = {  # SURVEY §8(c), produced by the reference (tests/golden/golden.json)
+    2: [0.30555555555555552, 0.16666666666666666, 0.30555555555555552, 0.36342592592592593,
+        0.16666666666666666, 0.23611111111111113],
+    3: [0.42129629629629622, 0.16666666666666666, 0.55793467078189296, 0.55056691529492463,
+        0.16666666666666666, 0.35281635802469136],
+}
+
+
+def _csr(oracle, n, src, dst, w):
+    return oracle.build_csr(n, src, dst, w)
+
+
+def test_fig8_golden(qvb, oracle):
+    ro, col, w = _csr(oracle, *fig8_edges())
+    for layers, gold in GOLD_FIG8.items():
+        p = qvb.compute_access_prob_ie(ro, col, w, layers).values
+        assert (bits(p) == bits(np.array(gold))).all(), (layers, p.tolist())
+    p1 = qvb.compute_access_prob_ie(ro, col, w, 1).values
+    assert (p1 == 1.0 / 6).all()
+
+
+def test_two_neighbor_parent(qvb, oracle):
+    # test_metrics.cpp:143-152
+    ro, col, w = _csr(oracle, 3, [1, 1], [0, 2], [1.0, 1.0])
+    p = qvb.compute_access_prob_ie(ro, col, w, 2).values
+    base = 1.0 / 3.0
+    assert abs(p[0] - (base + (1.0 - base) * (base * 0.5))) < 1e-14
+    assert (bits(p) == bits(oracle.access_prob(ro, col, w, 2))).all()
+
+
+@pytest.mark.parametrize("weighted", [True, False])
+def test_random_graphs_bit_exact(qvb, oracle, weighted):
+    # test_metrics.cpp:154-175 draws; every layer count 1..4, bit-exact.
+    rng = derive_stream(59, 5 if weighted else 6)
+    for _ in range(40):
+        n, s, d, w = random_edges(rng, 40, 250, weighted)
+        ro, col, ww = _csr(oracle, n, s, d, w)
+        g = qvb.DeviceGraph.upload(ro, col, ww if weighted else None)
+        for layers in range(1, 5):
+            got = g.access_prob(layers)
+            exp = oracle.access_prob(ro, col, ww, layers)
+            assert (bits(got) == bits(exp)).all(), (n, layers)
+        g.close()
+
+
+def test_star_and_properties(qvb, oracle):
+    # star centre with 5 leaves (test_metrics.cpp:167-174); bounds/monotone (:177-193)
+    ro, col, w = _csr(oracle, 6, [1, 2, 3, 4, 5], [0] * 5, [1.0] * 5)
+    p = qvb.compute_access_prob_ie(ro, col, w, 2).values
+    assert (bits(p) == bits(oracle.access_prob(ro, col, w, 2))).all()
+    rng = derive_stream(61, 6)
+    for _ in range(10):
+        n, s, d, ww = random_edges(rng, 30, 200, True)
+        ro, col, ww = _csr(oracle, n, s, d, ww)
+        g = qvb.DeviceGraph.upload(ro, col, ww)
+        prev = None
+        for j in range(1, 5):
+            v = g.access_prob(j)
+            assert (v >= 0).all() and (v <= 1 + 1e-15).all()
+            if prev is not None:
+                assert (v >= prev - 1e-15).all()
+            prev = v
+        g.close()
+
+
+def test_zero_edges_and_isolated(qvb, oracle):
+    ro = np.zeros(5, np.uint64)
+    p = qvb.compute_access_prob_ie(ro, np.zeros(0, np.uint64), None, 3).values
+    assert (p == 0.25).all()
+
+
+def test_errors(qvb, oracle):
+    ro, col, w = _csr(oracle, *fig8_edges())
+    with pytest.raises(qvb.ValidationError):
+        qvb.compute_access_prob_ie(ro, col, w, 0)
+    bad = col.copy()
+    bad[2] = 99
+    with pytest.raises(qvb.ValidationError, match="column index out of range at node 1"):
+        qvb.compute_access_prob_ie(ro, bad, w, 2)
+    neg = w.copy()
+    neg[3] = -1.0
+    with pytest.raises(qvb.ValidationError, match="negative or NaN edge weight at node 3"):
+        qvb.compute_access_prob_ie(ro, col, neg, 2)
+    zero = w.copy()
+    zero[0] = zero[1] = 0.0
+    with pytest.raises(qvb.ValidationError, match="node 0 has out-edges but all weights are zero"):
+        qvb.compute_access_prob_ie(ro, col, zero, 2)
+    with pytest.raises(qvb.ValidationError, match="empty graph"):
+        qvb.compute_access_prob_ie(np.zeros(1, np.uint64), np.zeros(0, np.uint64), None, 2)
+    nm = ro.copy()
+    nm[1], nm[2] = nm[2], nm[1]
+    with pytest.raises(qvb.ValidationError):
+        qvb.compute_access_prob_ie(nm, col, w, 2)
+
+
+@pytest.mark.parametrize("weighted,transposed,layers", [(False, False, 2), (False, False, 3),
+                                                        (True, False, 3), (False, True, 3),
+                                                        (True, True, 2)])
+def test_c1_bit_exact(qvb, oracle, weighted, transposed, layers):
+    c = CONFIGS["C1"]
+    ro, col, w = oracle.synthetic_graph(c["n"], c["e"], 7, weighted, transposed)
+    exp = oracle.access_prob(ro, col, w, layers)
+    got = qvb.compute_access_prob_ie(ro, col, w, layers).values
+    assert (bits(got) == bits(exp)).all()
+    # the device generator builds the identical graph
+    g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, weighted, transposed)
+    assert (bits(g.access_prob(layers)) == bits(exp)).all()
+    info = g.info()
+    assert info.edge_count == c["e"]
+    g.close()
+
+
+def test_c2_bit_exact(qvb, oracle):
+    c = CONFIGS["C2"]
+    ro, col, w = oracle.synthetic_graph(c["n"], c["e"], 7, False, False)
+    exp = oracle.access_prob(ro, col, w, 2)
+    g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, False, False)
+    assert (bits(g.access_prob(2)) == bits(exp)).all()
+    g.close()
+
+
+def test_layouts_exercised(qvb, oracle):
+    # unit weights with parallel edges -> compact layout with exceptions;
+    # real weights -> weighted layout
+    c = CONFIGS["C1"]
+    g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, False, False)
+    i = g.info()
+    assert i.layout == 0 and i.exception_count > 0 and i.unique_edge_count < c["e"]
+    g.close()
+    g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, True, False)
+    assert g.info().layout == 1
+    g.close()
