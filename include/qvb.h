@@ -222,6 +222,10 @@ int qvb_store_info_get(const qvb_store* s, qvb_store_info* info);
 int qvb_store_export_handle(const qvb_store* s, uint8_t handle[64]);
 /* Map peer GPU `peer_device`'s shard (from its exported handle). */
 int qvb_store_attach_peer(qvb_store* s, uint32_t peer_device, const uint8_t handle[64]);
+/* Same-process variant: map the shard of `peer` (a store of this process,
+ * reader GPU `peer_device`) directly — P2P access is enabled when the two
+ * stores live on different CUDA devices. */
+int qvb_store_attach_local_peer(qvb_store* s, uint32_t peer_device, const qvb_store* peer);
 int qvb_store_destroy(qvb_store* s);
 
 /* out[i][0:dim] = X[ids[i]][0:dim] for i < b; ids and out are DEVICE

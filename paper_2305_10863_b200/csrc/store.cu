@@ -1,0 +1,557 @@
+// store.cu — K5, the feature collection the reference only models
+// (fetch_cost, placement.cpp:382-404, called per batch from
+// simulator.cpp:320-326): a real one-sided gather
+//   out[i][0:dim] = X[ids[i]][0:dim]
+// from local HBM, peer HBM (CUDA IPC mapping over NVLink/NVSwitch) or host
+// pinned memory (zero-copy UVA), chosen per lookup-table entry.
+//
+// HBM layout of one store (reader GPU d):
+//   lut    u64[n]  packed loc << 48 | offset (this reader's per-reader table)
+//   local  shard of location d: rows of the features holding a copy at d,
+//          ascending feature id (== the reference's cursor offsets),
+//          stride = dim*4 rounded up to 16 bytes
+//   host   pinned + mapped shard of the host location, same layout
+//   base[] one base pointer per location (peers attached via IPC handles)
+//
+// Gather kernel: the batch is a flat array of VEC-byte chunks (VEC = 16 when
+// rows are 16-byte aligned, else 8 or 4); consecutive lanes take consecutive
+// chunks (coalesced row reads and writes), every thread keeps U independent
+// chunk loads in flight, loads use ld.global.nc.L1::no_allocate (the source
+// is read-only for the store's lifetime). The id and lookup-table reads of a
+// row are shared by its lanes (same address, one transaction).
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "placement.cuh"
+#include "reads.cuh"
+
+namespace qvb {
+namespace {
+
+struct Bases {
+  const char* p[kMaxLocations];
+};
+
+template <int VEC>
+struct Vec;
+template <>
+struct Vec<16> {
+  using T = uint4;
+  static __device__ __forceinline__ T load(const char* p) {
+    T r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+  }
+  static __device__ __forceinline__ void store(char* p, const T& v) {
+    *reinterpret_cast<T*>(p) = v;
+  }
+};
+template <>
+struct Vec<8> {
+  using T = uint2;
+  static __device__ __forceinline__ T load(const char* p) {
+    T r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                 : "=r"(r.x), "=r"(r.y)
+                 : "l"(p));
+    return r;
+  }
+  static __device__ __forceinline__ void store(char* p, const T& v) {
+    *reinterpret_cast<T*>(p) = v;
+  }
+};
+template <>
+struct Vec<4> {
+  using T = uint32_t;
+  static __device__ __forceinline__ T load(const char* p) {
+    T r;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+  }
+  static __device__ __forceinline__ void store(char* p, const T& v) {
+    *reinterpret_cast<T*>(p) = v;
+  }
+};
+
+constexpr int kGatherBlock = 256;
+constexpr int kUnroll = 4;
+
+// Direct gather over request order. rows < 2^32 / cpr per launch.
+template <int VEC>
+__global__ void __launch_bounds__(kGatherBlock)
+    k_gather(const uint64_t* __restrict__ ids, uint32_t rows, const uint64_t* __restrict__ lut,
+             Bases bases, uint64_t stride, uint32_t cpr, uint32_t row_bytes, uint64_t n,
+             char* __restrict__ out, uint64_t row_base, unsigned long long* err) {
+  using V = Vec<VEC>;
+  const uint32_t total = rows * cpr;
+  const uint32_t nthreads = gridDim.x * blockDim.x;
+  for (uint32_t c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < total; c0 += nthreads * kUnroll) {
+    typename V::T v[kUnroll];
+    uint64_t dst[kUnroll];
+    bool ok[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t c = c0 + u * nthreads;
+      ok[u] = c < total;
+      if (ok[u]) {
+        const uint32_t i = c / cpr;
+        const uint32_t k = c - i * cpr;
+        const uint64_t f = __ldg(ids + i);
+        if (f >= n) {
+          atomicMin(err, (unsigned long long)(row_base + i));
+          ok[u] = false;
+        } else {
+          const uint64_t e = __ldg(lut + f);
+          const char* src = bases.p[e >> kOffsetBits] + (e & kOffsetMask) * stride + k * VEC;
+          v[u] = V::load(src);
+          dst[u] = (uint64_t)i * row_bytes + (uint64_t)k * VEC;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (ok[u]) V::store(out + dst[u], v[u]);
+  }
+}
+
+// Planned gather: sorted (location, offset) keys with the request index as
+// payload (K4 order); no lookup-table read in the copy loop.
+template <int VEC>
+__global__ void __launch_bounds__(kGatherBlock)
+    k_gather_sorted(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ order,
+                    uint32_t rows, Bases bases, uint64_t stride, uint32_t cpr, uint32_t row_bytes,
+                    char* __restrict__ out) {
+  using V = Vec<VEC>;
+  const uint32_t total = rows * cpr;
+  const uint32_t nthreads = gridDim.x * blockDim.x;
+  for (uint32_t c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < total; c0 += nthreads * kUnroll) {
+    typename V::T v[kUnroll];
+    uint64_t dst[kUnroll];
+    bool ok[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t c = c0 + u * nthreads;
+      ok[u] = c < total;
+      if (ok[u]) {
+        const uint32_t j = c / cpr;
+        const uint32_t k = c - j * cpr;
+        const uint64_t e = __ldg(keys + j);
+        const uint32_t i = __ldg(order + j);
+        v[u] = V::load(bases.p[e >> kOffsetBits] + (e & kOffsetMask) * stride + k * VEC);
+        dst[u] = (uint64_t)i * row_bytes + (uint64_t)k * VEC;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (ok[u]) V::store(out + dst[u], v[u]);
+  }
+}
+
+__global__ void k_plan_keys_packed(const uint64_t* __restrict__ ids, uint64_t b,
+                                   const uint64_t* __restrict__ lut, uint64_t n,
+                                   uint64_t* __restrict__ keys, uint32_t* __restrict__ idx,
+                                   unsigned long long* err) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < b;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t f = ids[i];
+    uint64_t k = 0;
+    if (f >= n) atomicMin(err, (unsigned long long)i);
+    else k = lut[f];
+    keys[i] = k;
+    idx[i] = static_cast<uint32_t>(i);
+  }
+}
+
+__global__ void k_fill_synthetic(const uint64_t* __restrict__ feat_of_row, uint64_t rows,
+                                 uint32_t dim, uint64_t stride, char* __restrict__ shard) {
+  const uint64_t total = rows * dim;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = t / dim;
+    const uint32_t k = static_cast<uint32_t>(t - r * dim);
+    reinterpret_cast<float*>(shard + r * stride)[k] = feature_value(feat_of_row[r], dim, k);
+  }
+}
+
+__global__ void k_restride(const char* __restrict__ in, uint64_t rows, uint32_t row_bytes,
+                           uint64_t stride, char* __restrict__ out) {
+  const uint64_t words = row_bytes / 4;
+  const uint64_t total = rows * words;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = t / words, w = t - r * words;
+    reinterpret_cast<uint32_t*>(out + r * stride)[w] =
+        reinterpret_cast<const uint32_t*>(in + r * row_bytes)[w];
+  }
+}
+
+__global__ void k_request_ids(uint64_t state, uint64_t n, uint64_t* __restrict__ ids, uint64_t b) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < b;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    ids[k] = to_below(stream_draw(state, k), n);
+}
+
+
+}  // namespace
+}  // namespace qvb
+
+using namespace qvb;
+
+struct qvb_store {
+  int device = 0;
+  uint64_t n = 0;
+  uint32_t dim = 0;
+  uint32_t reader = 0;
+  int nloc = 0;
+  uint32_t row_bytes = 0;
+  uint64_t stride = 0;
+  uint64_t* lut = nullptr;
+  char* local = nullptr;
+  uint64_t local_rows = 0;
+  char* host = nullptr;
+  char* host_dev = nullptr;
+  uint64_t host_rows = 0;
+  Bases bases{};
+  void* peer[kMaxLocations] = {};
+  uint64_t used_mask = 0;
+  unsigned long long* err = nullptr;
+  // e2e / planned scratch
+  uint64_t* d_ids = nullptr;
+  char* d_out = nullptr;
+  uint64_t cap_b = 0;
+
+  void ensure_scratch(uint64_t b) {
+    if (b <= cap_b) return;
+    cudaFree(d_ids);
+    cudaFree(d_out);
+    d_ids = nullptr;
+    d_out = nullptr;
+    QVB_CUDA(cudaMalloc(&d_ids, b * 8));
+    QVB_CUDA(cudaMalloc(&d_out, b * (uint64_t)row_bytes));
+    cap_b = b;
+  }
+
+  void check_attached() const {
+    for (int l = 0; l < nloc; ++l)
+      if (((used_mask >> l) & 1) && !bases.p[l])
+        fail(QVB_ERR_VALIDATION, "location " + std::to_string(l) +
+                                     " is read by this store's lookup table but its shard is not "
+                                     "attached (qvb_store_attach_peer)");
+  }
+
+  int vec() const { return row_bytes % 16 == 0 ? 16 : (row_bytes % 8 == 0 ? 8 : 4); }
+
+  void launch_gather(const uint64_t* ids, uint64_t b, char* out, cudaStream_t s) {
+    check_attached();
+    if (reinterpret_cast<uintptr_t>(out) % vec() != 0)
+      fail(QVB_ERR_VALIDATION, "output buffer is not aligned to the row vector width");
+    const int V = vec();
+    const uint32_t cpr = row_bytes / V;
+    const uint64_t max_rows = std::max<uint64_t>(1, (0xFFFFFFFFull / cpr) / 2);
+    for (uint64_t r0 = 0; r0 < b; r0 += max_rows) {
+      const uint32_t rows = static_cast<uint32_t>(std::min(max_rows, b - r0));
+      const uint64_t chunks = (uint64_t)rows * cpr;
+      const unsigned grid = grid_for((chunks + kUnroll - 1) / kUnroll, kGatherBlock, 148u * 8u);
+      char* o = out + r0 * row_bytes;
+      if (V == 16)
+        k_gather<16><<<grid, kGatherBlock, 0, s>>>(ids + r0, rows, lut, bases, stride, cpr,
+                                                   row_bytes, n, o, r0, err);
+      else if (V == 8)
+        k_gather<8><<<grid, kGatherBlock, 0, s>>>(ids + r0, rows, lut, bases, stride, cpr,
+                                                  row_bytes, n, o, r0, err);
+      else
+        k_gather<4><<<grid, kGatherBlock, 0, s>>>(ids + r0, rows, lut, bases, stride, cpr,
+                                                  row_bytes, n, o, r0, err);
+      QVB_LAUNCH_CHECK();
+    }
+  }
+
+  void launch_planned(const uint64_t* ids, uint64_t b, char* out, cudaStream_t s) {
+    check_attached();
+    if (b >= (1ull << 32)) fail(QVB_ERR_UNSUPPORTED, "batch exceeds 2^32 ids");
+    const int V = vec();
+    const uint32_t cpr = row_bytes / V;
+    if ((uint64_t)b * cpr >= 0xFFFFFFFFull) fail(QVB_ERR_UNSUPPORTED, "planned batch too large");
+    DevBuf<uint64_t> keys(b, s), skeys(b, s);
+    DevBuf<uint32_t> idx(b, s), order(b, s);
+    k_plan_keys_packed<<<grid_for(b, 256), 256, 0, s>>>(ids, b, lut, n, keys.p, idx.p, err);
+    QVB_LAUNCH_CHECK();
+    const int loc_bits = bits_for(static_cast<uint64_t>(nloc - 1));
+    sort_pairs_u64_u32(keys.p, skeys.p, idx.p, order.p, b, 0, kOffsetBits + loc_bits, s);
+    const uint32_t rows = static_cast<uint32_t>(b);
+    const uint64_t chunks = (uint64_t)rows * cpr;
+    const unsigned grid = grid_for((chunks + kUnroll - 1) / kUnroll, kGatherBlock, 148u * 8u);
+    if (V == 16)
+      k_gather_sorted<16><<<grid, kGatherBlock, 0, s>>>(skeys.p, order.p, rows, bases, stride, cpr,
+                                                        row_bytes, out);
+    else if (V == 8)
+      k_gather_sorted<8><<<grid, kGatherBlock, 0, s>>>(skeys.p, order.p, rows, bases, stride, cpr,
+                                                       row_bytes, out);
+    else
+      k_gather_sorted<4><<<grid, kGatherBlock, 0, s>>>(skeys.p, order.p, rows, bases, stride, cpr,
+                                                       row_bytes, out);
+    QVB_LAUNCH_CHECK();
+  }
+
+  ~qvb_store() {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaDeviceSynchronize();
+    for (auto& p : peer)
+      if (p) cudaIpcCloseMemHandle(p);
+    cudaFree(lut);
+    cudaFree(local);
+    if (host) cudaFreeHost(host);
+    cudaFree(err);
+    cudaFree(d_ids);
+    cudaFree(d_out);
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+namespace {
+
+void fill_rows(qvb_store& st, int loc, const DeviceLut& L, const float* features, char* dst_dev,
+               char* dst_host, uint64_t rows, cudaStream_t s) {
+  if (rows == 0) return;
+  DevBuf<uint64_t> fr(rows, s);
+  lut_rows_of_location(L, loc, fr.p, s);
+  if (!features) {
+    k_fill_synthetic<<<grid_for(rows * st.dim, 256), 256, 0, s>>>(fr.p, rows, st.dim, st.stride,
+                                                                  dst_dev);
+    QVB_LAUNCH_CHECK();
+    return;
+  }
+  std::vector<uint64_t> feat(rows);
+  QVB_CUDA(cudaMemcpyAsync(feat.data(), fr.p, rows * 8, cudaMemcpyDeviceToHost, s));
+  QVB_CUDA(cudaStreamSynchronize(s));
+  if (dst_host) {  // host tier: plain CPU copy into the pinned shard
+    for (uint64_t r = 0; r < rows; ++r)
+      std::memcpy(dst_host + r * st.stride, features + feat[r] * st.dim, st.row_bytes);
+    return;
+  }
+  const uint64_t chunk = std::max<uint64_t>(1, (256ull << 20) / st.row_bytes);
+  char* pin = nullptr;
+  QVB_CUDA(cudaMallocHost(&pin, std::min(chunk, rows) * st.row_bytes));
+  DevBuf<char> stage(std::min(chunk, rows) * st.row_bytes, s);
+  for (uint64_t r0 = 0; r0 < rows; r0 += chunk) {
+    const uint64_t c = std::min(chunk, rows - r0);
+    QVB_CUDA(cudaStreamSynchronize(s));
+    for (uint64_t r = 0; r < c; ++r)
+      std::memcpy(pin + r * st.row_bytes, features + feat[r0 + r] * st.dim, st.row_bytes);
+    QVB_CUDA(cudaMemcpyAsync(stage.p, pin, c * st.row_bytes, cudaMemcpyHostToDevice, s));
+    k_restride<<<grid_for(c * st.row_bytes / 4, 256), 256, 0, s>>>(stage.p, c, st.row_bytes,
+                                                                   st.stride, dst_dev + r0 * st.stride);
+    QVB_LAUNCH_CHECK();
+  }
+  QVB_CUDA(cudaStreamSynchronize(s));
+  cudaFreeHost(pin);
+}
+
+}  // namespace
+
+extern "C" int qvb_store_create(int device, const uint64_t* loc_offsets, const int64_t* loc_ids,
+                                uint64_t n, uint32_t dim, const qvb_topology* topo,
+                                uint32_t reader_device, const float* features, qvb_store** out) {
+  return guarded([&] {
+    if (!out) fail(QVB_ERR_VALIDATION, "out is null");
+    *out = nullptr;
+    if (!topo || !loc_offsets || (loc_offsets[n] && !loc_ids)) fail(QVB_ERR_VALIDATION, "null argument");
+    if (n == 0 || dim == 0) fail(QVB_ERR_VALIDATION, "store needs features and dim > 0");
+    topology_validate(*topo);
+    if (topo->servers != 1)
+      fail(QVB_ERR_UNSUPPORTED, "the device store serves one server (cross-server reads are out of scope)");
+    if (reader_device >= topo->gpus_per_server) fail(QVB_ERR_VALIDATION, "reader_device out of range");
+    if (n > kOffsetMask) fail(QVB_ERR_UNSUPPORTED, "too many features");
+    DeviceGuard dg(device);
+    cudaStream_t s = nullptr;
+    auto st = std::make_unique<qvb_store>();
+    st->device = device;
+    st->n = n;
+    st->dim = dim;
+    st->reader = reader_device;
+    st->nloc = static_cast<int>(topo->gpus_per_server + 2);
+    st->row_bytes = dim * 4u;
+    st->stride = (st->row_bytes + 15u) / 16u * 16u;
+    QVB_CUDA(cudaMalloc(&st->err, sizeof(unsigned long long)));
+    QVB_CUDA(cudaMemset(st->err, 0xFF, sizeof(unsigned long long)));
+
+    const uint64_t copies = loc_offsets[n];
+    DevBuf<uint64_t> dlo(n + 1, s);
+    DevBuf<int64_t> dids(copies ? copies : 1, s);
+    QVB_CUDA(cudaMemcpyAsync(dlo.p, loc_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
+    if (copies) QVB_CUDA(cudaMemcpyAsync(dids.p, loc_ids, copies * 8, cudaMemcpyHostToDevice, s));
+    DeviceLut L;
+    lut_prepare(L, dlo.p, dids.p, n, st->nloc, s);
+    QVB_CUDA(cudaMalloc(&st->lut, n * 8));
+    uint64_t missing = ~0ull;
+    st->used_mask = lut_choose(L, replica_order(*topo, 0, reader_device), nullptr, nullptr,
+                               st->lut, s, &missing);
+    if (missing != ~0ull)
+      fail(QVB_ERR_VALIDATION, "feature " + std::to_string(missing) + " has no location");
+    const int host_loc = static_cast<int>(topo->gpus_per_server);
+    if ((st->used_mask >> (host_loc + 1)) & 1)
+      fail(QVB_ERR_UNSUPPORTED, "the lookup table reads the disk tier, which the device store does not serve");
+
+    st->local_rows = L.location_rows[reader_device];
+    QVB_CUDA(cudaMalloc(&st->local, std::max<uint64_t>(1, st->local_rows) * st->stride));
+    fill_rows(*st, static_cast<int>(reader_device), L, features, st->local, nullptr, st->local_rows, s);
+    st->bases.p[reader_device] = st->local;
+    if ((st->used_mask >> host_loc) & 1) {
+      st->host_rows = L.location_rows[host_loc];
+      QVB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&st->host),
+                             std::max<uint64_t>(1, st->host_rows) * st->stride,
+                             cudaHostAllocMapped | cudaHostAllocPortable));
+      QVB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&st->host_dev), st->host, 0));
+      fill_rows(*st, host_loc, L, features, st->host_dev, features ? st->host : nullptr,
+                st->host_rows, s);
+      st->bases.p[host_loc] = st->host_dev;
+    }
+    QVB_CUDA(cudaStreamSynchronize(s));
+    *out = st.release();
+  });
+}
+
+extern "C" int qvb_store_info_get(const qvb_store* s, qvb_store_info* info) {
+  return guarded([&] {
+    if (!s || !info) fail(QVB_ERR_VALIDATION, "null argument");
+    std::memset(info, 0, sizeof *info);
+    info->feature_count = s->n;
+    info->dim = s->dim;
+    info->reader_device = s->reader;
+    info->row_stride_bytes = s->stride;
+    info->local_rows = s->local_rows;
+    info->host_rows = s->host_rows;
+    info->lut_bytes = s->n * 8;
+    info->location_count = static_cast<uint32_t>(s->nloc);
+  });
+}
+
+extern "C" int qvb_store_export_handle(const qvb_store* s, uint8_t handle[64]) {
+  return guarded([&] {
+    if (!s || !handle) fail(QVB_ERR_VALIDATION, "null argument");
+    DeviceGuard dg(s->device);
+    cudaIpcMemHandle_t h;
+    QVB_CUDA(cudaIpcGetMemHandle(&h, s->local));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle, &h, 64);
+  });
+}
+
+extern "C" int qvb_store_attach_peer(qvb_store* s, uint32_t peer_device, const uint8_t handle[64]) {
+  return guarded([&] {
+    if (!s || !handle) fail(QVB_ERR_VALIDATION, "null argument");
+    if (peer_device == s->reader || (int)peer_device >= s->nloc - 2)
+      fail(QVB_ERR_VALIDATION, "peer_device must be another GPU of the server");
+    DeviceGuard dg(s->device);
+    if (s->peer[peer_device]) {
+      cudaIpcCloseMemHandle(s->peer[peer_device]);
+      s->peer[peer_device] = nullptr;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    void* p = nullptr;
+    QVB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    s->peer[peer_device] = p;
+    s->bases.p[peer_device] = static_cast<const char*>(p);
+  });
+}
+
+extern "C" int qvb_store_attach_local_peer(qvb_store* s, uint32_t peer_device,
+                                           const qvb_store* peer) {
+  return guarded([&] {
+    if (!s || !peer) fail(QVB_ERR_VALIDATION, "null argument");
+    if (peer_device == s->reader || (int)peer_device >= s->nloc - 2)
+      fail(QVB_ERR_VALIDATION, "peer_device must be another GPU of the server");
+    if (peer->reader != peer_device || peer->n != s->n || peer->dim != s->dim)
+      fail(QVB_ERR_VALIDATION, "peer store does not hold that device's shard of this table");
+    DeviceGuard dg(s->device);
+    if (peer->device != s->device) {
+      int can = 0;
+      QVB_CUDA(cudaDeviceCanAccessPeer(&can, s->device, peer->device));
+      if (!can) fail(QVB_ERR_CUDA, "no P2P access between the two devices");
+      cudaError_t e = cudaDeviceEnablePeerAccess(peer->device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else QVB_CUDA(e);
+    }
+    s->bases.p[peer_device] = peer->local;
+  });
+}
+
+extern "C" int qvb_store_destroy(qvb_store* s) {
+  return guarded([&] { delete s; });
+}
+
+extern "C" int qvb_gather(qvb_store* s, const uint64_t* ids, uint64_t b, float* out, void* stream) {
+  return guarded([&] {
+    if (!s) fail(QVB_ERR_VALIDATION, "null store");
+    if (b == 0) return;
+    if (!ids || !out) fail(QVB_ERR_VALIDATION, "null argument");
+    DeviceGuard dg(s->device);
+    s->launch_gather(ids, b, reinterpret_cast<char*>(out), static_cast<cudaStream_t>(stream));
+  });
+}
+
+extern "C" int qvb_gather_planned(qvb_store* s, const uint64_t* ids, uint64_t b, float* out,
+                                  void* stream) {
+  return guarded([&] {
+    if (!s) fail(QVB_ERR_VALIDATION, "null store");
+    if (b == 0) return;
+    if (!ids || !out) fail(QVB_ERR_VALIDATION, "null argument");
+    DeviceGuard dg(s->device);
+    s->launch_planned(ids, b, reinterpret_cast<char*>(out), static_cast<cudaStream_t>(stream));
+  });
+}
+
+extern "C" int qvb_store_check_error(qvb_store* s) {
+  return guarded([&] {
+    if (!s) fail(QVB_ERR_VALIDATION, "null store");
+    DeviceGuard dg(s->device);
+    unsigned long long e = 0;
+    QVB_CUDA(cudaMemcpy(&e, s->err, sizeof e, cudaMemcpyDeviceToHost));
+    if (e != ~0ull) {
+      QVB_CUDA(cudaMemset(s->err, 0xFF, sizeof(unsigned long long)));
+      fail(QVB_ERR_VALIDATION, "request " + std::to_string(e) + ": feature id outside lookup table");
+    }
+  });
+}
+
+extern "C" int qvb_gather_host(qvb_store* s, const uint64_t* ids, uint64_t b, float* out,
+                               void* stream) {
+  return guarded([&] {
+    if (!s) fail(QVB_ERR_VALIDATION, "null store");
+    if (b == 0) return;
+    if (!ids || !out) fail(QVB_ERR_VALIDATION, "null argument");
+    DeviceGuard dg(s->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    s->ensure_scratch(b);
+    QVB_CUDA(cudaMemcpyAsync(s->d_ids, ids, b * 8, cudaMemcpyHostToDevice, st));
+    s->launch_gather(s->d_ids, b, s->d_out, st);
+    QVB_CUDA(cudaMemcpyAsync(out, s->d_out, b * (uint64_t)s->row_bytes, cudaMemcpyDeviceToHost, st));
+    QVB_CUDA(cudaStreamSynchronize(st));
+    unsigned long long e = 0;
+    QVB_CUDA(cudaMemcpy(&e, s->err, sizeof e, cudaMemcpyDeviceToHost));
+    if (e != ~0ull) {
+      QVB_CUDA(cudaMemset(s->err, 0xFF, sizeof(unsigned long long)));
+      fail(QVB_ERR_VALIDATION, "feature id " + std::to_string(ids[e]) + " outside lookup table");
+    }
+  });
+}
+
+extern "C" int qvb_request_ids_synthetic(int device, uint64_t seed, uint64_t batch, uint64_t n,
+                                         uint64_t* ids, uint64_t b, void* stream) {
+  return guarded([&] {
+    if (b == 0) return;
+    if (!ids || n == 0) fail(QVB_ERR_VALIDATION, "null ids or n == 0");
+    DeviceGuard dg(device);
+    const uint64_t state = derive_state(seed, 0x5EEDULL, batch);
+    k_request_ids<<<grid_for(b, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(state, n, ids, b);
+    QVB_LAUNCH_CHECK();
+  });
+}

@@ -143,6 +143,7 @@ _SIGNATURES = {
     "qvb_store_info_get": (i32, [vp, P(StoreInfo)]),
     "qvb_store_export_handle": (i32, [vp, vp]),
     "qvb_store_attach_peer": (i32, [vp, u32, vp]),
+    "qvb_store_attach_local_peer": (i32, [vp, u32, vp]),
     "qvb_store_destroy": (i32, [vp]),
     "qvb_gather": (i32, [vp, vp, u64, vp, vp]),
     "qvb_gather_planned": (i32, [vp, vp, u64, vp, vp]),
@@ -161,9 +162,7 @@ def _lib():
                 "(the qvb path has no CPU fallback)")
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in _SIGNATURES.items():
-            f = getattr(L, name, None)
-            if f is None:  # tests/test_boundary.py requires every symbol to exist
-                continue
+            f = getattr(L, name)  # every declared entry point must be exported
             f.restype = res
             f.argtypes = args
         _LIB = L
@@ -303,3 +302,148 @@ def compute_access_prob_ie(row_offsets, col, weights, layers: int, device: int =
     if timings is not None:
         timings[:] = list(ms)
     return AccessProbTable(out[:n], layers)
+
+
+# ---- K2 / placement (placement.cpp:79-226) ------------------------------------
+def rank_desc(values, device: int = 0) -> np.ndarray:
+    """fap_ranking (placement.cpp:79-87): ids by value desc, id asc on ties."""
+    v = np.ascontiguousarray(values, np.float64)
+    r = np.zeros(max(len(v), 1), np.uint64)
+    _check(_lib().qvb_rank_desc(device, _ptr(v), len(v), _ptr(r), 0, None))
+    return r[: len(v)]
+
+
+def plan_placement(values, topo: Topology, device: int = 0):
+    """qv::plan_placement(FapTable{values}, topo) in canonical CSR form:
+    (loc_offsets[n+1], loc_ids[copies]) — feature f's copies are
+    loc_ids[loc_offsets[f]:loc_offsets[f+1]], ascending encoded location ids."""
+    v = np.ascontiguousarray(values, np.float64)
+    n = len(v)
+    cap = max(1, n * topo.servers * (topo.gpus_per_server + 1))
+    lo = np.zeros(n + 1, np.uint64)
+    ids = np.zeros(cap, np.int64)
+    copies = u64(0)
+    _check(_lib().qvb_plan_placement(device, _ptr(v) if n else None, n, C.byref(topo), _ptr(lo),
+                                     _ptr(ids), cap, C.byref(copies)))
+    return lo, ids[: copies.value].copy()
+
+
+def build_lookup_table(loc_offsets, loc_ids, topo: Topology, home_server: int = 0,
+                       reader: int = 0, device: int = 0):
+    """qv::build_lookup_table(plan, topo, home_server) -> (location_ids, offsets).
+    ``reader`` > 0 is the per-reader extension (the reference reads from GPU 0)."""
+    lo = np.ascontiguousarray(loc_offsets, np.uint64)
+    ids = np.ascontiguousarray(loc_ids, np.int64)
+    n = len(lo) - 1
+    loc = np.zeros(max(n, 1), np.int64)
+    off = np.zeros(max(n, 1), np.uint64)
+    _check(_lib().qvb_build_lookup_table(device, _ptr(lo), _ptr(ids) if len(ids) else None, n,
+                                         C.byref(topo), home_server, reader, _ptr(loc), _ptr(off)))
+    return loc[:n], off[:n]
+
+
+# ---- K4 read planner (placement.cpp:344-380) -----------------------------------
+def page_transitions(offsets, page_size: int) -> int:
+    o = np.ascontiguousarray(offsets, np.uint64)
+    out = u64(0)
+    _check(_lib().qvb_page_transitions(_ptr(o) if len(o) else None, len(o), page_size, C.byref(out)))
+    return out.value
+
+
+def plan_reads(location_ids, offsets, ids, page_size: int = 8, device: int = 0):
+    """qv::plan_reads flattened: (group_loc, group_count, group_transitions,
+    offsets) — groups ascending by location, offsets ascending per group."""
+    loc = np.ascontiguousarray(location_ids, np.int64)
+    off = np.ascontiguousarray(offsets, np.uint64)
+    req = np.ascontiguousarray(ids, np.uint64)
+    b = len(req)
+    m = max(b, 1)
+    gl = np.zeros(m, np.int64)
+    gc = np.zeros(m, np.uint64)
+    gt = np.zeros(m, np.uint64)
+    oo = np.zeros(m, np.uint64)
+    ng = u64(0)
+    _check(_lib().qvb_plan_reads(device, _ptr(loc), _ptr(off), len(loc), _ptr(req) if b else None, b,
+                                 page_size, _ptr(gl), _ptr(gc), _ptr(gt), C.byref(ng), _ptr(oo)))
+    g = ng.value
+    return gl[:g].copy(), gc[:g].copy(), gt[:g].copy(), oo[:b].copy()
+
+
+# ---- K5 feature store + gather ---------------------------------------------------
+class FeatureStore:
+    """One reader GPU's view of the placed feature table (qvb_store).
+
+    Built from a single-server plan (``plan_placement`` output); holds this
+    GPU's shard in HBM, the host tier in pinned mapped memory and the
+    reader's lookup table; peers are attached with ``attach_peer``."""
+
+    def __init__(self, loc_offsets, loc_ids, dim: int, topo: Topology, reader: int = 0,
+                 features=None, device: int | None = None):
+        lo = np.ascontiguousarray(loc_offsets, np.uint64)
+        ids = np.ascontiguousarray(loc_ids, np.int64)
+        self.n = len(lo) - 1
+        self.dim = dim
+        self.device = reader if device is None else device
+        x = None if features is None else np.ascontiguousarray(features, np.float32)
+        if x is not None and x.shape != (self.n, dim):
+            raise ValidationError(f"features must be ({self.n}, {dim})")
+        h = vp()
+        _check(_lib().qvb_store_create(self.device, _ptr(lo), _ptr(ids) if len(ids) else None, self.n,
+                                       dim, C.byref(topo), reader, _ptr(x), C.byref(h)))
+        self._h = h.value
+        self._keep = x
+
+    def info(self) -> StoreInfo:
+        i = StoreInfo()
+        _check(_lib().qvb_store_info_get(self._h, C.byref(i)))
+        return i
+
+    def export_handle(self) -> bytes:
+        buf = (C.c_uint8 * 64)()
+        _check(_lib().qvb_store_export_handle(self._h, buf))
+        return bytes(buf)
+
+    def attach_peer(self, peer_device: int, handle: bytes) -> None:
+        buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+        _check(_lib().qvb_store_attach_peer(self._h, peer_device, buf))
+
+    def attach_local_peer(self, peer_device: int, peer: "FeatureStore") -> None:
+        """Map another store of this process (P2P when on another device)."""
+        _check(_lib().qvb_store_attach_local_peer(self._h, peer_device, peer._h))
+        self._peers = getattr(self, "_peers", []) + [peer]
+
+    def gather(self, ids, out, stream=None, planned: bool = False) -> None:
+        """Device gather: ids (uint64) and out (float32, b x dim) are device
+        tensors; stream-ordered, no synchronisation."""
+        fn = _lib().qvb_gather_planned if planned else _lib().qvb_gather
+        _check(fn(self._h, _ptr(ids), int(ids.numel()), _ptr(out), _stream_ptr(stream)))
+
+    def check_error(self) -> None:
+        _check(_lib().qvb_store_check_error(self._h))
+
+    def gather_host(self, ids, out=None, stream=None) -> np.ndarray:
+        """End-to-end collect from host buffers (H2D ids, gather, D2H rows)."""
+        req = ids if isinstance(ids, np.ndarray) and ids.dtype == np.uint64 else \
+            np.ascontiguousarray(ids, np.uint64)
+        if out is None:
+            out = np.zeros((len(req), self.dim), np.float32)
+        _check(_lib().qvb_gather_host(self._h, _ptr(req), len(req), _ptr(out), _stream_ptr(stream)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib().qvb_store_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def request_ids_synthetic(seed: int, batch: int, n: int, out, device: int = 0, stream=None):
+    """ids[k] = derive_stream(seed, 0x5EED, batch).below(n) draw k, on device."""
+    _check(_lib().qvb_request_ids_synthetic(device, seed, batch, n, _ptr(out), int(out.numel()),
+                                            _stream_ptr(stream)))
+    return out

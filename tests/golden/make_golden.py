@@ -1,0 +1,160 @@
+"""Generates tests/golden/golden.json from the UNMODIFIED reference.
+
+Run in the build container (where /root/reference exists):
+    python tests/golden/make_golden.py
+It loads oracle/_ref/libqvref.so — the reference's own graph.cpp, metrics.cpp,
+placement.cpp and topology.cpp compiled by oracle/Makefile — and records its
+outputs on the reference's own fixtures (tests/testutil.hpp,
+tests/test_placement.cpp, tests/acceptance.cpp) plus the BASELINE C1 graphs.
+The GPU box never reads /root/reference; it reads this JSON.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+from oracle.oracle import Oracle, RefLib, build, topology_defaults  # noqa: E402
+from tests.util import derive_stream, fig8_edges  # noqa: E402
+
+
+def hexs(a):
+    return [f"{int(x):016x}" for x in np.ascontiguousarray(a, np.float64).view(np.uint64)]
+
+
+def digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def topo_dict(t):
+    return {f: (list(getattr(t, f)) if f.startswith("link_") else getattr(t, f))
+            for f, _ in t._fields_ if f != "_pad0"}
+
+
+def five_features():  # test_placement.cpp:18-24
+    return np.array([0.5, 0.4, 0.3, 0.2, 0.1])
+
+
+def scenarios():
+    """acceptance.cpp:183-268 (a)-(d) and test_placement.cpp:44-68."""
+    a = dict(servers=1, numa_per_server=2, gpus_per_server=4, gpu_feature_capacity=1,
+             host_feature_capacity=4, disk_feature_capacity=8, nvlink_within_numa=0, infiniband=0)
+    b = dict(a, nvlink_within_numa=1)
+    c = dict(servers=2, numa_per_server=1, gpus_per_server=1, gpu_feature_capacity=1,
+             host_feature_capacity=1, disk_feature_capacity=3, nvlink_within_numa=0, infiniband=0)
+    d = dict(c, infiniband=1)
+    e = dict(b, servers=2, infiniband=1)  # test_placement.cpp:180-200
+    return {"a": a, "b": b, "c": c, "d": d, "closest_replica": e}
+
+
+def random_topologies():
+    """test_placement.cpp:147-178 draws."""
+    rng = derive_stream(103, 1)
+    out = []
+    for _ in range(40):
+        n = 1 + rng.below(60)
+        vals = [rng.uniform() for _ in range(n)]
+        t = dict(servers=1 + rng.below(3), numa_per_server=1 + rng.below(2))
+        t["gpus_per_server"] = t["numa_per_server"] * (1 + rng.below(2))
+        t["gpu_feature_capacity"] = rng.below(4)
+        t["host_feature_capacity"] = rng.below(10)
+        t["disk_feature_capacity"] = 20 + rng.below(40)
+        t["nvlink_within_numa"] = int(rng.below(2) == 0)
+        t["infiniband"] = int(rng.below(2) == 0)
+        out.append((vals, t))
+    return out
+
+
+def main():
+    build(ref=True)
+    r = RefLib()
+    o = Oracle()
+    g = {"generator": "tests/golden/make_golden.py via oracle/_ref (unmodified reference)"}
+
+    n, s, d, w = fig8_edges()
+    ro, col, ww = o.build_csr(n, s, d, w)
+    g["fig8"] = {str(L): hexs(r.access_prob(ro, col, ww, L)) for L in (1, 2, 3, 4)}
+
+    c1 = {}
+    for name, weighted, transposed, layers in [("uniform_L2", False, False, 2),
+                                               ("uniform_L3", False, False, 3),
+                                               ("weighted_L3", True, False, 3),
+                                               ("transposed_L3", False, True, 3)]:
+        ro, col, ww = o.synthetic_graph(100_000, 1_000_000, 7, weighted, transposed)
+        p = r.access_prob(ro, col, ww, layers)
+        c1[name] = {"sha256": digest(p), "graph_sha256": digest(np.concatenate(
+            [ro.view(np.uint8), col.view(np.uint8), ww.view(np.uint8)])),
+            "head": hexs(p[:16])}
+        if name == "uniform_L2":
+            t8 = topology_defaults(gpus_per_server=8, numa_per_server=1, nvlink_within_numa=1,
+                                   gpu_feature_capacity=6_000, host_feature_capacity=100_000)
+            lo, ids = r.plan_placement(p, t8)
+            loc, off = r.build_lookup_table(lo, ids, t8, 0)
+            req = o.request_ids(11, 0, 100_000, 4096)
+            gl, gc, gt, oo = r.plan_reads(loc, off, req, 8)
+            c1[name]["placement8"] = {"topology": topo_dict(t8), "plan_sha256": digest(
+                np.concatenate([lo.view(np.uint8), ids.view(np.uint8)])),
+                "lut_sha256": digest(np.concatenate([loc.view(np.uint8), off.view(np.uint8)])),
+                "reads": {"group_loc": gl.tolist(), "group_count": gc.tolist(),
+                          "group_transitions": gt.tolist(), "offsets_sha256": digest(oo)}}
+    g["c1"] = c1
+
+    sc = {}
+    for name, kw in scenarios().items():
+        t = topology_defaults(**kw)
+        lo, ids = r.plan_placement(five_features(), t)
+        loc, off = r.build_lookup_table(lo, ids, t, 0)
+        ent = {"topology": topo_dict(t), "loc_offsets": lo.tolist(), "loc_ids": ids.tolist(),
+               "lut_loc": loc.tolist(), "lut_off": off.tolist()}
+        gl, gc, gt, oo = r.plan_reads(loc, off, [4, 1, 0, 3, 1], 2)
+        ent["reads_41031_p2"] = [gl.tolist(), gc.tolist(), gt.tolist(), oo.tolist()]
+        sc[name] = ent
+    g["scenarios"] = sc
+
+    # "short by 3" (test_placement.cpp:138-145)
+    t = topology_defaults(**dict(scenarios()["c"], disk_feature_capacity=0, host_feature_capacity=1))
+    try:
+        r.plan_placement(five_features(), t)
+        raise SystemExit("expected PlacementError")
+    except Exception as e:  # noqa: BLE001
+        g["short_by_3"] = {"code": getattr(e, "code", None), "msg": getattr(e, "msg", str(e)),
+                           "topology": topo_dict(t)}
+
+    rnd = []
+    for vals, kw in random_topologies():
+        t = topology_defaults(**kw)
+        ent = {"values": vals, "topology": topo_dict(t)}
+        try:
+            lo, ids = r.plan_placement(np.array(vals), t)
+            ent["loc_offsets"] = lo.tolist()
+            ent["loc_ids"] = ids.tolist()
+            homes = {}
+            for home in range(t.servers):
+                loc, off = r.build_lookup_table(lo, ids, t, home)
+                homes[str(home)] = [loc.tolist(), off.tolist()]
+            ent["luts"] = homes
+        except Exception as e:  # noqa: BLE001
+            ent["error"] = {"code": getattr(e, "code", None), "msg": getattr(e, "msg", str(e))}
+        rnd.append(ent)
+    g["random_placements"] = rnd
+
+    g["page_transitions"] = [[[2, 10, 3, 11], 2, r.page_transitions([2, 10, 3, 11], 2)],
+                             [[2, 3, 10, 11], 2, r.page_transitions([2, 3, 10, 11], 2)],
+                             [[5], 2, r.page_transitions([5], 2)],
+                             [[3, 1, 2, 0], 8, r.page_transitions([3, 1, 2, 0], 8)],
+                             [[], 4, r.page_transitions([], 4)]]
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
+    with open(path, "w") as f:
+        json.dump(g, f, indent=1, sort_keys=True)
+    print("wrote", path)
+
+
+if __name__ == "__main__":
+    main()
