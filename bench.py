@@ -1,0 +1,456 @@
+#!/usr/bin/env python
+"""bench.py — the north-star measurement of the B200 Quiver feature-store path.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is one collect call: gather one batch of B uniform request ids
+(derive_stream(11, 0x5EED, batch).below(N)) from the placed
+feature table. The workload at N=1 is BASELINE configs[1] (C2,
+ogbn-products-shaped: 2.4M nodes, 62M edges, 100-dim fp32, 2-layer P(n,j)):
+the graph is generated on the device, P(n,j) ranks the features, the
+placement manager partitions them over the N GPUs (hot replication / host
+fraction optional), every rank builds its store and lookup table and serves
+its own batches (weak scaling; no data-path collective).
+
+`value` = whole-job gathered payload GB/s with ids resident in HBM; `e2e` =
+the same through the public C-ABI from pinned host buffers (H2D ids, gather,
+D2H rows, sync) every step. The line also carries the P(n,j) pass
+(`access_prob`: edges/s, its roofline and the reference CPU timing), the
+`roofline` of the dominant gather kernel and the `cpu_baseline`.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "gathered feature GB/s at 1/2/4/8 B200 and access-prob edges/s vs HBM roofline"
+CONFIGS = {
+    "C1": dict(n=100_000, e=1_000_000, dim=128, layers=2, weighted=False,
+               desc="C1 synthetic power-law graph: 100K nodes, avg degree 10, 128-dim fp32"),
+    "C2": dict(n=2_400_000, e=62_000_000, dim=100, layers=2, weighted=False,
+               desc="C2 ogbn-products-shaped: 2.4M nodes, 62M edges, 100-dim fp32, 2-layer P"),
+    "C3": dict(n=233_000, e=114_000_000, dim=602, layers=3, weighted=True,
+               desc="C3 Reddit-shaped: 233K nodes, 114M edges, 602-dim fp32, 3-layer weighted P"),
+    "C4": dict(n=111_000_000, e=1_600_000_000, dim=128, layers=3, weighted=False,
+               desc="C4 ogbn-papers100M-shaped: 111M nodes, 1.6B edges, 128-dim fp32, 3-layer P"),
+}
+META_BYTES = 24  # 8 B id + 16 B reference-layout lookup row per request
+
+
+def peaks():
+    p = {"hbm_gbs": 6549.4, "source": "measured"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p["hbm_gbs"] = float(json.load(f)["hbm_gbs"])
+    except Exception:  # noqa: BLE001
+        p = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock/throttle sampling (NVML) during a window."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.01):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self.period = period_s
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.N = None
+
+    def _run(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.N:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def bytes_per_sweep(eu: int, n: int, weighted: bool) -> int:
+    """uniform 12 B/edge + 32 B/node; weighted 20 B/edge + 24 B/node."""
+    return eu * (20 if weighted else 12) + n * (24 if weighted else 32)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    from paper_2305_10863_b200 import dist as D
+    from paper_2305_10863_b200 import qvb
+
+    rank, world, local = D.init()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    cfg = CONFIGS[args.config]
+    n, e, dim, layers = cfg["n"], cfg["e"], cfg["dim"], cfg["layers"]
+    row_bytes = 4 * dim
+    B = args.batch
+    pk = peaks()
+
+    # ---- P(n,j): graph on device, K timed passes ------------------------------
+    g = qvb.DeviceGraph.synthetic(n, e, 7, cfg["weighted"], False, device=local, stream=stream)
+    info = g.info()
+    p_dev = torch.empty(n, dtype=torch.float64, device=dev)
+    for _ in range(args.warmup):
+        g.access_prob(layers, out=p_dev, stream=stream)
+    torch.cuda.synchronize(dev)
+    ap_call, ap_sweep = [], []
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for _ in range(args.steps):
+        ev[0].record(stream)
+        g.access_prob(layers, out=p_dev, stream=stream)
+        ev[1].record(stream)
+        ev[1].synchronize()
+        ap_call.append(ev[0].elapsed_time(ev[1]))
+        ap_sweep.append(g.last_sweep_ms())
+    p_host = p_dev.cpu().numpy()
+    sweeps = layers - 1
+    ap_bytes = bytes_per_sweep(info.unique_edge_count, n, info.layout == 1) * sweeps
+    ap_ms = statistics.mean(ap_call)
+    sweep_ms = statistics.mean(ap_sweep)
+    access_prob = {
+        "metric": "access-prob edges/s (coalesced in-edges x sweeps / device time of the P call)",
+        "value": info.unique_edge_count * sweeps / (ap_ms / 1e3),
+        "unit": "edges/s",
+        "ms_per_call": ap_ms,
+        "sweep_ms": sweep_ms,
+        "layers": layers,
+        "graph": {"nodes": n, "edges": e, "unique_edges": info.unique_edge_count,
+                  "exceptions": info.exception_count,
+                  "layout": "weighted" if info.layout else "compact",
+                  "in_csr_build_ms": info.build_ms, "device_bytes": info.device_bytes},
+        "roofline": {"bound": "hbm", "kernel": "k_sweep", "traffic": None,
+                     "algorithmic_bytes": ap_bytes,
+                     "achieved": ap_bytes / (sweep_ms / 1e3) / 1e9, "peak": pk["hbm_gbs"],
+                     "unit": "GB/s", "frac": ap_bytes / (sweep_ms / 1e3) / 1e9 / pk["hbm_gbs"],
+                     "peak_source": pk["source"]},
+        "gpu_launches": args.steps * (1 + sweeps),
+    }
+    g.close()
+
+    # ---- placement + store ------------------------------------------------------
+    topo = D.topology_for(qvb, n, world, args.replicate, args.host_frac)
+    t0 = time.perf_counter()
+    lo, ids = qvb.plan_placement(p_host, topo, device=local)
+    plan_s = time.perf_counter() - t0
+    loc, _ = qvb.build_lookup_table(lo, ids, topo, 0, rank, device=local)
+    f_l = float(np.mean(loc == rank))
+    f_h = float(np.mean(loc == world))
+    f_p = 1.0 - f_l - f_h
+    store = D.build_store(qvb, lo, ids, dim, topo, rank, local)
+
+    # request batches resident in HBM: (W + K) distinct batches per rank
+    nb = args.warmup + args.steps
+    req = torch.empty((nb, B), dtype=torch.int64, device=dev)
+    for k in range(nb):
+        qvb.request_ids_synthetic(11, rank * 1_000_003 + k, n, req[k], device=local, stream=stream)
+    out = torch.empty((B, dim), dtype=torch.float32, device=dev)
+    for k in range(args.warmup):
+        store.gather(req[k], out, stream=stream)
+    torch.cuda.synchronize(dev)
+    store.check_error()
+
+    clocks = ClockSampler(local)
+    with clocks:
+        # keep the clocks observable: ~1 s of the same gathers right before the
+        # timed region (untimed), sampled together with it
+        t_end = time.perf_counter() + args.clock_window
+        while time.perf_counter() < t_end:
+            for k in range(args.warmup):
+                store.gather(req[k], out, stream=stream)
+            torch.cuda.synchronize(dev)
+        D.barrier()
+        torch.cuda.synchronize(dev)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        evs[0].record(stream)
+        for k in range(args.steps):
+            store.gather(req[args.warmup + k], out, stream=stream)
+            evs[k + 1].record(stream)
+        torch.cuda.synchronize(dev)
+        D.barrier()
+    store.check_error()
+    launch_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
+    total_ms = evs[0].elapsed_time(evs[-1])
+    max_ms = D.max_over_ranks(total_ms)
+    payload = world * args.steps * B * row_bytes
+    value = payload / (max_ms / 1e3) / 1e9
+    per_launch_ms = statistics.mean(launch_ms)
+    hbm_per_id = META_BYTES + row_bytes * (1 + f_l + f_p)
+    alg = B * hbm_per_id
+    achieved = alg / (per_launch_ms / 1e3) / 1e9
+
+    # ---- e2e through the public API from pinned host buffers --------------------
+    e2e = None
+    if not args.no_e2e:
+        host_ids = [req[args.warmup + k].cpu().pin_memory() for k in range(args.steps)]
+        host_out = torch.empty((B, dim), dtype=torch.float32).pin_memory()
+        store.gather_host(host_ids[0].numpy().view(np.uint64), host_out.numpy(), stream=stream)
+        D.barrier()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            store.gather_host(host_ids[k].numpy().view(np.uint64), host_out.numpy(), stream=stream)
+        e2e_s = D.max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": payload / e2e_s / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": B * 8, "d2h_bytes_per_step": B * row_bytes,
+               "note": "qvb_gather_host per step: H2D ids (pinned) + gather + D2H rows (pinned) "
+                       "+ stream sync; wall clock, max over ranks"}
+        # P(n,j) end to end: host out-CSR -> device -> in-CSR -> sweeps -> host P
+        ro, col, w = qvb.synthetic_csr(n, e, 7, cfg["weighted"], False, device=local)
+        tm = [0.0, 0.0, 0.0]
+        t0 = time.perf_counter()
+        qvb.compute_access_prob_ie(ro, col, w if cfg["weighted"] else None, layers, device=local,
+                                   timings=tm)
+        wall = time.perf_counter() - t0
+        access_prob["e2e"] = {
+            "value": info.unique_edge_count * sweeps / wall, "unit": "edges/s",
+            "wall_s": wall, "upload_build_ms": tm[0], "sweeps_ms": tm[1], "download_ms": tm[2],
+            "h2d_bytes": int(ro.nbytes + col.nbytes + (w.nbytes if cfg["weighted"] else 0)),
+            "d2h_bytes": n * 8,
+            "note": "qvb_compute_access_prob_ie from a host qv::Graph-layout CSR (the reference "
+                    "call, which rebuilds its transpose every call)"}
+    else:
+        ro = col = w = None
+
+    # ---- CPU baseline (rank 0, N=1) ---------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu, ap_cpu = cpu_baseline(args, cfg, p_host, topo_host=topo, ro=ro, col=col, w=w,
+                                   steps=min(args.steps, args.cpu_steps))
+        access_prob["cpu_baseline"] = ap_cpu
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": max_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp32 rows copied bit-exact (P in fp64)",
+        "data": "synthetic (bench.cpp generator seed 7; SURVEY §8(d) features and request streams)",
+        "config": {
+            "workload": cfg["desc"] + f"; gather batches of {B} uniform ids per GPU",
+            "config": args.config, "batch": B, "dim": dim, "n_features": n,
+            "features_partitioned_over": world, "replicate_fraction": args.replicate,
+            "host_fraction": args.host_frac,
+            "fractions": {"local": f_l, "peer": f_p, "host": f_h},
+            "placement_s": plan_s,
+            "l2": "inputs larger than L2 (feature table %.0f MB, %.0f MB of rows per step)" % (
+                n * row_bytes / 1e6, B * row_bytes / 1e6),
+            "parallelism": f"feature-partitioned x{world}, one process per GPU",
+        },
+        "roofline": {"bound": "hbm", "kernel": "k_gather", "achieved": achieved,
+                     "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                     "traffic": None, "algorithmic_bytes_per_id": hbm_per_id,
+                     "per_launch_ms": per_launch_ms, "peak_source": pk["source"]},
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "access_prob": access_prob,
+        "clocks": clocks.summary(),
+        "cpu_baseline": cpu,
+    }
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):  # ncu dram bytes per launch, captured by profiles/run_ncu.sh
+        try:
+            tr = json.load(open(prof)).get(args.config, {})
+            if "k_gather" in tr:
+                line["roofline"]["traffic"] = tr["k_gather"]["bytes_per_launch"]
+                line["roofline"]["traffic_batch"] = tr["k_gather"].get("batch")
+            if "k_sweep" in tr:
+                access_prob["roofline"]["traffic"] = tr["k_sweep"]["bytes_per_launch"]
+        except Exception:  # noqa: BLE001
+            pass
+    store.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args, cfg, p_host, topo_host, ro, col, w, steps):
+    """Reference CPU path on this host (rank 0 only), bounded samples."""
+    import numpy as np
+
+    from oracle.oracle import Oracle, RefLib, topology_defaults
+
+    o = Oracle()
+    n, dim = cfg["n"], cfg["dim"]
+    threads = os.cpu_count() or 1
+    ref = RefLib() if RefLib.available() else None
+    if ro is None:
+        ro, col, w = o.synthetic_graph(n, cfg["e"], 7, cfg["weighted"], False)
+    # P(n,j): the reference call itself (OpenMP, includes its transpose)
+    if ref is not None:
+        ref.set_threads(threads)
+        t0 = time.perf_counter()
+        p_ref = ref.access_prob(ro, col, w, cfg["layers"], parallel=True)
+        ap_s = time.perf_counter() - t0
+        kind = "reference"
+    else:
+        t0 = time.perf_counter()
+        p_ref = o.access_prob(ro, col, w, cfg["layers"])
+        ap_s = time.perf_counter() - t0
+        kind = "port"
+    ap = {"value": cfg["e"] * (cfg["layers"] - 1) / ap_s, "unit": "edges/s (input edges)",
+          "cores": threads if kind == "reference" else 1, "kind": kind,
+          "sample": f"one qv::compute_access_prob_ie call on the full {cfg['desc']} graph "
+                    f"(L={cfg['layers']}, includes the reference's per-call transpose)",
+          "seconds": ap_s,
+          "bit_identical_to_gpu": bool((p_ref.view(np.uint64) == p_host.view(np.uint64)).all())}
+    # collect: the reference's read planner (placement.cpp:355-380) on each
+    # batch + the byte copy it only models, restated as a threaded memcpy
+    t = topology_defaults(gpus_per_server=1, gpu_feature_capacity=n, host_feature_capacity=n)
+    lo, ids = (ref or o).plan_placement(p_host, t)
+    loc, off = (ref or o).build_lookup_table(lo, ids, t, 0)
+    x = o.features(n, dim)
+    plan_s = gather_s = 0.0
+    b = args.batch
+    for k in range(steps):
+        req = o.request_ids(11, k, n, b)
+        t0 = time.perf_counter()
+        (ref or o).plan_reads(loc, off, req, 8)
+        t1 = time.perf_counter()
+        o.gather(x, req, threads=threads)
+        t2 = time.perf_counter()
+        plan_s += t1 - t0
+        gather_s += t2 - t1
+    payload = steps * b * 4 * dim
+    cpu = {"value": payload / (plan_s + gather_s) / 1e9, "unit": "GB/s", "cores": threads,
+           "kind": "reference" if ref is not None else "port",
+           "sample": f"{steps} batches x {b} uniform ids on the C2 table: qv::plan_reads "
+                     f"(the reference's collect call, 1 thread) + the row copy it only models "
+                     f"(memcpy restatement, {threads} threads)",
+           "plan_reads_s": plan_s, "memcpy_s": gather_s,
+           "memcpy_only_GBps": payload / gather_s / 1e9}
+    return cpu, ap
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU path, rank 0 only."""
+    import numpy as np
+
+    from oracle.oracle import Oracle, RefLib, topology_defaults
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    n, dim, B = cfg["n"], cfg["dim"], args.batch
+    o = Oracle()
+    ref = RefLib() if RefLib.available() else None
+    lib = ref or o
+    threads = os.cpu_count() or 1
+    if ref:
+        ref.set_threads(threads)
+    ro, col, w = o.synthetic_graph(n, cfg["e"], 7, cfg["weighted"], False)
+    t0 = time.perf_counter()
+    p = ref.access_prob(ro, col, w, cfg["layers"], True) if ref else o.access_prob(ro, col, w, cfg["layers"])
+    ap_s = time.perf_counter() - t0
+    t = topology_defaults(gpus_per_server=1, gpu_feature_capacity=n, host_feature_capacity=n)
+    lo, ids = lib.plan_placement(p, t)
+    loc, off = lib.build_lookup_table(lo, ids, t, 0)
+    x = o.features(n, dim)
+    reqs = [o.request_ids(11, k, n, B) for k in range(args.warmup + args.steps)]
+    for k in range(args.warmup):
+        lib.plan_reads(loc, off, reqs[k], 8)
+        o.gather(x, reqs[k], threads=threads)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        lib.plan_reads(loc, off, reqs[args.warmup + k], 8)
+        o.gather(x, reqs[args.warmup + k], threads=threads)
+    el = time.perf_counter() - t0
+    value = args.steps * B * 4 * dim / el / 1e9
+    kind = "reference" if ref else "port"
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 rows (P in fp64)",
+        "data": "synthetic (bench.cpp generator seed 7; SURVEY §8(d))",
+        "config": {"workload": cfg["desc"] + f"; gather batches of {B} uniform ids",
+                   "config": args.config, "batch": B, "dim": dim, "n_features": n},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
+                         "sample": f"each step: qv::plan_reads on a {B}-id batch (reference "
+                                   f"code, oracle/_ref) + the row copy it only models "
+                                   f"(memcpy restatement, {threads} threads)"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "access_prob": {"value": cfg["e"] * (cfg["layers"] - 1) / ap_s,
+                        "unit": "edges/s (input edges)", "seconds": ap_s, "kind": kind,
+                        "cores": threads},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=list(CONFIGS), default="C2")
+    ap.add_argument("--batch", type=int, default=1 << 20)
+    ap.add_argument("--replicate", type=float, default=0.0)
+    ap.add_argument("--host-frac", type=float, default=0.0)
+    ap.add_argument("--clock-window", type=float, default=1.0)
+    ap.add_argument("--cpu-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -126,7 +126,15 @@ int qvb_graph_upload(int device, uint64_t n, uint64_t e, const uint64_t* row_off
  * transposed=1 swaps source and destination (skewed in-degree variant). */
 int qvb_graph_synthetic(int device, uint64_t n, uint64_t e, uint64_t seed, int weighted,
                         int transposed, void* stream, qvb_graph** out);
+/* The same generator's out-CSR copied to host buffers in the qv::Graph
+ * layout (row_offsets[n+1], col[e], weights[e]) — the host-side input of the
+ * end-to-end compute_access_prob_ie path. */
+int qvb_synthetic_csr(int device, uint64_t n, uint64_t e, uint64_t seed, int weighted,
+                      int transposed, uint64_t* row_offsets, uint64_t* col, double* weights);
 int qvb_graph_info_get(const qvb_graph* g, qvb_graph_info* info);
+/* Device time (ms, CUDA events on the call's stream) of the P sweeps of the
+ * last qvb_access_prob on g. */
+int qvb_graph_last_sweep_ms(const qvb_graph* g, double* ms);
 int qvb_graph_destroy(qvb_graph* g);
 
 /* ---- K1: access probability P(n,j) (metrics.cpp:134-173) ---------------- */

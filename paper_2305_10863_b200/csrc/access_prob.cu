@@ -131,6 +131,9 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
   QVB_LAUNCH_CHECK();
   const uint64_t warps = (n + 31) / 32;
   const unsigned grid = static_cast<unsigned>((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  for (auto& e : g.ev)
+    if (!e) QVB_CUDA(cudaEventCreate(&e));
+  QVB_CUDA(cudaEventRecord(g.ev[0], s));
   for (uint32_t j = 2; j <= layers; ++j) {
     const int cur = (j - 2) & 1, nxt = cur ^ 1;
     double* yout = (compact && j < layers) ? g.y[nxt] : nullptr;
@@ -145,6 +148,7 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
     }
     QVB_LAUNCH_CHECK();
   }
+  QVB_CUDA(cudaEventRecord(g.ev[1], s));
   return g.p[(layers - 1) & 1];
 }
 

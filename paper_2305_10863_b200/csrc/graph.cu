@@ -40,6 +40,7 @@ qvb_graph::~qvb_graph() {
   for (int i = 0; i < 2; ++i) {
     cudaFree(p[i]);
     cudaFree(y[i]);
+    if (ev[i]) cudaEventDestroy(ev[i]);
   }
   if (prev >= 0) cudaSetDevice(prev);
 }
@@ -376,6 +377,53 @@ void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, con
 
 using namespace qvb;
 
+namespace qvb {
+namespace {
+
+// tools/bench.cpp:22-34 + Graph::from_edges/build_csr (graph.cpp:16-47) on
+// the device: out-CSR with rows in input order (stable sort by source).
+// ssrc receives the source of every CSR edge.
+void generate_out_csr(uint64_t n, uint64_t e, uint64_t seed, int weighted, int transposed,
+                      cudaStream_t s, DevBuf<uint64_t>& ro, DevBuf<uint32_t>& col,
+                      DevBuf<double>& w, DevBuf<uint32_t>& ssrc) {
+  ro.alloc(n + 1, s);
+  col.alloc(e, s);
+  ssrc.alloc(e, s);
+  if (e == 0) {
+    QVB_CUDA(cudaMemsetAsync(ro.p, 0, (n + 1) * 8, s));
+    return;
+  }
+  DevBuf<uint32_t> src(e, s), dst(e, s), iota(e, s), perm(e, s);
+  DevBuf<double> w_in;
+  if (weighted) w_in.alloc(e, s);
+  const uint64_t state = derive_state(seed, 0xBE9C4ULL);
+  k_gen_edges<<<grid_for(e, kBlock), kBlock, 0, s>>>(n, e, state, weighted, transposed, src.p,
+                                                    dst.p, w_in.p);
+  QVB_LAUNCH_CHECK();
+  k_iota<<<grid_for(e, kBlock), kBlock, 0, s>>>(iota.p, e);
+  QVB_LAUNCH_CHECK();
+  sort_pairs_u32_u32(src.p, ssrc.p, iota.p, perm.p, e, 0, bits_for(n - 1), s);
+  k_gather_by<uint32_t><<<grid_for(e, kBlock), kBlock, 0, s>>>(dst.p, perm.p, e, col.p);
+  QVB_LAUNCH_CHECK();
+  if (weighted) {
+    w.alloc(e, s);
+    k_gather_by<double><<<grid_for(e, kBlock), kBlock, 0, s>>>(w_in.p, perm.p, e, w.p);
+    QVB_LAUNCH_CHECK();
+  }
+  k_offsets_from_sorted<<<grid_for(e, kBlock), kBlock, 0, s>>>(ssrc.p, e, n, ro.p);
+  QVB_LAUNCH_CHECK();
+}
+
+__global__ void k_u32_to_u64(const uint32_t* __restrict__ in, uint64_t* __restrict__ out,
+                             uint64_t count) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+}  // namespace
+}  // namespace qvb
+
 namespace {
 
 void finish_build(qvb_graph* g, cudaEvent_t a, cudaEvent_t b, cudaStream_t s) {
@@ -494,38 +542,63 @@ extern "C" int qvb_graph_synthetic(int device, uint64_t n, uint64_t e, uint64_t 
     QVB_CUDA(cudaEventCreate(&ea));
     QVB_CUDA(cudaEventCreate(&eb));
     QVB_CUDA(cudaEventRecord(ea, s));
-    DevBuf<uint64_t> ro(n + 1, s);
-    DevBuf<uint32_t> col(e, s), ssrc(e, s);
+    DevBuf<uint64_t> ro;
+    DevBuf<uint32_t> col, ssrc;
     DevBuf<double> w;
-    if (e) {
-      DevBuf<uint32_t> src(e, s), dst(e, s), iota(e, s), perm(e, s);
-      DevBuf<double> w_in;
-      if (weighted) w_in.alloc(e, s);
-      const uint64_t state = derive_state(seed, 0xBE9C4ULL);
-      k_gen_edges<<<grid_for(e, kBlock), kBlock, 0, s>>>(n, e, state, weighted, transposed, src.p,
-                                                        dst.p, w_in.p);
-      QVB_LAUNCH_CHECK();
-      // Graph::from_edges / build_csr (graph.cpp:16-47): stable by source.
-      k_iota<<<grid_for(e, kBlock), kBlock, 0, s>>>(iota.p, e);
-      QVB_LAUNCH_CHECK();
-      sort_pairs_u32_u32(src.p, ssrc.p, iota.p, perm.p, e, 0, bits_for(n - 1), s);
-      k_gather_by<uint32_t><<<grid_for(e, kBlock), kBlock, 0, s>>>(dst.p, perm.p, e, col.p);
-      QVB_LAUNCH_CHECK();
-      if (weighted) {
-        w.alloc(e, s);
-        k_gather_by<double><<<grid_for(e, kBlock), kBlock, 0, s>>>(w_in.p, perm.p, e, w.p);
-        QVB_LAUNCH_CHECK();
-      }
-      k_offsets_from_sorted<<<grid_for(e, kBlock), kBlock, 0, s>>>(ssrc.p, e, n, ro.p);
-      QVB_LAUNCH_CHECK();
-    } else {
-      QVB_CUDA(cudaMemsetAsync(ro.p, 0, (n + 1) * 8, s));
-    }
+    generate_out_csr(n, e, seed, weighted, transposed, s, ro, col, w, ssrc);
     build_in_csr(*g, ro.p, col.p, w.p, ssrc.p, s);
     finish_build(g.get(), ea, eb, s);
     cudaEventDestroy(ea);
     cudaEventDestroy(eb);
     *out = g.release();
+  });
+}
+
+extern "C" int qvb_synthetic_csr(int device, uint64_t n, uint64_t e, uint64_t seed, int weighted,
+                                 int transposed, uint64_t* row_offsets, uint64_t* col,
+                                 double* weights) {
+  return guarded([&] {
+    if (n == 0) fail(QVB_ERR_VALIDATION, "empty graph: node count is zero");
+    if (n > kMaxNodes || e > kMaxEdges)
+      fail(QVB_ERR_UNSUPPORTED, "graph exceeds the device path limits (n < 2^31, e < 2^32)");
+    if (!row_offsets || (e && (!col || !weights))) fail(QVB_ERR_VALIDATION, "null argument");
+    DeviceGuard dg(device);
+    cudaStream_t s = nullptr;
+    DevBuf<uint64_t> ro;
+    DevBuf<uint32_t> c, ssrc;
+    DevBuf<double> w;
+    generate_out_csr(n, e, seed, weighted, transposed, s, ro, c, w, ssrc);
+    ssrc.release();
+    QVB_CUDA(cudaMemcpyAsync(row_offsets, ro.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+    if (e) {
+      const uint64_t chunk = 1ull << 26;
+      DevBuf<uint64_t> wide(std::min(chunk, e), s);
+      for (uint64_t b = 0; b < e; b += chunk) {
+        const uint64_t m = std::min(chunk, e - b);
+        k_u32_to_u64<<<grid_for(m, kBlock), kBlock, 0, s>>>(c.p + b, wide.p, m);
+        QVB_LAUNCH_CHECK();
+        QVB_CUDA(cudaMemcpyAsync(col + b, wide.p, m * 8, cudaMemcpyDeviceToHost, s));
+      }
+      if (weighted) {
+        QVB_CUDA(cudaMemcpyAsync(weights, w.p, e * 8, cudaMemcpyDeviceToHost, s));
+      } else {
+        QVB_CUDA(cudaStreamSynchronize(s));
+        std::fill(weights, weights + e, 1.0);
+      }
+    }
+    QVB_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+extern "C" int qvb_graph_last_sweep_ms(const qvb_graph* g, double* ms) {
+  return guarded([&] {
+    if (!g || !ms) fail(QVB_ERR_VALIDATION, "null argument");
+    if (!g->ev[0]) fail(QVB_ERR_VALIDATION, "no sweep has run on this graph");
+    DeviceGuard dg(g->device);
+    QVB_CUDA(cudaEventSynchronize(g->ev[1]));
+    float f = 0;
+    QVB_CUDA(cudaEventElapsedTime(&f, g->ev[0], g->ev[1]));
+    *ms = f;
   });
 }
 

@@ -32,6 +32,7 @@ struct qvb_graph {
   double* y[2] = {nullptr, nullptr};
   uint64_t bytes = 0;
   double build_ms = 0.0;
+  cudaEvent_t ev[2] = {nullptr, nullptr};  // bracket the sweeps of the last run
   ~qvb_graph();
 };
 

@@ -131,6 +131,8 @@ _SIGNATURES = {
     "qvb_graph_upload": (i32, [i32, u64, u64, vp, vp, vp, vp, P(vp)]),
     "qvb_graph_synthetic": (i32, [i32, u64, u64, u64, i32, i32, vp, P(vp)]),
     "qvb_graph_info_get": (i32, [vp, P(GraphInfo)]),
+    "qvb_synthetic_csr": (i32, [i32, u64, u64, u64, i32, i32, vp, vp, vp]),
+    "qvb_graph_last_sweep_ms": (i32, [vp, P(C.c_double)]),
     "qvb_graph_destroy": (i32, [vp]),
     "qvb_access_prob": (i32, [vp, u32, vp, i32, vp]),
     "qvb_compute_access_prob_ie": (i32, [i32, u64, u64, vp, vp, vp, u32, vp, vp]),
@@ -260,6 +262,12 @@ class DeviceGraph:
         _check(_lib().qvb_access_prob(self._h, layers, _ptr(out), on_dev, _stream_ptr(stream)))
         return out
 
+    def last_sweep_ms(self) -> float:
+        """Device time of the P sweeps of the last access_prob call."""
+        ms = C.c_double(0)
+        _check(_lib().qvb_graph_last_sweep_ms(self._h, C.byref(ms)))
+        return ms.value
+
     def close(self):
         if self._h:
             _lib().qvb_graph_destroy(self._h)
@@ -276,6 +284,18 @@ class DeviceGraph:
 
     def __exit__(self, *a):
         self.close()
+
+
+def synthetic_csr(n: int, e: int, seed: int = 7, weighted: bool = False,
+                  transposed: bool = False, device: int = 0):
+    """tools/bench.cpp:22-34 generator run on the device, returned as a host
+    out-CSR (row_offsets u64[n+1], col u64[e], weights f64[e])."""
+    ro = np.zeros(n + 1, np.uint64)
+    col = np.zeros(max(e, 1), np.uint64)
+    w = np.zeros(max(e, 1), np.float64)
+    _check(_lib().qvb_synthetic_csr(device, n, e, seed, int(weighted), int(transposed), _ptr(ro),
+                                    _ptr(col), _ptr(w)))
+    return ro, col[:e], w[:e]
 
 
 @dataclass
