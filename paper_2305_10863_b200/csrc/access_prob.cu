@@ -1,120 +1,158 @@
 // access_prob.cu — K1: the analytical access-probability estimator P(n,j)
 // (reference metrics.cpp:134-173, compute_access_prob_ie), as a per-layer
-// CSR pull over the device in-CSR of graph.cu.
+// pull over the sliced device in-CSR of graph.cuh.
 //
 // Exactness. The reference multiplies a node's factors (1 - P(s,j-1)*R(s,n))
 // strictly left to right in ascending source order, and its cancellation-
 // prone 1 - prod makes any re-association visible at 1e-9. So a
 // node's product is ONE sequential chain of __dmul_rn in the reference order;
 // every op is an explicit round-to-nearest intrinsic (no FMA contraction).
-// Parallelism is across nodes and across the gathers of a chunk:
 //
-//   warp  = 32 consecutive destination nodes (lane l owns node 32w+l)
-//   chunk = up to 256 consecutive in-edges of those nodes
-//   phase A: the 32 lanes load the chunk's col (coalesced) and gather the
-//            source operands (8 independent 8-byte gathers per lane in
-//            flight), form the factors and stage them in shared memory
-//   phase B: every lane multiplies the factors of its own node's slice of
-//            the chunk into its running product, in order; the product
-//            carries across chunks, so hub rows of any length work.
+// Regular rows: one warp per slice of 32 destination nodes, lane l owns node
+// perm[32s+l]; step k reads the 32 lanes' k-th sources as one coalesced
+// 128-byte line (evict-first: streamed once per sweep), gathers the 32
+// operands (8 steps in flight per lane) and each lane multiplies its own
+// factor into its own chain — no shared memory, no cross-lane traffic.
+// Padding slots point at operand N == 0, i.e. factor 1.0, an exact identity.
 //
 // Compact layout: the gathered operand is y[s] = P(s,j-1) * (1/row_sum(s)),
 // produced by the previous sweep's epilogue, which equals the reference's
 // P(s,j-1) * (w/row_sum(s)) bit for bit whenever w/row_sum == 1/row_sum (the
 // exception table covers every other edge). One 8-byte gather per edge.
 // Weighted layout: factor = 1 - P(s,j-1) * R_e with R_e streamed per edge.
+//
+// Long rows (in-degree above the slicing threshold): one warp per row
+// gathers 32 factors per step in parallel and lane 0 multiplies them in
+// order (shuffled to it), so the sequential chain is the only serial part.
+// Their blocks come first in the grid so these chains start immediately.
+#include <cstdlib>
+
 #include "graph.cuh"
 
 namespace qvb {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
-constexpr int kChunk = 256;
-constexpr int kPerLane = kChunk / 32;
+constexpr int kU = 8;  // sliced steps in flight per lane
+constexpr int kLongU = 4;
 constexpr unsigned kFull = 0xffffffffu;
 
 __global__ void k_init(uint64_t n, const double* __restrict__ inv, double* __restrict__ p,
                        double* __restrict__ y) {
   const double base = __ddiv_rn(1.0, static_cast<double>(n));  // metrics.cpp:143
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    p[i] = base;
-    if (y) y[i] = __dmul_rn(base, inv[i]);
+    const bool real = i < n;
+    p[i] = real ? base : 0.0;  // slot N: the padding operand
+    if (y) y[i] = real ? __dmul_rn(base, inv[i]) : 0.0;
   }
 }
 
 template <bool kWeighted>
+__device__ __forceinline__ double factor(uint32_t c, double v, double r,
+                                         const uint32_t* __restrict__ exc_src,
+                                         const double* __restrict__ exc_R,
+                                         const double* __restrict__ prev) {
+  if constexpr (kWeighted) {
+    return __dsub_rn(1.0, __dmul_rn(v, r));  // metrics.cpp:166
+  } else {
+    if (c & kExcFlag) {
+      const uint32_t x = c & ~kExcFlag;
+      return __dsub_rn(1.0, __dmul_rn(prev[exc_src[x]], exc_R[x]));
+    }
+    return __dsub_rn(1.0, v);
+  }
+}
+
+template <bool kWeighted>
+__device__ __forceinline__ void finish(uint32_t v, double miss, const double* __restrict__ prev,
+                                       const double* __restrict__ inv, double* __restrict__ out,
+                                       double* __restrict__ yout, uint64_t pol) {
+  const double p = prev[v];
+  // metrics.cpp:169: prev + (1 - prev) * (1 - miss_all)
+  const double P = __dadd_rn(p, __dmul_rn(__dsub_rn(1.0, p), __dsub_rn(1.0, miss)));
+  st_stream(out + v, P, pol);
+  if (yout) st_stream(yout + v, __dmul_rn(P, inv[v]), pol);
+}
+
+template <bool kWeighted>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    k_sweep(uint32_t n, const uint64_t* __restrict__ uptr, const uint32_t* __restrict__ col,
-            const double* __restrict__ R, const uint32_t* __restrict__ exc_src,
-            const double* __restrict__ exc_R, const double* __restrict__ prev,
-            const double* __restrict__ yprev, const double* __restrict__ inv,
-            double* __restrict__ out, double* __restrict__ yout) {
-  __shared__ double fbuf[kWarpsPerBlock][kChunk];
+    k_sweep(uint64_t nslices, uint64_t long_blocks, uint64_t nlong,
+            const uint32_t* __restrict__ perm, const uint64_t* __restrict__ sptr,
+            const uint32_t* __restrict__ scol, const double* __restrict__ sR,
+            const uint32_t* __restrict__ lnode, const uint64_t* __restrict__ lptr,
+            const uint32_t* __restrict__ lcol, const double* __restrict__ lR,
+            const uint32_t* __restrict__ exc_src, const double* __restrict__ exc_R,
+            const double* __restrict__ prev, const double* __restrict__ yprev,
+            const double* __restrict__ inv, double* __restrict__ out, double* __restrict__ yout,
+            int gmode) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const uint64_t node0 = ((uint64_t)blockIdx.x * kWarpsPerBlock + wib) * 32;
-  if (node0 >= n) return;
-  const uint64_t node = node0 + lane;
-  const bool valid = node < n;
-  const uint64_t last = node0 + 32 < n ? node0 + 32 : n;  // one past the warp's last node
-  const uint64_t rs = uptr[valid ? node : last];
-  const uint64_t end_all = uptr[last];
-  uint64_t re = __shfl_down_sync(kFull, rs, 1);
-  if (lane == 31) re = end_all;
-  const uint64_t ebeg = __shfl_sync(kFull, rs, 0);
-  double* fb = fbuf[wib];
+  const uint64_t pol = policy_evict_first();
+  // kWeighted gathers P(s, j-1); compact gathers y(s, j-1)
+  const double* __restrict__ opnd = kWeighted ? prev : yprev;
 
-  double miss = 1.0;  // metrics.cpp:152
-  for (uint64_t cs = ebeg; cs < end_all; cs += kChunk) {
-    const uint32_t cnt = static_cast<uint32_t>(end_all - cs < kChunk ? end_all - cs : kChunk);
-    uint32_t c[kPerLane];
-    double a[kPerLane];
-    double v[kPerLane];
+  if (blockIdx.x < long_blocks) {  // ---- long rows: one warp per row
+    const uint64_t i = (uint64_t)blockIdx.x * kWarpsPerBlock + wib;
+    if (i >= nlong) return;
+    const uint64_t a = lptr[i], b = lptr[i + 1];
+    double miss = 1.0;
+    for (uint64_t cs = a; cs < b; cs += 32 * kLongU) {
+      double f[kLongU];
 #pragma unroll
-    for (int j = 0; j < kPerLane; ++j) {
-      const uint32_t idx = j * 32 + lane;
-      c[j] = idx < cnt ? col[cs + idx] : 0u;
-      if constexpr (kWeighted) a[j] = idx < cnt ? R[cs + idx] : 0.0;
-    }
-#pragma unroll
-    for (int j = 0; j < kPerLane; ++j) {
-      const uint32_t idx = j * 32 + lane;
-      if constexpr (kWeighted) {
-        v[j] = idx < cnt ? prev[c[j]] : 0.0;
-      } else {
-        v[j] = (idx < cnt && !(c[j] & kExcFlag)) ? yprev[c[j]] : 0.0;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kPerLane; ++j) {
-      const uint32_t idx = j * 32 + lane;
-      if (idx < cnt) {
-        double f;
-        if constexpr (kWeighted) {
-          f = __dsub_rn(1.0, __dmul_rn(v[j], a[j]));  // metrics.cpp:166
-        } else if (c[j] & kExcFlag) {
-          const uint32_t x = c[j] & ~kExcFlag;
-          f = __dsub_rn(1.0, __dmul_rn(prev[exc_src[x]], exc_R[x]));
-        } else {
-          f = __dsub_rn(1.0, v[j]);
+      for (int u = 0; u < kLongU; ++u) {
+        const uint64_t e = cs + u * 32 + lane;
+        f[u] = 1.0;
+        if (e < b) {
+          const uint32_t c = ld_stream(lcol + e, pol);
+          const double r = kWeighted ? ld_stream(lR + e, pol) : 0.0;
+          const double v = (!kWeighted && (c & kExcFlag)) ? 0.0 : ld_gather(opnd + c, gmode);
+          f[u] = factor<kWeighted>(c, v, r, exc_src, exc_R, prev);
         }
-        fb[idx] = f;
+      }
+#pragma unroll
+      for (int u = 0; u < kLongU; ++u) {
+        const uint64_t base = cs + u * 32;
+        const int cnt = b > base ? static_cast<int>(b - base < 32 ? b - base : 32) : 0;
+        for (int j = 0; j < cnt; ++j) {
+          const double x = __shfl_sync(kFull, f[u], j);
+          miss = __dmul_rn(miss, x);  // every lane runs the same chain; lane 0 writes
+        }
       }
     }
-    __syncwarp();
-    const uint64_t lo = rs > cs ? rs : cs;
-    const uint64_t hi = re < cs + cnt ? re : cs + cnt;
-    for (uint64_t e = lo; e < hi; ++e) miss = __dmul_rn(miss, fb[e - cs]);
-    __syncwarp();
+    if (lane == 0) finish<kWeighted>(lnode[i], miss, prev, inv, out, yout, pol);
+    return;
   }
-  if (valid) {
-    const double p = prev[node];
-    // metrics.cpp:169: prev + (1 - prev) * (1 - miss_all)
-    const double P = __dadd_rn(p, __dmul_rn(__dsub_rn(1.0, p), __dsub_rn(1.0, miss)));
-    out[node] = P;
-    if (yout) yout[node] = __dmul_rn(P, inv[node]);
+
+  // ---- sliced rows: one warp per slice of 32 nodes
+  const uint64_t s = ((uint64_t)blockIdx.x - long_blocks) * kWarpsPerBlock + wib;
+  if (s >= nslices) return;
+  const uint32_t v = perm[s * 32 + lane];
+  const uint64_t base = sptr[s];
+  const uint32_t len = static_cast<uint32_t>((sptr[s + 1] - base) >> 5);
+  const uint32_t* __restrict__ cp = scol + base + lane;
+  const double* __restrict__ rp = kWeighted ? sR + base + lane : nullptr;
+  double miss = 1.0;  // metrics.cpp:152
+  for (uint32_t k = 0; k < len; k += kU) {
+    uint32_t c[kU];
+    double r[kU], x[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const bool in = k + u < len;
+      c[u] = in ? ld_stream(cp + (uint64_t)(k + u) * 32, pol) : 0u;
+      if constexpr (kWeighted) r[u] = in ? ld_stream(rp + (uint64_t)(k + u) * 32, pol) : 0.0;
+      else r[u] = 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const bool in = k + u < len;
+      x[u] = (in && (kWeighted || !(c[u] & kExcFlag))) ? ld_gather(opnd + c[u], gmode) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (k + u < len) miss = __dmul_rn(miss, factor<kWeighted>(c[u], x[u], r[u], exc_src, exc_R, prev));
   }
+  if (v != kNoNode) finish<kWeighted>(v, miss, prev, inv, out, yout, pol);
 }
 
 }  // namespace
@@ -122,29 +160,40 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
   if (layers < 1) fail(QVB_ERR_VALIDATION, "access probability needs layers >= 1");
   const uint64_t n = g.n;
-  for (int i = 0; i < 2; ++i) {
-    if (!g.p[i]) QVB_CUDA(cudaMalloc(&g.p[i], n * sizeof(double)));
-    if (g.layout == 0 && !g.y[i]) QVB_CUDA(cudaMalloc(&g.y[i], n * sizeof(double)));
-  }
   const bool compact = g.layout == 0;
-  k_init<<<grid_for(n, 256), 256, 0, s>>>(n, g.inv, g.p[0], (compact && layers >= 2) ? g.y[0] : nullptr);
+  for (int i = 0; i < 2; ++i) {
+    if (!g.p[i]) QVB_CUDA(cudaMalloc(&g.p[i], (n + 1) * sizeof(double)));
+    if (compact && !g.y[i]) QVB_CUDA(cudaMalloc(&g.y[i], (n + 1) * sizeof(double)));
+  }
+  // both ping-pong buffers carry the zero padding operand at index N
+  k_init<<<grid_for(n + 1, 256), 256, 0, s>>>(n, g.inv, g.p[0], (compact && layers >= 2) ? g.y[0] : nullptr);
   QVB_LAUNCH_CHECK();
-  const uint64_t warps = (n + 31) / 32;
-  const unsigned grid = static_cast<unsigned>((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  if (layers >= 3) {
+    QVB_CUDA(cudaMemsetAsync(g.p[1] + n, 0, sizeof(double), s));
+    if (compact) QVB_CUDA(cudaMemsetAsync(g.y[1] + n, 0, sizeof(double), s));
+  }
+  const uint64_t long_blocks = (g.nlong + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const uint64_t slice_blocks = (g.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const unsigned grid = static_cast<unsigned>(long_blocks + slice_blocks);
   for (auto& e : g.ev)
     if (!e) QVB_CUDA(cudaEventCreate(&e));
+  int gmode = 0;
+  if (const char* m = std::getenv("QVB_GATHER_MODE")) gmode = std::atoi(m);
+  if (const char* f = std::getenv("QVB_L2_FETCH")) {  // experiment knob
+    QVB_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, std::strtoul(f, nullptr, 10)));
+  }
   QVB_CUDA(cudaEventRecord(g.ev[0], s));
   for (uint32_t j = 2; j <= layers; ++j) {
     const int cur = (j - 2) & 1, nxt = cur ^ 1;
     double* yout = (compact && j < layers) ? g.y[nxt] : nullptr;
     if (compact) {
       k_sweep<false><<<grid, kWarpsPerBlock * 32, 0, s>>>(
-          static_cast<uint32_t>(n), g.uptr, g.col, nullptr, g.exc_src, g.exc_R, g.p[cur],
-          g.y[cur], g.inv, g.p[nxt], yout);
+          g.nslices, long_blocks, g.nlong, g.perm, g.sptr, g.scol, nullptr, g.lnode, g.lptr,
+          g.lcol, nullptr, g.exc_src, g.exc_R, g.p[cur], g.y[cur], g.inv, g.p[nxt], yout, gmode);
     } else {
       k_sweep<true><<<grid, kWarpsPerBlock * 32, 0, s>>>(
-          static_cast<uint32_t>(n), g.uptr, g.col, g.R, nullptr, nullptr, g.p[cur], nullptr,
-          g.inv, g.p[nxt], nullptr);
+          g.nslices, long_blocks, g.nlong, g.perm, g.sptr, g.scol, g.sR, g.lnode, g.lptr, g.lcol,
+          g.lR, nullptr, nullptr, g.p[cur], nullptr, g.inv, g.p[nxt], nullptr, gmode);
     }
     QVB_LAUNCH_CHECK();
   }

@@ -120,11 +120,86 @@ struct DevBuf {
   size_t bytes() const { return n * sizeof(T); }
 };
 
+// Persistent grid: as many blocks as fit on all SMs at once (one wave),
+// capped by the work available.
+template <typename Kernel>
+inline unsigned resident_grid(Kernel k, int block, size_t smem, uint64_t work_blocks) {
+  int dev = 0, sms = 0, per_sm = 0;
+  QVB_CUDA(cudaGetDevice(&dev));
+  QVB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  QVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, block, smem));
+  uint64_t g = static_cast<uint64_t>(sms) * (per_sm > 0 ? per_sm : 1);
+  if (work_blocks < g) g = work_blocks;
+  return static_cast<unsigned>(g ? g : 1);
+}
+
 inline unsigned grid_for(uint64_t items, unsigned block, unsigned cap = 148u * 64u) {
   uint64_t g = (items + block - 1) / block;
   if (g == 0) g = 1;
   if (g > cap) g = cap;
   return static_cast<unsigned>(g);
+}
+
+// ---- L2 cache-policy loads/stores ------------------------------------------
+// Streams that are touched once per pass (CSR columns, per-node vectors) are
+// marked evict_first so they do not push the gathered vector out of L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* a, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_stream(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_stream(const uint64_t* a, uint64_t pol) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;"
+               : "=l"(v)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_hint(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+// Gather of one operand: mode 0 = ld.global.nc (read-only path, L1 allocate),
+// 1 = ld.global.nc.L1::no_allocate, 2 = ld.global.cg (L2 only), 3 = .L2::evict_last.
+__device__ __forceinline__ double ld_gather(const double* a, int mode) {
+  double v;
+  if (mode == 1) {
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(a));
+  } else if (mode == 2) {
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(a));
+  } else if (mode == 3) {
+    asm volatile(
+        "{\n .reg .b64 p;\n createpolicy.fractional.L2::evict_last.b64 p, 1.0;\n"
+        " ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], p;\n}"
+        : "=d"(v)
+        : "l"(a));
+  } else {
+    v = __ldg(a);
+  }
+  return v;
+}
+__device__ __forceinline__ void st_stream(double* a, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
 }
 
 // ---- SplitMix64 (rng.hpp:10-57) ------------------------------------------

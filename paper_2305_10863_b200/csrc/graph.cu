@@ -31,9 +31,14 @@ qvb_graph::~qvb_graph() {
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   cudaDeviceSynchronize();
-  cudaFree(uptr);
-  cudaFree(col);
-  cudaFree(R);
+  cudaFree(perm);
+  cudaFree(sptr);
+  cudaFree(scol);
+  cudaFree(sR);
+  cudaFree(lnode);
+  cudaFree(lptr);
+  cudaFree(lcol);
+  cudaFree(lR);
   cudaFree(exc_src);
   cudaFree(exc_R);
   cudaFree(inv);
@@ -219,6 +224,106 @@ __global__ void k_compact(const uint32_t* __restrict__ ucol, const double* __res
   }
 }
 
+// ---- slicing (see graph.cuh) ------------------------------------------------
+__device__ __forceinline__ uint32_t eff_degree(const uint64_t* uptr, uint32_t v, uint32_t thr) {
+  const uint64_t d = uptr[v + 1] - uptr[v];
+  return d > thr ? 0u : static_cast<uint32_t>(d);
+}
+
+__global__ void k_window_keys(const uint64_t* __restrict__ uptr, uint64_t n, uint32_t thr,
+                              uint64_t* __restrict__ keys, uint32_t* __restrict__ ids) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t d = eff_degree(uptr, static_cast<uint32_t>(v), thr);
+    keys[v] = ((v / kWindow) << 32) | (0xFFFFFFFFull - d);  // window asc, degree desc
+    ids[v] = static_cast<uint32_t>(v);
+  }
+}
+
+// Slot -> node (kNoNode for padding slots and long rows) and 32*len per slice.
+__global__ void k_slice_lens(const uint32_t* __restrict__ sorted, const uint64_t* __restrict__ uptr,
+                             uint64_t n, uint32_t thr, uint64_t nslices,
+                             uint32_t* __restrict__ perm, uint32_t* __restrict__ len32) {
+  const uint64_t slots = nslices * 32;
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < slots;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t v = kNoNode, d = 0;
+    if (p < n) {
+      v = sorted[p];
+      const uint64_t deg = uptr[v + 1] - uptr[v];
+      if (deg > thr) v = kNoNode;  // long row: served by the long path
+      else d = static_cast<uint32_t>(deg);
+    }
+    perm[p] = v;
+    if ((p & 31) == 0) len32[p >> 5] = 32u * d;  // first slot holds the slice maximum
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) len32[nslices] = 0;
+}
+
+template <bool kWithR>
+__global__ void k_fill_slices(const uint32_t* __restrict__ perm, const uint64_t* __restrict__ sptr,
+                              const uint64_t* __restrict__ uptr, const uint32_t* __restrict__ col,
+                              const double* __restrict__ R, uint64_t nslices, uint32_t pad,
+                              uint32_t* __restrict__ scol, double* __restrict__ sR) {
+  const uint64_t slots = nslices * 32;
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < slots;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = p >> 5, lane = p & 31;
+    const uint64_t base = sptr[s];
+    const uint64_t len = (sptr[s + 1] - base) >> 5;
+    const uint32_t v = perm[p];
+    uint64_t r0 = 0, deg = 0;
+    if (v != kNoNode) {
+      r0 = uptr[v];
+      deg = uptr[v + 1] - r0;
+    }
+    for (uint64_t k = 0; k < len; ++k) {
+      const uint64_t at = base + k * 32 + lane;
+      if (k < deg) {
+        scol[at] = col[r0 + k];
+        if (kWithR) sR[at] = R[r0 + k];
+      } else {
+        scol[at] = pad;
+        if (kWithR) sR[at] = 0.0;
+      }
+    }
+  }
+}
+
+__global__ void k_long_marks(const uint64_t* __restrict__ uptr, uint64_t n, uint32_t thr,
+                             uint8_t* __restrict__ mark) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x)
+    mark[v] = (uptr[v + 1] - uptr[v]) > thr ? 1 : 0;
+}
+
+__global__ void k_long_list(const uint8_t* __restrict__ mark, const uint32_t* __restrict__ lidx,
+                            const uint64_t* __restrict__ uptr, uint64_t n,
+                            uint32_t* __restrict__ lnode, uint32_t* __restrict__ ldeg) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x)
+    if (mark[v]) {
+      lnode[lidx[v]] = static_cast<uint32_t>(v);
+      ldeg[lidx[v]] = static_cast<uint32_t>(uptr[v + 1] - uptr[v]);
+    }
+}
+
+// One warp per long row: copy its CSR segment.
+__global__ void k_long_copy(const uint32_t* __restrict__ lnode, const uint64_t* __restrict__ lptr,
+                            const uint64_t* __restrict__ uptr, const uint32_t* __restrict__ col,
+                            const double* __restrict__ R, uint64_t nlong,
+                            uint32_t* __restrict__ lcol, double* __restrict__ lR) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (warp >= nlong) return;
+  const uint64_t src = uptr[lnode[warp]];
+  const uint64_t dst = lptr[warp], len = lptr[warp + 1] - dst;
+  for (uint64_t k = lane; k < len; k += 32) {
+    lcol[dst + k] = col[src + k];
+    if (R) lR[dst + k] = R[src + k];
+  }
+}
+
 // tools/bench.cpp:22-34 on the device: edge i consumes draws 3i, 3i+1, 3i+2
 // of derive_stream(seed, 0xBE9C4).
 __global__ void k_gen_edges(uint64_t n, uint64_t e, uint64_t state, int weighted, int transposed,
@@ -289,9 +394,11 @@ void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, con
     g.eu = 0;
     g.nexc = 0;
     g.layout = 0;
-    g.uptr = persist(uptr);
+    DevBuf<uint32_t> none(1, s);
+    build_slices(g, uptr.p, none.p, nullptr, s);
     g.inv = persist(inv);
-    g.bytes = (n + 1) * 8 + n * 8;
+    g.bytes += n * 8;
+    QVB_CUDA(cudaStreamSynchronize(s));
     return;
   }
 
@@ -357,20 +464,96 @@ void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, con
     k_compact<<<grid_for(eu, kBlock), kBlock, 0, s>>>(ucol.p, uR.p, uexc.p, xidx.p, eu, col.p,
                                                       xsrc.p, xR.p);
     QVB_LAUNCH_CHECK();
-    g.col = persist(col);
+    uR.release();
+    ucol.release();
+    uexc.release();
     g.exc_src = persist(xsrc);
     g.exc_R = persist(xR);
-    g.bytes = eu * 4 + (nexc ? nexc : 1) * 12;
+    g.bytes = (nexc ? nexc : 1) * 12;
+    build_slices(g, uptr.p, col.p, nullptr, s);
   } else {
     g.layout = 1;
-    g.col = persist(ucol);
-    g.R = persist(uR);
-    g.bytes = eu * 12;
+    uexc.release();
+    build_slices(g, uptr.p, ucol.p, uR.p, s);
   }
-  g.uptr = persist(uptr);
   g.inv = persist(inv);
-  g.bytes += (n + 1) * 8 + n * 8;
+  g.bytes += n * 8;
   QVB_CUDA(cudaStreamSynchronize(s));
+}
+
+void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const double* R,
+                  cudaStream_t s) {
+  const uint64_t n = g.n;
+  const uint64_t avg = g.eu ? (g.eu + n - 1) / n : 1;
+  g.long_threshold = static_cast<uint32_t>(std::max<uint64_t>(64, 4 * avg));
+  const uint32_t thr = g.long_threshold;
+  g.nslices = (n + 31) / 32;
+  const uint64_t S = g.nslices;
+
+  // windows of 256 ids sorted by in-degree (descending, stable)
+  DevBuf<uint32_t> sorted(n, s);
+  {
+    DevBuf<uint64_t> keys(n, s), skeys(n, s);
+    DevBuf<uint32_t> ids(n, s);
+    k_window_keys<<<grid_for(n, kBlock), kBlock, 0, s>>>(uptr, n, thr, keys.p, ids.p);
+    QVB_LAUNCH_CHECK();
+    sort_pairs_u64_u32(keys.p, skeys.p, ids.p, sorted.p, n, 0, 32 + bits_for((n - 1) / kWindow), s);
+  }
+  DevBuf<uint32_t> perm(S * 32, s), len32(S + 1, s);
+  DevBuf<uint64_t> sptr(S + 1, s);
+  k_slice_lens<<<grid_for(S * 32, kBlock), kBlock, 0, s>>>(sorted.p, uptr, n, thr, S, perm.p,
+                                                           len32.p);
+  QVB_LAUNCH_CHECK();
+  sorted.release();
+  exclusive_sum_u32_u64(len32.p, sptr.p, S + 1, s);
+  g.slots = read_scalar(sptr.p + S, s);
+  DevBuf<uint32_t> scol(g.slots ? g.slots : 1, s);
+  DevBuf<double> sR;
+  const uint32_t pad = static_cast<uint32_t>(n);  // operand slot N holds 0
+  if (R) {
+    sR.alloc(g.slots ? g.slots : 1, s);
+    k_fill_slices<true><<<grid_for(S * 32, kBlock), kBlock, 0, s>>>(perm.p, sptr.p, uptr, col, R,
+                                                                    S, pad, scol.p, sR.p);
+  } else {
+    k_fill_slices<false><<<grid_for(S * 32, kBlock), kBlock, 0, s>>>(perm.p, sptr.p, uptr, col,
+                                                                     nullptr, S, pad, scol.p,
+                                                                     nullptr);
+  }
+  QVB_LAUNCH_CHECK();
+
+  // long rows
+  DevBuf<uint8_t> mark(n, s);
+  DevBuf<uint32_t> lidx(n, s);
+  k_long_marks<<<grid_for(n, kBlock), kBlock, 0, s>>>(uptr, n, thr, mark.p);
+  QVB_LAUNCH_CHECK();
+  exclusive_sum_u8_u32(mark.p, lidx.p, n, s);
+  g.nlong = (uint64_t)read_scalar(lidx.p + (n - 1), s) + read_scalar(mark.p + (n - 1), s);
+  if (g.nlong) {
+    const uint64_t L = g.nlong;
+    DevBuf<uint32_t> lnode(L, s), ldeg(L + 1, s);
+    DevBuf<uint64_t> lptr(L + 1, s);
+    k_long_list<<<grid_for(n, kBlock), kBlock, 0, s>>>(mark.p, lidx.p, uptr, n, lnode.p, ldeg.p);
+    QVB_LAUNCH_CHECK();
+    QVB_CUDA(cudaMemsetAsync(ldeg.p + L, 0, sizeof(uint32_t), s));
+    exclusive_sum_u32_u64(ldeg.p, lptr.p, L + 1, s);
+    const uint64_t lsum = read_scalar(lptr.p + L, s);
+    DevBuf<uint32_t> lcol(lsum, s);
+    DevBuf<double> lR;
+    if (R) lR.alloc(lsum, s);
+    k_long_copy<<<static_cast<unsigned>((L * 32 + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+        lnode.p, lptr.p, uptr, col, R, L, lcol.p, lR.p);
+    QVB_LAUNCH_CHECK();
+    g.lnode = persist(lnode);
+    g.lptr = persist(lptr);
+    g.lcol = persist(lcol);
+    g.lR = lR.p ? persist(lR) : nullptr;
+    g.bytes += L * 12 + lsum * (R ? 12 : 4);
+  }
+  g.perm = persist(perm);
+  g.sptr = persist(sptr);
+  g.scol = persist(scol);
+  g.sR = sR.p ? persist(sR) : nullptr;
+  g.bytes += S * 32 * 4 + (S + 1) * 8 + g.slots * (R ? 12 : 4);
 }
 
 }  // namespace qvb

@@ -3,17 +3,28 @@
 // (metrics.cpp:145 -> in_adjacency, graph.cpp:260-281) plus the row sums of
 // transition_view (graph.cpp:292-318).
 //
-// HBM layout (N nodes, E_u coalesced in-edges):
-//   uptr   u64[N+1]   in-row pointers over coalesced edges, rows by destination
-//   col    u32[E_u]   source of each coalesced in-edge, ascending within a row
-//                     (the reference's factor order). Compact layout: bit 31
-//                     set => index into the exception table instead.
-//   R      f64[E_u]   weighted layout only: R = w_sum / row_sum(s)
-//   exc_*             compact layout only: (source, R) of the few edges whose
-//                     R differs bitwise from 1/row_sum(s) (parallel edges,
-//                     non-unit weights)
-//   inv    f64[N]     1/row_sum(s) (0 for sinks)
-//   p[2], y[2] f64[N] ping-pong P_{j-1}/P_j and y = P * inv (compact layout)
+// HBM layout (N nodes, E_u coalesced in-edges) — "sliced" in-CSR:
+//   windows of 256 consecutive destination ids are sorted by in-degree
+//   (descending, ties by id) and cut into slices of 32 nodes; slice s holds
+//   its nodes' in-edges lane-major: edge k of the node in lane l sits at
+//   sptr[s] + 32*k + l, padded to the slice's longest row with a sentinel
+//   source (index N, whose operand is 0, so its factor is exactly 1.0 and
+//   multiplying by it leaves the product bit-identical). A warp therefore
+//   reads one coalesced 128-byte line of sources per step and every lane
+//   owns its node's whole product chain in registers, in the reference's
+//   ascending-source order.
+//   perm   u32[S*32]   node of each slot (kNoNode: padding / long row)
+//   sptr   u64[S+1]    slice starts (elements)
+//   scol   u32[...]    sources, lane-major; compact layout: bit 31 set =>
+//                      index into the exception table instead
+//   sR     f64[...]    weighted layout only: R = w_sum / row_sum(s)
+//   long rows (in-degree > long_threshold) keep a plain CSR (lnode, lptr,
+//   lcol, lR) and are multiplied by one warp each (the chain is sequential
+//   by definition; the gathers are warp-parallel).
+//   exc_*              compact layout: (source, R) of the few edges whose R
+//                      differs bitwise from 1/row_sum(s)
+//   inv    f64[N]      1/row_sum(s) (0 for sinks)
+//   p[2], y[2] f64[N+1] ping-pong P_{j-1}/P_j and y = P * inv; entry N = 0
 #pragma once
 
 #include "common.cuh"
@@ -22,9 +33,18 @@ struct qvb_graph {
   int device = 0;
   uint64_t n = 0, e = 0, eu = 0, nexc = 0;
   uint32_t layout = 0;  // 0 compact, 1 weighted
-  uint64_t* uptr = nullptr;
-  uint32_t* col = nullptr;
-  double* R = nullptr;
+  uint64_t nslices = 0;
+  uint32_t* perm = nullptr;
+  uint64_t* sptr = nullptr;
+  uint32_t* scol = nullptr;
+  double* sR = nullptr;
+  uint64_t slots = 0;  // sptr[nslices] (padded elements)
+  uint64_t nlong = 0;
+  uint32_t long_threshold = 0;
+  uint32_t* lnode = nullptr;
+  uint64_t* lptr = nullptr;
+  uint32_t* lcol = nullptr;
+  double* lR = nullptr;
   uint32_t* exc_src = nullptr;
   double* exc_R = nullptr;
   double* inv = nullptr;
@@ -39,13 +59,19 @@ struct qvb_graph {
 namespace qvb {
 
 constexpr uint32_t kExcFlag = 0x80000000u;
-constexpr uint64_t kMaxNodes = (1ull << 31) - 1;
+constexpr uint32_t kNoNode = 0xFFFFFFFFu;
+constexpr uint32_t kWindow = 256;  // nodes sorted together (one CTA of 8 warps)
+constexpr uint64_t kMaxNodes = (1ull << 31) - 2;
 constexpr uint64_t kMaxEdges = 0xFFFFFFFFull;
 
 // Builds the in-CSR from a device out-CSR. d_w == nullptr means unit weights.
 // d_src (nullable): source of every out-CSR edge if already known.
 void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, const double* d_w,
                   const uint32_t* d_src, cudaStream_t s);
+
+// Sliced layout + long-row CSR from the coalesced in-CSR (uptr, col, R).
+void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const double* R,
+                  cudaStream_t s);
 
 // Runs layers-1 sweeps; returns the device buffer holding P_layers.
 const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s);

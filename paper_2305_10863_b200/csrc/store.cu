@@ -9,7 +9,7 @@
 //   lut    u64[n]  packed loc << 48 | offset (this reader's per-reader table)
 //   local  shard of location d: rows of the features holding a copy at d,
 //          ascending feature id (== the reference's cursor offsets),
-//          stride = dim*4 rounded up to 16 bytes
+//          stride = dim*4 rounded up to 64 bytes (16 for rows < 64 B)
 //   host   pinned + mapped shard of the host location, same layout
 //   base[] one base pointer per location (peers attached via IPC handles)
 //
@@ -79,7 +79,7 @@ struct Vec<4> {
 };
 
 constexpr int kGatherBlock = 256;
-constexpr int kUnroll = 4;
+constexpr int kUnroll = 8;
 
 // Direct gather over request order. rows < 2^32 / cpr per launch.
 template <int VEC>
@@ -255,20 +255,38 @@ struct qvb_store {
     const uint64_t max_rows = std::max<uint64_t>(1, (0xFFFFFFFFull / cpr) / 2);
     for (uint64_t r0 = 0; r0 < b; r0 += max_rows) {
       const uint32_t rows = static_cast<uint32_t>(std::min(max_rows, b - r0));
-      const uint64_t chunks = (uint64_t)rows * cpr;
-      const unsigned grid = grid_for((chunks + kUnroll - 1) / kUnroll, kGatherBlock, 148u * 8u);
       char* o = out + r0 * row_bytes;
-      if (V == 16)
-        k_gather<16><<<grid, kGatherBlock, 0, s>>>(ids + r0, rows, lut, bases, stride, cpr,
-                                                   row_bytes, n, o, r0, err);
-      else if (V == 8)
-        k_gather<8><<<grid, kGatherBlock, 0, s>>>(ids + r0, rows, lut, bases, stride, cpr,
-                                                  row_bytes, n, o, r0, err);
-      else
-        k_gather<4><<<grid, kGatherBlock, 0, s>>>(ids + r0, rows, lut, bases, stride, cpr,
-                                                  row_bytes, n, o, r0, err);
-      QVB_LAUNCH_CHECK();
+      if (V == 16) launch_direct<16>(ids + r0, rows, cpr, o, r0, s);
+      else if (V == 8) launch_direct<8>(ids + r0, rows, cpr, o, r0, s);
+      else launch_direct<4>(ids + r0, rows, cpr, o, r0, s);
     }
+  }
+
+  static uint64_t work_blocks(uint64_t chunks) {
+    const uint64_t per_block = (uint64_t)kGatherBlock * kUnroll;
+    return (chunks + per_block - 1) / per_block;
+  }
+
+  template <int V>
+  void launch_direct(const uint64_t* ids, uint32_t rows, uint32_t cpr, char* o, uint64_t r0,
+                     cudaStream_t s) {
+    static unsigned full = 0;  // resident blocks on this GPU (one wave)
+    if (!full) full = resident_grid(k_gather<V>, kGatherBlock, 0, ~0ull);
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(full, work_blocks((uint64_t)rows * cpr)));
+    k_gather<V><<<grid, kGatherBlock, 0, s>>>(ids, rows, lut, bases, stride, cpr, row_bytes, n, o,
+                                              r0, err);
+    QVB_LAUNCH_CHECK();
+  }
+
+  template <int V>
+  void launch_sorted(const uint64_t* keys, const uint32_t* order, uint32_t rows, uint32_t cpr,
+                     char* o, cudaStream_t s) {
+    static unsigned full = 0;
+    if (!full) full = resident_grid(k_gather_sorted<V>, kGatherBlock, 0, ~0ull);
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(full, work_blocks((uint64_t)rows * cpr)));
+    k_gather_sorted<V><<<grid, kGatherBlock, 0, s>>>(keys, order, rows, bases, stride, cpr,
+                                                     row_bytes, o);
+    QVB_LAUNCH_CHECK();
   }
 
   void launch_planned(const uint64_t* ids, uint64_t b, char* out, cudaStream_t s) {
@@ -284,18 +302,9 @@ struct qvb_store {
     const int loc_bits = bits_for(static_cast<uint64_t>(nloc - 1));
     sort_pairs_u64_u32(keys.p, skeys.p, idx.p, order.p, b, 0, kOffsetBits + loc_bits, s);
     const uint32_t rows = static_cast<uint32_t>(b);
-    const uint64_t chunks = (uint64_t)rows * cpr;
-    const unsigned grid = grid_for((chunks + kUnroll - 1) / kUnroll, kGatherBlock, 148u * 8u);
-    if (V == 16)
-      k_gather_sorted<16><<<grid, kGatherBlock, 0, s>>>(skeys.p, order.p, rows, bases, stride, cpr,
-                                                        row_bytes, out);
-    else if (V == 8)
-      k_gather_sorted<8><<<grid, kGatherBlock, 0, s>>>(skeys.p, order.p, rows, bases, stride, cpr,
-                                                       row_bytes, out);
-    else
-      k_gather_sorted<4><<<grid, kGatherBlock, 0, s>>>(skeys.p, order.p, rows, bases, stride, cpr,
-                                                       row_bytes, out);
-    QVB_LAUNCH_CHECK();
+    if (V == 16) launch_sorted<16>(skeys.p, order.p, rows, cpr, out, s);
+    else if (V == 8) launch_sorted<8>(skeys.p, order.p, rows, cpr, out, s);
+    else launch_sorted<4>(skeys.p, order.p, rows, cpr, out, s);
   }
 
   ~qvb_store() {
@@ -378,7 +387,10 @@ extern "C" int qvb_store_create(int device, const uint64_t* loc_offsets, const i
     st->reader = reader_device;
     st->nloc = static_cast<int>(topo->gpus_per_server + 2);
     st->row_bytes = dim * 4u;
-    st->stride = (st->row_bytes + 15u) / 16u * 16u;
+    // HBM is read in 64-byte bursts: rows of >= 64 B start on a 64-B boundary
+    // so a row costs ceil(row/64) bursts instead of one more on average.
+    const uint64_t align = st->row_bytes >= 64 ? 64 : 16;
+    st->stride = (st->row_bytes + align - 1) / align * align;
     QVB_CUDA(cudaMalloc(&st->err, sizeof(unsigned long long)));
     QVB_CUDA(cudaMemset(st->err, 0xFF, sizeof(unsigned long long)));
 
