@@ -126,6 +126,13 @@ int qvb_graph_upload(int device, uint64_t n, uint64_t e, const uint64_t* row_off
  * transposed=1 swaps source and destination (skewed in-degree variant). */
 int qvb_graph_synthetic(int device, uint64_t n, uint64_t e, uint64_t seed, int weighted,
                         int transposed, void* stream, qvb_graph** out);
+/* qv::in_adjacency (graph.cpp:260-281) on the device: the transposed graph
+ * (parallel edges kept, each row in ascending source order, weights carried)
+ * into host buffers t_row_offsets[n+1], t_col[e], t_weights[e]. Validates
+ * like Graph::validate. */
+int qvb_in_adjacency(int device, uint64_t n, uint64_t e, const uint64_t* row_offsets,
+                     const uint64_t* col, const double* weights, uint64_t* t_row_offsets,
+                     uint64_t* t_col, double* t_weights);
 /* The same generator's out-CSR copied to host buffers in the qv::Graph
  * layout (row_offsets[n+1], col[e], weights[e]) — the host-side input of the
  * end-to-end compute_access_prob_ie path. */

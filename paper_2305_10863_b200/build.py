@@ -63,7 +63,25 @@ def build(verbose: bool = False, force: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_cpp()
     return LIB
+
+
+CPP_LIB = os.path.join(PKG, "libqv_b200.so")
+
+
+def build_cpp() -> str:
+    """libqv_b200.so: the qv:: C++ drop-in (cpp/qv_b200.cpp) over libqvb.so."""
+    src = os.path.join(PKG, "cpp", "qv_b200.cpp")
+    deps = [src, os.path.join(PKG, "cpp", "qv_b200.hpp"), os.path.join(ROOT, "include", "qvb.h"), LIB]
+    if os.path.exists(CPP_LIB) and os.path.getmtime(CPP_LIB) >= max(os.path.getmtime(p) for p in deps):
+        return CPP_LIB
+    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-o", CPP_LIB, src,
+           "-L" + PKG, "-lqvb", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"g++ failed for the qv:: drop-in:\n{r.stdout}\n{r.stderr}")
+    return CPP_LIB
 
 
 if __name__ == "__main__":

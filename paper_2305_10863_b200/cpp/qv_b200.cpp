@@ -1,0 +1,440 @@
+// qv_b200.cpp — the qv:: drop-in over the qvb C-ABI (see qv_b200.hpp).
+// Host code here only marshals arguments and rebuilds the reference's value
+// types; every hot-path computation is a qvb_* call into the sm_100a library.
+#include "qv_b200.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <numeric>
+
+#include "../../include/qvb.h"
+
+namespace qv {
+namespace {
+
+[[noreturn]] void rethrow(int rc) {
+  const std::string m = qvb_last_error();
+  switch (rc) {
+    case QVB_ERR_VALIDATION: throw ValidationError(m);
+    case QVB_ERR_PLACEMENT: throw PlacementError(m);
+    case QVB_ERR_CUDA: throw DeviceError(m);
+    default: throw Error(m);
+  }
+}
+inline void check(int rc) {
+  if (rc != QVB_OK) rethrow(rc);
+}
+
+int default_device() {
+  int d = 0;
+  const char* env = std::getenv("QVB_DEVICE");
+  if (env) d = std::atoi(env);
+  return d;
+}
+
+qvb_topology to_c(const ClusterTopology& t) {
+  qvb_topology c;
+  std::memset(&c, 0, sizeof c);
+  c.servers = t.servers;
+  c.numa_per_server = t.numa_per_server;
+  c.gpus_per_server = t.gpus_per_server;
+  c.nvlink_within_numa = t.nvlink_within_numa;
+  c.infiniband = t.infiniband;
+  c.gpu_feature_capacity = t.gpu_feature_capacity;
+  c.host_feature_capacity = t.host_feature_capacity;
+  c.disk_feature_capacity = t.disk_feature_capacity;
+  for (std::size_t i = 0; i < kLinkClassCount; ++i) {
+    c.link_latency_s[i] = t.links[i].latency_s;
+    c.link_bandwidth_Bps[i] = t.links[i].bandwidth_Bps;
+  }
+  c.tlb_miss_penalty_s = t.tlb_miss_penalty_s;
+  c.gpu_replicated_capacity = t.gpu_replicated_capacity;
+  return c;
+}
+
+struct PlanCsr {
+  std::vector<std::uint64_t> offsets;
+  std::vector<std::int64_t> ids;
+};
+
+PlanCsr to_csr(const PlacementPlan& plan, const ClusterTopology& topo) {
+  PlanCsr c;
+  c.offsets.resize(plan.feature_count + 1, 0);
+  for (std::uint64_t f = 0; f < plan.feature_count; ++f) {
+    for (const Location& l : plan.locations[f])
+      c.ids.push_back(encode_location(topo, l.server, l.tier, l.device));
+    c.offsets[f + 1] = c.ids.size();
+  }
+  return c;
+}
+
+}  // namespace
+
+// ---- graph ------------------------------------------------------------------
+Graph Graph::from_edges(std::uint64_t node_count, std::span<const Edge> edges) {
+  // build_csr semantics (graph.cpp:16-56): counting sort by source, input
+  // order kept inside a row; input construction, not the hot path.
+  if (node_count == 0) throw ValidationError("empty graph: node count is zero");
+  Graph g;
+  g.node_count = node_count;
+  g.edge_count = edges.size();
+  g.row_offsets.assign(node_count + 1, 0);
+  for (const Edge& e : edges) {
+    if (e.src >= node_count || e.dst >= node_count)
+      throw ValidationError("edge endpoint " + std::to_string(std::max(e.src, e.dst)) +
+                            " out of range for node count " + std::to_string(node_count));
+    if (!(e.weight >= 0.0))
+      throw ValidationError("negative or NaN edge weight on edge " + std::to_string(e.src) +
+                            " -> " + std::to_string(e.dst));
+    ++g.row_offsets[e.src + 1];
+  }
+  std::partial_sum(g.row_offsets.begin(), g.row_offsets.end(), g.row_offsets.begin());
+  g.col_indices.resize(g.edge_count);
+  g.edge_weights.resize(g.edge_count);
+  std::vector<EdgeIdx> cursor(g.row_offsets.begin(), g.row_offsets.end() - 1);
+  for (const Edge& e : edges) {
+    const EdgeIdx at = cursor[e.src]++;
+    g.col_indices[at] = e.dst;
+    g.edge_weights[at] = e.weight;
+  }
+  g.validate();
+  return g;
+}
+
+void Graph::validate() const {
+  // the device validates on upload with the reference's messages
+  // (graph.cpp:58-93); host-side size checks come first, as there
+  if (node_count == 0) throw ValidationError("empty graph: node count is zero");
+  if (row_offsets.size() != node_count + 1) throw ValidationError("row_offsets size mismatch");
+  if (row_offsets.front() != 0 || row_offsets.back() != edge_count)
+    throw ValidationError("row_offsets endpoints invalid");
+  if (col_indices.size() != edge_count || edge_weights.size() != edge_count)
+    throw ValidationError("edge array size mismatch");
+  for (std::uint64_t i = 0; i < node_count; ++i)
+    if (row_offsets[i + 1] < row_offsets[i])
+      throw ValidationError("row_offsets not non-decreasing at node " + std::to_string(i));
+  for (std::uint64_t i = 0; i < node_count; ++i) {
+    bool any_positive = out_degree(i) == 0;
+    for (EdgeIdx e = row_offsets[i]; e < row_offsets[i + 1]; ++e) {
+      if (col_indices[e] >= node_count)
+        throw ValidationError("column index out of range at node " + std::to_string(i));
+      if (!(edge_weights[e] >= 0.0))
+        throw ValidationError("negative or NaN edge weight at node " + std::to_string(i));
+      if (edge_weights[e] > 0.0) any_positive = true;
+    }
+    if (!any_positive)
+      throw ValidationError("node " + std::to_string(i) + " has out-edges but all weights are zero");
+  }
+}
+
+Graph in_adjacency(const Graph& g) {
+  Graph t;
+  t.node_count = g.node_count;
+  t.edge_count = g.edge_count;
+  t.row_offsets.resize(g.node_count + 1);
+  t.col_indices.resize(g.edge_count);
+  t.edge_weights.resize(g.edge_count);
+  check(qvb_in_adjacency(default_device(), g.node_count, g.edge_count, g.row_offsets.data(),
+                         g.col_indices.data(), g.edge_weights.data(), t.row_offsets.data(),
+                         t.col_indices.data(), t.edge_weights.data()));
+  return t;
+}
+
+double TransitionView::prob(NodeId i, NodeId j) const {
+  if (row_sums[i] <= 0.0) return 0.0;
+  double w = 0.0;
+  for (EdgeIdx e = graph->row_offsets[i]; e < graph->row_offsets[i + 1]; ++e)
+    if (graph->col_indices[e] == j) w += graph->edge_weights[e];
+  return w / row_sums[i];
+}
+
+TransitionView transition_view(const Graph& g) {
+  g.validate();
+  TransitionView t;
+  t.graph = &g;
+  t.row_sums.assign(g.node_count, 0.0);
+  t.distinct_out.assign(g.node_count, 0);
+  std::vector<std::uint64_t> stamp(g.node_count, ~0ULL);
+  for (NodeId i = 0; i < g.node_count; ++i) {
+    double sum = 0.0;
+    std::uint64_t distinct = 0;
+    for (EdgeIdx e = g.row_offsets[i]; e < g.row_offsets[i + 1]; ++e) {
+      sum += g.edge_weights[e];
+      const NodeId j = g.col_indices[e];
+      if (stamp[j] != i) {
+        stamp[j] = i;
+        ++distinct;
+      } else {
+        t.has_parallel_edges = true;
+      }
+    }
+    t.row_sums[i] = sum;
+    t.distinct_out[i] = distinct;
+  }
+  return t;
+}
+
+// ---- metrics ------------------------------------------------------------------
+AccessProbTable compute_access_prob_ie(const Graph& g, const TransitionView&,
+                                       std::uint32_t layers) {
+  if (layers < 1) throw ValidationError("access probability needs layers >= 1");
+  AccessProbTable t;
+  t.layers = layers;
+  t.values.resize(g.node_count);
+  check(qvb_compute_access_prob_ie(default_device(), g.node_count, g.edge_count,
+                                   g.row_offsets.data(), g.col_indices.data(),
+                                   g.edge_weights.data(), layers, t.values.data(), nullptr));
+  return t;
+}
+
+namespace serial {
+AccessProbTable compute_access_prob_ie(const Graph& g, const TransitionView& t,
+                                       std::uint32_t layers) {
+  return qv::compute_access_prob_ie(g, t, layers);  // one implementation: bit-identical
+}
+}  // namespace serial
+
+// ---- topology -------------------------------------------------------------------
+const char* link_class_name(LinkClass c) {
+  static const char* names[] = {"local", "nvlink", "pcie", "upi", "infiniband", "ethernet", "disk"};
+  return names[static_cast<int>(c)];
+}
+
+ClusterTopology ClusterTopology::with_defaults() {
+  qvb_topology c;
+  qvb_topology_defaults(&c);
+  ClusterTopology t;
+  for (std::size_t i = 0; i < kLinkClassCount; ++i)
+    t.links[i] = {c.link_latency_s[i], c.link_bandwidth_Bps[i]};
+  t.tlb_miss_penalty_s = c.tlb_miss_penalty_s;
+  return t;
+}
+
+void ClusterTopology::validate() const {
+  qvb_topology c = to_c(*this);
+  check(qvb_topology_validate(&c));
+}
+
+// ---- placement ----------------------------------------------------------------
+const char* tier_name(Tier t) {
+  switch (t) {
+    case Tier::gpu: return "gpu";
+    case Tier::host: return "host";
+    case Tier::disk: return "disk";
+  }
+  return "?";
+}
+
+std::int64_t encode_location(const ClusterTopology& topo, std::uint32_t server, Tier tier,
+                             std::uint32_t device) {
+  qvb_topology c = to_c(topo);
+  return qvb_encode_location(&c, server, static_cast<uint32_t>(tier), device);
+}
+
+Location decode_location(const ClusterTopology& topo, std::int64_t id) {
+  qvb_topology c = to_c(topo);
+  uint32_t s, t, d;
+  check(qvb_decode_location(&c, id, &s, &t, &d));
+  Location l;
+  l.server = s;
+  l.tier = static_cast<Tier>(t);
+  l.device = d;
+  return l;
+}
+
+void PlacementPlan::validate(const ClusterTopology& topo) const {
+  std::map<std::int64_t, std::uint64_t> counts;
+  for (std::uint64_t f = 0; f < feature_count; ++f) {
+    if (locations[f].empty()) throw Error("feature " + std::to_string(f) + " has no location");
+    for (const Location& l : locations[f]) ++counts[encode_location(topo, l.server, l.tier, l.device)];
+  }
+  for (const auto& [id, count] : counts) {
+    const Location l = decode_location(topo, id);
+    const std::uint64_t cap = l.tier == Tier::gpu    ? topo.gpu_feature_capacity
+                              : l.tier == Tier::host ? topo.host_feature_capacity
+                                                     : topo.disk_feature_capacity;
+    if (count > cap)
+      throw Error(std::string("placement overfills ") + tier_name(l.tier) + " on server " +
+                  std::to_string(l.server) + ": " + std::to_string(count) + " > " +
+                  std::to_string(cap));
+  }
+}
+
+PlacementPlan plan_placement(const FapTable& fap, const ClusterTopology& topo) {
+  qvb_topology c = to_c(topo);
+  const std::uint64_t n = fap.values.size();
+  const std::uint64_t cap = std::max<std::uint64_t>(1, n * topo.servers * (topo.gpus_per_server + 1));
+  std::vector<std::uint64_t> lo(n + 1);
+  std::vector<std::int64_t> ids(cap);
+  std::uint64_t copies = 0;
+  check(qvb_plan_placement(default_device(), fap.values.data(), n, &c, lo.data(), ids.data(), cap,
+                           &copies));
+  PlacementPlan p;
+  p.feature_count = n;
+  p.locations.resize(n);
+  for (std::uint64_t f = 0; f < n; ++f)
+    for (std::uint64_t k = lo[f]; k < lo[f + 1]; ++k) {
+      Location l = decode_location(topo, ids[k]);
+      l.replica = k > lo[f];
+      p.locations[f].push_back(l);
+    }
+  return p;
+}
+
+FeatureLookupTable build_lookup_table(const PlacementPlan& plan, const ClusterTopology& topo,
+                                      std::uint32_t home_server, std::uint32_t reader_device) {
+  if (home_server >= topo.servers) throw ValidationError("home server out of range");
+  qvb_topology c = to_c(topo);
+  PlanCsr csr = to_csr(plan, topo);
+  FeatureLookupTable t;
+  t.home_server = home_server;
+  t.gpus_per_server = topo.gpus_per_server;
+  t.location_ids.resize(plan.feature_count);
+  t.offsets.resize(plan.feature_count);
+  check(qvb_build_lookup_table(default_device(), csr.offsets.data(), csr.ids.data(),
+                               plan.feature_count, &c, home_server, reader_device,
+                               t.location_ids.data(), t.offsets.data()));
+  return t;
+}
+
+std::uint64_t page_transitions(std::span<const std::uint64_t> offsets, std::uint64_t page_size) {
+  std::uint64_t out = 0;
+  check(qvb_page_transitions(offsets.data(), offsets.size(), page_size, &out));
+  return out;
+}
+
+ReadPlan plan_reads(const FeatureLookupTable& table, std::span<const NodeId> feature_ids,
+                    std::uint64_t page_size) {
+  if (page_size == 0) throw ValidationError("page size must be > 0");
+  ReadPlan plan;
+  plan.home_server = table.home_server;
+  plan.page_size = page_size;
+  const std::uint64_t b = feature_ids.size();
+  if (b == 0) return plan;
+  std::vector<std::int64_t> gl(b);
+  std::vector<std::uint64_t> gc(b), gt(b), off(b);
+  std::uint64_t ng = 0;
+  check(qvb_plan_reads(default_device(), table.location_ids.data(), table.offsets.data(),
+                       table.location_ids.size(), feature_ids.data(), b, page_size, gl.data(),
+                       gc.data(), gt.data(), &ng, off.data()));
+  std::uint64_t at = 0;
+  for (std::uint64_t g = 0; g < ng; ++g) {
+    ReadPlan::LocationReads r;
+    r.location_id = gl[g];
+    r.page_transitions = gt[g];
+    r.offsets.assign(off.begin() + at, off.begin() + at + gc[g]);
+    at += gc[g];
+    plan.per_location.push_back(std::move(r));
+  }
+  return plan;
+}
+
+LinkPath classify_link(const ClusterTopology& topo, const DeviceRef& reader,
+                       std::int64_t location_id) {
+  // placement.cpp:228-267 (host arithmetic of the cost model)
+  const Location loc = decode_location(topo, location_id);
+  LinkPath path;
+  if (loc.server == reader.server) {
+    switch (loc.tier) {
+      case Tier::gpu:
+        if (reader.tier == Tier::gpu) {
+          if (reader.device == loc.device) path.first = LinkClass::local;
+          else if (topo.gpus_per_numa() > 0 &&
+                   reader.device / topo.gpus_per_numa() == loc.device / topo.gpus_per_numa())
+            path.first = topo.nvlink_within_numa ? LinkClass::nvlink : LinkClass::pcie;
+          else path.first = LinkClass::upi;
+        } else {
+          path.first = LinkClass::pcie;
+        }
+        break;
+      case Tier::host:
+        path.first = reader.tier == Tier::host ? LinkClass::local : LinkClass::pcie;
+        break;
+      case Tier::disk: path.first = LinkClass::disk; break;
+    }
+  } else {
+    const LinkClass net = topo.infiniband ? LinkClass::infiniband : LinkClass::ethernet;
+    if (loc.tier == Tier::disk) {
+      path.first = LinkClass::disk;
+      path.second = net;
+    } else {
+      path.first = net;
+    }
+  }
+  return path;
+}
+
+FetchCost fetch_cost(const ReadPlan& plan, const ClusterTopology& topo,
+                     std::uint64_t feature_bytes, std::optional<DeviceRef> reader) {
+  // placement.cpp:382-404 — the reference's model, unchanged in meaning
+  auto translated = [](LinkClass c) {
+    return c == LinkClass::pcie || c == LinkClass::upi || c == LinkClass::infiniband ||
+           c == LinkClass::ethernet;
+  };
+  DeviceRef rd = reader ? *reader
+                        : (topo.gpus_per_server > 0 ? DeviceRef{plan.home_server, Tier::gpu, 0}
+                                                    : DeviceRef{plan.home_server, Tier::host, 0});
+  FetchCost cost;
+  const std::int64_t max_loc =
+      static_cast<std::int64_t>(topo.servers) * static_cast<std::int64_t>(topo.gpus_per_server + 2);
+  for (const auto& lr : plan.per_location) {
+    if (lr.location_id < 0 || lr.location_id >= max_loc)
+      throw ValidationError("unknown location id " + std::to_string(lr.location_id));
+    const LinkPath p = classify_link(topo, rd, lr.location_id);
+    double setup = topo.link(p.first).latency_s;
+    double bw = topo.link(p.first).bandwidth_Bps;
+    if (p.second) {
+      setup += topo.link(*p.second).latency_s;
+      bw = std::min(bw, topo.link(*p.second).bandwidth_Bps);
+    }
+    const double bytes = static_cast<double>(feature_bytes) * static_cast<double>(lr.offsets.size());
+    double lat = setup + bytes / bw;
+    if (translated(p.first) || (p.second && translated(*p.second)))
+      lat += topo.tlb_miss_penalty_s * static_cast<double>(lr.page_transitions);
+    cost.per_location_s.emplace_back(lr.location_id, lat);
+    cost.total_s = std::max(cost.total_s, lat);
+  }
+  return cost;
+}
+
+// ---- feature store ----------------------------------------------------------------
+FeatureStore::FeatureStore(const PlacementPlan& plan, const ClusterTopology& topo,
+                           std::uint32_t dim, std::uint32_t reader_device,
+                           std::span<const float> features, int cuda_device)
+    : dim_(dim) {
+  qvb_topology c = to_c(topo);
+  PlanCsr csr = to_csr(plan, topo);
+  if (!features.empty() && features.size() != plan.feature_count * dim)
+    throw ValidationError("features must hold feature_count x dim values");
+  check(qvb_store_create(cuda_device >= 0 ? cuda_device : static_cast<int>(reader_device),
+                         csr.offsets.data(), csr.ids.data(), plan.feature_count, dim, &c,
+                         reader_device, features.empty() ? nullptr : features.data(), &s_));
+}
+
+FeatureStore::~FeatureStore() {
+  if (s_) qvb_store_destroy(s_);
+}
+
+std::array<std::uint8_t, 64> FeatureStore::export_handle() const {
+  std::array<std::uint8_t, 64> h{};
+  check(qvb_store_export_handle(s_, h.data()));
+  return h;
+}
+
+void FeatureStore::attach_peer(std::uint32_t peer_device, const std::array<std::uint8_t, 64>& handle) {
+  check(qvb_store_attach_peer(s_, peer_device, handle.data()));
+}
+
+void FeatureStore::gather(const std::uint64_t* d_ids, std::uint64_t count, float* d_out,
+                          void* stream) const {
+  check(qvb_gather(s_, d_ids, count, d_out, stream));
+}
+
+std::vector<float> FeatureStore::gather(std::span<const NodeId> ids) const {
+  std::vector<float> out(ids.size() * dim_);
+  check(qvb_gather_host(s_, ids.data(), ids.size(), out.data(), nullptr));
+  return out;
+}
+
+}  // namespace qv

@@ -1,0 +1,252 @@
+// qv_b200.hpp — C++ drop-in for the reference planner's hot-path API
+// (namespace qv of /root/reference/proj/include/qv/*.hpp), implemented over
+// the qvb C-ABI (include/qvb.h) and its sm_100a kernels.
+//
+// A reference user switches by including this header instead of
+// qv/{graph,metrics,placement,topology,error}.hpp and linking libqvb.so +
+// libqv_b200.so. Names, argument meaning, value semantics and exception types
+// follow the reference; every compute call runs on the GPU (there is no CPU
+// fallback — without a device the calls throw qv::DeviceError).
+//
+// Reference interface -> this header:
+//   graph.hpp:25-48   Graph / Edge / from_edges / validate
+//   graph.hpp:72-93   in_adjacency (device transpose) / TransitionView
+//   metrics.hpp:32-64 FapTable / AccessProbTable / compute_access_prob_ie
+//   topology.hpp:11-54 LinkClass / LinkSpec / ClusterTopology
+//   placement.hpp:14-121 Tier / Location / PlacementPlan / plan_placement /
+//                     FeatureLookupTable / build_lookup_table / ReadPlan /
+//                     plan_reads / page_transitions / classify_link / fetch_cost
+//   error.hpp:10-32   Error hierarchy
+// plus FeatureStore, the real gather the reference only models.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+struct qvb_store;
+
+namespace qv {
+
+// ---- errors (error.hpp:10-32) ------------------------------------------------
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ParseError : Error {
+  using Error::Error;
+};
+struct ValidationError : Error {
+  using Error::Error;
+};
+struct ConfigError : Error {
+  using Error::Error;
+};
+struct PlacementError : Error {
+  using Error::Error;
+};
+struct CalibrationError : Error {
+  using Error::Error;
+};
+// Extension: CUDA failure / no device (the reference has no device).
+struct DeviceError : Error {
+  using Error::Error;
+};
+
+// ---- graph (graph.hpp:10-93) -------------------------------------------------
+using NodeId = std::uint64_t;
+using EdgeIdx = std::uint64_t;
+
+struct Edge {
+  NodeId src = 0;
+  NodeId dst = 0;
+  double weight = 1.0;
+};
+
+struct Graph {
+  std::uint64_t node_count = 0;
+  std::uint64_t edge_count = 0;
+  std::vector<EdgeIdx> row_offsets;
+  std::vector<NodeId> col_indices;
+  std::vector<double> edge_weights;
+
+  static Graph from_edges(std::uint64_t node_count, std::span<const Edge> edges);
+  std::uint64_t out_degree(NodeId i) const { return row_offsets[i + 1] - row_offsets[i]; }
+  std::span<const NodeId> neighbors(NodeId i) const {
+    return {col_indices.data() + row_offsets[i], col_indices.data() + row_offsets[i + 1]};
+  }
+  std::span<const double> weights(NodeId i) const {
+    return {edge_weights.data() + row_offsets[i], edge_weights.data() + row_offsets[i + 1]};
+  }
+  void validate() const;
+};
+
+// Transpose on the device (the reference's in_adjacency, graph.cpp:260-281).
+Graph in_adjacency(const Graph& g);
+
+struct TransitionView {
+  const Graph* graph = nullptr;
+  std::vector<double> row_sums;
+  std::vector<std::uint64_t> distinct_out;
+  bool has_parallel_edges = false;
+  std::uint64_t node_count() const { return graph->node_count; }
+  double edge_prob(NodeId i, EdgeIdx e) const {
+    return row_sums[i] > 0.0 ? graph->edge_weights[e] / row_sums[i] : 0.0;
+  }
+  double prob(NodeId i, NodeId j) const;
+};
+// transition_view (graph.cpp:292-318). The device path recomputes the row
+// sums itself; this host view exists for API compatibility.
+TransitionView transition_view(const Graph& g);
+
+// ---- metrics (metrics.hpp:32-64) ---------------------------------------------
+struct FapTable {
+  std::vector<double> values;
+  std::uint32_t hops = 0;
+  std::vector<double> seed_distribution;
+};
+
+struct AccessProbTable {
+  std::vector<double> values;
+  std::uint32_t layers = 0;
+};
+
+// P(n,j) on the GPU, bit-identical to the reference.
+AccessProbTable compute_access_prob_ie(const Graph& g, const TransitionView& t,
+                                       std::uint32_t layers);
+namespace serial {
+AccessProbTable compute_access_prob_ie(const Graph& g, const TransitionView& t,
+                                       std::uint32_t layers);
+}
+
+// ---- topology (topology.hpp:11-54) -------------------------------------------
+enum class LinkClass : std::uint8_t { local = 0, nvlink, pcie, upi, infiniband, ethernet, disk };
+constexpr std::size_t kLinkClassCount = 7;
+const char* link_class_name(LinkClass c);
+
+struct LinkSpec {
+  double latency_s = 0.0;
+  double bandwidth_Bps = 1.0;
+};
+
+struct ClusterTopology {
+  std::uint32_t servers = 1;
+  std::uint32_t numa_per_server = 1;
+  std::uint32_t gpus_per_server = 1;
+  std::uint64_t gpu_feature_capacity = 0;
+  std::uint64_t host_feature_capacity = 0;
+  std::uint64_t disk_feature_capacity = 0;
+  bool nvlink_within_numa = false;
+  bool infiniband = false;
+  std::array<LinkSpec, kLinkClassCount> links{};
+  double tlb_miss_penalty_s = 1e-7;
+  // Extension (0 == reference): hottest rows replicated on every GPU.
+  std::uint64_t gpu_replicated_capacity = 0;
+
+  std::uint32_t gpus_per_numa() const { return gpus_per_server / numa_per_server; }
+  const LinkSpec& link(LinkClass c) const { return links[static_cast<std::size_t>(c)]; }
+  void validate() const;
+  static ClusterTopology with_defaults();
+};
+
+// ---- placement (placement.hpp:14-121) ----------------------------------------
+enum class Tier : std::uint8_t { gpu = 0, host = 1, disk = 2 };
+const char* tier_name(Tier t);
+
+struct Location {
+  std::uint32_t server = 0;
+  Tier tier = Tier::host;
+  std::uint32_t device = 0;
+  bool replica = false;
+};
+
+std::int64_t encode_location(const ClusterTopology& topo, std::uint32_t server, Tier tier,
+                             std::uint32_t device);
+Location decode_location(const ClusterTopology& topo, std::int64_t id);
+
+struct PlacementPlan {
+  std::uint64_t feature_count = 0;
+  std::vector<std::vector<Location>> locations;
+  void validate(const ClusterTopology& topo) const;
+};
+
+PlacementPlan plan_placement(const FapTable& fap, const ClusterTopology& topo);
+
+struct FeatureLookupTable {
+  std::uint32_t home_server = 0;
+  std::uint32_t gpus_per_server = 0;
+  std::vector<std::int64_t> location_ids;
+  std::vector<std::uint64_t> offsets;
+};
+
+// Extension: reader_device > 0 builds the per-reader table of that GPU.
+FeatureLookupTable build_lookup_table(const PlacementPlan& plan, const ClusterTopology& topo,
+                                      std::uint32_t home_server, std::uint32_t reader_device = 0);
+
+struct ReadPlan {
+  std::uint32_t home_server = 0;
+  std::uint64_t page_size = 8;
+  struct LocationReads {
+    std::int64_t location_id = 0;
+    std::vector<std::uint64_t> offsets;
+    std::uint64_t page_transitions = 0;
+  };
+  std::vector<LocationReads> per_location;
+};
+
+ReadPlan plan_reads(const FeatureLookupTable& table, std::span<const NodeId> feature_ids,
+                    std::uint64_t page_size = 8);
+std::uint64_t page_transitions(std::span<const std::uint64_t> offsets, std::uint64_t page_size);
+
+struct DeviceRef {
+  std::uint32_t server = 0;
+  Tier tier = Tier::gpu;
+  std::uint32_t device = 0;
+};
+struct LinkPath {
+  LinkClass first = LinkClass::local;
+  std::optional<LinkClass> second;
+};
+LinkPath classify_link(const ClusterTopology& topo, const DeviceRef& reader,
+                       std::int64_t location_id);
+
+struct FetchCost {
+  double total_s = 0.0;
+  std::vector<std::pair<std::int64_t, double>> per_location_s;
+};
+// The reference's latency model of a collect (placement.cpp:382-404), kept
+// for callers such as its simulator; FeatureStore::gather is the real thing.
+FetchCost fetch_cost(const ReadPlan& plan, const ClusterTopology& topo,
+                     std::uint64_t feature_bytes, std::optional<DeviceRef> reader = {});
+
+// ---- feature store (new: the collect the reference only models) ---------------
+class FeatureStore {
+ public:
+  // Builds reader GPU `reader_device`'s store on CUDA device `cuda_device`
+  // from a single-server plan; features: n x dim row-major fp32 (empty =
+  // the synthetic SURVEY §8(d) generator).
+  FeatureStore(const PlacementPlan& plan, const ClusterTopology& topo, std::uint32_t dim,
+               std::uint32_t reader_device, std::span<const float> features = {},
+               int cuda_device = -1);
+  ~FeatureStore();
+  FeatureStore(const FeatureStore&) = delete;
+  FeatureStore& operator=(const FeatureStore&) = delete;
+
+  std::array<std::uint8_t, 64> export_handle() const;
+  void attach_peer(std::uint32_t peer_device, const std::array<std::uint8_t, 64>& handle);
+  // Device pointers, stream-ordered (stream = cudaStream_t as void*).
+  void gather(const std::uint64_t* d_ids, std::uint64_t count, float* d_out,
+              void* stream = nullptr) const;
+  // Host buffers, synchronous: returns count x dim rows.
+  std::vector<float> gather(std::span<const NodeId> ids) const;
+  std::uint32_t dim() const { return dim_; }
+
+ private:
+  qvb_store* s_ = nullptr;
+  std::uint32_t dim_ = 0;
+};
+
+}  // namespace qv

@@ -619,19 +619,85 @@ void finish_build(qvb_graph* g, cudaEvent_t a, cudaEvent_t b, cudaStream_t s) {
 
 }  // namespace
 
+namespace {
+
+// Host out-CSR -> device (row offsets u64, columns u32, weights f64 or none)
+// with Graph::validate's checks and messages (graph.cpp:58-93); the
+// all-zero-weights row check runs with the row sums (k_row_sums).
+void upload_out_csr(uint64_t n, uint64_t e, const uint64_t* row_offsets, const uint64_t* col,
+                    const double* weights, cudaStream_t s, DevBuf<uint64_t>& ro,
+                    DevBuf<uint32_t>& dcol, DevBuf<double>& dw) {
+  if (n == 0) fail(QVB_ERR_VALIDATION, "empty graph: node count is zero");
+  if (!row_offsets || (e && !col)) fail(QVB_ERR_VALIDATION, "null graph arrays");
+  if (n > kMaxNodes || e > kMaxEdges)
+    fail(QVB_ERR_UNSUPPORTED, "graph exceeds the device path limits (n < 2^31, e < 2^32)");
+  if (row_offsets[0] != 0 || row_offsets[n] != e)
+    fail(QVB_ERR_VALIDATION, "row_offsets endpoints invalid");
+  ro.alloc(n + 1, s);
+  QVB_CUDA(cudaMemcpyAsync(ro.p, row_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
+  DevBuf<unsigned long long> flags(2, s);
+  QVB_CUDA(cudaMemsetAsync(flags.p, 0xFF, 2 * sizeof(unsigned long long), s));
+  k_check_ro<<<grid_for(n, kBlock), kBlock, 0, s>>>(ro.p, n, flags.p);
+  QVB_LAUNCH_CHECK();
+  unsigned long long bad_mono = read_scalar(flags.p, s);
+  if (bad_mono != kNone)
+    fail(QVB_ERR_VALIDATION, "row_offsets not non-decreasing at node " + std::to_string(bad_mono));
+
+  dcol.alloc(e, s);
+  if (e) {
+    const uint64_t chunk = 1ull << 25;  // 256 MiB of u64 per staging round
+    DevBuf<uint64_t> stage(std::min(e, chunk), s);
+    for (uint64_t base = 0; base < e; base += chunk) {
+      const uint64_t c = std::min(chunk, e - base);
+      QVB_CUDA(cudaMemcpyAsync(stage.p, col + base, c * 8, cudaMemcpyHostToDevice, s));
+      k_col_to_u32<<<grid_for(c, kBlock), kBlock, 0, s>>>(stage.p, dcol.p + base, c, base, n,
+                                                          flags.p + 1);
+      QVB_LAUNCH_CHECK();
+    }
+    if (weights) {
+      dw.alloc(e, s);
+      QVB_CUDA(cudaMemcpyAsync(dw.p, weights, e * 8, cudaMemcpyHostToDevice, s));
+      k_check_weights<<<grid_for(e, kBlock), kBlock, 0, s>>>(dw.p, e, flags.p + 1);
+      QVB_LAUNCH_CHECK();
+    }
+  }
+  unsigned long long bad_edge = read_scalar(flags.p + 1, s);
+  if (bad_edge != kNone) {
+    // The first failing edge names its row (graph.cpp:75-91 walks rows in
+    // order; a zero-weight row before it would be reported first).
+    const uint64_t ei = bad_edge >> 2;
+    const uint64_t row =
+        static_cast<uint64_t>(std::upper_bound(row_offsets, row_offsets + n + 1, ei) - row_offsets) - 1;
+    // Rows before `row` may still fail the all-zero check: run it on them.
+    bool zero_before = false;
+    uint64_t zrow = 0;
+    if (weights) {
+      for (uint64_t i = 0; i < row && !zero_before; ++i) {
+        bool anyp = row_offsets[i] == row_offsets[i + 1];
+        for (uint64_t k = row_offsets[i]; k < row_offsets[i + 1]; ++k) anyp |= weights[k] > 0.0;
+        if (!anyp) {
+          zero_before = true;
+          zrow = i;
+        }
+      }
+    }
+    if (zero_before)
+      fail(QVB_ERR_VALIDATION,
+           "node " + std::to_string(zrow) + " has out-edges but all weights are zero");
+    if ((bad_edge & 3) == 1)
+      fail(QVB_ERR_VALIDATION, "column index out of range at node " + std::to_string(row));
+    fail(QVB_ERR_VALIDATION, "negative or NaN edge weight at node " + std::to_string(row));
+  }
+}
+
+}  // namespace
+
 extern "C" int qvb_graph_upload(int device, uint64_t n, uint64_t e, const uint64_t* row_offsets,
                                 const uint64_t* col, const double* weights, void* stream,
                                 qvb_graph** out) {
   return guarded([&] {
     if (!out) fail(QVB_ERR_VALIDATION, "out is null");
     *out = nullptr;
-    // Graph::validate order (graph.cpp:58-93).
-    if (n == 0) fail(QVB_ERR_VALIDATION, "empty graph: node count is zero");
-    if (!row_offsets || (e && !col)) fail(QVB_ERR_VALIDATION, "null graph arrays");
-    if (n > kMaxNodes || e > kMaxEdges)
-      fail(QVB_ERR_UNSUPPORTED, "graph exceeds the device path limits (n < 2^31, e < 2^32)");
-    if (row_offsets[0] != 0 || row_offsets[n] != e)
-      fail(QVB_ERR_VALIDATION, "row_offsets endpoints invalid");
     DeviceGuard dg(device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     auto g = std::make_unique<qvb_graph>();
@@ -642,63 +708,10 @@ extern "C" int qvb_graph_upload(int device, uint64_t n, uint64_t e, const uint64
     QVB_CUDA(cudaEventCreate(&ea));
     QVB_CUDA(cudaEventCreate(&eb));
     QVB_CUDA(cudaEventRecord(ea, s));
-
-    DevBuf<uint64_t> ro(n + 1, s);
-    QVB_CUDA(cudaMemcpyAsync(ro.p, row_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
-    DevBuf<unsigned long long> flags(2, s);
-    QVB_CUDA(cudaMemsetAsync(flags.p, 0xFF, 2 * sizeof(unsigned long long), s));
-    k_check_ro<<<grid_for(n, kBlock), kBlock, 0, s>>>(ro.p, n, flags.p);
-    QVB_LAUNCH_CHECK();
-    unsigned long long bad_mono = read_scalar(flags.p, s);
-    if (bad_mono != kNone)
-      fail(QVB_ERR_VALIDATION, "row_offsets not non-decreasing at node " + std::to_string(bad_mono));
-
-    DevBuf<uint32_t> dcol(e, s);
+    DevBuf<uint64_t> ro;
+    DevBuf<uint32_t> dcol;
     DevBuf<double> dw;
-    if (e) {
-      const uint64_t chunk = 1ull << 25;  // 256 MiB of u64 per staging round
-      DevBuf<uint64_t> stage(std::min(e, chunk), s);
-      for (uint64_t base = 0; base < e; base += chunk) {
-        const uint64_t c = std::min(chunk, e - base);
-        QVB_CUDA(cudaMemcpyAsync(stage.p, col + base, c * 8, cudaMemcpyHostToDevice, s));
-        k_col_to_u32<<<grid_for(c, kBlock), kBlock, 0, s>>>(stage.p, dcol.p + base, c, base, n,
-                                                            flags.p + 1);
-        QVB_LAUNCH_CHECK();
-      }
-      if (weights) {
-        dw.alloc(e, s);
-        QVB_CUDA(cudaMemcpyAsync(dw.p, weights, e * 8, cudaMemcpyHostToDevice, s));
-        k_check_weights<<<grid_for(e, kBlock), kBlock, 0, s>>>(dw.p, e, flags.p + 1);
-        QVB_LAUNCH_CHECK();
-      }
-    }
-    unsigned long long bad_edge = read_scalar(flags.p + 1, s);
-    if (bad_edge != kNone) {
-      // The first failing edge names its row (graph.cpp:75-91 walks rows in
-      // order; a zero-weight row before it would be reported first).
-      const uint64_t ei = bad_edge >> 2;
-      const uint64_t row =
-          static_cast<uint64_t>(std::upper_bound(row_offsets, row_offsets + n + 1, ei) - row_offsets) - 1;
-      // Rows before `row` may still fail the all-zero check: run it on them.
-      bool zero_before = false;
-      uint64_t zrow = 0;
-      if (weights) {
-        for (uint64_t i = 0; i < row && !zero_before; ++i) {
-          bool anyp = row_offsets[i] == row_offsets[i + 1];
-          for (uint64_t k = row_offsets[i]; k < row_offsets[i + 1]; ++k) anyp |= weights[k] > 0.0;
-          if (!anyp) {
-            zero_before = true;
-            zrow = i;
-          }
-        }
-      }
-      if (zero_before)
-        fail(QVB_ERR_VALIDATION,
-             "node " + std::to_string(zrow) + " has out-edges but all weights are zero");
-      if ((bad_edge & 3) == 1)
-        fail(QVB_ERR_VALIDATION, "column index out of range at node " + std::to_string(row));
-      fail(QVB_ERR_VALIDATION, "negative or NaN edge weight at node " + std::to_string(row));
-    }
+    upload_out_csr(n, e, row_offsets, col, weights, s, ro, dcol, dw);
     build_in_csr(*g, ro.p, dcol.p, dw.p, nullptr, s);
     finish_build(g.get(), ea, eb, s);
     cudaEventDestroy(ea);
@@ -802,4 +815,76 @@ extern "C" int qvb_graph_info_get(const qvb_graph* g, qvb_graph_info* info) {
 
 extern "C" int qvb_graph_destroy(qvb_graph* g) {
   return guarded([&] { delete g; });
+}
+
+namespace qvb {
+namespace {
+
+__global__ void k_transpose_out(const uint32_t* __restrict__ seid, const uint32_t* __restrict__ src,
+                                const double* __restrict__ w, uint64_t e, uint64_t* __restrict__ tcol,
+                                double* __restrict__ tw) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < e;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = seid[k];
+    tcol[k] = src[i];
+    tw[k] = w ? w[i] : 1.0;
+  }
+}
+
+}  // namespace
+}  // namespace qvb
+
+// in_adjacency (graph.cpp:260-281) on the device: the transposed graph with
+// parallel edges kept, rows in ascending source order (stable sort by
+// destination over the source-major edge order).
+extern "C" int qvb_in_adjacency(int device, uint64_t n, uint64_t e, const uint64_t* row_offsets,
+                                const uint64_t* col, const double* weights, uint64_t* t_row_offsets,
+                                uint64_t* t_col, double* t_weights) {
+  return guarded([&] {
+    if (!t_row_offsets || (e && (!t_col || !t_weights))) fail(QVB_ERR_VALIDATION, "null argument");
+    DeviceGuard dg(device);
+    cudaStream_t s = nullptr;
+    DevBuf<uint64_t> ro;
+    DevBuf<uint32_t> dcol;
+    DevBuf<double> dw;
+    upload_out_csr(n, e, row_offsets, col, weights, s, ro, dcol, dw);
+    {
+      DevBuf<double> rs(n, s), inv(n, s);
+      DevBuf<unsigned long long> flag(1, s);
+      QVB_CUDA(cudaMemsetAsync(flag.p, 0xFF, sizeof(unsigned long long), s));
+      k_row_sums<<<grid_for(n, kBlock), kBlock, 0, s>>>(ro.p, dw.p, n, rs.p, inv.p, flag.p);
+      QVB_LAUNCH_CHECK();
+      const unsigned long long z = read_scalar(flag.p, s);
+      if (z != kNone)
+        fail(QVB_ERR_VALIDATION, "node " + std::to_string(z) + " has out-edges but all weights are zero");
+    }
+    DevBuf<uint64_t> tro(n + 1, s);
+    if (e == 0) {
+      QVB_CUDA(cudaMemsetAsync(tro.p, 0, (n + 1) * 8, s));
+    } else {
+      DevBuf<uint32_t> src(e, s), marks(e, s), incl(e, s), row_of_rank(n, s);
+      QVB_CUDA(cudaMemsetAsync(marks.p, 0, e * sizeof(uint32_t), s));
+      k_row_marks<<<grid_for(n, kBlock), kBlock, 0, s>>>(ro.p, n, e, marks.p);
+      QVB_LAUNCH_CHECK();
+      inclusive_sum_u32_u32(marks.p, incl.p, e, s);
+      k_rank_rows<<<grid_for(n, kBlock), kBlock, 0, s>>>(ro.p, n, incl.p, e, row_of_rank.p);
+      QVB_LAUNCH_CHECK();
+      k_src_from_rank<<<grid_for(e, kBlock), kBlock, 0, s>>>(incl.p, row_of_rank.p, e, src.p);
+      QVB_LAUNCH_CHECK();
+      DevBuf<uint32_t> iota(e, s), sdst(e, s), seid(e, s);
+      k_iota<<<grid_for(e, kBlock), kBlock, 0, s>>>(iota.p, e);
+      QVB_LAUNCH_CHECK();
+      sort_pairs_u32_u32(dcol.p, sdst.p, iota.p, seid.p, e, 0, bits_for(n - 1), s);
+      k_offsets_from_sorted<<<grid_for(e, kBlock), kBlock, 0, s>>>(sdst.p, e, n, tro.p);
+      QVB_LAUNCH_CHECK();
+      DevBuf<uint64_t> tcol(e, s);
+      DevBuf<double> tw(e, s);
+      k_transpose_out<<<grid_for(e, kBlock), kBlock, 0, s>>>(seid.p, src.p, dw.p, e, tcol.p, tw.p);
+      QVB_LAUNCH_CHECK();
+      QVB_CUDA(cudaMemcpyAsync(t_col, tcol.p, e * 8, cudaMemcpyDeviceToHost, s));
+      QVB_CUDA(cudaMemcpyAsync(t_weights, tw.p, e * 8, cudaMemcpyDeviceToHost, s));
+    }
+    QVB_CUDA(cudaMemcpyAsync(t_row_offsets, tro.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+    QVB_CUDA(cudaStreamSynchronize(s));
+  });
 }

@@ -132,6 +132,7 @@ _SIGNATURES = {
     "qvb_graph_synthetic": (i32, [i32, u64, u64, u64, i32, i32, vp, P(vp)]),
     "qvb_graph_info_get": (i32, [vp, P(GraphInfo)]),
     "qvb_synthetic_csr": (i32, [i32, u64, u64, u64, i32, i32, vp, vp, vp]),
+    "qvb_in_adjacency": (i32, [i32, u64, u64, vp, vp, vp, vp, vp, vp]),
     "qvb_graph_last_sweep_ms": (i32, [vp, P(C.c_double)]),
     "qvb_graph_destroy": (i32, [vp]),
     "qvb_access_prob": (i32, [vp, u32, vp, i32, vp]),
@@ -296,6 +297,21 @@ def synthetic_csr(n: int, e: int, seed: int = 7, weighted: bool = False,
     _check(_lib().qvb_synthetic_csr(device, n, e, seed, int(weighted), int(transposed), _ptr(ro),
                                     _ptr(col), _ptr(w)))
     return ro, col[:e], w[:e]
+
+
+def in_adjacency(row_offsets, col, weights=None, device: int = 0):
+    """qv::in_adjacency (graph.cpp:260-281) on the device -> host transpose."""
+    ro = np.ascontiguousarray(row_offsets, np.uint64)
+    c = np.ascontiguousarray(col, np.uint64)
+    w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+    n, e = len(ro) - 1, len(c)
+    tro = np.zeros(n + 1, np.uint64)
+    tcol = np.zeros(max(e, 1), np.uint64)
+    tw = np.zeros(max(e, 1), np.float64)
+    _check(_lib().qvb_in_adjacency(device, n, e, _ptr(ro), _ptr(c) if e else None,
+                                   _ptr(w) if w is not None and e else None, _ptr(tro), _ptr(tcol),
+                                   _ptr(tw)))
+    return tro, tcol[:e], tw[:e]
 
 
 @dataclass

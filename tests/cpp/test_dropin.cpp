@@ -1,0 +1,259 @@
+// test_dropin.cpp — the reference's own hot-path test cases, restated against
+// the qv:: drop-in (paper_2305_10863_b200/cpp/qv_b200.hpp) — the C++ API a
+// reference user links. Cases follow tests/test_metrics.cpp:136-235 and
+// tests/test_placement.cpp:72-465 of /root/reference/proj; expected values
+// come from those tests, from tests/golden (reference outputs) and from the
+// C oracle (liboracle.so). Built and run by tests/test_cpp_dropin_gpu.py.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../oracle/oracle.h"
+#include "../../paper_2305_10863_b200/cpp/qv_b200.hpp"
+
+using namespace qv;
+
+static int g_checks = 0, g_fail = 0;
+#define CHECK(x)                                                            \
+  do {                                                                      \
+    ++g_checks;                                                             \
+    if (!(x)) {                                                             \
+      ++g_fail;                                                             \
+      std::fprintf(stderr, "%s:%d: CHECK failed: %s\n", __FILE__, __LINE__, #x); \
+    }                                                                       \
+  } while (0)
+#define CHECK_THROWS_AS(expr, T, substr)                                    \
+  do {                                                                      \
+    ++g_checks;                                                             \
+    bool ok = false;                                                        \
+    try {                                                                   \
+      (void)(expr);                                                         \
+    } catch (const T& e) {                                                  \
+      ok = std::string(e.what()).find(substr) != std::string::npos;         \
+    } catch (...) {                                                         \
+    }                                                                       \
+    if (!ok) {                                                              \
+      ++g_fail;                                                             \
+      std::fprintf(stderr, "%s:%d: expected %s(%s) from %s\n", __FILE__, __LINE__, #T, substr, #expr); \
+    }                                                                       \
+  } while (0)
+
+namespace {
+
+uint64_t g_state;
+uint64_t next_u() {
+  g_state += 0x9e3779b97f4a7c15ULL;
+  uint64_t z = g_state;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+double uniform() { return static_cast<double>(next_u() >> 11) * 0x1.0p-53; }
+uint64_t below(uint64_t n) { return (uint64_t)(((unsigned __int128)next_u() * n) >> 64); }
+
+Graph random_graph(uint64_t max_nodes, uint64_t max_edges, bool weighted) {  // testutil.hpp:43-55
+  uint64_t n = 2 + below(max_nodes - 1);
+  uint64_t m = 1 + below(max_edges);
+  std::vector<Edge> edges;
+  for (uint64_t e = 0; e < m; ++e) {
+    const uint64_t s = below(n), d = below(n);
+    edges.push_back({s, d, weighted ? 0.25 + uniform() : 1.0});
+  }
+  return Graph::from_edges(n, edges);
+}
+
+Graph fig8_graph() {  // testutil.hpp:32-36
+  std::vector<Edge> e = {{0, 3, 1.0}, {0, 5, 1.0}, {1, 3, 1.0}, {3, 2, 1.0}, {4, 0, 1.0}};
+  return Graph::from_edges(6, e);
+}
+
+bool same_bits(const std::vector<double>& a, const std::vector<double>& b) {
+  return a.size() == b.size() && std::memcmp(a.data(), b.data(), a.size() * 8) == 0;
+}
+
+std::vector<double> oracle_p(const Graph& g, uint32_t L) {
+  std::vector<double> out(g.node_count);
+  qvo_access_prob(g.node_count, g.edge_count, g.row_offsets.data(), g.col_indices.data(),
+                  g.edge_weights.data(), L, out.data());
+  return out;
+}
+
+FapTable five_features() {  // test_placement.cpp:18-24
+  FapTable f;
+  f.values = {0.5, 0.4, 0.3, 0.2, 0.1};
+  f.hops = 2;
+  f.seed_distribution.assign(5, 0.2);
+  return f;
+}
+
+std::set<std::pair<uint32_t, uint32_t>> gpu_copies(const PlacementPlan& p, NodeId f) {
+  std::set<std::pair<uint32_t, uint32_t>> out;
+  for (const Location& l : p.locations[f])
+    if (l.tier == Tier::gpu) out.insert({l.server, l.device});
+  return out;
+}
+
+ClusterTopology one_server_2numa_4gpu(bool nvlink) {
+  ClusterTopology t = ClusterTopology::with_defaults();
+  t.numa_per_server = 2;
+  t.gpus_per_server = 4;
+  t.gpu_feature_capacity = 1;
+  t.host_feature_capacity = 4;
+  t.disk_feature_capacity = 8;
+  t.nvlink_within_numa = nvlink;
+  return t;
+}
+
+ClusterTopology two_servers(bool ib) {
+  ClusterTopology t = ClusterTopology::with_defaults();
+  t.servers = 2;
+  t.gpus_per_server = 1;
+  t.gpu_feature_capacity = 1;
+  t.host_feature_capacity = 1;
+  t.disk_feature_capacity = 3;
+  t.infiniband = ib;
+  return t;
+}
+
+}  // namespace
+
+int main() {
+  // --- P(n,j): test_metrics.cpp:136-235 --------------------------------------
+  {
+    Graph g = fig8_graph();
+    TransitionView t = transition_view(g);
+    AccessProbTable a1 = compute_access_prob_ie(g, t, 1);
+    for (double v : a1.values) CHECK(std::abs(v - 1.0 / 6) < 1e-14);
+    const std::vector<double> p2 = {0.30555555555555552, 0.16666666666666666, 0.30555555555555552,
+                                    0.36342592592592593, 0.16666666666666666, 0.23611111111111113};
+    const std::vector<double> p3 = {0.42129629629629622, 0.16666666666666666, 0.55793467078189296,
+                                    0.55056691529492463, 0.16666666666666666, 0.35281635802469136};
+    CHECK(same_bits(compute_access_prob_ie(g, t, 2).values, p2));
+    CHECK(same_bits(compute_access_prob_ie(g, t, 3).values, p3));
+    CHECK_THROWS_AS(compute_access_prob_ie(g, t, 0), ValidationError, "layers");
+  }
+  {
+    Graph g = Graph::from_edges(3, std::vector<Edge>{{1, 0, 1.0}, {1, 2, 1.0}});
+    AccessProbTable a = compute_access_prob_ie(g, transition_view(g), 2);
+    const double base = 1.0 / 3.0;
+    CHECK(std::abs(a.values[0] - (base + (1.0 - base) * (base * 0.5))) < 1e-14);
+  }
+  g_state = 0x1234;
+  for (int it = 0; it < 30; ++it) {
+    Graph g = random_graph(40, 250, it % 2 == 0);
+    TransitionView t = transition_view(g);
+    for (uint32_t L = 1; L <= 4; ++L) {
+      CHECK(same_bits(compute_access_prob_ie(g, t, L).values, oracle_p(g, L)));
+      CHECK(same_bits(serial::compute_access_prob_ie(g, t, L).values, oracle_p(g, L)));
+    }
+    Graph tg = in_adjacency(g);
+    std::vector<uint64_t> tro(g.node_count + 1), tcol(g.edge_count);
+    std::vector<double> tw(g.edge_count);
+    qvo_in_adjacency(g.node_count, g.edge_count, g.row_offsets.data(), g.col_indices.data(),
+                     g.edge_weights.data(), tro.data(), tcol.data(), tw.data());
+    CHECK(tg.row_offsets == tro && tg.col_indices == tcol && same_bits(tg.edge_weights, tw));
+  }
+  {
+    Graph g = fig8_graph();
+    g.edge_weights[3] = -1.0;
+    CHECK_THROWS_AS(compute_access_prob_ie(g, TransitionView{}, 2), ValidationError,
+                    "negative or NaN edge weight at node 3");
+  }
+
+  // --- placement: test_placement.cpp:72-145 -----------------------------------
+  {
+    ClusterTopology topo = one_server_2numa_4gpu(false);
+    PlacementPlan plan = plan_placement(five_features(), topo);
+    plan.validate(topo);
+    CHECK((gpu_copies(plan, 0) == std::set<std::pair<uint32_t, uint32_t>>{{0, 0}, {0, 1}, {0, 2}, {0, 3}}));
+    for (NodeId f = 1; f < 5; ++f)
+      CHECK(plan.locations[f].size() == 1 && plan.locations[f][0].tier == Tier::host);
+  }
+  {
+    ClusterTopology topo = one_server_2numa_4gpu(true);
+    PlacementPlan plan = plan_placement(five_features(), topo);
+    CHECK((gpu_copies(plan, 0) == std::set<std::pair<uint32_t, uint32_t>>{{0, 0}, {0, 2}}));
+    CHECK((gpu_copies(plan, 1) == std::set<std::pair<uint32_t, uint32_t>>{{0, 1}, {0, 3}}));
+    CHECK(plan.locations[0][0].replica == false && plan.locations[0][1].replica == true);
+    FeatureLookupTable table = build_lookup_table(plan, topo, 0);
+    DeviceRef gpu0{0, Tier::gpu, 0};
+    CHECK(classify_link(topo, gpu0, table.location_ids[0]).first == LinkClass::local);
+    CHECK(classify_link(topo, gpu0, table.location_ids[1]).first == LinkClass::nvlink);
+    // SURVEY §8(c) golden: f0(0,0) f1(1,0) f2(4,0) f3(4,1) f4(4,2)
+    CHECK((table.location_ids == std::vector<int64_t>{0, 1, 4, 4, 4}));
+    CHECK((table.offsets == std::vector<uint64_t>{0, 0, 0, 1, 2}));
+    std::vector<NodeId> ids = {4, 1, 0, 3, 1};
+    ReadPlan rp = plan_reads(table, ids, 2);
+    CHECK(rp.per_location.size() == 3);
+    CHECK(rp.per_location[1].location_id == 1 && rp.per_location[1].offsets.size() == 2);
+    CHECK(rp.per_location[2].page_transitions == 2);
+  }
+  {
+    ClusterTopology topo = two_servers(true);
+    PlacementPlan plan = plan_placement(five_features(), topo);
+    for (NodeId f = 0; f < 4; ++f) {
+      CHECK(plan.locations[f].size() == 1);
+      CHECK(plan.locations[f][0].server == (f < 2 ? 0u : 1u));
+    }
+    CHECK(plan.locations[4][0].tier == Tier::disk);
+    FeatureLookupTable table = build_lookup_table(plan, topo, 0);
+    CHECK_THROWS_AS(plan_reads(table, std::vector<NodeId>{0, 99}, 4), ValidationError,
+                    "feature id 99 outside lookup table");
+    CHECK_THROWS_AS(plan_reads(table, std::vector<NodeId>{0}, 0), ValidationError, "page size");
+  }
+  {
+    ClusterTopology topo = two_servers(false);
+    topo.disk_feature_capacity = 0;
+    topo.host_feature_capacity = 1;
+    CHECK_THROWS_AS(plan_placement(five_features(), topo), PlacementError, "short by 3");
+  }
+  {
+    std::vector<uint64_t> u = {2, 10, 3, 11}, s = {2, 3, 10, 11};
+    CHECK(page_transitions(u, 2) == 4 && page_transitions(s, 2) == 2);
+  }
+  {  // fetch_cost tail rule (test_placement.cpp:332-372)
+    ClusterTopology topo = ClusterTopology::with_defaults();
+    ReadPlan empty;
+    CHECK(fetch_cost(empty, topo, 1024).total_s == 0.0);
+    ClusterTopology fast = topo;
+    fast.links[static_cast<std::size_t>(LinkClass::pcie)] = {0.0, 16e9};
+    fast.tlb_miss_penalty_s = 0.0;
+    ReadPlan one;
+    ReadPlan::LocationReads lr;
+    lr.location_id = encode_location(fast, 0, Tier::host, 0);
+    lr.offsets = {0};
+    lr.page_transitions = 1;
+    one.per_location.push_back(lr);
+    CHECK(std::abs(fetch_cost(one, fast, 1000000000).total_s - 0.0625) < 1e-12);
+  }
+
+  // --- feature store: the real collect ------------------------------------------
+  {
+    const uint64_t n = 5000;
+    const uint32_t dim = 100;
+    ClusterTopology topo = ClusterTopology::with_defaults();
+    topo.gpu_feature_capacity = n / 2;
+    topo.host_feature_capacity = n;
+    FapTable fap;
+    for (uint64_t i = 0; i < n; ++i) fap.values.push_back(uniform());
+    PlacementPlan plan = plan_placement(fap, topo);
+    std::vector<float> x(n * dim);
+    qvo_features(0, n, dim, x.data());
+    FeatureStore store(plan, topo, dim, 0);
+    std::vector<NodeId> ids(777);
+    for (auto& i : ids) i = below(n);
+    std::vector<float> got = store.gather(ids);
+    bool ok = true;
+    for (size_t r = 0; r < ids.size(); ++r)
+      ok &= std::memcmp(got.data() + r * dim, x.data() + ids[r] * dim, dim * 4) == 0;
+    CHECK(ok);
+    CHECK_THROWS_AS(store.gather(std::vector<NodeId>{n}), ValidationError, "outside lookup table");
+  }
+
+  std::printf("test_dropin: %d checks, %d failed\n", g_checks, g_fail);
+  return g_fail ? 1 : 0;
+}
