@@ -77,7 +77,7 @@ __device__ __forceinline__ void finish(uint32_t v, double miss, const double* __
 
 template <bool kWeighted>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    k_sweep(uint64_t nslices, uint64_t long_blocks, uint64_t nlong,
+    k_sweep(uint64_t s0, uint64_t s1, uint64_t long_blocks, uint64_t nlong, double* __restrict__ state,
             const uint32_t* __restrict__ perm, const uint64_t* __restrict__ sptr,
             const uint32_t* __restrict__ scol, const double* __restrict__ sR,
             const uint32_t* __restrict__ lnode, const uint64_t* __restrict__ lptr,
@@ -124,15 +124,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     return;
   }
 
-  // ---- sliced rows: one warp per slice of 32 nodes
-  const uint64_t s = ((uint64_t)blockIdx.x - long_blocks) * kWarpsPerBlock + wib;
-  if (s >= nslices) return;
-  const uint32_t v = perm[s * 32 + lane];
+  // ---- sliced rows: one warp per slice of 32 (node, pass) slots
+  const uint64_t s = s0 + ((uint64_t)blockIdx.x - long_blocks) * kWarpsPerBlock + wib;
+  if (s >= s1) return;
+  const uint32_t pv = perm[s * 32 + lane];
+  const uint32_t v = pv & kNodeMask;
   const uint64_t base = sptr[s];
   const uint32_t len = static_cast<uint32_t>((sptr[s + 1] - base) >> 5);
   const uint32_t* __restrict__ cp = scol + base + lane;
   const double* __restrict__ rp = kWeighted ? sR + base + lane : nullptr;
-  double miss = 1.0;  // metrics.cpp:152
+  // metrics.cpp:152 starts every product at 1.0; a later pass resumes it
+  double miss = (v == kNoNode || (pv & kFirst)) ? 1.0 : ld_stream(state + v, pol);
   for (uint32_t k = 0; k < len; k += kU) {
     uint32_t c[kU];
     double r[kU], x[kU];
@@ -152,7 +154,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     for (int u = 0; u < kU; ++u)
       if (k + u < len) miss = __dmul_rn(miss, factor<kWeighted>(c[u], x[u], r[u], exc_src, exc_R, prev));
   }
-  if (v != kNoNode) finish<kWeighted>(v, miss, prev, inv, out, yout, pol);
+  if (v == kNoNode) return;
+  if (pv & kLast) finish<kWeighted>(v, miss, prev, inv, out, yout, pol);
+  else st_stream(state + v, miss, pol);
 }
 
 }  // namespace
@@ -173,29 +177,33 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
     if (compact) QVB_CUDA(cudaMemsetAsync(g.y[1] + n, 0, sizeof(double), s));
   }
   const uint64_t long_blocks = (g.nlong + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  const uint64_t slice_blocks = (g.nslices + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  const unsigned grid = static_cast<unsigned>(long_blocks + slice_blocks);
+  const int nseg = static_cast<int>(g.seg_slice.size()) - 1;
   for (auto& e : g.ev)
     if (!e) QVB_CUDA(cudaEventCreate(&e));
   int gmode = 0;
   if (const char* m = std::getenv("QVB_GATHER_MODE")) gmode = std::atoi(m);
-  if (const char* f = std::getenv("QVB_L2_FETCH")) {  // experiment knob
-    QVB_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, std::strtoul(f, nullptr, 10)));
-  }
   QVB_CUDA(cudaEventRecord(g.ev[0], s));
   for (uint32_t j = 2; j <= layers; ++j) {
     const int cur = (j - 2) & 1, nxt = cur ^ 1;
     double* yout = (compact && j < layers) ? g.y[nxt] : nullptr;
-    if (compact) {
-      k_sweep<false><<<grid, kWarpsPerBlock * 32, 0, s>>>(
-          g.nslices, long_blocks, g.nlong, g.perm, g.sptr, g.scol, nullptr, g.lnode, g.lptr,
-          g.lcol, nullptr, g.exc_src, g.exc_R, g.p[cur], g.y[cur], g.inv, g.p[nxt], yout, gmode);
-    } else {
-      k_sweep<true><<<grid, kWarpsPerBlock * 32, 0, s>>>(
-          g.nslices, long_blocks, g.nlong, g.perm, g.sptr, g.scol, g.sR, g.lnode, g.lptr, g.lcol,
-          g.lR, nullptr, nullptr, g.p[cur], nullptr, g.inv, g.p[nxt], nullptr, gmode);
+    // pass k multiplies the factors of source segment k; the long rows ride
+    // along in the first pass's grid (their blocks first)
+    for (int k = 0; k < nseg; ++k) {
+      const uint64_t s0 = g.seg_slice[k], s1 = g.seg_slice[k + 1];
+      const uint64_t lb = k == 0 ? long_blocks : 0;
+      const uint64_t blocks = lb + (s1 - s0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
+      if (blocks == 0) continue;
+      if (compact) {
+        k_sweep<false><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
+            s0, s1, lb, g.nlong, g.state, g.perm, g.sptr, g.scol, nullptr, g.lnode, g.lptr,
+            g.lcol, nullptr, g.exc_src, g.exc_R, g.p[cur], g.y[cur], g.inv, g.p[nxt], yout, gmode);
+      } else {
+        k_sweep<true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
+            s0, s1, lb, g.nlong, g.state, g.perm, g.sptr, g.scol, g.sR, g.lnode, g.lptr, g.lcol,
+            g.lR, nullptr, nullptr, g.p[cur], nullptr, g.inv, g.p[nxt], nullptr, gmode);
+      }
+      QVB_LAUNCH_CHECK();
     }
-    QVB_LAUNCH_CHECK();
   }
   QVB_CUDA(cudaEventRecord(g.ev[1], s));
   return g.p[(layers - 1) & 1];

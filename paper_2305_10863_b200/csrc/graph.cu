@@ -19,6 +19,7 @@
 //                            every R equals 1/row_sum(s) bitwise, else
 //                            weighted (u32 col + f64 R per edge)
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -42,6 +43,7 @@ qvb_graph::~qvb_graph() {
   cudaFree(exc_src);
   cudaFree(exc_R);
   cudaFree(inv);
+  cudaFree(state);
   for (int i = 0; i < 2; ++i) {
     cudaFree(p[i]);
     cudaFree(y[i]);
@@ -224,58 +226,136 @@ __global__ void k_compact(const uint32_t* __restrict__ ucol, const double* __res
   }
 }
 
-// ---- slicing (see graph.cuh) ------------------------------------------------
-__device__ __forceinline__ uint32_t eff_degree(const uint64_t* uptr, uint32_t v, uint32_t thr) {
-  const uint64_t d = uptr[v + 1] - uptr[v];
-  return d > thr ? 0u : static_cast<uint32_t>(d);
-}
-
-__global__ void k_window_keys(const uint64_t* __restrict__ uptr, uint64_t n, uint32_t thr,
-                              uint64_t* __restrict__ keys, uint32_t* __restrict__ ids) {
+// ---- segmented slicing (see graph.cuh) ---------------------------------------
+// (node, segment) pairs: for every regular row, one pair per source segment
+// its (source-sorted) in-row touches; zero-degree rows get one empty pair in
+// pass 0 so their P(n,j) = P(n,j-1) is written too. Long rows get none.
+__global__ void k_pair_count(const uint64_t* __restrict__ uptr, const uint32_t* __restrict__ src,
+                             uint64_t n, uint32_t thr, uint64_t seg, uint32_t* __restrict__ cnt) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t d = eff_degree(uptr, static_cast<uint32_t>(v), thr);
-    keys[v] = ((v / kWindow) << 32) | (0xFFFFFFFFull - d);  // window asc, degree desc
-    ids[v] = static_cast<uint32_t>(v);
+    const uint64_t a = uptr[v], b = uptr[v + 1];
+    uint32_t c = 0;
+    if (b == a) {
+      c = 1;
+    } else if (b - a <= thr) {
+      uint64_t prev = ~0ull;
+      for (uint64_t u = a; u < b; ++u) {
+        const uint64_t k = src[u] / seg;
+        c += k != prev;
+        prev = k;
+      }
+    }
+    cnt[v] = c;
   }
 }
 
-// Slot -> node (kNoNode for padding slots and long rows) and 32*len per slice.
-__global__ void k_slice_lens(const uint32_t* __restrict__ sorted, const uint64_t* __restrict__ uptr,
-                             uint64_t n, uint32_t thr, uint64_t nslices,
-                             uint32_t* __restrict__ perm, uint32_t* __restrict__ len32) {
-  const uint64_t slots = nslices * 32;
-  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < slots;
-       p += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t v = kNoNode, d = 0;
-    if (p < n) {
-      v = sorted[p];
-      const uint64_t deg = uptr[v + 1] - uptr[v];
-      if (deg > thr) v = kNoNode;  // long row: served by the long path
-      else d = static_cast<uint32_t>(deg);
+__global__ void k_pair_emit(const uint64_t* __restrict__ uptr, const uint32_t* __restrict__ src,
+                            uint64_t n, uint32_t thr, uint64_t seg, const uint64_t* __restrict__ po,
+                            uint32_t* __restrict__ pk, uint32_t* __restrict__ pv,
+                            uint64_t* __restrict__ pstart, uint32_t* __restrict__ pdeg) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = uptr[v], b = uptr[v + 1];
+    uint64_t at = po[v];
+    if (b == a) {
+      pk[at] = 0;
+      pv[at] = static_cast<uint32_t>(v) | kFirst | kLast;
+      pstart[at] = 0;
+      pdeg[at] = 0;
+      continue;
     }
-    perm[p] = v;
-    if ((p & 31) == 0) len32[p >> 5] = 32u * d;  // first slot holds the slice maximum
+    if (b - a > thr) continue;
+    uint64_t run = a;
+    for (uint64_t u = a; u < b; ++u) {
+      const uint64_t k = src[u] / seg;
+      const bool end = u + 1 == b || src[u + 1] / seg != k;
+      if (end) {
+        uint32_t flags = (run == a ? kFirst : 0u) | (u + 1 == b ? kLast : 0u);
+        pk[at] = static_cast<uint32_t>(k);
+        pv[at] = static_cast<uint32_t>(v) | flags;
+        pstart[at] = run;
+        pdeg[at] = static_cast<uint32_t>(u + 1 - run);
+        ++at;
+        run = u + 1;
+      }
+    }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) len32[nslices] = 0;
+}
+
+// One CTA per group of up to 256 pairs of one pass: order them by degree
+// (descending, node id ascending) into the group's 256 slots, so each slice
+// of 32 holds similar row lengths and pads little.
+__global__ void __launch_bounds__(kWindow)
+    k_group_sort(const uint32_t* __restrict__ sorted_idx, const uint64_t* __restrict__ seg_pair_begin,
+                 const uint64_t* __restrict__ seg_group_begin, int nseg,
+                 const uint32_t* __restrict__ pv, const uint32_t* __restrict__ pdeg,
+                 uint32_t* __restrict__ slot_pair) {
+  __shared__ uint32_t sdeg[kWindow];
+  __shared__ uint32_t snode[kWindow];
+  const uint64_t grp = blockIdx.x;
+  int k = 0;
+  while (k + 1 < nseg && seg_group_begin[k + 1] <= grp) ++k;
+  const uint64_t q0 = seg_pair_begin[k] + (grp - seg_group_begin[k]) * kWindow;
+  const uint64_t q1 = seg_pair_begin[k + 1];
+  const uint32_t t = threadIdx.x;
+  const bool real = q0 + t < q1;
+  uint32_t idx = 0, d = 0, node = 0;
+  if (real) {
+    idx = sorted_idx[q0 + t];
+    d = pdeg[idx];
+    node = pv[idx] & kNodeMask;
+  }
+  sdeg[t] = real ? d : 0u;
+  snode[t] = real ? node : 0xFFFFFFFFu;
+  __syncthreads();
+  const uint32_t cnt = static_cast<uint32_t>(q1 - q0 < kWindow ? q1 - q0 : kWindow);
+  if (real) {
+    uint32_t rank = 0;
+    for (uint32_t j = 0; j < cnt; ++j) {
+      const uint32_t dj = sdeg[j], nj = snode[j];
+      rank += (dj > d) || (dj == d && nj < node);
+    }
+    slot_pair[grp * kWindow + rank] = idx;
+  } else {
+    slot_pair[grp * kWindow + t] = 0xFFFFFFFFu;
+  }
+}
+
+__global__ void k_slot_lens(const uint32_t* __restrict__ slot_pair, const uint32_t* __restrict__ pdeg,
+                            uint64_t nslices, uint32_t* __restrict__ len32) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= nslices;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t len = 0;
+    if (j < nslices) {
+      const uint32_t i = slot_pair[j * 32];  // first slot holds the slice maximum
+      len = i == 0xFFFFFFFFu ? 0u : pdeg[i];
+    }
+    len32[j] = 32u * len;
+  }
 }
 
 template <bool kWithR>
-__global__ void k_fill_slices(const uint32_t* __restrict__ perm, const uint64_t* __restrict__ sptr,
-                              const uint64_t* __restrict__ uptr, const uint32_t* __restrict__ col,
-                              const double* __restrict__ R, uint64_t nslices, uint32_t pad,
-                              uint32_t* __restrict__ scol, double* __restrict__ sR) {
+__global__ void k_fill_slots(const uint32_t* __restrict__ slot_pair, const uint32_t* __restrict__ pv,
+                             const uint64_t* __restrict__ pstart, const uint32_t* __restrict__ pdeg,
+                             const uint64_t* __restrict__ sptr, const uint32_t* __restrict__ col,
+                             const double* __restrict__ R, uint64_t nslices, uint32_t pad,
+                             uint32_t* __restrict__ perm, uint32_t* __restrict__ scol,
+                             double* __restrict__ sR) {
   const uint64_t slots = nslices * 32;
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < slots;
        p += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t s = p >> 5, lane = p & 31;
     const uint64_t base = sptr[s];
     const uint64_t len = (sptr[s + 1] - base) >> 5;
-    const uint32_t v = perm[p];
+    const uint32_t i = slot_pair[p];
     uint64_t r0 = 0, deg = 0;
-    if (v != kNoNode) {
-      r0 = uptr[v];
-      deg = uptr[v + 1] - r0;
+    if (i != 0xFFFFFFFFu) {
+      perm[p] = pv[i];
+      r0 = pstart[i];
+      deg = pdeg[i];
+    } else {
+      perm[p] = kNoNode;
     }
     for (uint64_t k = 0; k < len; ++k) {
       const uint64_t at = base + k * 32 + lane;
@@ -395,7 +475,7 @@ void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, con
     g.nexc = 0;
     g.layout = 0;
     DevBuf<uint32_t> none(1, s);
-    build_slices(g, uptr.p, none.p, nullptr, s);
+    build_slices(g, uptr.p, none.p, none.p, nullptr, s);
     g.inv = persist(inv);
     g.bytes += n * 8;
     QVB_CUDA(cudaStreamSynchronize(s));
@@ -465,61 +545,108 @@ void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, con
                                                       xsrc.p, xR.p);
     QVB_LAUNCH_CHECK();
     uR.release();
-    ucol.release();
     uexc.release();
     g.exc_src = persist(xsrc);
     g.exc_R = persist(xR);
     g.bytes = (nexc ? nexc : 1) * 12;
-    build_slices(g, uptr.p, col.p, nullptr, s);
+    build_slices(g, uptr.p, col.p, ucol.p, nullptr, s);
   } else {
     g.layout = 1;
     uexc.release();
-    build_slices(g, uptr.p, ucol.p, uR.p, s);
+    build_slices(g, uptr.p, ucol.p, ucol.p, uR.p, s);
   }
   g.inv = persist(inv);
   g.bytes += n * 8;
   QVB_CUDA(cudaStreamSynchronize(s));
 }
 
-void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const double* R,
-                  cudaStream_t s) {
+uint64_t segment_size(uint64_t n) {
+  uint64_t mb = 64;
+  if (const char* e = std::getenv("QVB_SEG_MB")) mb = std::strtoull(e, nullptr, 10);
+  uint64_t seg = std::max<uint64_t>(1, (mb << 20) / 8);
+  if (const char* e = std::getenv("QVB_SEG_SOURCES")) seg = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
+  return std::min<uint64_t>(seg, std::max<uint64_t>(n, 1));
+}
+
+void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const uint32_t* src,
+                  const double* R, cudaStream_t s) {
   const uint64_t n = g.n;
   const uint64_t avg = g.eu ? (g.eu + n - 1) / n : 1;
   g.long_threshold = static_cast<uint32_t>(std::max<uint64_t>(64, 4 * avg));
   const uint32_t thr = g.long_threshold;
-  g.nslices = (n + 31) / 32;
+  g.seg_size = segment_size(n);
+  const uint64_t seg = g.seg_size;
+  const int nseg = static_cast<int>((n + seg - 1) / seg);
+  if (nseg > 255) fail(QVB_ERR_UNSUPPORTED, "too many source segments (raise QVB_SEG_MB)");
+
+  // (node, segment) pairs
+  DevBuf<uint32_t> cnt(n + 1, s);
+  DevBuf<uint64_t> po(n + 1, s);
+  QVB_CUDA(cudaMemsetAsync(cnt.p + n, 0, sizeof(uint32_t), s));
+  k_pair_count<<<grid_for(n, kBlock), kBlock, 0, s>>>(uptr, src, n, thr, seg, cnt.p);
+  QVB_LAUNCH_CHECK();
+  exclusive_sum_u32_u64(cnt.p, po.p, n + 1, s);
+  cnt.release();
+  const uint64_t H = read_scalar(po.p + n, s);
+  g.pairs = H;
+  DevBuf<uint32_t> pk(H, s), pv(H, s), pdeg(H, s);
+  DevBuf<uint64_t> pstart(H, s);
+  k_pair_emit<<<grid_for(n, kBlock), kBlock, 0, s>>>(uptr, src, n, thr, seg, po.p, pk.p, pv.p,
+                                                     pstart.p, pdeg.p);
+  QVB_LAUNCH_CHECK();
+  po.release();
+
+  // group the pairs by pass (stable: node order inside a pass)
+  DevBuf<uint32_t> sorted_idx(H, s);
+  DevBuf<uint64_t> seg_pair_begin(nseg + 1, s);
+  {
+    DevBuf<uint32_t> iota(H, s), sk(H, s);
+    k_iota<<<grid_for(H, kBlock), kBlock, 0, s>>>(iota.p, H);
+    QVB_LAUNCH_CHECK();
+    sort_pairs_u32_u32(pk.p, sk.p, iota.p, sorted_idx.p, H, 0, bits_for(nseg - 1), s);
+    k_offsets_from_sorted<<<grid_for(H, kBlock), kBlock, 0, s>>>(sk.p, H, nseg, seg_pair_begin.p);
+    QVB_LAUNCH_CHECK();
+  }
+  pk.release();
+  std::vector<uint64_t> spb(nseg + 1), sgb(nseg + 1);
+  QVB_CUDA(cudaMemcpyAsync(spb.data(), seg_pair_begin.p, (nseg + 1) * 8, cudaMemcpyDeviceToHost, s));
+  QVB_CUDA(cudaStreamSynchronize(s));
+  sgb[0] = 0;
+  for (int k = 0; k < nseg; ++k) sgb[k + 1] = sgb[k] + (spb[k + 1] - spb[k] + kWindow - 1) / kWindow;
+  const uint64_t groups = sgb[nseg];
+  DevBuf<uint64_t> seg_group_begin(nseg + 1, s);
+  QVB_CUDA(cudaMemcpyAsync(seg_group_begin.p, sgb.data(), (nseg + 1) * 8, cudaMemcpyHostToDevice, s));
+  g.nslices = groups * (kWindow / 32);
+  g.seg_slice.resize(nseg + 1);
+  for (int k = 0; k <= nseg; ++k) g.seg_slice[k] = sgb[k] * (kWindow / 32);
   const uint64_t S = g.nslices;
 
-  // windows of 256 ids sorted by in-degree (descending, stable)
-  DevBuf<uint32_t> sorted(n, s);
-  {
-    DevBuf<uint64_t> keys(n, s), skeys(n, s);
-    DevBuf<uint32_t> ids(n, s);
-    k_window_keys<<<grid_for(n, kBlock), kBlock, 0, s>>>(uptr, n, thr, keys.p, ids.p);
-    QVB_LAUNCH_CHECK();
-    sort_pairs_u64_u32(keys.p, skeys.p, ids.p, sorted.p, n, 0, 32 + bits_for((n - 1) / kWindow), s);
-  }
-  DevBuf<uint32_t> perm(S * 32, s), len32(S + 1, s);
-  DevBuf<uint64_t> sptr(S + 1, s);
-  k_slice_lens<<<grid_for(S * 32, kBlock), kBlock, 0, s>>>(sorted.p, uptr, n, thr, S, perm.p,
-                                                           len32.p);
+  DevBuf<uint32_t> slot_pair(S * 32 ? S * 32 : 1, s);
+  if (groups)
+    k_group_sort<<<static_cast<unsigned>(groups), kWindow, 0, s>>>(
+        sorted_idx.p, seg_pair_begin.p, seg_group_begin.p, nseg, pv.p, pdeg.p, slot_pair.p);
   QVB_LAUNCH_CHECK();
-  sorted.release();
+  sorted_idx.release();
+  DevBuf<uint32_t> len32(S + 1, s);
+  DevBuf<uint64_t> sptr(S + 1, s);
+  k_slot_lens<<<grid_for(S + 1, kBlock), kBlock, 0, s>>>(slot_pair.p, pdeg.p, S, len32.p);
+  QVB_LAUNCH_CHECK();
   exclusive_sum_u32_u64(len32.p, sptr.p, S + 1, s);
+  len32.release();
   g.slots = read_scalar(sptr.p + S, s);
-  DevBuf<uint32_t> scol(g.slots ? g.slots : 1, s);
+  DevBuf<uint32_t> perm(S * 32 ? S * 32 : 1, s), scol(g.slots ? g.slots : 1, s);
   DevBuf<double> sR;
   const uint32_t pad = static_cast<uint32_t>(n);  // operand slot N holds 0
   if (R) {
     sR.alloc(g.slots ? g.slots : 1, s);
-    k_fill_slices<true><<<grid_for(S * 32, kBlock), kBlock, 0, s>>>(perm.p, sptr.p, uptr, col, R,
-                                                                    S, pad, scol.p, sR.p);
+    k_fill_slots<true><<<grid_for(S * 32, kBlock), kBlock, 0, s>>>(
+        slot_pair.p, pv.p, pstart.p, pdeg.p, sptr.p, col, R, S, pad, perm.p, scol.p, sR.p);
   } else {
-    k_fill_slices<false><<<grid_for(S * 32, kBlock), kBlock, 0, s>>>(perm.p, sptr.p, uptr, col,
-                                                                     nullptr, S, pad, scol.p,
-                                                                     nullptr);
+    k_fill_slots<false><<<grid_for(S * 32, kBlock), kBlock, 0, s>>>(
+        slot_pair.p, pv.p, pstart.p, pdeg.p, sptr.p, col, nullptr, S, pad, perm.p, scol.p, nullptr);
   }
   QVB_LAUNCH_CHECK();
+  if (nseg > 1) QVB_CUDA(cudaMalloc(&g.state, n * sizeof(double)));
 
   // long rows
   DevBuf<uint8_t> mark(n, s);
@@ -553,7 +680,7 @@ void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const
   g.sptr = persist(sptr);
   g.scol = persist(scol);
   g.sR = sR.p ? persist(sR) : nullptr;
-  g.bytes += S * 32 * 4 + (S + 1) * 8 + g.slots * (R ? 12 : 4);
+  g.bytes += S * 32 * 4 + (S + 1) * 8 + g.slots * (R ? 12 : 4) + (nseg > 1 ? n * 8 : 0);
 }
 
 }  // namespace qvb

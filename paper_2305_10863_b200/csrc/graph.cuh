@@ -25,7 +25,17 @@
 //                      differs bitwise from 1/row_sum(s)
 //   inv    f64[N]      1/row_sum(s) (0 for sinks)
 //   p[2], y[2] f64[N+1] ping-pong P_{j-1}/P_j and y = P * inv; entry N = 0
+//
+// Source segments. At papers scale the gathered vector (8 B x N) is far
+// larger than L2 and every random 8-byte gather that misses pulls a whole
+// line from HBM. The sweep is therefore split into passes over source
+// ranges small enough to stay L2-resident; a node's running product is
+// carried between passes (state), and because each in-row is sorted by
+// source, pass order == the reference's factor order: still bit-exact.
+// Each pass has its own slices built only over the nodes it touches.
 #pragma once
+
+#include <vector>
 
 #include "common.cuh"
 
@@ -33,6 +43,12 @@ struct qvb_graph {
   int device = 0;
   uint64_t n = 0, e = 0, eu = 0, nexc = 0;
   uint32_t layout = 0;  // 0 compact, 1 weighted
+  // source segments: sweep pass k multiplies the factors whose source lies
+  // in [k*seg_size, (k+1)*seg_size); its slices are seg_slice[k]..seg_slice[k+1]
+  uint64_t seg_size = 0;
+  std::vector<uint64_t> seg_slice;  // host, nseg + 1
+  double* state = nullptr;          // running products between passes (nseg > 1)
+  uint64_t pairs = 0;               // (node, segment) pairs with slots
   uint64_t nslices = 0;
   uint32_t* perm = nullptr;
   uint64_t* sptr = nullptr;
@@ -59,9 +75,14 @@ struct qvb_graph {
 namespace qvb {
 
 constexpr uint32_t kExcFlag = 0x80000000u;
-constexpr uint32_t kNoNode = 0xFFFFFFFFu;
-constexpr uint32_t kWindow = 256;  // nodes sorted together (one CTA of 8 warps)
-constexpr uint64_t kMaxNodes = (1ull << 31) - 2;
+// perm slot = node | kFirst (first pass touching the node: start from 1.0)
+//                  | kLast  (last pass: finish P instead of storing the state)
+constexpr uint32_t kFirst = 0x80000000u;
+constexpr uint32_t kLast = 0x40000000u;
+constexpr uint32_t kNodeMask = 0x3FFFFFFFu;
+constexpr uint32_t kNoNode = kNodeMask;  // padding slot
+constexpr uint32_t kWindow = 256;  // slots sorted together (one CTA of 8 warps)
+constexpr uint64_t kMaxNodes = (1ull << 30) - 2;
 constexpr uint64_t kMaxEdges = 0xFFFFFFFFull;
 
 // Builds the in-CSR from a device out-CSR. d_w == nullptr means unit weights.
@@ -69,9 +90,12 @@ constexpr uint64_t kMaxEdges = 0xFFFFFFFFull;
 void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, const double* d_w,
                   const uint32_t* d_src, cudaStream_t s);
 
-// Sliced layout + long-row CSR from the coalesced in-CSR (uptr, col, R).
-void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const double* R,
-                  cudaStream_t s);
+// Segmented sliced layout + long-row CSR from the coalesced in-CSR (uptr,
+// col as stored (flagged exceptions), true sources src, R).
+void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const uint32_t* src,
+                  const double* R, cudaStream_t s);
+// Segment size in sources: QVB_SEG_MB (default 64) MiB of 8-byte operands.
+uint64_t segment_size(uint64_t n);
 
 // Runs layers-1 sweeps; returns the device buffer holding P_layers.
 const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s);

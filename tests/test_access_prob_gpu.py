@@ -144,3 +144,31 @@ def test_layouts_exercised(qvb, oracle):
     g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, True, False)
     assert g.info().layout == 1
     g.close()
+
+
+@pytest.mark.parametrize("seg_sources", ["1", "7", "1000", "31337"])
+def test_segmented_passes_bit_exact(qvb, oracle, seg_sources, monkeypatch):
+    """Force many source segments (passes carrying the running product in
+    source order) on small graphs: results must stay bit-identical."""
+    monkeypatch.setenv("QVB_SEG_SOURCES", seg_sources)
+    rng = derive_stream(79, int(seg_sources))
+    if seg_sources in ("1", "7"):  # <= 255 segments: tiny graphs only
+        for _ in range(10):
+            n, s, d, w = random_edges(rng, 40 if seg_sources == "7" else 200, 250, True)
+            if (n + int(seg_sources) - 1) // int(seg_sources) > 255:
+                continue
+            ro, col, ww = _csr(oracle, n, s, d, w)
+            for weighted in (True, False):
+                g = qvb.DeviceGraph.upload(ro, col, ww if weighted else None)
+                for layers in (2, 3, 4):
+                    exp = oracle.access_prob(ro, col, ww if weighted else np.ones_like(ww), layers)
+                    assert (bits(g.access_prob(layers)) == bits(exp)).all()
+                g.close()
+        return
+    c = CONFIGS["C1"]
+    for weighted, transposed in [(False, False), (True, False), (False, True)]:
+        ro, col, w = oracle.synthetic_graph(c["n"], c["e"], 7, weighted, transposed)
+        g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, weighted, transposed)
+        for layers in (2, 3):
+            assert (bits(g.access_prob(layers)) == bits(oracle.access_prob(ro, col, w, layers))).all()
+        g.close()
