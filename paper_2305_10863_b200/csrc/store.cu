@@ -20,6 +20,7 @@
 // is read-only for the store's lifetime). The id and lookup-table reads of a
 // row are shared by its lanes (same address, one transaction).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -116,6 +117,79 @@ __global__ void __launch_bounds__(kGatherBlock)
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
       if (ok[u]) V::store(out + dst[u], v[u]);
+  }
+}
+
+// Row-group gather (v3): a warp serves 32 consecutive requests at a time.
+// Lane l resolves request l of the group (id -> lookup entry -> source row
+// address) once; the group's 32 rows are then copied as one flat run of
+// VEC-byte chunks — chunk c of the group lands at out + c*VEC because the
+// output rows are contiguous, and its source is the row address shuffled
+// from lane c/cpr plus (c%cpr)*VEC, with (row, offset) advanced
+// incrementally. Ids and lookup entries of the next groups are fetched one
+// and two groups ahead so the dependent id -> entry -> row chain overlaps the
+// current copy.
+template <int VEC, int kU, int kMinBlocks>
+__global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
+    k_gather_rows(const uint64_t* __restrict__ ids, uint64_t rows,
+                  const uint64_t* __restrict__ lut, Bases bases, uint64_t stride, uint32_t cpr,
+                  uint32_t row_bytes, uint64_t n, char* __restrict__ out,
+                  unsigned long long* err) {
+  using V = Vec<VEC>;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t groups = (rows + 31) / 32;
+  const uint32_t q32 = 32 / cpr, r32 = 32 % cpr;
+  const uint32_t row0 = lane / cpr, k0 = lane - row0 * cpr;
+
+  auto load_id = [&](uint64_t g) -> uint64_t {
+    const uint64_t r = g * 32 + lane;
+    return (g < groups && r < rows) ? __ldg(ids + r) : ~0ull;
+  };
+  auto resolve = [&](uint64_t g, uint64_t f) -> uint64_t {  // source row address or 0
+    const uint64_t r = g * 32 + lane;
+    if (g >= groups || r >= rows) return 0;
+    if (f >= n) {
+      atomicMin(err, (unsigned long long)r);
+      return 0;
+    }
+    const uint64_t e = __ldg(lut + f);
+    return reinterpret_cast<uint64_t>(bases.p[e >> kOffsetBits]) + (e & kOffsetMask) * stride;
+  };
+
+  uint64_t g = warp;
+  uint64_t src = resolve(g, load_id(g));
+  uint64_t id_next = load_id(g + nwarps);
+  for (; g < groups; g += nwarps) {
+    const uint64_t src_next = resolve(g + nwarps, id_next);  // one group ahead
+    id_next = load_id(g + 2 * nwarps);                      // two groups ahead
+    const uint32_t nr = static_cast<uint32_t>(rows - g * 32 < 32 ? rows - g * 32 : 32);
+    const uint32_t tot = nr * cpr;
+    char* dst0 = out + g * 32 * (uint64_t)row_bytes;
+    uint32_t row = row0, k = k0;
+    for (uint32_t cb = 0; cb < tot; cb += 32 * kU) {  // warp-uniform trip count
+      const uint32_t c0 = cb + lane;
+      typename V::T v[kU];
+      bool ok[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t c = c0 + u * 32;
+        const uint64_t s = __shfl_sync(0xffffffffu, src, row < 32 ? row : 31);
+        ok[u] = c < tot && s != 0;
+        if (ok[u]) v[u] = V::load(reinterpret_cast<const char*>(s) + (uint64_t)k * VEC);
+        row += q32;
+        k += r32;
+        if (k >= cpr) {
+          k -= cpr;
+          ++row;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (ok[u]) V::store(dst0 + (uint64_t)(c0 + u * 32) * VEC, v[u]);
+    }
+    src = src_next;
   }
 }
 
@@ -252,6 +326,16 @@ struct qvb_store {
       fail(QVB_ERR_VALIDATION, "output buffer is not aligned to the row vector width");
     const int V = vec();
     const uint32_t cpr = row_bytes / V;
+    static const bool flat = [] {
+      const char* k = std::getenv("QVB_GATHER_KERNEL");
+      return k && std::string(k) == "flat";
+    }();
+    if (!flat) {
+      if (V == 16) launch_rows<16>(ids, b, cpr, out, s);
+      else if (V == 8) launch_rows<8>(ids, b, cpr, out, s);
+      else launch_rows<4>(ids, b, cpr, out, s);
+      return;
+    }
     const uint64_t max_rows = std::max<uint64_t>(1, (0xFFFFFFFFull / cpr) / 2);
     for (uint64_t r0 = 0; r0 < b; r0 += max_rows) {
       const uint32_t rows = static_cast<uint32_t>(std::min(max_rows, b - r0));
@@ -275,6 +359,30 @@ struct qvb_store {
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(full, work_blocks((uint64_t)rows * cpr)));
     k_gather<V><<<grid, kGatherBlock, 0, s>>>(ids, rows, lut, bases, stride, cpr, row_bytes, n, o,
                                               r0, err);
+    QVB_LAUNCH_CHECK();
+  }
+
+  template <int V>
+  void launch_rows(const uint64_t* ids, uint64_t rows, uint32_t cpr, char* o, cudaStream_t s) {
+    static const int variant = [] {
+      const char* u = std::getenv("QVB_GATHER_U");
+      return u ? std::atoi(u) : 0;
+    }();
+    if (variant == 8) launch_rows_u<V, 8, 1>(ids, rows, cpr, o, s);
+    else if (variant == 4) launch_rows_u<V, 4, 4>(ids, rows, cpr, o, s);
+    else if (variant == 2) launch_rows_u<V, 2, 6>(ids, rows, cpr, o, s);
+    else launch_rows_u<V, 4, 4>(ids, rows, cpr, o, s);
+  }
+
+  template <int V, int U, int MB>
+  void launch_rows_u(const uint64_t* ids, uint64_t rows, uint32_t cpr, char* o, cudaStream_t s) {
+    static unsigned full = 0;
+    if (!full) full = resident_grid(k_gather_rows<V, U, MB>, kGatherBlock, 0, ~0ull);
+    const uint64_t warps_needed = (rows + 31) / 32;
+    const uint64_t blocks = (warps_needed + kGatherBlock / 32 - 1) / (kGatherBlock / 32);
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(full, blocks));
+    k_gather_rows<V, U, MB><<<grid, kGatherBlock, 0, s>>>(ids, rows, lut, bases, stride, cpr,
+                                                          row_bytes, n, o, err);
     QVB_LAUNCH_CHECK();
   }
 
