@@ -153,6 +153,9 @@ _SIGNATURES = {
     "qvb_gather_host": (i32, [vp, vp, u64, vp, vp]),
     "qvb_store_check_error": (i32, [vp]),
     "qvb_request_ids_synthetic": (i32, [i32, u64, u64, u64, vp, u64, vp]),
+    # include/qvb_test.h
+    "qvb_test_sort_pairs_u64": (i32, [i32, vp, vp, u64, i32, i32, vp, vp]),
+    "qvb_test_scan_u32": (i32, [i32, vp, u64, i32, vp]),
 }
 
 

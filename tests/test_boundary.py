@@ -22,7 +22,9 @@ def q():
 
 
 def declared():
-    src = open(os.path.join(ROOT, "include", "qvb.h")).read()
+    import glob
+
+    src = "".join(open(p).read() for p in glob.glob(os.path.join(ROOT, "include", "*.h")))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(qvb_[a-z0-9_]+)\s*\(", src)))
 
