@@ -172,3 +172,32 @@ def test_segmented_passes_bit_exact(qvb, oracle, seg_sources, monkeypatch):
         for layers in (2, 3):
             assert (bits(g.access_prob(layers)) == bits(oracle.access_prob(ro, col, w, layers))).all()
         g.close()
+
+
+def test_c3_weighted_bit_exact(qvb, oracle):
+    """C3 (Reddit-shaped, 233K nodes, 114M edges, 3-layer edge-weighted) at full size."""
+    c = CONFIGS["C3"]
+    ro, col, w = oracle.synthetic_graph(c["n"], c["e"], 7, True, False)
+    exp = oracle.access_prob(ro, col, w, 3)
+    g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, True, False)
+    assert g.info().layout == 1
+    assert (bits(g.access_prob(3)) == bits(exp)).all()
+    g.close()
+
+
+def test_c4_segmented_equals_single_pass(qvb, monkeypatch):
+    """C4 (papers-shaped, 111M nodes, 1.6B edges): the source-segmented sweep
+    (14 passes carrying the running products) and a single-pass sweep over
+    the same device graph are bit-identical, and P obeys its invariants."""
+    c = CONFIGS["C4"]
+    monkeypatch.setenv("QVB_SEG_MB", "64")
+    g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, False, False)
+    p_seg = g.access_prob(3)
+    g.close()
+    monkeypatch.setenv("QVB_SEG_MB", "4096")
+    g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, False, False)
+    p_one = g.access_prob(3)
+    p2 = g.access_prob(2)
+    g.close()
+    assert (bits(p_seg) == bits(p_one)).all()
+    assert (p_one >= p2).all() and (p2 >= 1.0 / c["n"]).all() and (p_one <= 1.0).all()
