@@ -43,6 +43,8 @@ CONFIGS = {
                desc="C4 ogbn-papers100M-shaped: 111M nodes, 1.6B edges, 128-dim fp32, 3-layer P"),
 }
 META_BYTES = 24  # 8 B id + 16 B reference-layout lookup row per request
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+PCIE_GBS = 64.0  # PCIe Gen5 x16 per direction, nominal
 
 
 def peaks():
@@ -180,7 +182,25 @@ def run_ours(args):
     t0 = time.perf_counter()
     lo, ids = qvb.plan_placement(p_host, topo, device=local)
     plan_s = time.perf_counter() - t0
-    loc, _ = qvb.build_lookup_table(lo, ids, topo, 0, rank, device=local)
+    t0 = time.perf_counter()
+    loc, off = qvb.build_lookup_table(lo, ids, topo, 0, rank, device=local)
+    lut_s = time.perf_counter() - t0
+    rank_ms = None
+    if rank == 0:
+        p_dev_rank = torch.empty(n, dtype=torch.int64, device=dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        qvb._check(qvb._lib().qvb_rank_desc(local, p_dev.data_ptr(), n, p_dev_rank.data_ptr(), 1,
+                                             stream.cuda_stream))
+        e1.record(stream)
+        e1.synchronize()
+        rank_ms = e0.elapsed_time(e1)
+        del p_dev_rank
+    planner = {"rank_desc_device_ms": rank_ms, "plan_placement_s": plan_s,
+               "build_lookup_table_s": lut_s,
+               "note": "plan_placement = device rank + the reference's sequential planner on the "
+                       "host; build_lookup_table / plan_reads = C-ABI calls incl. host<->device "
+                       "copies of their arguments and results"}
     f_l = float(np.mean(loc == rank))
     f_h = float(np.mean(loc == world))
     f_p = 1.0 - f_l - f_h
@@ -191,9 +211,16 @@ def run_ours(args):
     req = torch.empty((nb, B), dtype=torch.int64, device=dev)
     for k in range(nb):
         qvb.request_ids_synthetic(11, rank * 1_000_003 + k, n, req[k], device=local, stream=stream)
+    if rank == 0:  # K4 read planner on one batch, through the C-ABI
+        req0 = req[0].cpu().numpy().view(np.uint64)
+        qvb.plan_reads(loc, off, req0[:1024], 8)
+        t0 = time.perf_counter()
+        qvb.plan_reads(loc, off, req0, 8)
+        planner["plan_reads_s"] = time.perf_counter() - t0
+        planner["plan_reads_ids"] = int(len(req0))
     out = torch.empty((B, dim), dtype=torch.float32, device=dev)
     for k in range(args.warmup):
-        store.gather(req[k], out, stream=stream)
+        store.gather(req[k], out, stream=stream, planned=args.planned)
     torch.cuda.synchronize(dev)
     store.check_error()
 
@@ -204,14 +231,14 @@ def run_ours(args):
         t_end = time.perf_counter() + args.clock_window
         while time.perf_counter() < t_end:
             for k in range(args.warmup):
-                store.gather(req[k], out, stream=stream)
+                store.gather(req[k], out, stream=stream, planned=args.planned)
             torch.cuda.synchronize(dev)
         D.barrier()
         torch.cuda.synchronize(dev)
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         evs[0].record(stream)
         for k in range(args.steps):
-            store.gather(req[args.warmup + k], out, stream=stream)
+            store.gather(req[args.warmup + k], out, stream=stream, planned=args.planned)
             evs[k + 1].record(stream)
         torch.cuda.synchronize(dev)
         D.barrier()
@@ -222,8 +249,16 @@ def run_ours(args):
     payload = world * args.steps * B * row_bytes
     value = payload / (max_ms / 1e3) / 1e9
     per_launch_ms = statistics.mean(launch_ms)
+    # mixed local-HBM / NVLink / PCIe roofline: per id, HBM
+    # moves the metadata, this GPU's reads and writes and the peers' reads of
+    # this GPU's shard (symmetric partition); NVLink carries the peer rows;
+    # PCIe the host rows. The slowest link bounds the launch.
     hbm_per_id = META_BYTES + row_bytes * (1 + f_l + f_p)
-    alg = B * hbm_per_id
+    links = {"hbm": (B * hbm_per_id, pk["hbm_gbs"], pk["source"]),
+             "nvlink": (B * row_bytes * f_p, NVLINK_GBS, "measured peer copy (B200_PROFILING.md)"),
+             "pcie": (B * row_bytes * f_h, PCIE_GBS, "nominal Gen5 x16")}
+    bound = max(links, key=lambda k: links[k][0] / links[k][1])
+    alg, link_peak, link_src = links[bound]
     achieved = alg / (per_launch_ms / 1e3) / 1e9
 
     # ---- e2e through the public API from pinned host buffers --------------------
@@ -289,13 +324,16 @@ def run_ours(args):
                 n * row_bytes / 1e6, B * row_bytes / 1e6),
             "parallelism": f"feature-partitioned x{world}, one process per GPU",
         },
-        "roofline": {"bound": "hbm", "kernel": "k_gather", "achieved": achieved,
-                     "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+        "roofline": {"bound": bound, "kernel": "k_gather_rows", "achieved": achieved,
+                     "peak": link_peak, "unit": "GB/s", "frac": achieved / link_peak,
                      "traffic": None, "algorithmic_bytes_per_id": hbm_per_id,
-                     "per_launch_ms": per_launch_ms, "peak_source": pk["source"]},
+                     "algorithmic_bytes_per_launch": alg,
+                     "per_launch_ms": per_launch_ms, "peak_source": link_src,
+                     "link_times_ms": {k: v[0] / v[1] / 1e6 for k, v in links.items()}},
         "e2e": e2e,
         "gpu_launches": args.steps,
         "access_prob": access_prob,
+        "planner": planner,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
     }
@@ -348,8 +386,14 @@ def cpu_baseline(args, cfg, p_host, topo_host, ro, col, w, steps):
     # collect: the reference's read planner (placement.cpp:355-380) on each
     # batch + the byte copy it only models, restated as a threaded memcpy
     t = topology_defaults(gpus_per_server=1, gpu_feature_capacity=n, host_feature_capacity=n)
+    t0 = time.perf_counter()
     lo, ids = (ref or o).plan_placement(p_host, t)
+    t1 = time.perf_counter()
     loc, off = (ref or o).build_lookup_table(lo, ids, t, 0)
+    t2 = time.perf_counter()
+    ap["planner_reference"] = {"plan_placement_s": t1 - t0, "build_lookup_table_s": t2 - t1,
+                               "kind": kind, "cores": 1,
+                               "note": "single-threaded reference code (placement.cpp), C2 table"}
     x = o.features(n, dim)
     plan_s = gather_s = 0.0
     b = args.batch
@@ -443,6 +487,7 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--planned", action="store_true", help="location-bucketed, offset-sorted gather (K4 order)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -15,6 +15,9 @@ extern "C" {
 /* Stable LSD radix sort of (key, value) on key bits [begin_bit, end_bit). */
 int qvb_test_sort_pairs_u64(int device, const uint64_t* keys, const uint64_t* vals, uint64_t n,
                             int begin_bit, int end_bit, uint64_t* keys_out, uint64_t* vals_out);
+/* Device time (ms per sort) of sorting n random (u64 key, u64 value) pairs on
+ * key bits [0, bits). */
+int qvb_test_sort_bench(int device, uint64_t n, int bits, int reps, double* ms);
 /* Exclusive (inclusive=0) or inclusive scan of u32 values, widened to u64. */
 int qvb_test_scan_u32(int device, const uint32_t* in, uint64_t n, int inclusive, uint64_t* out);
 

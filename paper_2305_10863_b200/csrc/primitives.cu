@@ -173,8 +173,13 @@ __global__ void __launch_bounds__(kSortThreads)
     __syncwarp();
   }
   __syncthreads();
-  // prefix of the warp counts over warps (warp order == input order)
-  for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
+  // prefix of the warp counts over warps (warp order == input order), and
+  // the digit's start inside the tile (exclusive over digits)
+  __shared__ uint32_t dstart[kRadix];
+  __shared__ uint64_t gbase[kRadix];
+  uint32_t total = 0;
+  {
+    const int d = threadIdx.x;  // kSortThreads == kRadix
     uint32_t acc = 0;
 #pragma unroll
     for (int w = 0; w < kSortWarps; ++w) {
@@ -182,16 +187,46 @@ __global__ void __launch_bounds__(kSortThreads)
       whist[w][d] = acc;
       acc += c;
     }
+    total = acc;
+    gbase[d] = digit_base[(uint64_t)d * tiles + blockIdx.x];
+  }
+  // exclusive scan of the digit totals across the block
+  {
+    __shared__ uint32_t wsum[kSortWarps];
+    uint32_t inc = total;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    uint32_t before = 0;
+    for (int w = 0; w < warp; ++w) before += wsum[w];
+    dstart[threadIdx.x] = before + inc - total;
   }
   __syncthreads();
+  // stage the tile in digit order, then write each digit's run contiguously
+  __shared__ K sk[kSortTile];
+  __shared__ V sv[kSortTile];
+  __shared__ uint8_t sd[kSortTile];
 #pragma unroll
   for (int r = 0; r < kSortRounds; ++r) {
     const uint32_t d = dig[r];
     if (d < kRadix) {
-      const uint64_t pos = digit_base[(uint64_t)d * tiles + blockIdx.x] + whist[warp][d] + rank[r];
-      kout[pos] = k[r];
-      vout[pos] = v[r];
+      const uint32_t at = dstart[d] + whist[warp][d] + rank[r];
+      sk[at] = k[r];
+      sv[at] = v[r];
+      sd[at] = static_cast<uint8_t>(d);
     }
+  }
+  __syncthreads();
+  const uint64_t tile_n = n - blockIdx.x * kSortTile < kSortTile ? n - blockIdx.x * kSortTile : kSortTile;
+  for (uint32_t i = threadIdx.x; i < tile_n; i += kSortThreads) {
+    const uint32_t d = sd[i];
+    const uint64_t pos = gbase[d] + (i - dstart[d]);
+    kout[pos] = sk[i];
+    vout[pos] = sv[i];
   }
 }
 
@@ -289,6 +324,41 @@ extern "C" int qvb_test_sort_pairs_u64(int device, const uint64_t* keys, const u
     QVB_CUDA(cudaMemcpyAsync(keys_out, ko.p, n * 8, cudaMemcpyDeviceToHost, s));
     QVB_CUDA(cudaMemcpyAsync(vals_out, vo.p, n * 8, cudaMemcpyDeviceToHost, s));
     QVB_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+namespace qvb {
+namespace {
+__global__ void k_test_keys(uint64_t* k, uint64_t* v, uint64_t n, uint64_t mask) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    k[i] = splitmix64(i) & mask;
+    v[i] = i;
+  }
+}
+}  // namespace
+}  // namespace qvb
+
+extern "C" int qvb_test_sort_bench(int device, uint64_t n, int bits, int reps, double* ms) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    cudaStream_t s = nullptr;
+    DevBuf<uint64_t> k(n, s), v(n, s), ko(n, s), vo(n, s);
+    k_test_keys<<<grid_for(n, 256), 256, 0, s>>>(k.p, v.p, n, bits >= 64 ? ~0ull : ((1ull << bits) - 1));
+    QVB_LAUNCH_CHECK();
+    sort_pairs_u64_u64(k.p, ko.p, v.p, vo.p, n, 0, bits, s);  // warm the pool
+    cudaEvent_t a, b;
+    QVB_CUDA(cudaEventCreate(&a));
+    QVB_CUDA(cudaEventCreate(&b));
+    QVB_CUDA(cudaEventRecord(a, s));
+    for (int r = 0; r < reps; ++r) sort_pairs_u64_u64(k.p, ko.p, v.p, vo.p, n, 0, bits, s);
+    QVB_CUDA(cudaEventRecord(b, s));
+    QVB_CUDA(cudaEventSynchronize(b));
+    float f = 0;
+    QVB_CUDA(cudaEventElapsedTime(&f, a, b));
+    *ms = f / reps;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
   });
 }
 

@@ -156,6 +156,7 @@ _SIGNATURES = {
     # include/qvb_test.h
     "qvb_test_sort_pairs_u64": (i32, [i32, vp, vp, u64, i32, i32, vp, vp]),
     "qvb_test_scan_u32": (i32, [i32, vp, u64, i32, vp]),
+    "qvb_test_sort_bench": (i32, [i32, u64, i32, i32, P(C.c_double)]),
 }
 
 
