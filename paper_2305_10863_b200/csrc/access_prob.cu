@@ -182,6 +182,11 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
     if (!e) QVB_CUDA(cudaEventCreate(&e));
   int gmode = 0;
   if (const char* m = std::getenv("QVB_GATHER_MODE")) gmode = std::atoi(m);
+  int persist_mb = 0;
+  if (const char* m = std::getenv("QVB_L2_PERSIST_MB")) persist_mb = std::atoi(m);
+  if (persist_mb > 0) {
+    QVB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)persist_mb << 20));
+  }
   QVB_CUDA(cudaEventRecord(g.ev[0], s));
   for (uint32_t j = 2; j <= layers; ++j) {
     const int cur = (j - 2) & 1, nxt = cur ^ 1;
@@ -193,6 +198,44 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
       const uint64_t lb = k == 0 ? long_blocks : 0;
       const uint64_t blocks = lb + (s1 - s0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
       if (blocks == 0) continue;
+      if (persist_mb > 0 && nseg > 1) {
+        // experiment: pin this pass's operand slice in the persisting L2 carve-out
+        const double* opnd = compact ? g.y[cur] : g.p[cur];
+        const uint64_t first = (uint64_t)k * g.seg_size;
+        const uint64_t count = std::min<uint64_t>(g.seg_size, n - first);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+        cfg.blockDim = dim3(kWarpsPerBlock * 32);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = const_cast<double*>(opnd + first);
+        attr[0].val.accessPolicyWindow.num_bytes = count * sizeof(double);
+        attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (compact)
+          QVB_CUDA(cudaLaunchKernelEx(&cfg, k_sweep<false>, s0, s1, lb, g.nlong, g.state,
+                                      (const uint32_t*)g.perm, (const uint64_t*)g.sptr,
+                                      (const uint32_t*)g.scol, (const double*)nullptr,
+                                      (const uint32_t*)g.lnode, (const uint64_t*)g.lptr,
+                                      (const uint32_t*)g.lcol, (const double*)nullptr,
+                                      (const uint32_t*)g.exc_src, (const double*)g.exc_R,
+                                      (const double*)g.p[cur], (const double*)g.y[cur],
+                                      (const double*)g.inv, g.p[nxt], yout, gmode));
+        else
+          QVB_CUDA(cudaLaunchKernelEx(&cfg, k_sweep<true>, s0, s1, lb, g.nlong, g.state,
+                                      (const uint32_t*)g.perm, (const uint64_t*)g.sptr,
+                                      (const uint32_t*)g.scol, (const double*)g.sR,
+                                      (const uint32_t*)g.lnode, (const uint64_t*)g.lptr,
+                                      (const uint32_t*)g.lcol, (const double*)g.lR,
+                                      (const uint32_t*)nullptr, (const double*)nullptr,
+                                      (const double*)g.p[cur], (const double*)nullptr,
+                                      (const double*)g.inv, g.p[nxt], (double*)nullptr, gmode));
+        continue;
+      }
       if (compact) {
         k_sweep<false><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
             s0, s1, lb, g.nlong, g.state, g.perm, g.sptr, g.scol, nullptr, g.lnode, g.lptr,
