@@ -159,6 +159,16 @@ int qvb_compute_access_prob_ie(int device, uint64_t n, uint64_t e, const uint64_
                                const uint64_t* col, const double* weights, uint32_t layers,
                                double* out, double* ms_out);
 
+/* ---- FAP estimator (metrics.cpp:95-132) -------- */
+/* qv::compute_fap(transition_view(g), hops, seed): values[i] = sum over
+ * k = 0..hops of the k-hop visit mass of a walk started from `seed`
+ * (NULL = uniform 1/|V|), each step a Neumaier-compensated pull in the
+ * reference's edge order — bit-identical to the reference. Seed errors are
+ * ValidationErrors with the reference's messages. */
+int qvb_compute_fap(int device, uint64_t n, uint64_t e, const uint64_t* row_offsets,
+                    const uint64_t* col, const double* weights, uint32_t hops,
+                    const double* seed, double* values);
+
 /* ---- K2: ranking (placement.cpp:79-87) ----------------------------------- */
 /* ranks[i] = feature id of rank i: value descending, id ascending on ties
  * (std::stable_sort order). values/ranks are host (on_device=0) or device. */

@@ -10,6 +10,7 @@
 #include <pthread.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <math.h>
 #include <string.h>
 
 static __thread char g_err[512];
@@ -224,6 +225,68 @@ int qvo_access_prob_sweep_nodes(uint64_t n, const uint64_t* tro, const uint64_t*
     if (nodes[k] >= n) return fail(QVB_ERR_VALIDATION, "node %llu out of range %llu", nodes[k], n);
     out[k] = sweep_node(nodes[k], tro, tcol, tw, rs, prev);
   }
+  return 0;
+}
+
+/* ---- compute_fap (metrics.cpp:95-132), distribution_step (:42-58) ------- */
+static inline void neumaier_add(double* sum, double* comp, double v) { /* numeric.hpp:14-23 */
+  double t = *sum + v;
+  if (fabs(*sum) >= fabs(v)) *comp += (*sum - t) + v;
+  else *comp += (v - t) + *sum;
+  *sum = t;
+}
+
+int qvo_compute_fap(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col,
+                    const double* w, uint32_t hops, const double* seed, double* values) {
+  int rc = qvo_validate(n, e, ro, col, w); /* transition_view validates */
+  if (rc) return rc;
+  double* p0 = (double*)malloc(n * sizeof(double));
+  if (seed) { /* :100-112 */
+    double sum = 0.0, comp = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+      if (!(seed[i] >= 0.0)) {
+        free(p0);
+        return fail(QVB_ERR_VALIDATION, "seed distribution has negative mass%.0llu%.0llu", 0, 0);
+      }
+      neumaier_add(&sum, &comp, seed[i]);
+    }
+    if (fabs((sum + comp) - 1.0) > 1e-12) {
+      free(p0);
+      return fail(QVB_ERR_VALIDATION, "seed distribution does not sum to 1%.0llu%.0llu", 0, 0);
+    }
+    memcpy(p0, seed, n * sizeof(double));
+  } else {
+    for (uint64_t i = 0; i < n; ++i) p0[i] = 1.0 / (double)n;
+  }
+  memcpy(values, p0, n * sizeof(double)); /* hop-0 term */
+  uint64_t* tro = (uint64_t*)malloc((n + 1) * sizeof(uint64_t));
+  uint64_t* tcol = (uint64_t*)malloc((e ? e : 1) * sizeof(uint64_t));
+  double* tw = (double*)malloc((e ? e : 1) * sizeof(double));
+  double* rs = (double*)malloc(n * sizeof(double));
+  double* next = (double*)malloc(n * sizeof(double));
+  qvo_row_sums(n, ro, w, rs);
+  qvo_in_adjacency(n, e, ro, col, w, tro, tcol, tw);
+  double* cur = p0;
+  for (uint32_t k = 1; k <= hops; ++k) {
+    for (uint64_t i = 0; i < n; ++i) {
+      double sum = 0.0, comp = 0.0;
+      for (uint64_t q = tro[i]; q < tro[i + 1]; ++q) {
+        uint64_t j = tcol[q];
+        if (rs[j] > 0.0) neumaier_add(&sum, &comp, cur[j] * tw[q] / rs[j]);
+      }
+      next[i] = sum + comp;
+    }
+    for (uint64_t i = 0; i < n; ++i) values[i] += next[i];
+    double* t = cur;
+    cur = next;
+    next = t;
+  }
+  free(cur == p0 ? next : p0);
+  free(cur);
+  free(tro);
+  free(tcol);
+  free(tw);
+  free(rs);
   return 0;
 }
 

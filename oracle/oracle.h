@@ -53,6 +53,11 @@ int qvo_access_prob_sweep_nodes(uint64_t n, const uint64_t* t_row_offsets, const
                                 const double* t_w, const double* row_sums, const double* prev,
                                 const uint64_t* nodes, uint64_t count, double* out);
 
+/* compute_fap (metrics.cpp:95-132) with distribution_step (:42-58); seed
+ * NULL = uniform. values[n]. */
+int qvo_compute_fap(uint64_t n, uint64_t e, const uint64_t* row_offsets, const uint64_t* col,
+                    const double* w, uint32_t hops, const double* seed, double* values);
+
 /* fap_ranking (placement.cpp:79-87) */
 int qvo_rank_desc(const double* values, uint64_t n, uint64_t* ranks);
 /* plan_placement (placement.cpp:94-226) + the gpu_replicated_capacity

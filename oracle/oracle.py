@@ -113,6 +113,8 @@ class Oracle(_Lib):
         L.qvo_access_prob_sweep_nodes.argtypes = [C.c_uint64, u64p, u64p, f64p, f64p, f64p, u64p,
                                                   C.c_uint64, f64p]
         L.qvo_rank_desc.argtypes = [f64p, C.c_uint64, u64p]
+        L.qvo_compute_fap.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, C.c_uint32,
+                                      C.c_void_p, f64p]
         L.qvo_plan_placement.argtypes = [f64p, C.c_uint64, C.POINTER(Topology), u64p, i64p,
                                          C.c_uint64, C.POINTER(C.c_uint64)]
         L.qvo_build_lookup_table.argtypes = [u64p, i64p, C.c_uint64, C.POINTER(Topology),
@@ -186,6 +188,16 @@ class Oracle(_Lib):
         self._check(self._lib.qvo_access_prob_sweep_nodes(len(tro) - 1, tro, _pad(tcol, np.uint64),
                                                           _pad(tw, np.float64), rs, prev, nodes,
                                                           len(nodes), out))
+        return out
+
+    def compute_fap(self, ro, col, w, hops: int, seed=None):
+        """compute_fap (metrics.cpp:95-132)."""
+        n = len(ro) - 1
+        out = np.zeros(n, np.float64)
+        sd = None if seed is None else np.ascontiguousarray(seed, np.float64)
+        self._check(self._lib.qvo_compute_fap(n, len(col), ro, _pad(col, np.uint64),
+                                              _pad(w, np.float64), hops,
+                                              None if sd is None else sd.ctypes.data, out))
         return out
 
     # placement ---------------------------------------------------------------
@@ -266,6 +278,8 @@ class RefLib(_Lib):
         L.qvr_access_prob.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, C.c_uint32, C.c_int,
                                       f64p, dp]
         L.qvr_in_adjacency.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, u64p, u64p, f64p]
+        L.qvr_compute_fap.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, C.c_uint32, C.c_int,
+                                      C.c_void_p, f64p]
         L.qvr_row_sums.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, f64p]
         L.qvr_plan_placement.argtypes = [f64p, C.c_uint64, C.POINTER(Topology), u64p, i64p,
                                          C.c_uint64, C.POINTER(C.c_uint64), dp]
@@ -295,6 +309,15 @@ class RefLib(_Lib):
                                               _pad(w, np.float64), layers, int(parallel), out,
                                               C.byref(ms)))
         self.last_ms = ms.value
+        return out
+
+    def compute_fap(self, ro, col, w, hops: int, seed=None, parallel: bool = True):
+        n = len(ro) - 1
+        out = np.zeros(n, np.float64)
+        sd = None if seed is None else np.ascontiguousarray(seed, np.float64)
+        self._check(self._lib.qvr_compute_fap(n, len(col), ro, _pad(col, np.uint64),
+                                              _pad(w, np.float64), hops, int(parallel),
+                                              None if sd is None else sd.ctypes.data, out))
         return out
 
     def in_adjacency(self, ro, col, w):

@@ -153,6 +153,19 @@ int qvr_access_prob(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* 
   });
 }
 
+int qvr_compute_fap(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col,
+                    const double* w, uint32_t hops, int parallel, const double* seed,
+                    double* values) {
+  return guard([&] {
+    qv::Graph g = make_graph(n, e, ro, col, w);
+    qv::TransitionView t = qv::transition_view(g);
+    std::optional<std::span<const double>> sd;
+    if (seed) sd = std::span<const double>(seed, n);
+    qv::FapTable f = parallel ? qv::compute_fap(t, hops, sd) : qv::serial::compute_fap(t, hops, sd);
+    std::memcpy(values, f.values.data(), n * sizeof(double));
+  });
+}
+
 int qvr_in_adjacency(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col,
                      const double* w, uint64_t* tro, uint64_t* tcol, double* tw) {
   return guard([&] {

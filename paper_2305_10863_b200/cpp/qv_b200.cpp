@@ -188,10 +188,30 @@ AccessProbTable compute_access_prob_ie(const Graph& g, const TransitionView&,
   return t;
 }
 
+FapTable compute_fap(const TransitionView& t, std::uint32_t hops,
+                     std::optional<std::span<const double>> seed_dist) {
+  const Graph& g = *t.graph;
+  if (seed_dist && seed_dist->size() != g.node_count)
+    throw ValidationError("seed distribution size does not match node count");
+  FapTable f;
+  f.hops = hops;
+  f.values.resize(g.node_count);
+  check(qvb_compute_fap(default_device(), g.node_count, g.edge_count, g.row_offsets.data(),
+                        g.col_indices.data(), g.edge_weights.data(), hops,
+                        seed_dist ? seed_dist->data() : nullptr, f.values.data()));
+  if (seed_dist) f.seed_distribution.assign(seed_dist->begin(), seed_dist->end());
+  else f.seed_distribution.assign(g.node_count, 1.0 / static_cast<double>(g.node_count));
+  return f;
+}
+
 namespace serial {
 AccessProbTable compute_access_prob_ie(const Graph& g, const TransitionView& t,
                                        std::uint32_t layers) {
   return qv::compute_access_prob_ie(g, t, layers);  // one implementation: bit-identical
+}
+FapTable compute_fap(const TransitionView& t, std::uint32_t hops,
+                     std::optional<std::span<const double>> seed_dist) {
+  return qv::compute_fap(t, hops, seed_dist);
 }
 }  // namespace serial
 

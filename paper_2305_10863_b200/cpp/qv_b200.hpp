@@ -114,12 +114,19 @@ struct AccessProbTable {
   std::uint32_t layers = 0;
 };
 
+// FAP visit mass (metrics.cpp:95-132) on the GPU, bit-identical; seed_dist
+// must sum to 1 (1e-12), uniform when absent.
+FapTable compute_fap(const TransitionView& t, std::uint32_t hops,
+                     std::optional<std::span<const double>> seed_dist = {});
+
 // P(n,j) on the GPU, bit-identical to the reference.
 AccessProbTable compute_access_prob_ie(const Graph& g, const TransitionView& t,
                                        std::uint32_t layers);
 namespace serial {
 AccessProbTable compute_access_prob_ie(const Graph& g, const TransitionView& t,
                                        std::uint32_t layers);
+FapTable compute_fap(const TransitionView& t, std::uint32_t hops,
+                     std::optional<std::span<const double>> seed_dist = {});
 }
 
 // ---- topology (topology.hpp:11-54) -------------------------------------------

@@ -574,7 +574,7 @@ void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const
   const uint64_t avg = g.eu ? (g.eu + n - 1) / n : 1;
   g.long_threshold = static_cast<uint32_t>(std::max<uint64_t>(64, 4 * avg));
   const uint32_t thr = g.long_threshold;
-  g.seg_size = segment_size(n);
+  g.seg_size = g.seg_size ? g.seg_size : segment_size(n);
   const uint64_t seg = g.seg_size;
   const int nseg = static_cast<int>((n + seg - 1) / seg);
   if (nseg > 255) fail(QVB_ERR_UNSUPPORTED, "too many source segments (raise QVB_SEG_MB)");
@@ -964,6 +964,92 @@ __global__ void k_transpose_out(const uint32_t* __restrict__ seid, const uint32_
 // in_adjacency (graph.cpp:260-281) on the device: the transposed graph with
 // parallel edges kept, rows in ascending source order (stable sort by
 // destination over the source-major edge order).
+namespace qvb {
+namespace {
+__global__ void k_unit_check(const double* __restrict__ w, uint64_t e, int* __restrict__ non_unit) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < e;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (w[i] != 1.0) *non_unit = 1;
+}
+__global__ void k_gather_weights(const uint32_t* __restrict__ seid, const double* __restrict__ w,
+                                 uint64_t e, double* __restrict__ tw) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < e;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    tw[k] = w[seid[k]];
+}
+__global__ void k_gather_src(const uint32_t* __restrict__ seid, const uint32_t* __restrict__ src,
+                             uint64_t e, uint32_t* __restrict__ tsrc) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < e;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    tsrc[k] = src[seid[k]];
+}
+}  // namespace
+
+void device_transpose(uint64_t n, uint64_t e, const uint64_t* ro_h, const uint64_t* col_h,
+                      const double* w_h, cudaStream_t s, DevBuf<uint64_t>& tptr,
+                      DevBuf<uint32_t>& tsrc, DevBuf<double>& tw, DevBuf<double>& rs,
+                      bool* unit_weights) {
+  DevBuf<uint64_t> ro;
+  DevBuf<uint32_t> dcol;
+  DevBuf<double> dw;
+  upload_out_csr(n, e, ro_h, col_h, w_h, s, ro, dcol, dw);
+  rs.alloc(n, s);
+  {
+    DevBuf<double> inv(n, s);
+    DevBuf<unsigned long long> flag(1, s);
+    QVB_CUDA(cudaMemsetAsync(flag.p, 0xFF, sizeof(unsigned long long), s));
+    k_row_sums<<<grid_for(n, kBlock), kBlock, 0, s>>>(ro.p, dw.p, n, rs.p, inv.p, flag.p);
+    QVB_LAUNCH_CHECK();
+    const unsigned long long z = read_scalar(flag.p, s);
+    if (z != kNone)
+      fail(QVB_ERR_VALIDATION, "node " + std::to_string(z) + " has out-edges but all weights are zero");
+  }
+  *unit_weights = true;
+  if (dw.p && e) {
+    DevBuf<int> nu(1, s);
+    QVB_CUDA(cudaMemsetAsync(nu.p, 0, sizeof(int), s));
+    k_unit_check<<<grid_for(e, kBlock), kBlock, 0, s>>>(dw.p, e, nu.p);
+    QVB_LAUNCH_CHECK();
+    *unit_weights = read_scalar(nu.p, s) == 0;
+  }
+  tptr.alloc(n + 1, s);
+  tsrc.alloc(e ? e : 1, s);
+  if (e == 0) {
+    QVB_CUDA(cudaMemsetAsync(tptr.p, 0, (n + 1) * 8, s));
+    return;
+  }
+  DevBuf<uint32_t> src(e, s);
+  {
+    DevBuf<uint32_t> marks(e, s), incl(e, s), row_of_rank(n, s);
+    QVB_CUDA(cudaMemsetAsync(marks.p, 0, e * sizeof(uint32_t), s));
+    k_row_marks<<<grid_for(n, kBlock), kBlock, 0, s>>>(ro.p, n, e, marks.p);
+    QVB_LAUNCH_CHECK();
+    inclusive_sum_u32_u32(marks.p, incl.p, e, s);
+    k_rank_rows<<<grid_for(n, kBlock), kBlock, 0, s>>>(ro.p, n, incl.p, e, row_of_rank.p);
+    QVB_LAUNCH_CHECK();
+    k_src_from_rank<<<grid_for(e, kBlock), kBlock, 0, s>>>(incl.p, row_of_rank.p, e, src.p);
+    QVB_LAUNCH_CHECK();
+  }
+  DevBuf<uint32_t> sdst(e, s), seid(e, s);
+  {
+    DevBuf<uint32_t> iota(e, s);
+    k_iota<<<grid_for(e, kBlock), kBlock, 0, s>>>(iota.p, e);
+    QVB_LAUNCH_CHECK();
+    sort_pairs_u32_u32(dcol.p, sdst.p, iota.p, seid.p, e, 0, bits_for(n - 1), s);
+  }
+  k_offsets_from_sorted<<<grid_for(e, kBlock), kBlock, 0, s>>>(sdst.p, e, n, tptr.p);
+  QVB_LAUNCH_CHECK();
+  k_gather_src<<<grid_for(e, kBlock), kBlock, 0, s>>>(seid.p, src.p, e, tsrc.p);
+  QVB_LAUNCH_CHECK();
+  if (dw.p) {
+    tw.alloc(e, s);
+    k_gather_weights<<<grid_for(e, kBlock), kBlock, 0, s>>>(seid.p, dw.p, e, tw.p);
+    QVB_LAUNCH_CHECK();
+  }
+}
+
+}  // namespace qvb
+
 extern "C" int qvb_in_adjacency(int device, uint64_t n, uint64_t e, const uint64_t* row_offsets,
                                 const uint64_t* col, const double* weights, uint64_t* t_row_offsets,
                                 uint64_t* t_col, double* t_weights) {

@@ -97,6 +97,16 @@ void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const
 // Segment size in sources: QVB_SEG_MB (default 64) MiB of 8-byte operands.
 uint64_t segment_size(uint64_t n);
 
+// Raw transpose of a host out-CSR on the device (in_adjacency,
+// graph.cpp:260-281): row pointers tptr[n+1], sources tsrc[e] ascending in
+// each row with parallel edges kept in CSR order, carried weights tw[e]
+// (left empty for unit weights), and transition_view's row sums rs[n].
+// Validates like Graph::validate. *unit_weights: every weight is 1.0.
+void device_transpose(uint64_t n, uint64_t e, const uint64_t* ro_h, const uint64_t* col_h,
+                      const double* w_h, cudaStream_t s, DevBuf<uint64_t>& tptr,
+                      DevBuf<uint32_t>& tsrc, DevBuf<double>& tw, DevBuf<double>& rs,
+                      bool* unit_weights);
+
 // Runs layers-1 sweeps; returns the device buffer holding P_layers.
 const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s);
 

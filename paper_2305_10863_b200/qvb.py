@@ -137,6 +137,7 @@ _SIGNATURES = {
     "qvb_graph_destroy": (i32, [vp]),
     "qvb_access_prob": (i32, [vp, u32, vp, i32, vp]),
     "qvb_compute_access_prob_ie": (i32, [i32, u64, u64, vp, vp, vp, u32, vp, vp]),
+    "qvb_compute_fap": (i32, [i32, u64, u64, vp, vp, vp, u32, vp, vp]),
     "qvb_rank_desc": (i32, [i32, vp, u64, vp, i32, vp]),
     "qvb_plan_placement": (i32, [i32, vp, u64, P(Topology), vp, vp, u64, P(u64)]),
     "qvb_build_lookup_table": (i32, [i32, vp, vp, u64, P(Topology), u32, u32, vp, vp]),
@@ -342,6 +343,32 @@ def compute_access_prob_ie(row_offsets, col, weights, layers: int, device: int =
     if timings is not None:
         timings[:] = list(ms)
     return AccessProbTable(out[:n], layers)
+
+
+@dataclass
+class FapTable:
+    """qv::FapTable (metrics.hpp:32-36)."""
+
+    values: np.ndarray
+    hops: int
+    seed_distribution: np.ndarray
+
+
+def compute_fap(row_offsets, col, weights, hops: int, seed=None, device: int = 0) -> FapTable:
+    """qv::compute_fap(transition_view(g), hops, seed) (metrics.cpp:95-132) on the GPU."""
+    ro = np.ascontiguousarray(row_offsets, np.uint64)
+    c = np.ascontiguousarray(col, np.uint64)
+    w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+    n = len(ro) - 1
+    sd = None if seed is None else np.ascontiguousarray(seed, np.float64)
+    if sd is not None and len(sd) != n:
+        raise ValidationError("seed distribution size does not match node count")
+    out = np.zeros(max(n, 1), np.float64)
+    _check(_lib().qvb_compute_fap(device, n, len(c), _ptr(ro), _ptr(c) if len(c) else None,
+                                  _ptr(w) if w is not None and len(w) else None, hops, _ptr(sd),
+                                  _ptr(out)))
+    p0 = sd if sd is not None else np.full(n, 1.0 / n) if n else np.zeros(0)
+    return FapTable(out[:n], hops, p0)
 
 
 # ---- K2 / placement (placement.cpp:79-226) ------------------------------------

@@ -157,6 +157,19 @@ int main() {
                      g.edge_weights.data(), tro.data(), tcol.data(), tw.data());
     CHECK(tg.row_offsets == tro && tg.col_indices == tcol && same_bits(tg.edge_weights, tw));
   }
+  {  // FAP (test_metrics.cpp): the worked example's node 3 has visit mass 1/2 at K=2
+    Graph g = fig8_graph();
+    TransitionView t = transition_view(g);
+    FapTable f = compute_fap(t, 2);
+    CHECK(std::abs(f.values[3] - 0.5) < 1e-12);
+    std::vector<double> exp(g.node_count);
+    qvo_compute_fap(g.node_count, g.edge_count, g.row_offsets.data(), g.col_indices.data(),
+                    g.edge_weights.data(), 2, nullptr, exp.data());
+    CHECK(same_bits(f.values, exp));
+    std::vector<double> bad(g.node_count, 1.0);
+    CHECK_THROWS_AS(compute_fap(t, 2, std::span<const double>(bad)), ValidationError,
+                    "does not sum to 1");
+  }
   {
     Graph g = fig8_graph();
     g.edge_weights[3] = -1.0;

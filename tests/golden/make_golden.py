@@ -105,6 +105,19 @@ def main():
                           "group_transitions": gt.tolist(), "offsets_sha256": digest(oo)}}
     g["c1"] = c1
 
+    # FAP (metrics.cpp:95-132): fig8 at K=1..3, uniform and seeded; C1 hashes
+    n, s, d, w = fig8_edges()
+    ro, col, ww = o.build_csr(n, s, d, w)
+    seed = np.array([0.5, 0.1, 0.1, 0.1, 0.1, 0.1])
+    g["fap_fig8"] = {str(K): hexs(r.compute_fap(ro, col, ww, K)) for K in (0, 1, 2, 3)}
+    g["fap_fig8_seeded"] = {"seed": seed.tolist(),
+                            "values": hexs(r.compute_fap(ro, col, ww, 2, seed))}
+    fc1 = {}
+    for name, weighted in [("uniform_K2", False), ("weighted_K3", True)]:
+        ro, col, ww = o.synthetic_graph(100_000, 1_000_000, 7, weighted, False)
+        fc1[name] = digest(r.compute_fap(ro, col, ww, 2 if not weighted else 3))
+    g["fap_c1"] = fc1
+
     sc = {}
     for name, kw in scenarios().items():
         t = topology_defaults(**kw)

@@ -198,3 +198,35 @@ def test_gather_restatement(oracle):
     assert ids.tolist() == [s.below(1000) for _ in range(500)]
     out = oracle.gather(x, ids, threads=4)
     assert (out == x[ids.astype(np.int64)]).all()
+
+
+def test_fap_golden(oracle):
+    n, s, d, w = fig8_edges()
+    ro, col, ww = oracle.build_csr(n, s, d, w)
+    for K, gold in GOLD["fap_fig8"].items():
+        assert hexs(oracle.compute_fap(ro, col, ww, int(K))) == gold
+    sd = GOLD["fap_fig8_seeded"]
+    assert hexs(oracle.compute_fap(ro, col, ww, 2, np.array(sd["seed"]))) == sd["values"]
+    # test_metrics.cpp worked example: node 3's visit mass is 1/2 at K=2
+    assert abs(oracle.compute_fap(ro, col, ww, 2)[3] - 0.5) < 1e-12
+    for name, weighted in [("uniform_K2", False), ("weighted_K3", True)]:
+        ro, col, ww = oracle.synthetic_graph(100_000, 1_000_000, 7, weighted, False)
+        assert sha(oracle.compute_fap(ro, col, ww, 2 if not weighted else 3)) == GOLD["fap_c1"][name]
+
+
+def test_fap_matches_reference_random(oracle, ref):
+    rng = derive_stream(5, 5)
+    for it in range(30):
+        n, s, d, w = random_edges(rng, 60, 400, it % 2 == 0)
+        ro, col, ww = oracle.build_csr(n, s, d, w)
+        seed = None
+        if it % 3 == 0:
+            x = np.array([rng.uniform() for _ in range(n)])
+            seed = x / x.sum()
+        for hops in range(4):
+            assert (bits(oracle.compute_fap(ro, col, ww, hops, seed)) ==
+                    bits(ref.compute_fap(ro, col, ww, hops, seed))).all()
+    with pytest.raises(Exception, match="negative mass"):
+        oracle.compute_fap(ro, col, ww, 2, -np.ones(len(ro) - 1))
+    with pytest.raises(Exception, match="does not sum to 1"):
+        oracle.compute_fap(ro, col, ww, 2, np.ones(len(ro) - 1))
