@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <span>
 #include <string>
 #include <vector>
@@ -251,6 +252,60 @@ int qvr_plan_reads(const int64_t* location_ids, const uint64_t* offsets, uint64_
       for (uint64_t o : lr.offsets) offsets_out[at++] = o;
     }
     *n_groups = g;
+  });
+}
+
+// ---- file formats (graph.cpp:197-258, metrics.cpp:203-250, placement.cpp:406-459)
+int qvr_save_graph_csr(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col,
+                       const double* w, const char* path) {
+  return guard([&] { qv::save_graph_csr(make_graph(n, e, ro, col, w), path); });
+}
+
+// Two calls: sizes (ro/col/w null), then fill.
+int qvr_load_graph(const char* path, int csr_binary, int remap, uint64_t* n, uint64_t* e,
+                   uint64_t* ro, uint64_t* col, double* w) {
+  return guard([&] {
+    qv::Graph g = qv::load_graph(path, csr_binary ? qv::GraphFormat::csr_binary
+                                                  : qv::GraphFormat::edge_list_text,
+                                 remap != 0);
+    *n = g.node_count;
+    *e = g.edge_count;
+    if (ro) {
+      std::memcpy(ro, g.row_offsets.data(), (g.node_count + 1) * 8);
+      std::memcpy(col, g.col_indices.data(), g.edge_count * 8);
+      std::memcpy(w, g.edge_weights.data(), g.edge_count * 8);
+    }
+  });
+}
+
+int qvr_save_table_binary(const char* path, const double* v, uint64_t n, uint64_t k) {
+  return guard([&] { qv::save_table_binary(path, std::span<const double>(v, n), k); });
+}
+
+int qvr_save_table_csv(const char* path, const double* v, uint64_t n) {
+  return guard([&] { qv::save_table_csv(path, std::span<const double>(v, n)); });
+}
+
+int qvr_placement_exports(const uint64_t* lo, const int64_t* ids, uint64_t n,
+                          const qvb_topology* topo, const char* json_path, const char* csv_path) {
+  return guard([&] {
+    qv::ClusterTopology t = make_topo(topo);
+    qv::PlacementPlan p = make_plan(lo, ids, n, t);
+    std::ofstream(json_path) << qv::placement_to_json_text(p);
+    qv::save_placement_csv(p, csv_path);
+  });
+}
+
+int qvr_lookup_exports(const int64_t* loc, const uint64_t* off, uint64_t n, uint32_t home,
+                       uint32_t gps, const char* json_path, const char* csv_path) {
+  return guard([&] {
+    qv::FeatureLookupTable t;
+    t.home_server = home;
+    t.gpus_per_server = gps;
+    t.location_ids.assign(loc, loc + n);
+    t.offsets.assign(off, off + n);
+    std::ofstream(json_path) << qv::lookup_to_json_text(t);
+    qv::save_lookup_csv(t, csv_path);
   });
 }
 

@@ -4,9 +4,12 @@
 #include "qv_b200.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <map>
 #include <numeric>
+#include <sstream>
 
 #include "../../include/qvb.h"
 
@@ -416,6 +419,225 @@ FetchCost fetch_cost(const ReadPlan& plan, const ClusterTopology& topo,
     cost.total_s = std::max(cost.total_s, lat);
   }
   return cost;
+}
+
+// ---- on-disk formats ----------------------------------------------------------------
+namespace {
+constexpr char kCsrMagic[6] = {'Q', 'V', 'C', 'S', 'R', '1'};
+constexpr char kTabMagic[6] = {'Q', 'V', 'T', 'A', 'B', '1'};
+
+template <typename T>
+void read_pod(std::ifstream& in, T* p, std::size_t n, const std::string& path, const char* what) {
+  in.read(reinterpret_cast<char*>(p), static_cast<std::streamsize>(sizeof(T) * n));
+  if (!in) throw ParseError(path + what);
+}
+
+Graph load_edge_list(const std::string& path, bool remap) {
+  std::ifstream in(path);
+  if (!in) throw ParseError("cannot open graph file: " + path);
+  std::vector<Edge> edges;
+  std::string line;
+  std::uint64_t line_no = 0;
+  NodeId max_id = 0;
+  while (std::getline(in, line)) {
+    ++line_no;
+    const auto hash = line.find('#');
+    if (hash != std::string::npos) line.resize(hash);
+    std::istringstream ls(line);
+    std::uint64_t src, dst;
+    if (!(ls >> src)) {
+      std::string left;
+      std::istringstream probe(line);
+      if (probe >> left)
+        throw ParseError(path + ":" + std::to_string(line_no) + ": malformed edge line: '" + line + "'");
+      continue;
+    }
+    if (!(ls >> dst))
+      throw ParseError(path + ":" + std::to_string(line_no) + ": malformed edge line: '" + line + "'");
+    double w = 1.0;
+    std::string rest;
+    if (ls >> rest) {
+      try {
+        std::size_t used = 0;
+        w = std::stod(rest, &used);
+        if (used != rest.size()) throw std::invalid_argument(rest);
+      } catch (const std::exception&) {
+        throw ParseError(path + ":" + std::to_string(line_no) + ": malformed weight '" + rest + "'");
+      }
+      std::string extra;
+      if (ls >> extra)
+        throw ParseError(path + ":" + std::to_string(line_no) +
+                         ": trailing tokens after weight: '" + extra + "'");
+    }
+    edges.push_back({src, dst, w});
+    max_id = std::max(max_id, std::max(src, dst));
+  }
+  if (edges.empty()) throw ValidationError("empty graph: no edges in " + path);
+  std::uint64_t n = max_id + 1;
+  std::vector<bool> present(n, false);
+  for (const Edge& e : edges) present[e.src] = present[e.dst] = true;
+  if (!std::all_of(present.begin(), present.end(), [](bool b) { return b; })) {
+    if (!remap)
+      throw ValidationError(path + ": node ids are not contiguous 0..N-1 (use id remapping "
+                                   "for sparse-id inputs)");
+    std::vector<NodeId> map(n, 0);
+    NodeId next = 0;
+    for (NodeId i = 0; i < n; ++i)
+      if (present[i]) map[i] = next++;
+    for (Edge& e : edges) {
+      e.src = map[e.src];
+      e.dst = map[e.dst];
+    }
+    n = next;
+  }
+  return Graph::from_edges(n, edges);
+}
+
+void json_escape_free_write(std::ostringstream& o, int indent) {
+  for (int i = 0; i < indent; ++i) o << ' ';
+}
+}  // namespace
+
+Graph load_graph(const std::string& path, GraphFormat format, bool remap_sparse_ids) {
+  if (format == GraphFormat::edge_list_text) return load_edge_list(path, remap_sparse_ids);
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw ParseError("cannot open graph file: " + path);
+  char magic[6];
+  read_pod(in, magic, 6, path, ": truncated csr-binary file");
+  if (std::memcmp(magic, kCsrMagic, 6) != 0) throw ParseError(path + ": bad magic, not a QVCSR1 file");
+  Graph g;
+  read_pod(in, &g.node_count, 1, path, ": truncated csr-binary file");
+  read_pod(in, &g.edge_count, 1, path, ": truncated csr-binary file");
+  if (g.node_count == 0) throw ValidationError("empty graph in " + path);
+  g.row_offsets.resize(g.node_count + 1);
+  g.col_indices.resize(g.edge_count);
+  g.edge_weights.resize(g.edge_count);
+  read_pod(in, g.row_offsets.data(), g.row_offsets.size(), path, ": truncated csr-binary file");
+  read_pod(in, g.col_indices.data(), g.col_indices.size(), path, ": truncated csr-binary file");
+  read_pod(in, g.edge_weights.data(), g.edge_weights.size(), path, ": truncated csr-binary file");
+  g.validate();
+  return g;
+}
+
+void save_graph_csr(const Graph& g, const std::string& path) {
+  std::ofstream out(path, std::ios::binary | std::ios::trunc);
+  if (!out) throw Error("cannot write graph file: " + path);
+  out.write(kCsrMagic, 6);
+  out.write(reinterpret_cast<const char*>(&g.node_count), 8);
+  out.write(reinterpret_cast<const char*>(&g.edge_count), 8);
+  out.write(reinterpret_cast<const char*>(g.row_offsets.data()), g.row_offsets.size() * 8);
+  out.write(reinterpret_cast<const char*>(g.col_indices.data()), g.col_indices.size() * 8);
+  out.write(reinterpret_cast<const char*>(g.edge_weights.data()), g.edge_weights.size() * 8);
+  if (!out) throw Error("short write to " + path);
+}
+
+void save_table_binary(const std::string& path, std::span<const double> values, std::uint64_t k) {
+  std::ofstream out(path, std::ios::binary | std::ios::trunc);
+  if (!out) throw Error("cannot write table file: " + path);
+  const std::uint64_t n = values.size();
+  out.write(kTabMagic, 6);
+  out.write(reinterpret_cast<const char*>(&n), 8);
+  out.write(reinterpret_cast<const char*>(&k), 8);
+  out.write(reinterpret_cast<const char*>(values.data()), n * 8);
+  if (!out) throw Error("short write to " + path);
+}
+
+LoadedTable load_table_binary(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw ParseError("cannot open table file: " + path);
+  char magic[6];
+  in.read(magic, 6);
+  if (!in || std::memcmp(magic, kTabMagic, 6) != 0) throw ParseError(path + ": bad magic, not a QVTAB1 file");
+  std::uint64_t n = 0;
+  LoadedTable t;
+  in.read(reinterpret_cast<char*>(&n), 8);
+  in.read(reinterpret_cast<char*>(&t.k), 8);
+  if (!in) throw ParseError(path + ": truncated table header");
+  t.values.resize(n);
+  in.read(reinterpret_cast<char*>(t.values.data()), n * 8);
+  if (!in) throw ParseError(path + ": truncated table values");
+  return t;
+}
+
+void save_table_csv(const std::string& path, std::span<const double> values) {
+  std::ofstream out(path, std::ios::trunc);
+  if (!out) throw Error("cannot write csv file: " + path);
+  out << "node_id,value\n";
+  char buf[64];
+  for (std::size_t i = 0; i < values.size(); ++i) {
+    std::snprintf(buf, sizeof buf, "%zu,%.17g\n", i, values[i]);
+    out << buf;
+  }
+  if (!out) throw Error("short write to " + path);
+}
+
+std::string placement_to_json_text(const PlacementPlan& plan) {
+  // nlohmann ordered_json::dump(2) layout (placement.cpp:406-422)
+  std::ostringstream o;
+  o << "{\n  \"feature_count\": " << plan.feature_count << ",\n  \"features\": ";
+  if (plan.feature_count == 0) o << "[]";
+  else {
+    o << "[\n";
+    for (std::uint64_t f = 0; f < plan.feature_count; ++f) {
+      o << "    {\n      \"id\": " << f << ",\n      \"locations\": ";
+      const auto& locs = plan.locations[f];
+      if (locs.empty()) o << "[]";
+      else {
+        o << "[\n";
+        for (std::size_t i = 0; i < locs.size(); ++i) {
+          const Location& l = locs[i];
+          json_escape_free_write(o, 8);
+          o << "{\n          \"server\": " << l.server << ",\n          \"tier\": \""
+            << tier_name(l.tier) << "\",\n          \"device\": " << l.device
+            << ",\n          \"replica\": " << (l.replica ? "true" : "false") << "\n        }"
+            << (i + 1 < locs.size() ? ",\n" : "\n");
+        }
+        o << "      ]";
+      }
+      o << "\n    }" << (f + 1 < plan.feature_count ? ",\n" : "\n");
+    }
+    o << "  ]";
+  }
+  o << "\n}\n";
+  return o.str();
+}
+
+void save_placement_csv(const PlacementPlan& plan, const std::string& path) {
+  std::ofstream out(path, std::ios::trunc);
+  if (!out) throw Error("cannot write csv file: " + path);
+  out << "feature_id,server,tier,device,replica\n";
+  for (std::uint64_t f = 0; f < plan.feature_count; ++f)
+    for (const Location& l : plan.locations[f])
+      out << f << ',' << l.server << ',' << tier_name(l.tier) << ',' << l.device << ','
+          << (l.replica ? 1 : 0) << '\n';
+  if (!out) throw Error("short write to " + path);
+}
+
+std::string lookup_to_json_text(const FeatureLookupTable& table) {
+  // nlohmann ordered_json::dump(2) layout (placement.cpp:437-449)
+  std::ostringstream o;
+  o << "{\n  \"home_server\": " << table.home_server << ",\n  \"gpus_per_server\": "
+    << table.gpus_per_server << ",\n  \"rows\": ";
+  const std::size_t n = table.location_ids.size();
+  if (n == 0) o << "[]";
+  else {
+    o << "[\n";
+    for (std::size_t f = 0; f < n; ++f)
+      o << "    {\n      \"feature\": " << f << ",\n      \"location\": " << table.location_ids[f]
+        << ",\n      \"offset\": " << table.offsets[f] << "\n    }" << (f + 1 < n ? ",\n" : "\n");
+    o << "  ]";
+  }
+  o << "\n}\n";
+  return o.str();
+}
+
+void save_lookup_csv(const FeatureLookupTable& table, const std::string& path) {
+  std::ofstream out(path, std::ios::trunc);
+  if (!out) throw Error("cannot write csv file: " + path);
+  out << "feature_id,location_id,offset\n";
+  for (std::size_t f = 0; f < table.location_ids.size(); ++f)
+    out << f << ',' << table.location_ids[f] << ',' << table.offsets[f] << '\n';
+  if (!out) throw Error("short write to " + path);
 }
 
 // ---- feature store ----------------------------------------------------------------

@@ -229,6 +229,23 @@ struct FetchCost {
 FetchCost fetch_cost(const ReadPlan& plan, const ClusterTopology& topo,
                      std::uint64_t feature_bytes, std::optional<DeviceRef> reader = {});
 
+// ---- on-disk formats (graph.cpp:197-258, metrics.cpp:203-250,
+//      placement.cpp:406-459), byte-compatible with the reference ------------
+enum class GraphFormat { edge_list_text, csr_binary };
+Graph load_graph(const std::string& path, GraphFormat format, bool remap_sparse_ids = false);
+void save_graph_csr(const Graph& g, const std::string& path);
+void save_table_binary(const std::string& path, std::span<const double> values, std::uint64_t k);
+struct LoadedTable {
+  std::vector<double> values;
+  std::uint64_t k = 0;
+};
+LoadedTable load_table_binary(const std::string& path);
+void save_table_csv(const std::string& path, std::span<const double> values);
+std::string placement_to_json_text(const PlacementPlan& plan);
+void save_placement_csv(const PlacementPlan& plan, const std::string& path);
+std::string lookup_to_json_text(const FeatureLookupTable& table);
+void save_lookup_csv(const FeatureLookupTable& table, const std::string& path);
+
 // ---- feature store (new: the collect the reference only models) ---------------
 class FeatureStore {
  public:

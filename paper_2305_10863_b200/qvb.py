@@ -40,6 +40,10 @@ class PlacementError(Error):
     """qv::PlacementError"""
 
 
+class ParseError(Error):
+    """qv::ParseError (file formats; error.hpp:14-16)"""
+
+
 class CudaError(Error):
     """CUDA failure or no usable device (the library has no CPU fallback)."""
 

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <set>
 #include <string>
 #include <vector>
@@ -18,6 +19,7 @@
 using namespace qv;
 
 static int g_checks = 0, g_fail = 0;
+static const char* g_outdir = nullptr;
 #define CHECK(x)                                                            \
   do {                                                                      \
     ++g_checks;                                                             \
@@ -121,7 +123,8 @@ ClusterTopology two_servers(bool ib) {
 
 }  // namespace
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) g_outdir = argv[1];
   // --- P(n,j): test_metrics.cpp:136-235 --------------------------------------
   {
     Graph g = fig8_graph();
@@ -199,6 +202,23 @@ int main() {
     // SURVEY §8(c) golden: f0(0,0) f1(1,0) f2(4,0) f3(4,1) f4(4,2)
     CHECK((table.location_ids == std::vector<int64_t>{0, 1, 4, 4, 4}));
     CHECK((table.offsets == std::vector<uint64_t>{0, 0, 0, 1, 2}));
+    if (g_outdir) {  // reference-format exports, compared with golden texts by the test
+      const std::string d = g_outdir;
+      std::ofstream(d + "/placement_b.json") << placement_to_json_text(plan);
+      save_placement_csv(plan, d + "/placement_b.csv");
+      std::ofstream(d + "/lookup_b.json") << lookup_to_json_text(table);
+      save_lookup_csv(table, d + "/lookup_b.csv");
+      Graph f8 = fig8_graph();
+      save_graph_csr(f8, d + "/fig8.qvcsr");
+      Graph back = load_graph(d + "/fig8.qvcsr", GraphFormat::csr_binary);
+      CHECK(back.row_offsets == f8.row_offsets && back.col_indices == f8.col_indices);
+      std::vector<double> tab = {0.5, 1.0 / 3.0, 1e-300, 12345.678};
+      save_table_binary(d + "/table.qvtab", tab, 2);
+      save_table_csv(d + "/table.csv", tab);
+      LoadedTable lt = load_table_binary(d + "/table.qvtab");
+      CHECK(lt.k == 2 && same_bits(lt.values, tab));
+      CHECK_THROWS_AS(load_graph(d + "/table.qvtab", GraphFormat::csr_binary), ParseError, "bad magic");
+    }
     std::vector<NodeId> ids = {4, 1, 0, 3, 1};
     ReadPlan rp = plan_reads(table, ids, 2);
     CHECK(rp.per_location.size() == 3);

@@ -130,6 +130,27 @@ def main():
         sc[name] = ent
     g["scenarios"] = sc
 
+    # reference export texts of scenario (b) (placement.cpp:406-459)
+    import ctypes as C
+    import tempfile
+
+    L = r._lib
+    u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+    i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+    L.qvr_placement_exports.argtypes = [u64p, i64p, C.c_uint64, C.c_void_p, C.c_char_p, C.c_char_p]
+    L.qvr_lookup_exports.argtypes = [i64p, u64p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_char_p,
+                                     C.c_char_p]
+    tb = topology_defaults(**scenarios()["b"])
+    lo, ids = r.plan_placement(five_features(), tb)
+    loc, off = r.build_lookup_table(lo, ids, tb, 0)
+    with tempfile.TemporaryDirectory() as d:
+        pj, pc, lj, lc = (os.path.join(d, x) for x in ("p.json", "p.csv", "l.json", "l.csv"))
+        L.qvr_placement_exports(lo, ids, len(lo) - 1, C.addressof(tb), pj.encode(), pc.encode())
+        L.qvr_lookup_exports(loc, off, len(loc), 0, tb.gpus_per_server, lj.encode(), lc.encode())
+        g["exports_b"] = {k: open(p).read() for k, p in
+                          [("placement_json", pj), ("placement_csv", pc), ("lookup_json", lj),
+                           ("lookup_csv", lc)]}
+
     # "short by 3" (test_placement.cpp:138-145)
     t = topology_defaults(**dict(scenarios()["c"], disk_feature_capacity=0, host_feature_capacity=1))
     try:

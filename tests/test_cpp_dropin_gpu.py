@@ -31,9 +31,30 @@ def test_dropin_compiles_against_headers():
 
 
 @pytest.mark.gpu
-def test_dropin_reference_cases(qvb):
+def test_dropin_reference_cases(qvb, tmp_path):
+    import json
+
+    import numpy as np
+
+    from paper_2305_10863_b200 import formats as F
+    from tests.util import fig8_edges
+
     exe = build_test_binary()
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=600)
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stderr
     assert "0 failed" in r.stdout
+    # the C++ exports are byte-identical to the reference's own (golden texts)
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))["exports_b"]
+    for name, key in [("placement_b.json", "placement_json"), ("placement_b.csv", "placement_csv"),
+                      ("lookup_b.json", "lookup_json"), ("lookup_b.csv", "lookup_csv")]:
+        assert open(tmp_path / name).read() == gold[key], name
+    n, s, d, w = fig8_edges()
+    ro, col, ww = F.from_edges(n, s, d, w)
+    F.save_graph_csr(str(tmp_path / "py.qvcsr"), ro, col, ww)
+    assert open(tmp_path / "py.qvcsr", "rb").read() == open(tmp_path / "fig8.qvcsr", "rb").read()
+    tab = np.array([0.5, 1.0 / 3.0, 1e-300, 12345.678])
+    F.save_table_binary(str(tmp_path / "py.qvtab"), tab, 2)
+    F.save_table_csv(str(tmp_path / "py.csv"), tab)
+    assert open(tmp_path / "py.qvtab", "rb").read() == open(tmp_path / "table.qvtab", "rb").read()
+    assert open(tmp_path / "py.csv").read() == open(tmp_path / "table.csv").read()
