@@ -193,6 +193,78 @@ __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
   }
 }
 
+// Rows that are 8-byte but not 16-byte multiples (e.g. 602 fp32 = 2408 B):
+// the shard stride is 64-byte aligned, so the source side still moves 16-byte
+// vectors; the destination rows are only 8-byte aligned, so every 16-byte
+// chunk is stored as two 8-byte halves (the row's last chunk keeps one).
+template <int kU, int kMinBlocks>
+__global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
+    k_gather_rows_w(const uint64_t* __restrict__ ids, uint64_t rows,
+                    const uint64_t* __restrict__ lut, Bases bases, uint64_t stride, uint32_t cpr,
+                    uint32_t row_bytes, uint64_t n, char* __restrict__ out,
+                    unsigned long long* err) {
+  using V = Vec<16>;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t groups = (rows + 31) / 32;
+  const uint32_t q32 = 32 / cpr, r32 = 32 % cpr;
+  const uint32_t row0 = lane / cpr, k0 = lane - row0 * cpr;
+  auto load_id = [&](uint64_t g) -> uint64_t {
+    const uint64_t r = g * 32 + lane;
+    return (g < groups && r < rows) ? __ldg(ids + r) : ~0ull;
+  };
+  auto resolve = [&](uint64_t g, uint64_t f) -> uint64_t {
+    const uint64_t r = g * 32 + lane;
+    if (g >= groups || r >= rows) return 0;
+    if (f >= n) {
+      atomicMin(err, (unsigned long long)r);
+      return 0;
+    }
+    const uint64_t e = __ldg(lut + f);
+    return reinterpret_cast<uint64_t>(bases.p[e >> kOffsetBits]) + (e & kOffsetMask) * stride;
+  };
+  uint64_t g = warp;
+  uint64_t src = resolve(g, load_id(g));
+  uint64_t id_next = load_id(g + nwarps);
+  for (; g < groups; g += nwarps) {
+    const uint64_t src_next = resolve(g + nwarps, id_next);
+    id_next = load_id(g + 2 * nwarps);
+    const uint32_t nr = static_cast<uint32_t>(rows - g * 32 < 32 ? rows - g * 32 : 32);
+    const uint32_t tot = nr * cpr;
+    char* out0 = out + g * 32 * (uint64_t)row_bytes;
+    uint32_t row = row0, k = k0;
+    for (uint32_t cb = 0; cb < tot; cb += 32 * kU) {
+      typename V::T v[kU];
+      uint64_t dst[kU];
+      bool ok[kU], half[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t c = cb + lane + u * 32;
+        const uint64_t s = __shfl_sync(0xffffffffu, src, row < 32 ? row : 31);
+        ok[u] = c < tot && s != 0;
+        half[u] = (k + 1) * 16 > row_bytes;
+        dst[u] = (uint64_t)row * row_bytes + (uint64_t)k * 16;
+        if (ok[u]) v[u] = V::load(reinterpret_cast<const char*>(s) + (uint64_t)k * 16);
+        row += q32;
+        k += r32;
+        if (k >= cpr) {
+          k -= cpr;
+          ++row;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (!ok[u]) continue;
+        uint2* d = reinterpret_cast<uint2*>(out0 + dst[u]);
+        d[0] = make_uint2(v[u].x, v[u].y);
+        if (!half[u]) d[1] = make_uint2(v[u].z, v[u].w);
+      }
+    }
+    src = src_next;
+  }
+}
+
 // Planned gather: sorted (location, offset) keys with the request index as
 // payload (K4 order); no lookup-table read in the copy loop.
 template <int VEC>
@@ -332,6 +404,7 @@ struct qvb_store {
     }();
     if (!flat) {
       if (V == 16) launch_rows<16>(ids, b, cpr, out, s);
+      else if (V == 8 && stride % 16 == 0) launch_rows_wide(ids, b, out, s);
       else if (V == 8) launch_rows<8>(ids, b, cpr, out, s);
       else launch_rows<4>(ids, b, cpr, out, s);
       return;
@@ -372,6 +445,18 @@ struct qvb_store {
     else if (variant == 4) launch_rows_u<V, 4, 4>(ids, rows, cpr, o, s);
     else if (variant == 2) launch_rows_u<V, 2, 6>(ids, rows, cpr, o, s);
     else launch_rows_u<V, 4, 4>(ids, rows, cpr, o, s);
+  }
+
+  void launch_rows_wide(const uint64_t* ids, uint64_t rows, char* o, cudaStream_t s) {
+    static unsigned full = 0;
+    if (!full) full = resident_grid(k_gather_rows_w<4, 4>, kGatherBlock, 0, ~0ull);
+    const uint32_t cpr16 = (row_bytes + 15) / 16;
+    const uint64_t warps_needed = (rows + 31) / 32;
+    const uint64_t blocks = (warps_needed + kGatherBlock / 32 - 1) / (kGatherBlock / 32);
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(full, blocks));
+    k_gather_rows_w<4, 4><<<grid, kGatherBlock, 0, s>>>(ids, rows, lut, bases, stride, cpr16,
+                                                         row_bytes, n, o, err);
+    QVB_LAUNCH_CHECK();
   }
 
   template <int V, int U, int MB>
