@@ -265,6 +265,109 @@ __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
   }
 }
 
+// TMA bulk-copy gather (rows that are 16-byte multiples, device-resident
+// sources): each lane owns one request of a 32-row group; it issues one
+// cp.async.bulk global->shared copy of its row (completion counted on the
+// group's mbarrier) and, once the group has landed, one cp.async.bulk
+// shared->global copy to the output row. Two row buffers per warp let the
+// next group's loads overlap the previous group's stores; no row data ever
+// passes through registers, so every SM keeps hundreds of rows in flight.
+constexpr int kTmaBuffers = 3;  // per warp: 2 groups of loads + 1 of stores in flight
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(256)
+    k_gather_tma(const uint64_t* __restrict__ ids, uint64_t rows, const uint64_t* __restrict__ lut,
+                 Bases bases, uint64_t stride, uint32_t row_bytes, uint64_t n,
+                 char* __restrict__ out, unsigned long long* err) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int NB = kTmaBuffers;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t warps = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // NB per warp
+  unsigned char* buf = smem + 8 * NB * warps + (128 - (8 * NB * warps) % 128) % 128;
+  if (lane == 0) {
+    for (int i = 0; i < NB; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[NB * wid + i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t groups = (rows + 31) / 32;
+  uint32_t phases = 0;  // bit i: parity to wait for on buffer i
+  // group j of this warp is global group warp + j*nwarps, buffer j % NB
+  auto resolve = [&](uint64_t j) -> uint64_t {
+    const uint64_t g = warp + j * nwarps;
+    const uint64_t r = g * 32 + lane;
+    if (g >= groups || r >= rows) return 0;
+    const uint64_t f = __ldg(ids + r);
+    if (f >= n) {
+      atomicMin(err, (unsigned long long)r);
+      return 0;
+    }
+    const uint64_t e = __ldg(lut + f);
+    return reinterpret_cast<uint64_t>(bases.p[e >> kOffsetBits]) + (e & kOffsetMask) * stride;
+  };
+  auto issue_loads = [&](uint64_t j, uint64_t src) {
+    const int bi = static_cast<int>(j % NB);
+    const uint32_t bar = smem_addr(&bars[NB * wid + bi]);
+    const uint32_t valid = __popc(__ballot_sync(0xffffffffu, src != 0));
+    if (valid == 0) return;
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"(valid * row_bytes)
+                   : "memory");
+    __syncwarp();
+    if (src) {
+      const uint32_t slot = smem_addr(buf + ((uint64_t)(NB * wid + bi) * 32 + lane) * row_bytes);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              slot),
+          "l"(src), "r"(row_bytes), "r"(bar)
+          : "memory");
+    }
+  };
+  const uint64_t mine = warp < groups ? (groups - warp + nwarps - 1) / nwarps : 0;
+  uint64_t srcs[NB];
+  for (int j = 0; j < NB - 1; ++j) {  // prologue: NB-1 groups of loads in flight
+    srcs[j] = resolve(j);
+    issue_loads(j, srcs[j]);
+  }
+  for (uint64_t j = 0; j < mine; ++j) {
+    const int bi = static_cast<int>(j % NB);
+    const uint64_t src = srcs[bi];
+    const uint32_t valid = __popc(__ballot_sync(0xffffffffu, src != 0));
+    if (valid) {
+      asm volatile(
+          "{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+          " @!p bra W_%=;\n}" ::"r"(smem_addr(&bars[NB * wid + bi])),
+          "r"((phases >> bi) & 1u)
+          : "memory");
+      phases ^= 1u << bi;
+      if (src) {
+        const uint64_t r = (warp + j * nwarps) * 32 + lane;
+        const uint32_t slot = smem_addr(buf + ((uint64_t)(NB * wid + bi) * 32 + lane) * row_bytes);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                         out + r * (uint64_t)row_bytes),
+                     "r"(slot), "r"(row_bytes)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    // the next loads reuse the buffer whose stores were committed NB-1 groups ago
+    const uint64_t jn = j + NB - 1;
+    const uint64_t s_next = resolve(jn);
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NB - 2) : "memory");
+    __syncwarp();
+    srcs[jn % NB] = s_next;
+    issue_loads(jn, s_next);
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // Planned gather: sorted (location, offset) keys with the request index as
 // payload (K4 order); no lookup-table read in the copy loop.
 template <int VEC>
@@ -398,11 +501,18 @@ struct qvb_store {
       fail(QVB_ERR_VALIDATION, "output buffer is not aligned to the row vector width");
     const int V = vec();
     const uint32_t cpr = row_bytes / V;
-    static const bool flat = [] {
+    static const int kind = [] {  // 0 rows (default), 1 flat, 2 tma
       const char* k = std::getenv("QVB_GATHER_KERNEL");
-      return k && std::string(k) == "flat";
+      if (!k) return 0;
+      const std::string v(k);
+      return v == "flat" ? 1 : (v == "tma" ? 2 : 0);
     }();
-    if (!flat) {
+    const bool host_used = (used_mask >> (nloc - 2)) & 1;
+    if (kind == 2 && row_bytes % 16 == 0 && !host_used) {
+      launch_tma(ids, b, out, s);
+      return;
+    }
+    if (kind != 1) {
       if (V == 16) launch_rows<16>(ids, b, cpr, out, s);
       else if (V == 8 && stride % 16 == 0) launch_rows_wide(ids, b, out, s);
       else if (V == 8) launch_rows<8>(ids, b, cpr, out, s);
@@ -445,6 +555,30 @@ struct qvb_store {
     else if (variant == 4) launch_rows_u<V, 4, 4>(ids, rows, cpr, o, s);
     else if (variant == 2) launch_rows_u<V, 2, 6>(ids, rows, cpr, o, s);
     else launch_rows_u<V, 4, 4>(ids, rows, cpr, o, s);
+  }
+
+  void launch_tma(const uint64_t* ids, uint64_t rows, char* o, cudaStream_t s) {
+    const uint64_t per_warp = (uint64_t)kTmaBuffers * 32 * row_bytes;
+    const uint32_t warps = static_cast<uint32_t>(
+        std::max<uint64_t>(1, std::min<uint64_t>(8, (200u << 10) / per_warp)));
+    const size_t smem = 8 * kTmaBuffers * warps + 128 + (size_t)warps * per_warp;
+    if (smem > (227u << 10)) fail(QVB_ERR_UNSUPPORTED, "row too large for the TMA gather");
+    static size_t configured = 0;
+    if (configured < smem) {
+      QVB_CUDA(cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      configured = smem;
+    }
+    int per_sm = 0, dev = 0, sms = 0;
+    QVB_CUDA(cudaGetDevice(&dev));
+    QVB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    QVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_tma, warps * 32, smem));
+    const uint64_t groups = (rows + 31) / 32;
+    const uint64_t blocks = std::min<uint64_t>((uint64_t)std::max(per_sm, 1) * sms,
+                                               (groups + warps - 1) / warps);
+    k_gather_tma<<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(ids, rows, lut, bases,
+                                                                        stride, row_bytes, n, o, err);
+    QVB_LAUNCH_CHECK();
   }
 
   void launch_rows_wide(const uint64_t* ids, uint64_t rows, char* o, cudaStream_t s) {
