@@ -272,6 +272,91 @@ __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
 // shared->global copy to the output row. Two row buffers per warp let the
 // next group's loads overlap the previous group's stores; no row data ever
 // passes through registers, so every SM keeps hundreds of rows in flight.
+// cp.async (LDGSTS) row-group gather for rows of <= 512 B in 16-byte chunks:
+// the loads of group j+1 land in shared memory (no registers held) while
+// group j is written out, so each SM keeps ~100 KB of rows in flight. Every
+// lane reads back only the slots it filled itself (layout [buffer][m][lane]),
+// so no cross-lane synchronisation is needed.
+__global__ void __launch_bounds__(256)
+    k_gather_cp(const uint64_t* __restrict__ ids, uint64_t rows, const uint64_t* __restrict__ lut,
+                Bases bases, uint64_t stride, uint32_t cpr, uint32_t row_bytes, uint64_t n,
+                char* __restrict__ out, unsigned long long* err) {
+  extern __shared__ __align__(128) uint4 slots[];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint4* mine = slots + (uint64_t)wid * 2 * cpr * 32;  // [2][cpr][32]
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t groups = (rows + 31) / 32;
+  const uint32_t q32 = 32 / cpr, r32 = 32 % cpr;
+  const uint32_t row0 = lane / cpr, k0 = lane - row0 * cpr;
+  auto resolve = [&](uint64_t g) -> uint64_t {
+    const uint64_t r = g * 32 + lane;
+    if (g >= groups || r >= rows) return 0;
+    const uint64_t f = __ldg(ids + r);
+    if (f >= n) {
+      atomicMin(err, (unsigned long long)r);
+      return 0;
+    }
+    const uint64_t e = __ldg(lut + f);
+    return reinterpret_cast<uint64_t>(bases.p[e >> kOffsetBits]) + (e & kOffsetMask) * stride;
+  };
+  // issue this lane's chunks of group g into buffer b
+  auto issue = [&](uint64_t g, uint64_t src, int b) {
+    if (g >= groups) return;
+    const uint32_t nr = static_cast<uint32_t>(rows - g * 32 < 32 ? rows - g * 32 : 32);
+    const uint32_t tot = nr * cpr;
+    uint32_t row = row0, k = k0;
+    for (uint32_t m = 0; m < cpr; ++m) {
+      const uint32_t c = lane + 32 * m;
+      const uint64_t s = __shfl_sync(0xffffffffu, src, row < 32 ? row : 31);
+      if (c < tot && s) {
+        const uint32_t dst = static_cast<uint32_t>(
+            __cvta_generic_to_shared(mine + ((uint64_t)b * cpr + m) * 32 + lane));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                     "l"(s + (uint64_t)k * 16)
+                     : "memory");
+      }
+      row += q32;
+      k += r32;
+      if (k >= cpr) {
+        k -= cpr;
+        ++row;
+      }
+    }
+  };
+  uint64_t g = warp;
+  uint64_t src = resolve(g);
+  issue(g, src, 0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  int b = 0;
+  for (; g < groups; g += nwarps, b ^= 1) {
+    const uint64_t gn = g + nwarps;
+    const uint64_t sn = resolve(gn);
+    issue(gn, sn, b ^ 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // group g has landed
+    const uint32_t nr = static_cast<uint32_t>(rows - g * 32 < 32 ? rows - g * 32 : 32);
+    const uint32_t tot = nr * cpr;
+    const bool ok_row = true;
+    uint4* dst0 = reinterpret_cast<uint4*>(out + g * 32 * (uint64_t)row_bytes);
+    uint32_t row = row0;
+    uint32_t k = k0;
+    for (uint32_t m = 0; m < cpr; ++m) {
+      const uint32_t c = lane + 32 * m;
+      const uint64_t s = __shfl_sync(0xffffffffu, src, row < 32 ? row : 31);
+      if (c < tot && s && ok_row) dst0[c] = mine[((uint64_t)b * cpr + m) * 32 + lane];
+      row += q32;
+      k += r32;
+      if (k >= cpr) {
+        k -= cpr;
+        ++row;
+      }
+    }
+    src = sn;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 constexpr int kTmaBuffers = 3;  // per warp: 2 groups of loads + 1 of stores in flight
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -505,9 +590,13 @@ struct qvb_store {
       const char* k = std::getenv("QVB_GATHER_KERNEL");
       if (!k) return 0;
       const std::string v(k);
-      return v == "flat" ? 1 : (v == "tma" ? 2 : 0);
+      return v == "flat" ? 1 : (v == "tma" ? 2 : (v == "cp" ? 3 : 0));
     }();
     const bool host_used = (used_mask >> (nloc - 2)) & 1;
+    if (kind == 3 && row_bytes % 16 == 0 && row_bytes <= 512) {
+      launch_cp(ids, b, out, s);
+      return;
+    }
     if (kind == 2 && row_bytes % 16 == 0 && !host_used) {
       launch_tma(ids, b, out, s);
       return;
@@ -555,6 +644,30 @@ struct qvb_store {
     else if (variant == 4) launch_rows_u<V, 4, 4>(ids, rows, cpr, o, s);
     else if (variant == 2) launch_rows_u<V, 2, 6>(ids, rows, cpr, o, s);
     else launch_rows_u<V, 4, 4>(ids, rows, cpr, o, s);
+  }
+
+  void launch_cp(const uint64_t* ids, uint64_t rows, char* o, cudaStream_t s) {
+    const uint32_t cpr = row_bytes / 16;
+    const uint64_t per_warp = 2ull * cpr * 32 * 16;
+    const uint32_t warps = static_cast<uint32_t>(
+        std::max<uint64_t>(1, std::min<uint64_t>(8, (200u << 10) / per_warp)));
+    const size_t smem = warps * per_warp;
+    static size_t configured = 0;
+    if (configured < smem) {
+      QVB_CUDA(cudaFuncSetAttribute(k_gather_cp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      configured = smem;
+    }
+    int per_sm = 0, dev = 0, sms = 0;
+    QVB_CUDA(cudaGetDevice(&dev));
+    QVB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    QVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather_cp, warps * 32, smem));
+    const uint64_t groups = (rows + 31) / 32;
+    const uint64_t blocks = std::min<uint64_t>((uint64_t)std::max(per_sm, 1) * sms,
+                                               (groups + warps - 1) / warps);
+    k_gather_cp<<<static_cast<unsigned>(blocks), warps * 32, smem, s>>>(ids, rows, lut, bases, stride,
+                                                                       cpr, row_bytes, n, o, err);
+    QVB_LAUNCH_CHECK();
   }
 
   void launch_tma(const uint64_t* ids, uint64_t rows, char* o, cudaStream_t s) {
