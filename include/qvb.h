@@ -274,6 +274,69 @@ int qvb_store_check_error(qvb_store* s);
 int qvb_request_ids_synthetic(int device, uint64_t seed, uint64_t batch, uint64_t n,
                               uint64_t* ids, uint64_t b, void* stream);
 
+/* ---- K0: k-hop neighbour sampler (include/qv/sampler.hpp:11-53) --------- */
+/* The request-ID producer upstream of the collect call
+ * (simulator.cpp:250-254 -> :320). A qvb_sampler holds the out-CSR's
+ * sampling candidates on the device: one per edge, or — when the graph has
+ * parallel edges (transition_view's has_parallel_edges, graph.cpp:299-313) —
+ * one per distinct neighbour in first-occurrence order with the weights summed
+ * in CSR order (sampler.cpp:75-90). Built once, reused by every batch. */
+typedef struct qvb_sampler qvb_sampler;
+typedef struct qvb_sample qvb_sample;
+typedef struct {
+  uint64_t node_count, edge_count;
+  uint64_t candidates;        /* coalesced candidate count (== edges without parallel edges) */
+  int32_t parallel_edges;     /* 1 when neighbours were coalesced */
+  int32_t unit_weights;       /* 1 when every candidate weight is 1.0 */
+  uint64_t max_candidates;    /* longest candidate row */
+  uint64_t device_bytes;
+  double build_ms;
+} qvb_sampler_info;
+typedef struct {
+  uint64_t seeds;
+  uint32_t hops;
+  uint32_t reserved;
+  uint64_t total_instances;   /* BatchSampleStats::total_instances */
+  uint64_t unique_count;      /* BatchSampleStats::unique_count */
+  double device_ms;           /* CUDA-event time of the sampling kernels */
+} qvb_sample_info;
+
+/* From a host out-CSR (qv::Graph layout; weights NULL = 1.0), validated like
+ * Graph::validate (graph.cpp:58-93). */
+int qvb_sampler_create(int device, uint64_t n, uint64_t e, const uint64_t* row_offsets,
+                       const uint64_t* col, const double* weights, void* stream,
+                       qvb_sampler** out);
+/* From the tools/bench.cpp:22-34 generator, built on the device. */
+int qvb_sampler_synthetic(int device, uint64_t n, uint64_t e, uint64_t seed, int weighted,
+                          int transposed, void* stream, qvb_sampler** out);
+int qvb_sampler_info_get(const qvb_sampler* s, qvb_sampler_info* info);
+int qvb_sampler_destroy(qvb_sampler* s);
+
+/* qv::batch_sample (sampler.cpp:114-149) with sample_khop (:56-112) and
+ * draw_without_replacement (:21-52): per seed, hop k draws
+ * min(#positive candidates, fanouts[k-1]) distinct neighbours of every
+ * frontier instance with exponential keys Exp(1)/w from
+ * derive_stream(splitmix64(rng_seed ^ seed*gamma), k, idx, parent) — the
+ * same streams, keys (glibc log1p reproduced bit-exactly) and tie order as
+ * the reference, so every frontier is identical. `seeds` are host
+ * (seeds_on_device=0) or device pointers; seeds >= n and an empty fanout list
+ * are ValidationErrors with the reference's messages. The result lives on the
+ * device until qvb_sample_destroy. */
+int qvb_batch_sample(qvb_sampler* s, const uint64_t* seeds, uint64_t nseeds, int seeds_on_device,
+                     const uint32_t* fanouts, uint32_t hops, uint64_t rng_seed, void* stream,
+                     qvb_sample** out);
+int qvb_sample_info_get(const qvb_sample* r, qvb_sample_info* info);
+/* Copies to host buffers (each may be NULL): nodes[total_instances] = every
+ * per-seed frontier flattened seed-major then hop-major (SampleResult::
+ * frontiers), counts[seeds*(hops+1)] = instance_counts, unique[unique_count]
+ * = BatchSampleStats::unique_nodes (sorted). Synchronises. */
+int qvb_sample_copy(const qvb_sample* r, uint64_t* nodes, uint64_t* counts, uint64_t* unique);
+/* Device pointers of the same arrays (owned by r), e.g. to feed
+ * qvb_gather(store, unique, unique_count, ...) without a host round trip. */
+int qvb_sample_device(const qvb_sample* r, const uint64_t** nodes, const uint64_t** counts,
+                      const uint64_t** unique);
+int qvb_sample_destroy(qvb_sample* r);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,10 @@ int qvb_test_sort_bench(int device, uint64_t n, int bits, int reps, double* ms);
 /* Exclusive (inclusive=0) or inclusive scan of u32 values, widened to u64. */
 int qvb_test_scan_u32(int device, const uint32_t* in, uint64_t n, int inclusive, uint64_t* out);
 
+/* out[i] = log1p(x[i]) by the device restatement of glibc's x86-64 FMA
+ * log1p that the sampler's exponential keys use (sampler.cu). */
+int qvb_test_log1p(int device, const double* x, uint64_t n, double* out);
+
 #ifdef __cplusplus
 }
 #endif

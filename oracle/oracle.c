@@ -290,6 +290,163 @@ int qvo_compute_fap(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* 
   return 0;
 }
 
+/* ---- sampler (sampler.cpp:21-149) ---------------------------------------- */
+typedef struct {
+  double key;
+  uint64_t idx;
+} keyidx_t;
+static int cmp_keyidx(const void* a, const void* b) { /* std::pair<double,size_t> order */
+  const keyidx_t *x = (const keyidx_t*)a, *y = (const keyidx_t*)b;
+  if (x->key < y->key) return -1;
+  if (y->key < x->key) return 1;
+  return x->idx < y->idx ? -1 : (x->idx > y->idx ? 1 : 0);
+}
+static int cmp_u64(const void* a, const void* b) {
+  uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* One seed's k-hop sample (sample_khop, sampler.cpp:56-112). Appends the
+ * frontier instances of hops 0..hops to nodes (seed first) and writes the
+ * per-hop counts. Returns the number of instances appended, or -1 on error. */
+static int64_t sample_khop(uint64_t n, const uint64_t* ro, const uint64_t* col, const double* w,
+                           int parallel, uint64_t seed, const uint32_t* fanouts, uint32_t hops,
+                           uint64_t rng_seed, uint64_t** nodes, uint64_t* cap, uint64_t at,
+                           uint64_t* counts) {
+  uint64_t start = at;
+  if (at + 1 > *cap) {
+    *cap = (*cap + 1) * 2;
+    *nodes = (uint64_t*)realloc(*nodes, *cap * sizeof(uint64_t));
+  }
+  (*nodes)[at++] = seed;
+  counts[0] = 1;
+  uint64_t prev_lo = start, prev_hi = at;
+  for (uint32_t k = 1; k <= hops; ++k) {
+    for (uint64_t pi = prev_lo; pi < prev_hi; ++pi) {
+      uint64_t p = (*nodes)[pi], idx = pi - prev_lo;
+      uint64_t a = ro[p], b = ro[p + 1];
+      /* candidates: coalesced in first-occurrence order when the graph has
+       * parallel edges (sampler.cpp:75-90) */
+      uint64_t L = 0;
+      uint64_t* cn = (uint64_t*)malloc((b - a + 1) * sizeof(uint64_t));
+      double* cw = (double*)malloc((b - a + 1) * sizeof(double));
+      for (uint64_t q = a; q < b; ++q) {
+        uint64_t j = col[q];
+        int merged = 0;
+        if (parallel)
+          for (uint64_t t = 0; t < L; ++t)
+            if (cn[t] == j) {
+              cw[t] += w[q];
+              merged = 1;
+              break;
+            }
+        if (!merged) {
+          cn[L] = j;
+          cw[L] = w[q];
+          ++L;
+        }
+      }
+      uint64_t st = qvo_derive_state(rng_seed, k, idx, p); /* sampler.cpp:94 */
+      uint64_t positive = 0;
+      for (uint64_t t = 0; t < L; ++t) positive += cw[t] > 0.0;
+      uint64_t m = positive < fanouts[k - 1] ? positive : fanouts[k - 1];
+      if (at + m > *cap) {
+        *cap = (at + m) * 2;
+        *nodes = (uint64_t*)realloc(*nodes, *cap * sizeof(uint64_t));
+      }
+      if (m > 0 && m == positive) {
+        for (uint64_t t = 0; t < L; ++t)
+          if (cw[t] > 0.0) (*nodes)[at++] = cn[t];
+      } else if (m > 0) {
+        keyidx_t* keys = (keyidx_t*)malloc(L * sizeof(keyidx_t));
+        uint64_t nk = 0;
+        for (uint64_t t = 0; t < L; ++t) {
+          double e = -log1p(-rng_uniform(&st)); /* rng.hpp:38: exponential() */
+          if (cw[t] > 0.0) {
+            keys[nk].key = e / cw[t];
+            keys[nk].idx = t;
+            ++nk;
+          }
+        }
+        qsort(keys, nk, sizeof(keyidx_t), cmp_keyidx); /* == nth_element's m smallest */
+        uint64_t* pick = (uint64_t*)malloc(m * sizeof(uint64_t));
+        for (uint64_t t = 0; t < m; ++t) pick[t] = keys[t].idx;
+        qsort(pick, m, sizeof(uint64_t), cmp_u64); /* candidate order */
+        for (uint64_t t = 0; t < m; ++t) (*nodes)[at++] = cn[pick[t]];
+        free(pick);
+        free(keys);
+      }
+      free(cn);
+      free(cw);
+    }
+    counts[k] = at - prev_hi;
+    prev_lo = prev_hi;
+    prev_hi = at;
+  }
+  (void)n;
+  return (int64_t)(at - start);
+}
+
+/* batch_sample (sampler.cpp:114-149): per-seed frontiers flattened into
+ * nodes_out (seed-major, hop-major, instance order) with counts_out[s*(hops+1)+k];
+ * the sorted union of all sampled nodes in unique_out. Two-phase: call with
+ * nodes_out == NULL to get *total and *unique_count. */
+int qvo_batch_sample(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col,
+                     const double* w, const uint64_t* seeds, uint64_t nseeds,
+                     const uint32_t* fanouts, uint32_t hops, uint64_t rng_seed,
+                     uint64_t* total, uint64_t* unique_count, uint64_t* nodes_out,
+                     uint64_t* counts_out, uint64_t* unique_out) {
+  int rc = qvo_validate(n, e, ro, col, w);
+  if (rc) return rc;
+  if (hops == 0) return fail(QVB_ERR_VALIDATION, "sampling config needs >= 1 hop%.0llu%.0llu", 0, 0);
+  for (uint32_t k = 0; k < hops; ++k)
+    if (fanouts[k] < 1) return fail(QVB_ERR_VALIDATION, "fanouts must be >= 1%.0llu%.0llu", 0, 0);
+  for (uint64_t i = 0; i < nseeds; ++i)
+    if (seeds[i] >= n)
+      return fail(QVB_ERR_VALIDATION, "batch seed at position %llu (node %llu) out of range", i,
+                  seeds[i]);
+  /* transition_view's has_parallel_edges (graph.cpp:299-313) */
+  int parallel = 0;
+  uint64_t* stamp = (uint64_t*)malloc(n * sizeof(uint64_t));
+  for (uint64_t i = 0; i < n; ++i) stamp[i] = ~0ull;
+  for (uint64_t i = 0; i < n && !parallel; ++i)
+    for (uint64_t q = ro[i]; q < ro[i + 1]; ++q) {
+      if (stamp[col[q]] == i) {
+        parallel = 1;
+        break;
+      }
+      stamp[col[q]] = i;
+    }
+  free(stamp);
+  uint64_t cap = 1024, at = 0;
+  uint64_t* nodes = (uint64_t*)malloc(cap * sizeof(uint64_t));
+  uint64_t* counts = (uint64_t*)malloc((hops + 1) * (nseeds ? nseeds : 1) * sizeof(uint64_t));
+  for (uint64_t i = 0; i < nseeds; ++i) {
+    uint64_t s = seeds[i];
+    uint64_t rs = qvo_splitmix64(rng_seed ^ s * 0x9e3779b97f4a7c15ULL); /* sampler.cpp:136 */
+    int64_t got = sample_khop(n, ro, col, w, parallel, s, fanouts, hops, rs, &nodes, &cap, at,
+                              counts + i * (hops + 1));
+    at += (uint64_t)got;
+  }
+  *total = at;
+  uint64_t* u = (uint64_t*)malloc((at ? at : 1) * sizeof(uint64_t));
+  memcpy(u, nodes, at * sizeof(uint64_t));
+  qsort(u, at, sizeof(uint64_t), cmp_u64);
+  uint64_t uc = 0;
+  for (uint64_t i = 0; i < at; ++i)
+    if (i == 0 || u[i] != u[i - 1]) u[uc++] = u[i];
+  *unique_count = uc;
+  if (nodes_out) {
+    memcpy(nodes_out, nodes, at * sizeof(uint64_t));
+    memcpy(counts_out, counts, nseeds * (hops + 1) * sizeof(uint64_t));
+    memcpy(unique_out, u, uc * sizeof(uint64_t));
+  }
+  free(u);
+  free(nodes);
+  free(counts);
+  return 0;
+}
+
 /* ---- fap_ranking (placement.cpp:79-87) ---------------------------------- */
 static const double* g_rank_values;
 static int rank_cmp(const void* pa, const void* pb) {

@@ -58,6 +58,15 @@ int qvo_access_prob_sweep_nodes(uint64_t n, const uint64_t* t_row_offsets, const
 int qvo_compute_fap(uint64_t n, uint64_t e, const uint64_t* row_offsets, const uint64_t* col,
                     const double* w, uint32_t hops, const double* seed, double* values);
 
+/* batch_sample / sample_khop (sampler.cpp:21-149): frontiers flattened
+ * seed-major then hop-major (counts_out[s*(hops+1)+k]) and the sorted union.
+ * Call with nodes_out == NULL first to size the outputs. */
+int qvo_batch_sample(uint64_t n, uint64_t e, const uint64_t* row_offsets, const uint64_t* col,
+                     const double* w, const uint64_t* seeds, uint64_t nseeds,
+                     const uint32_t* fanouts, uint32_t hops, uint64_t rng_seed, uint64_t* total,
+                     uint64_t* unique_count, uint64_t* nodes_out, uint64_t* counts_out,
+                     uint64_t* unique_out);
+
 /* fap_ranking (placement.cpp:79-87) */
 int qvo_rank_desc(const double* values, uint64_t n, uint64_t* ranks);
 /* plan_placement (placement.cpp:94-226) + the gpu_replicated_capacity

@@ -26,6 +26,9 @@ i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
 f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
 LINK_COUNT = 7
+_BATCH_SAMPLE_ARGS = [C.c_uint64, C.c_uint64] + [C.c_void_p] * 4 + [C.c_uint64, C.c_void_p,
+                                                                     C.c_uint32, C.c_uint64] \
+    + [C.POINTER(C.c_uint64)] * 2 + [C.c_void_p] * 3
 
 
 class Topology(C.Structure):
@@ -125,6 +128,7 @@ class Oracle(_Lib):
         L.qvo_features.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, f32p]
         L.qvo_request_ids.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, u64p, C.c_uint64]
         L.qvo_gather.argtypes = [f32p, C.c_uint64, C.c_uint32, u64p, C.c_uint64, f32p, C.c_int]
+        L.qvo_batch_sample.argtypes = _BATCH_SAMPLE_ARGS
 
     # rng / generators -------------------------------------------------------
     def splitmix64(self, x: int) -> int:
@@ -189,6 +193,11 @@ class Oracle(_Lib):
                                                           _pad(tw, np.float64), rs, prev, nodes,
                                                           len(nodes), out))
         return out
+
+    def batch_sample(self, ro, col, w, seeds, fanouts, rng_seed: int):
+        """batch_sample (sampler.cpp:114-149) -> (nodes, counts[seed][hop], unique)."""
+        return _batch_sample(self._lib.qvo_batch_sample, self._check, ro, col, w, seeds, fanouts,
+                             rng_seed)
 
     def compute_fap(self, ro, col, w, hops: int, seed=None):
         """compute_fap (metrics.cpp:95-132)."""
@@ -288,6 +297,7 @@ class RefLib(_Lib):
         L.qvr_page_transitions.argtypes = [u64p, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64)]
         L.qvr_plan_reads.argtypes = [i64p, u64p, C.c_uint64, u64p, C.c_uint64, C.c_uint64, i64p,
                                      u64p, u64p, C.POINTER(C.c_uint64), u64p, dp]
+        L.qvr_batch_sample.argtypes = _BATCH_SAMPLE_ARGS + [dp]
         self.last_ms = 0.0
 
     def max_threads(self) -> int:
@@ -310,6 +320,13 @@ class RefLib(_Lib):
                                               C.byref(ms)))
         self.last_ms = ms.value
         return out
+
+    def batch_sample(self, ro, col, w, seeds, fanouts, rng_seed: int):
+        ms = C.c_double(0)
+        res = _batch_sample(self._lib.qvr_batch_sample, self._check, ro, col, w, seeds, fanouts,
+                            rng_seed, (C.byref(ms),))
+        self.last_ms = ms.value
+        return res
 
     def compute_fap(self, ro, col, w, hops: int, seed=None, parallel: bool = True):
         n = len(ro) - 1
@@ -376,6 +393,26 @@ class RefLib(_Lib):
         res = _plan_reads_call(call, self._check, loc, off, ids, len(ids), page)
         self.last_ms = ms.value
         return res
+
+
+def _batch_sample(fn, check, ro, col, w, seeds, fanouts, rng_seed, extra=()):
+    """Shared two-call driver of qvo_/qvr_batch_sample -> (nodes, counts, unique)."""
+    n = len(ro) - 1
+    s = _pad(seeds, np.uint64)
+    f = np.ascontiguousarray(fanouts, np.uint32)
+    hops = len(f)
+    tot, uc = C.c_uint64(0), C.c_uint64(0)
+    ro = np.ascontiguousarray(ro, np.uint64)
+    col_, w_ = _pad(col, np.uint64), _pad(w, np.float64)  # keep alive across both calls
+    args = [n, len(col), ro.ctypes.data, col_.ctypes.data, w_.ctypes.data, s.ctypes.data,
+            len(seeds), f.ctypes.data, hops, rng_seed, C.byref(tot), C.byref(uc)]
+    check(fn(*args, None, None, None, *extra))
+    nodes = np.zeros(max(tot.value, 1), np.uint64)
+    counts = np.zeros(max(len(seeds) * (hops + 1), 1), np.uint64)
+    uniq = np.zeros(max(uc.value, 1), np.uint64)
+    check(fn(*args, nodes.ctypes.data, counts.ctypes.data, uniq.ctypes.data, *extra))
+    return nodes[: tot.value], counts[: len(seeds) * (hops + 1)].reshape(len(seeds), hops + 1), \
+        uniq[: uc.value]
 
 
 def _pad(a, dtype):

@@ -22,6 +22,7 @@
 #include "qv/graph.hpp"
 #include "qv/metrics.hpp"
 #include "qv/placement.hpp"
+#include "qv/sampler.hpp"
 #include "qv/topology.hpp"
 #include "../include/qvb.h"
 
@@ -252,6 +253,36 @@ int qvr_plan_reads(const int64_t* location_ids, const uint64_t* offsets, uint64_
       for (uint64_t o : lr.offsets) offsets_out[at++] = o;
     }
     *n_groups = g;
+  });
+}
+
+// qv::batch_sample, flattened like qvo_batch_sample (two calls: sizes, fill).
+int qvr_batch_sample(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col,
+                     const double* w, const uint64_t* seeds, uint64_t nseeds,
+                     const uint32_t* fanouts, uint32_t hops, uint64_t rng_seed, uint64_t* total,
+                     uint64_t* unique_count, uint64_t* nodes_out, uint64_t* counts_out,
+                     uint64_t* unique_out, double* ms_out) {
+  return guard([&] {
+    qv::Graph g = make_graph(n, e, ro, col, w);
+    qv::TransitionView t = qv::transition_view(g);
+    qv::SamplingConfig cfg;
+    cfg.fanouts.assign(fanouts, fanouts + hops);
+    auto t0 = std::chrono::steady_clock::now();
+    qv::BatchSampleResult r =
+        qv::batch_sample(t, std::span<const qv::NodeId>(seeds, nseeds), cfg, rng_seed);
+    auto t1 = std::chrono::steady_clock::now();
+    if (ms_out) *ms_out = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    *total = r.stats.total_instances;
+    *unique_count = r.stats.unique_count;
+    if (!nodes_out) return;
+    uint64_t at = 0;
+    for (std::size_t i = 0; i < r.per_seed.size(); ++i) {
+      for (std::size_t k = 0; k < r.per_seed[i].frontiers.size(); ++k) {
+        counts_out[i * (hops + 1) + k] = r.per_seed[i].frontiers[k].size();
+        for (qv::NodeId v : r.per_seed[i].frontiers[k]) nodes_out[at++] = v;
+      }
+    }
+    std::copy(r.stats.unique_nodes.begin(), r.stats.unique_nodes.end(), unique_out);
   });
 }
 

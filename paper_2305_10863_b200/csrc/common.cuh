@@ -223,8 +223,8 @@ __host__ __device__ __forceinline__ double to_uniform(uint64_t r) {
 // RngStream::below (rng.hpp:42-45): high 64 bits of r * n.
 __device__ __forceinline__ uint64_t to_below(uint64_t r, uint64_t n) { return __umul64hi(r, n); }
 
-// derive_stream (rng.hpp:50-57), host side.
-inline uint64_t derive_state(uint64_t master, uint64_t a, uint64_t b = 0, uint64_t c = 0) {
+// derive_stream (rng.hpp:50-57).
+__host__ __device__ __forceinline__ uint64_t derive_state(uint64_t master, uint64_t a, uint64_t b = 0, uint64_t c = 0) {
   uint64_t s = splitmix64(master ^ 0x6a09e667f3bcc909ULL);
   s = splitmix64(s ^ splitmix64(a ^ 0xbb67ae8584caa73bULL));
   s = splitmix64(s ^ splitmix64(b ^ 0x3c6ef372fe94f82bULL));
@@ -237,7 +237,7 @@ __host__ __device__ __forceinline__ float feature_value(uint64_t f, uint32_t dim
   return static_cast<float>(splitmix64(f * dim + k) >> 40) * 0x1.0p-24f;
 }
 
-// ---- primitives implemented in primitives.cu (CUB-backed for now) ----------
+// ---- hand-written primitives (primitives.cu) --------------------------------
 // Stable LSD radix sort of (key, value) pairs on bits [begin_bit, end_bit).
 void sort_pairs_u32_u32(const uint32_t* kin, uint32_t* kout, const uint32_t* vin, uint32_t* vout,
                         uint64_t n, int begin_bit, int end_bit, cudaStream_t s);

@@ -688,7 +688,6 @@ void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const
 using namespace qvb;
 
 namespace qvb {
-namespace {
 
 // tools/bench.cpp:22-34 + Graph::from_edges/build_csr (graph.cpp:16-47) on
 // the device: out-CSR with rows in input order (stable sort by source).
@@ -724,6 +723,8 @@ void generate_out_csr(uint64_t n, uint64_t e, uint64_t seed, int weighted, int t
   QVB_LAUNCH_CHECK();
 }
 
+namespace {
+
 __global__ void k_u32_to_u64(const uint32_t* __restrict__ in, uint64_t* __restrict__ out,
                              uint64_t count) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
@@ -746,7 +747,7 @@ void finish_build(qvb_graph* g, cudaEvent_t a, cudaEvent_t b, cudaStream_t s) {
 
 }  // namespace
 
-namespace {
+namespace qvb {
 
 // Host out-CSR -> device (row offsets u64, columns u32, weights f64 or none)
 // with Graph::validate's checks and messages (graph.cpp:58-93); the
@@ -817,7 +818,7 @@ void upload_out_csr(uint64_t n, uint64_t e, const uint64_t* row_offsets, const u
   }
 }
 
-}  // namespace
+}  // namespace qvb
 
 extern "C" int qvb_graph_upload(int device, uint64_t n, uint64_t e, const uint64_t* row_offsets,
                                 const uint64_t* col, const double* weights, void* stream,

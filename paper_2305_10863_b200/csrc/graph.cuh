@@ -107,6 +107,18 @@ void device_transpose(uint64_t n, uint64_t e, const uint64_t* ro_h, const uint64
                       DevBuf<uint32_t>& tsrc, DevBuf<double>& tw, DevBuf<double>& rs,
                       bool* unit_weights);
 
+// Host out-CSR (qv::Graph layout) -> device: row offsets u64, columns u32,
+// weights f64 (left empty when weights == nullptr), with Graph::validate's
+// checks and messages (graph.cpp:58-93).
+void upload_out_csr(uint64_t n, uint64_t e, const uint64_t* row_offsets, const uint64_t* col,
+                    const double* weights, cudaStream_t s, DevBuf<uint64_t>& ro,
+                    DevBuf<uint32_t>& dcol, DevBuf<double>& dw);
+// tools/bench.cpp:22-34 generator + build_csr on the device (w left empty
+// when !weighted; ssrc = source of every CSR edge).
+void generate_out_csr(uint64_t n, uint64_t e, uint64_t seed, int weighted, int transposed,
+                      cudaStream_t s, DevBuf<uint64_t>& ro, DevBuf<uint32_t>& col,
+                      DevBuf<double>& w, DevBuf<uint32_t>& ssrc);
+
 // Runs layers-1 sweeps; returns the device buffer holding P_layers.
 const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s);
 

@@ -117,6 +117,30 @@ class StoreInfo(C.Structure):
     ]
 
 
+class SamplerInfo(C.Structure):
+    _fields_ = [
+        ("node_count", C.c_uint64),
+        ("edge_count", C.c_uint64),
+        ("candidates", C.c_uint64),
+        ("parallel_edges", C.c_int32),
+        ("unit_weights", C.c_int32),
+        ("max_candidates", C.c_uint64),
+        ("device_bytes", C.c_uint64),
+        ("build_ms", C.c_double),
+    ]
+
+
+class SampleInfo(C.Structure):
+    _fields_ = [
+        ("seeds", C.c_uint64),
+        ("hops", C.c_uint32),
+        ("reserved", C.c_uint32),
+        ("total_instances", C.c_uint64),
+        ("unique_count", C.c_uint64),
+        ("device_ms", C.c_double),
+    ]
+
+
 _LIB = None
 vp = C.c_void_p
 u64 = C.c_uint64
@@ -158,10 +182,20 @@ _SIGNATURES = {
     "qvb_gather_host": (i32, [vp, vp, u64, vp, vp]),
     "qvb_store_check_error": (i32, [vp]),
     "qvb_request_ids_synthetic": (i32, [i32, u64, u64, u64, vp, u64, vp]),
+    "qvb_sampler_create": (i32, [i32, u64, u64, vp, vp, vp, vp, P(vp)]),
+    "qvb_sampler_synthetic": (i32, [i32, u64, u64, u64, i32, i32, vp, P(vp)]),
+    "qvb_sampler_info_get": (i32, [vp, P(SamplerInfo)]),
+    "qvb_sampler_destroy": (i32, [vp]),
+    "qvb_batch_sample": (i32, [vp, vp, u64, i32, vp, u32, u64, vp, P(vp)]),
+    "qvb_sample_info_get": (i32, [vp, P(SampleInfo)]),
+    "qvb_sample_copy": (i32, [vp, vp, vp, vp]),
+    "qvb_sample_device": (i32, [vp, P(vp), P(vp), P(vp)]),
+    "qvb_sample_destroy": (i32, [vp]),
     # include/qvb_test.h
     "qvb_test_sort_pairs_u64": (i32, [i32, vp, vp, u64, i32, i32, vp, vp]),
     "qvb_test_scan_u32": (i32, [i32, vp, u64, i32, vp]),
     "qvb_test_sort_bench": (i32, [i32, u64, i32, i32, P(C.c_double)]),
+    "qvb_test_log1p": (i32, [i32, vp, u64, vp]),
 }
 
 
@@ -518,3 +552,153 @@ def request_ids_synthetic(seed: int, batch: int, n: int, out, device: int = 0, s
     _check(_lib().qvb_request_ids_synthetic(device, seed, batch, n, _ptr(out), int(out.numel()),
                                             _stream_ptr(stream)))
     return out
+
+
+# ---- K0: k-hop sampler (sampler.cpp:21-149) -----------------------------------
+@dataclass
+class SampleResult:
+    """qv::SampleResult (sampler.hpp:14-28) for one seed."""
+
+    seed: int
+    frontiers: list
+    instance_counts: list
+    unique_nodes: np.ndarray
+
+    def total_instances(self) -> int:
+        return int(sum(self.instance_counts))
+
+
+class BatchSample:
+    """Result of one batch_sample on the device (qvb_sample). ``nodes`` is
+    every per-seed frontier flattened seed-major then hop-major, ``counts``
+    [seeds, hops+1] the instance counts, ``unique`` the sorted union
+    (BatchSampleStats::unique_nodes)."""
+
+    def __init__(self, handle: int):
+        self._h = handle
+
+    def info(self) -> SampleInfo:
+        i = SampleInfo()
+        _check(_lib().qvb_sample_info_get(self._h, C.byref(i)))
+        return i
+
+    def arrays(self):
+        i = self.info()
+        nodes = np.zeros(max(i.total_instances, 1), np.uint64)
+        counts = np.zeros(max(i.seeds * (i.hops + 1), 1), np.uint64)
+        uniq = np.zeros(max(i.unique_count, 1), np.uint64)
+        _check(_lib().qvb_sample_copy(self._h, _ptr(nodes), _ptr(counts), _ptr(uniq)))
+        return (nodes[: i.total_instances], counts[: i.seeds * (i.hops + 1)].reshape(i.seeds, i.hops + 1),
+                uniq[: i.unique_count])
+
+    def device_unique(self):
+        """(device pointer, count) of the sorted union — qvb_gather's ids."""
+        u = vp()
+        _check(_lib().qvb_sample_device(self._h, None, None, C.byref(u)))
+        return u.value, self.info().unique_count
+
+    def per_seed(self, seeds) -> list:
+        """The reference's BatchSampleResult::per_seed view."""
+        nodes, counts, _ = self.arrays()
+        out, at = [], 0
+        for s, row in zip(seeds, counts):
+            fr = []
+            for c in row:
+                fr.append(nodes[at: at + int(c)])
+                at += int(c)
+            out.append(SampleResult(int(s), fr, [int(c) for c in row],
+                                    np.unique(np.concatenate(fr)) if fr else np.zeros(0, np.uint64)))
+        return out
+
+    def close(self):
+        if self._h:
+            _lib().qvb_sample_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Sampler:
+    """Device-resident sampling candidates (qvb_sampler) of an out-CSR."""
+
+    def __init__(self, handle: int):
+        self._h = handle
+
+    @classmethod
+    def upload(cls, row_offsets, col, weights=None, device: int = 0, stream=None):
+        ro = np.ascontiguousarray(row_offsets, np.uint64)
+        c = np.ascontiguousarray(col, np.uint64)
+        w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+        h = vp()
+        _check(_lib().qvb_sampler_create(device, len(ro) - 1, len(c), _ptr(ro), _ptr(c) if len(c) else None,
+                                         _ptr(w) if w is not None and len(w) else None,
+                                         _stream_ptr(stream), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def synthetic(cls, n: int, e: int, seed: int = 7, weighted: bool = False,
+                  transposed: bool = False, device: int = 0, stream=None):
+        h = vp()
+        _check(_lib().qvb_sampler_synthetic(device, n, e, seed, int(weighted), int(transposed),
+                                            _stream_ptr(stream), C.byref(h)))
+        return cls(h.value)
+
+    def info(self) -> SamplerInfo:
+        i = SamplerInfo()
+        _check(_lib().qvb_sampler_info_get(self._h, C.byref(i)))
+        return i
+
+    def batch_sample(self, seeds, fanouts, rng_seed: int, stream=None) -> BatchSample:
+        """qv::batch_sample(t, seeds, SamplingConfig{fanouts}, rng_seed). ``seeds``:
+        host numpy array or device tensor of uint64/int64 node ids."""
+        f = np.ascontiguousarray(fanouts, np.uint32)
+        on_dev = 0
+        if isinstance(seeds, np.ndarray) or isinstance(seeds, (list, tuple)):
+            sd = np.ascontiguousarray(seeds, np.uint64)
+            n = len(sd)
+        else:
+            sd, on_dev, n = seeds, 1, int(seeds.numel())
+        h = vp()
+        _check(_lib().qvb_batch_sample(self._h, _ptr(sd) if n else None, n, on_dev,
+                                       _ptr(f) if len(f) else None, len(f), rng_seed,
+                                       _stream_ptr(stream), C.byref(h)))
+        return BatchSample(h.value)
+
+    def close(self):
+        if self._h:
+            _lib().qvb_sampler_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def batch_sample(row_offsets, col, weights, seeds, fanouts, rng_seed: int, device: int = 0):
+    """One-shot qv::batch_sample from a host out-CSR -> (nodes, counts, unique)."""
+    with Sampler.upload(row_offsets, col, weights, device=device) as s:
+        r = s.batch_sample(seeds, fanouts, rng_seed)
+        try:
+            return r.arrays()
+        finally:
+            r.close()
+
+
+def test_log1p(x, device: int = 0) -> np.ndarray:
+    """Device glibc-log1p restatement (test entry point)."""
+    a = np.ascontiguousarray(x, np.float64)
+    out = np.zeros(max(len(a), 1), np.float64)
+    _check(_lib().qvb_test_log1p(device, _ptr(a), len(a), _ptr(out)))
+    return out[: len(a)]

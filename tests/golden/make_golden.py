@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle.oracle import Oracle, RefLib, build, topology_defaults  # noqa: E402
-from tests.util import derive_stream, fig8_edges  # noqa: E402
+from tests.util import derive_stream, fig8_edges, random_edges  # noqa: E402
 
 
 def hexs(a):
@@ -71,6 +71,45 @@ def random_topologies():
     return out
 
 
+def sampler_goldens(o, r):
+    """batch_sample (sampler.cpp:114-149) on the fixtures of test_sampler.cpp."""
+    def run(ro, col, ww, seeds, fan, rs):
+        nodes, counts, uniq = r.batch_sample(ro, col, ww, np.array(seeds, np.uint64), fan, rs)
+        return {"seeds": [int(x) for x in seeds], "fanouts": list(fan), "rng_seed": rs,
+                "nodes": nodes.tolist(), "counts": counts.tolist(), "unique": uniq.tolist()}
+
+    out = {}
+    n, s, d, w = fig8_edges()
+    ro, col, ww = o.build_csr(n, s, d, w)
+    out["fig8_full"] = run(ro, col, ww, [4], [10, 10], 1)  # test_sampler.cpp:15-26
+    rng = derive_stream(83, 3)  # test_sampler.cpp:109-111
+    out["fig8_batch"] = run(ro, col, ww, [rng.below(n) for _ in range(100)], [2, 2], 7)
+    out["fig8_dup"] = run(ro, col, ww, [0, 0, 3, 0], [2, 2], 7)
+    out["fig8_empty"] = run(ro, col, ww, [], [2, 2], 5)
+    ro, col, ww = o.build_csr(3, [0, 1], [1, 2], [1.0, 1.0])  # chain3, test_sampler.cpp:28-35
+    out["chain3"] = run(ro, col, ww, [0], [1, 1], 99)
+    ro, col, ww = o.build_csr(3, [0, 0, 0, 0], [1, 1, 1, 2], [1.0] * 4)  # :135-150
+    out["parallel"] = [run(ro, col, ww, [0], [2], i) for i in range(50)]
+    rnd = []
+    rng = derive_stream(79, 2)  # test_sampler.cpp:57-80
+    for it in range(20):
+        n, s, d, w = random_edges(rng, 30, 300, True)
+        ro, col, ww = o.build_csr(n, s, d, w)
+        ent = run(ro, col, ww, [rng.below(n)], [2, 3], it)
+        ent["edges"] = [n, s, d, w]
+        rnd.append(ent)
+    out["random"] = rnd
+    c1 = {}
+    for name, weighted in [("uniform", False), ("weighted", True)]:
+        ro, col, ww = o.synthetic_graph(100_000, 1_000_000, 7, weighted, False)
+        seeds = o.request_ids(11, 0, 100_000, 4096)  # tools/bench.cpp:89-94
+        nodes, counts, uniq = r.batch_sample(ro, col, ww, seeds, [15, 10], 3)
+        c1[name] = {"total": int(len(nodes)), "unique": int(len(uniq)), "nodes_sha256": digest(nodes),
+                    "counts_sha256": digest(counts), "unique_sha256": digest(uniq)}
+    out["c1_bench"] = c1
+    return out
+
+
 def main():
     build(ref=True)
     r = RefLib()
@@ -117,6 +156,8 @@ def main():
         ro, col, ww = o.synthetic_graph(100_000, 1_000_000, 7, weighted, False)
         fc1[name] = digest(r.compute_fap(ro, col, ww, 2 if not weighted else 3))
     g["fap_c1"] = fc1
+
+    g["sampler"] = sampler_goldens(o, r)
 
     sc = {}
     for name, kw in scenarios().items():

@@ -230,3 +230,68 @@ def test_fap_matches_reference_random(oracle, ref):
         oracle.compute_fap(ro, col, ww, 2, -np.ones(len(ro) - 1))
     with pytest.raises(Exception, match="does not sum to 1"):
         oracle.compute_fap(ro, col, ww, 2, np.ones(len(ro) - 1))
+
+
+# ---- sampler (sampler.cpp:21-149) ---------------------------------------------
+def _sample_case(oracle, ro, col, ww, ent):
+    nodes, counts, uniq = oracle.batch_sample(ro, col, ww, np.array(ent["seeds"], np.uint64),
+                                              ent["fanouts"], ent["rng_seed"])
+    assert nodes.tolist() == ent["nodes"]
+    assert counts.tolist() == (ent["counts"] if ent["seeds"] else [])
+    assert uniq.tolist() == ent["unique"]
+
+
+def test_sampler_golden(oracle):
+    S = GOLD["sampler"]
+    n, s, d, w = fig8_edges()
+    ro, col, ww = oracle.build_csr(n, s, d, w)
+    for name in ("fig8_full", "fig8_batch", "fig8_dup", "fig8_empty"):
+        _sample_case(oracle, ro, col, ww, S[name])
+    # test_sampler.cpp:15-26: 4 -> 0 -> {3, 5}
+    assert S["fig8_full"]["nodes"] == [4, 0, 3, 5]
+    ro, col, ww = oracle.build_csr(3, [0, 1], [1, 2], [1.0, 1.0])
+    _sample_case(oracle, ro, col, ww, S["chain3"])
+    assert S["chain3"]["nodes"] == [0, 1, 2]
+    ro, col, ww = oracle.build_csr(3, [0, 0, 0, 0], [1, 1, 1, 2], [1.0] * 4)
+    for ent in S["parallel"]:
+        _sample_case(oracle, ro, col, ww, ent)
+        assert sorted(ent["nodes"][1:]) == [1, 2]  # coalesced: two distinct neighbours
+    for ent in S["random"]:
+        n, s, d, w = ent["edges"]
+        ro, col, ww = oracle.build_csr(n, s, d, w)
+        _sample_case(oracle, ro, col, ww, ent)
+    for name, weighted in [("uniform", False), ("weighted", True)]:
+        ro, col, ww = oracle.synthetic_graph(100_000, 1_000_000, 7, weighted, False)
+        seeds = oracle.request_ids(11, 0, 100_000, 4096)
+        nodes, counts, uniq = oracle.batch_sample(ro, col, ww, seeds, [15, 10], 3)
+        g = S["c1_bench"][name]
+        assert (len(nodes), len(uniq)) == (g["total"], g["unique"])
+        assert (sha(nodes), sha(counts), sha(uniq)) == (g["nodes_sha256"], g["counts_sha256"],
+                                                         g["unique_sha256"])
+
+
+def test_sampler_matches_reference_random(oracle, ref):
+    rng = derive_stream(9, 9)
+    for it in range(40):
+        n, s, d, w = random_edges(rng, 60, 400, it % 2 == 0)
+        ro, col, ww = oracle.build_csr(n, s, d, w)
+        if it % 4 == 1:  # zero-weight edges inside positive rows
+            ww = ww.copy()
+            ww[::3] = 0.0
+            ro2 = ro.astype(np.int64)
+            for i in range(n):
+                a, b = ro2[i], ro2[i + 1]
+                if b > a and not (ww[a:b] > 0).any():
+                    ww[a] = 1.0
+        seeds = np.array([rng.below(n) for _ in range(25)], np.uint64)
+        fan = [1 + rng.below(5) for _ in range(1 + rng.below(3))]
+        a = oracle.batch_sample(ro, col, ww, seeds, fan, 1000 + it)
+        b = ref.batch_sample(ro, col, ww, seeds, fan, 1000 + it)
+        for x, y in zip(a, b):
+            assert (x == y).all(), it
+    with pytest.raises(Exception, match="position 1"):
+        oracle.batch_sample(ro, col, ww, np.array([0, 10**6], np.uint64), [1], 1)
+    with pytest.raises(Exception, match=">= 1 hop"):
+        oracle.batch_sample(ro, col, ww, np.array([0], np.uint64), [], 1)
+    with pytest.raises(Exception, match="fanouts must be"):
+        oracle.batch_sample(ro, col, ww, np.array([0], np.uint64), [2, 0], 1)
