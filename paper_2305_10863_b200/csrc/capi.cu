@@ -1,5 +1,6 @@
 // capi.cu — C-ABI plumbing: error strings, version, device query and the
 // topology helpers (reference topology.cpp:27-64, placement.cpp:25-51).
+#include <atomic>
 #include <cstring>
 #include <string>
 
@@ -11,6 +12,19 @@ namespace {
 thread_local std::string g_last_error;
 }
 void set_last_error(const std::string& m) { g_last_error = m; }
+
+void retain_pool(int device) {
+  static std::atomic<uint64_t> done{0};  // bit per device (< 64)
+  const uint64_t bit = device < 64 ? 1ull << device : 0;
+  if (!bit || (done.load(std::memory_order_acquire) & bit)) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done.fetch_or(bit, std::memory_order_acq_rel);
+}
 }  // namespace qvb
 
 using namespace qvb;

@@ -35,6 +35,10 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define QVB_LAUNCH_CHECK() ::qvb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
 
 void set_last_error(const std::string& m);
+// Keeps the device's stream-ordered pool (cudaMallocAsync) from returning
+// memory to the driver at every synchronisation, so per-call scratch is
+// recycled instead of re-mapped. Once per device.
+void retain_pool(int device);
 
 // Runs `f` and maps exceptions to status codes (the reference's exception
 // hierarchy, include/qv/error.hpp:10-32, is mirrored by the codes).
@@ -69,6 +73,7 @@ struct DeviceGuard {
     if (device < 0 || device >= count) fail(QVB_ERR_VALIDATION, "device index out of range");
     QVB_CUDA(cudaGetDevice(&prev));
     if (prev != device) QVB_CUDA(cudaSetDevice(device));
+    retain_pool(device);
   }
   ~DeviceGuard() {
     if (prev >= 0) cudaSetDevice(prev);
@@ -223,13 +228,20 @@ __host__ __device__ __forceinline__ double to_uniform(uint64_t r) {
 // RngStream::below (rng.hpp:42-45): high 64 bits of r * n.
 __device__ __forceinline__ uint64_t to_below(uint64_t r, uint64_t n) { return __umul64hi(r, n); }
 
-// derive_stream (rng.hpp:50-57).
-__host__ __device__ __forceinline__ uint64_t derive_state(uint64_t master, uint64_t a, uint64_t b = 0, uint64_t c = 0) {
-  uint64_t s = splitmix64(master ^ 0x6a09e667f3bcc909ULL);
-  s = splitmix64(s ^ splitmix64(a ^ 0xbb67ae8584caa73bULL));
-  s = splitmix64(s ^ splitmix64(b ^ 0x3c6ef372fe94f82bULL));
-  s = splitmix64(s ^ splitmix64(c ^ 0xa54ff53a5f1d36f1ULL));
-  return s;
+// derive_stream (rng.hpp:50-57), split after the (master, a) words so a
+// prefix shared by many streams is chained once.
+__host__ __device__ __forceinline__ uint64_t derive_prefix(uint64_t master, uint64_t a) {
+  const uint64_t s = splitmix64(master ^ 0x6a09e667f3bcc909ULL);
+  return splitmix64(s ^ splitmix64(a ^ 0xbb67ae8584caa73bULL));
+}
+__host__ __device__ __forceinline__ uint64_t derive_finish(uint64_t prefix, uint64_t b, uint64_t c) {
+  const uint64_t mb = splitmix64(b ^ 0x3c6ef372fe94f82bULL);
+  const uint64_t mc = splitmix64(c ^ 0xa54ff53a5f1d36f1ULL);
+  return splitmix64(splitmix64(prefix ^ mb) ^ mc);
+}
+__host__ __device__ __forceinline__ uint64_t derive_state(uint64_t master, uint64_t a, uint64_t b = 0,
+                                                          uint64_t c = 0) {
+  return derive_finish(derive_prefix(master, a), b, c);
 }
 
 // Synthetic feature value X[f][k].

@@ -26,7 +26,8 @@
 //
 // Selection. Rows of <= 32 candidates rank the keys across the warp (one key
 // per lane); rows of <= 256 keep 8 keys per lane in registers; longer rows
-// stage their keys in a per-warp scratch slab. The latter two find the m-th
+// take one CTA each and stage their keys in its scratch slab (on a side
+// stream, concurrently with the warp kernel). The latter two find the m-th
 // smallest key by an 8-bit radix select over the key bits (non-negative
 // doubles order like their bit patterns) and then take keys < T plus the
 // first keys == T in candidate order — exactly the reference's
@@ -46,8 +47,9 @@ struct qvb_sampler {
   uint32_t* ccol = nullptr;
   double* cw = nullptr;  // nullptr: unit weights
   uint32_t* cpos = nullptr;
-  uint64_t* scratch = nullptr;  // long-row key slabs, large_warps * max_len
-  uint32_t large_warps = 0;
+  uint64_t* scratch = nullptr;  // long-row key slabs, large_ctas * max_len
+  uint32_t large_ctas = 0;
+  cudaStream_t side = nullptr;  // long-row kernel runs beside the warp kernel
   double build_ms = 0.0;
   ~qvb_sampler() {
     int prev = -1;
@@ -59,6 +61,7 @@ struct qvb_sampler {
     cudaFree(cw);
     cudaFree(cpos);
     cudaFree(scratch);
+    if (side) cudaStreamDestroy(side);
     if (prev >= 0) cudaSetDevice(prev);
   }
 };
@@ -178,7 +181,8 @@ __device__ double glibc_log1p(double x) {
 // pattern of the non-negative double (order-preserving); kNoKey for w <= 0.
 __device__ __forceinline__ uint64_t sample_key(uint64_t state, uint64_t t, double w) {
   const double e = -glibc_log1p(-to_uniform(stream_draw(state, t)));
-  return w > 0.0 ? static_cast<uint64_t>(__double_as_longlong(e / w)) : kNoKey;
+  if (!(w > 0.0)) return kNoKey;
+  return static_cast<uint64_t>(__double_as_longlong(w == 1.0 ? e : e / w));  // e/1.0 == e
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -293,21 +297,16 @@ __global__ void k_hop_count(const uint32_t* __restrict__ pn, uint64_t P, uint32_
   }
 }
 
-// Per-parent stream of sample_khop (sampler.cpp:94) under batch_sample's
-// per-seed master (sampler.cpp:136).
-__device__ __forceinline__ uint64_t parent_state(uint64_t rng_seed, uint64_t seed, uint32_t hop,
-                                                 uint64_t idx, uint32_t p) {
-  return derive_state(splitmix64(rng_seed ^ (seed * kGamma)), hop, idx, p);
-}
-
 struct HopArgs {
   const uint32_t* pn;  // parents: node, seed slot
   const uint32_t* ps;
   uint64_t P;
   const uint64_t* ss_prev;  // seed starts of the parents' frontier
   const uint64_t* O;        // child offsets
-  const uint64_t* seeds;
-  uint64_t rng_seed;
+  // derive_prefix(splitmix64(rng ^ seed*gamma), hop) per seed: the part of
+  // sample_khop's derive_stream(rs, k, idx, p) (sampler.cpp:94, :136) shared
+  // by every parent of the seed at this hop
+  const uint64_t* hop_state;
   uint32_t hop, fanout;
   const uint64_t* cro;
   const uint32_t* ccol;
@@ -320,6 +319,8 @@ struct HopArgs {
 // Finds the m-th smallest key (1-based) among the keys `each` visits: 8-bit
 // digits from the top, one shared 256-bin histogram per warp. Returns the
 // threshold T and how many keys == T (in candidate order) belong to the m.
+// Stops early once the digit's whole bin is selected: then T = prefix with
+// all lower bits set and every key <= T is taken (take_eq = all).
 template <typename Each>
 __device__ __forceinline__ void radix_select(Each&& each, uint32_t m, uint32_t* hist, uint64_t& T,
                                              uint32_t& take_eq) {
@@ -349,12 +350,13 @@ __device__ __forceinline__ void radix_select(Each&& each, uint32_t m, uint32_t* 
     }
     const uint32_t excl = incl - sum;
     const uint32_t owner = __ffs(__ballot_sync(0xffffffffu, excl < need && need <= incl)) - 1;
-    uint32_t digit = 0, below = excl;
+    uint32_t digit = 0, below = excl, bin = 0;
     if (lane == owner) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         if (below + c[j] >= need) {
           digit = lane * 8 + j;
+          bin = c[j];
           break;
         }
         below += c[j];
@@ -362,10 +364,16 @@ __device__ __forceinline__ void radix_select(Each&& each, uint32_t m, uint32_t* 
     }
     digit = __shfl_sync(0xffffffffu, digit, owner);
     below = __shfl_sync(0xffffffffu, below, owner);
+    bin = __shfl_sync(0xffffffffu, bin, owner);
     need -= below;
     prefix |= static_cast<uint64_t>(digit) << shift;
     mask |= 0xFFull << shift;
     __syncwarp();
+    if (bin == need) {  // the whole bin is in: keys <= prefix|~mask
+      T = prefix | ~mask;
+      take_eq = 0xFFFFFFFFu;
+      return;
+    }
   }
   T = prefix;
   take_eq = need;
@@ -430,15 +438,24 @@ __global__ void __launch_bounds__(kBlock) k_hop_sample(HopArgs a) {
     }
     if (L > kRegMax) continue;  // k_hop_sample_large
     const uint64_t state =
-        parent_state(a.rng_seed, a.seeds[s], a.hop, i - a.ss_prev[s], p);
+        derive_finish(a.hop_state[s], i - a.ss_prev[s], p);
     if (L <= 32) {
       // rank of (key, idx) among the row's keys; the m smallest are chosen
       const bool in = lane < L;
       const uint64_t key = in ? sample_key(state, lane, w ? w[lane] : 1.0) : kNoKey;
+      // Rank by the high words; only when two valid keys share a high word
+      // (rare: exponent and 20 mantissa bits equal) compare all 64 bits.
+      const uint32_t hi = static_cast<uint32_t>(key >> 32);
+      const uint32_t same_hi = __match_any_sync(0xffffffffu, hi);  // all lanes take part
+      const bool tie = key != kNoKey && __popc(same_hi) > 1;
       uint32_t rank = 0;
-      for (uint32_t u = 0; u < L; ++u) {
-        const uint64_t ku = __shfl_sync(0xffffffffu, key, u);
-        rank += (ku < key) || (ku == key && u < lane);
+      if (!__any_sync(0xffffffffu, tie)) {
+        for (uint32_t u = 0; u < L; ++u) rank += __shfl_sync(0xffffffffu, hi, u) < hi;
+      } else {
+        for (uint32_t u = 0; u < L; ++u) {
+          const uint64_t ku = __shfl_sync(0xffffffffu, key, u);
+          rank += (ku < key) || (ku == key && u < lane);
+        }
       }
       const bool sel = in && key != kNoKey && rank < m;
       const uint32_t selm = __ballot_sync(0xffffffffu, sel);
@@ -475,20 +492,23 @@ __global__ void __launch_bounds__(kBlock) k_hop_sample(HopArgs a) {
   }
 }
 
-// Selecting parents with more than 256 candidates: keys staged in this
-// warp's scratch slab (max_len keys), then the same radix select.
+// Selecting parents with more than 256 candidates: one CTA per parent, keys
+// staged in the CTA's scratch slab (max_len keys), then the radix select of
+// radix_select with a block-wide histogram, and the emit in candidate order
+// with block-wide ballot prefixes.
 __global__ void __launch_bounds__(kBlock)
     k_hop_sample_large(HopArgs a, const uint32_t* __restrict__ large,
                        const unsigned long long* __restrict__ nlarge,
                        uint64_t* __restrict__ scratch, uint64_t slab) {
-  __shared__ uint32_t hist_all[kWarpsPerBlock][256];
-  uint32_t* hist = hist_all[threadIdx.x >> 5];
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t gw = blockIdx.x * (uint64_t)kWarpsPerBlock + (threadIdx.x >> 5);
-  const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
-  uint64_t* K = scratch + gw * slab;
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t wsum[kWarpsPerBlock];
+  __shared__ uint32_t wsel[kWarpsPerBlock], weq[kWarpsPerBlock];
+  __shared__ uint32_t s_digit, s_below, s_bin;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt_mask = lanemask_lt();
+  uint64_t* K = scratch + blockIdx.x * slab;
   const uint64_t count = *nlarge;
-  for (uint64_t j = gw; j < count; j += warps) {
+  for (uint64_t j = blockIdx.x; j < count; j += gridDim.x) {
     const uint64_t i = large[j];
     const uint32_t p = a.pn[i], s = a.ps[i];
     const uint64_t c0 = a.cro[p];
@@ -497,37 +517,96 @@ __global__ void __launch_bounds__(kBlock)
     const uint32_t m = pos < a.fanout ? pos : a.fanout;
     const uint32_t* col = a.ccol + c0;
     const double* w = a.cw ? a.cw + c0 : nullptr;
-    const uint64_t state =
-        parent_state(a.rng_seed, a.seeds[s], a.hop, i - a.ss_prev[s], p);
-    for (uint32_t t = lane; t < L; t += 32) K[t] = sample_key(state, t, w ? w[t] : 1.0);
-    __syncwarp();
-    uint64_t T;
-    uint32_t take_eq;
-    radix_select(
-        [&](auto&& f) {
-          for (uint32_t base = 0; base < L; base += 32) {
-            const uint32_t t = base + lane;
-            f(t < L ? K[t] : kNoKey, t < L);
-          }
-        },
-        m, hist, T, take_eq);
-    emit_selected(
-        [&](auto&& f) {
-          for (uint32_t base = 0; base < L; base += 32) {
-            const uint32_t t = base + lane;
-            f(t < L ? K[t] : kNoKey, t < L, t);
-          }
-        },
-        T, take_eq, col, s, a.cn, a.cs, a.O[i]);
-    __syncwarp();
+    const uint64_t state = derive_finish(a.hop_state[s], i - a.ss_prev[s], p);
+    for (uint32_t t = tid; t < L; t += kBlock) K[t] = sample_key(state, t, w ? w[t] : 1.0);
+    // radix select (see radix_select), block-wide
+    uint64_t prefix = 0, mask = 0, T = 0;
+    uint32_t need = m, take_eq = 0;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      hist[tid] = 0;  // kBlock == 256 bins
+      __syncthreads();
+      for (uint32_t t = tid; t < L; t += kBlock) {
+        const uint64_t key = K[t];
+        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xFF], 1u);
+      }
+      __syncthreads();
+      const uint32_t c = hist[tid];
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (lane == 31) wsum[warp] = incl;
+      __syncthreads();
+      uint32_t before = 0;
+      for (uint32_t x = 0; x < warp; ++x) before += wsum[x];
+      incl += before;
+      if (incl - c < need && need <= incl) {
+        s_digit = tid;
+        s_below = incl - c;
+        s_bin = c;
+      }
+      __syncthreads();
+      need -= s_below;
+      prefix |= static_cast<uint64_t>(s_digit) << shift;
+      mask |= 0xFFull << shift;
+      const uint32_t bin = s_bin;
+      __syncthreads();  // s_* and wsum reused next pass
+      if (bin == need) {
+        T = prefix | ~mask;
+        take_eq = 0xFFFFFFFFu;
+        break;
+      }
+      T = prefix;
+      take_eq = need;
+    }
+    // emit in candidate order: rounds of kBlock candidates
+    uint64_t out = a.O[i];
+    uint32_t eq_seen = 0;
+    for (uint32_t base = 0; base < L; base += kBlock) {
+      const uint32_t t = base + tid;
+      const uint64_t key = t < L ? K[t] : kNoKey;
+      const bool in = t < L;
+      const bool eq = in && key == T;
+      const uint32_t eqm = __ballot_sync(0xffffffffu, eq);
+      if (lane == 0) weq[warp] = __popc(eqm);
+      __syncthreads();
+      uint32_t eq_before = eq_seen, eq_round = 0;
+      for (uint32_t x = 0; x < kWarpsPerBlock; ++x) {
+        if (x < warp) eq_before += weq[x];
+        eq_round += weq[x];
+      }
+      const bool sel = (in && key < T) || (eq && eq_before + __popc(eqm & lt_mask) < take_eq);
+      const uint32_t selm = __ballot_sync(0xffffffffu, sel);
+      if (lane == 0) wsel[warp] = __popc(selm);
+      __syncthreads();
+      uint64_t sel_before = out, sel_round = 0;
+      for (uint32_t x = 0; x < kWarpsPerBlock; ++x) {
+        if (x < warp) sel_before += wsel[x];
+        sel_round += wsel[x];
+      }
+      if (sel) {
+        const uint64_t at = sel_before + __popc(selm & lt_mask);
+        a.cn[at] = col[t];
+        a.cs[at] = s;
+      }
+      out += sel_round;
+      eq_seen += eq_round;
+      __syncthreads();  // weq/wsel reused next round
+    }
   }
 }
 
 __global__ void k_seed_starts(const uint64_t* __restrict__ ss_prev, const uint64_t* __restrict__ O,
-                              uint64_t nseeds, uint64_t* __restrict__ ss) {
+                              uint64_t nseeds, uint64_t* __restrict__ ss,
+                              const uint64_t* __restrict__ seeds, uint64_t rng_seed, uint32_t hop,
+                              uint64_t* __restrict__ hop_state) {
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s <= nseeds;
-       s += (uint64_t)gridDim.x * blockDim.x)
+       s += (uint64_t)gridDim.x * blockDim.x) {
     ss[s] = O[ss_prev[s]];
+    if (s < nseeds) hop_state[s] = derive_prefix(splitmix64(rng_seed ^ (seeds[s] * kGamma)), hop);
+  }
 }
 
 __global__ void k_hop0(const uint64_t* __restrict__ seeds, uint64_t nseeds, uint32_t* __restrict__ pn,
@@ -682,14 +761,14 @@ void build_candidates(qvb_sampler& sp, DevBuf<uint64_t>& ro, DevBuf<uint32_t>& c
   sp.max_len = st[2];
   if (sp.max_len > kRegMax) {
     const uint64_t slab_bytes = sp.max_len * sizeof(uint64_t);
-    uint64_t warps = std::max<uint64_t>(1, kScratchBudget / slab_bytes);
-    warps = std::min<uint64_t>(warps, 148ull * 16);
-    warps = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock;
-    sp.large_warps = static_cast<uint32_t>(warps);
-    QVB_CUDA(cudaMalloc(&sp.scratch, warps * slab_bytes));
+    uint64_t ctas = std::max<uint64_t>(1, kScratchBudget / slab_bytes);
+    ctas = std::min<uint64_t>(ctas, 148ull * 4);
+    sp.large_ctas = static_cast<uint32_t>(ctas);
+    QVB_CUDA(cudaMalloc(&sp.scratch, ctas * slab_bytes));
+    QVB_CUDA(cudaStreamCreateWithFlags(&sp.side, cudaStreamNonBlocking));
   }
   sp.bytes = (n + 1) * 8 + sp.ncand * (4 + (sp.cw ? 8 : 0)) + n * 4 +
-             sp.large_warps * sp.max_len * 8;
+             sp.large_ctas * sp.max_len * 8;
 }
 
 uint64_t* to_device_owned(DevBuf<uint64_t>& b) { return b.release_ownership(); }
@@ -820,9 +899,17 @@ extern "C" int qvb_batch_sample(qvb_sampler* sp, const uint64_t* seeds, uint64_t
         QVB_CUDA(cudaMemcpyAsync(dseeds.p, seeds, nseeds * 8, cudaMemcpyHostToDevice, s));
       }
     }
-    cudaEvent_t ea, eb;
+    cudaEvent_t ea, eb, fork, join;
     QVB_CUDA(cudaEventCreate(&ea));
     QVB_CUDA(cudaEventCreate(&eb));
+    QVB_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    QVB_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    struct Events {
+      cudaEvent_t* e[4];
+      ~Events() {
+        for (auto* x : e) cudaEventDestroy(*x);
+      }
+    } events{{&ea, &eb, &fork, &join}};
     QVB_CUDA(cudaEventRecord(ea, s));
 
     // seed starts of every frontier, [H+1][nseeds+1]
@@ -835,6 +922,7 @@ extern "C" int qvb_batch_sample(qvb_sampler* sp, const uint64_t* seeds, uint64_t
     k_hop0<<<grid_for(nseeds + 1, kBlock), kBlock, 0, s>>>(dseeds.p, nseeds, fn[0].p, fs[0].p, ss.p);
     QVB_LAUNCH_CHECK();
     DevBuf<unsigned long long> nlarge(1, s);
+    DevBuf<uint64_t> hop_state(nseeds ? nseeds : 1, s);
     for (uint32_t k = 1; k <= H; ++k) {
       const uint64_t P = fsize[k - 1];
       DevBuf<uint32_t> m(P + 1, s), large(P ? P : 1, s);
@@ -846,7 +934,8 @@ extern "C" int qvb_batch_sample(qvb_sampler* sp, const uint64_t* seeds, uint64_t
       exclusive_sum_u32_u64(m.p, O.p, P + 1, s);
       uint64_t* ssk = ss.p + (uint64_t)k * (nseeds + 1);
       k_seed_starts<<<grid_for(nseeds + 1, kBlock), kBlock, 0, s>>>(
-          ss.p + (uint64_t)(k - 1) * (nseeds + 1), O.p, nseeds, ssk);
+          ss.p + (uint64_t)(k - 1) * (nseeds + 1), O.p, nseeds, ssk, dseeds.p, rng_seed, k,
+          hop_state.p);
       QVB_LAUNCH_CHECK();
       const uint64_t C = read_scalar(O.p + P, s);
       if (C >= 0xFFFFFFFFull) fail(QVB_ERR_UNSUPPORTED, "frontier exceeds 2^32 instances");
@@ -855,16 +944,20 @@ extern "C" int qvb_batch_sample(qvb_sampler* sp, const uint64_t* seeds, uint64_t
       fs[k].alloc(C ? C : 1, s);
       if (P == 0) continue;
       HopArgs a{fn[k - 1].p, fs[k - 1].p, P,         ss.p + (uint64_t)(k - 1) * (nseeds + 1),
-                O.p,         dseeds.p,    rng_seed,  k,
+                O.p,         hop_state.p, k,
                 fanouts[k - 1], sp->cro,  sp->ccol,  sp->cw,
                 sp->cpos,    fn[k].p,     fs[k].p};
-      k_hop_sample<<<warp_grid(P), kBlock, 0, s>>>(a);
-      QVB_LAUNCH_CHECK();
-      if (sp->scratch) {
-        k_hop_sample_large<<<sp->large_warps / kWarpsPerBlock, kBlock, 0, s>>>(
+      if (sp->scratch) {  // fork: long rows on the side stream, concurrently
+        QVB_CUDA(cudaEventRecord(fork, s));
+        QVB_CUDA(cudaStreamWaitEvent(sp->side, fork, 0));
+        k_hop_sample_large<<<sp->large_ctas, kBlock, 0, sp->side>>>(
             a, large.p, nlarge.p, sp->scratch, sp->max_len);
         QVB_LAUNCH_CHECK();
+        QVB_CUDA(cudaEventRecord(join, sp->side));
       }
+      k_hop_sample<<<warp_grid(P), kBlock, 0, s>>>(a);
+      QVB_LAUNCH_CHECK();
+      if (sp->scratch) QVB_CUDA(cudaStreamWaitEvent(s, join, 0));
     }
     // flatten: instance_counts (seed-major) -> offsets -> scatter
     const uint64_t ncounts = nseeds * (H + 1);
@@ -902,8 +995,6 @@ extern "C" int qvb_batch_sample(qvb_sampler* sp, const uint64_t* seeds, uint64_t
     QVB_CUDA(cudaEventSynchronize(eb));
     float ms = 0;
     QVB_CUDA(cudaEventElapsedTime(&ms, ea, eb));
-    cudaEventDestroy(ea);
-    cudaEventDestroy(eb);
     r->ms = ms;
     r->total = total;
     r->unique_count = uc;
