@@ -16,7 +16,10 @@ its own batches (weak scaling; no data-path collective).
 the same through the public C-ABI from pinned host buffers (H2D ids, gather,
 D2H rows, sync) every step. The line also carries the P(n,j) pass
 (`access_prob`: edges/s, its roofline and the reference CPU timing), the
-`roofline` of the dominant gather kernel and the `cpu_baseline`.
+request-ID producer upstream of the collect call (`sampler`: qv_bench's
+batch_sample of 4096 seeds with fanouts {15, 10}, instances/s vs the
+reference's OpenMP batch_sample), the `roofline` of the dominant gather
+kernel and the `cpu_baseline`.
 """
 from __future__ import annotations
 
@@ -177,6 +180,10 @@ def run_ours(args):
     }
     g.close()
 
+    # ---- K0 sampler: qv_bench's batch_sample (tools/bench.cpp:89-94) ----------
+    sampler, sample_first = (sampler_leg(args, qvb, cfg, local, stream, rank) if args.sample_seeds
+                             else (None, None))
+
     # ---- placement + store ------------------------------------------------------
     topo = D.topology_for(qvb, n, world, args.replicate, args.host_frac)
     t0 = time.perf_counter()
@@ -299,6 +306,8 @@ def run_ours(args):
         cpu, ap_cpu = cpu_baseline(args, cfg, p_host, topo_host=topo, ro=ro, col=col, w=w,
                                    steps=min(args.steps, args.cpu_steps))
         access_prob["cpu_baseline"] = ap_cpu
+        if sampler is not None:
+            sampler["cpu_baseline"] = sampler_cpu(args, cfg, ro, col, w, sample_first)
 
     line = {
         "metric": METRIC,
@@ -333,6 +342,7 @@ def run_ours(args):
         "e2e": e2e,
         "gpu_launches": args.steps,
         "access_prob": access_prob,
+        "sampler": sampler,
         "planner": planner,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
@@ -351,6 +361,86 @@ def run_ours(args):
     store.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+SAMPLE_FANOUTS = [15, 10]  # tools/bench.cpp:66
+SAMPLE_RNG = 3               # tools/bench.cpp:92
+
+
+def sample_seeds(n, k, count):
+    """Seed batch k: derive_stream(11, 0x5EED, k).below(n) — batch 0 is qv_bench's."""
+    from tests.util import derive_stream
+    import numpy as np
+
+    st = derive_stream(11, 0x5EED, k)
+    return np.array([st.below(n) for _ in range(count)], np.uint64)
+
+
+def sampler_leg(args, qvb, cfg, local, stream, rank):
+    import numpy as np
+
+    S = args.sample_seeds
+    smp = qvb.Sampler.synthetic(cfg["n"], cfg["e"], 7, cfg["weighted"], device=local, stream=stream)
+    info = smp.info()
+    batches = [sample_seeds(cfg["n"], rank * 1_000_003 + k, S) for k in range(args.warmup + args.steps)]
+    for k in range(args.warmup):
+        smp.batch_sample(batches[k], SAMPLE_FANOUTS, SAMPLE_RNG, stream=stream).close()
+    dev_ms, wall_ms, inst, uniq = [], [], 0, 0
+    first = None
+    for k in range(args.steps):
+        t0 = time.perf_counter()
+        r = smp.batch_sample(batches[args.warmup + k], SAMPLE_FANOUTS, SAMPLE_RNG, stream=stream)
+        u = r.arrays()[2] if k == 0 else None  # e2e of the first: unique ids back on the host
+        wall_ms.append((time.perf_counter() - t0) * 1e3)
+        i = r.info()
+        dev_ms.append(i.device_ms)
+        inst += i.total_instances
+        uniq += i.unique_count
+        if k == 0:
+            first = (r.arrays(), u)
+        r.close()
+    smp.close()
+    ms = statistics.mean(dev_ms)
+    return {
+        "metric": "sampled node instances/s (batch_sample, device time per call)",
+        "value": inst / (sum(dev_ms) / 1e3), "unit": "instances/s",
+        "ms_per_batch": ms, "seeds_per_batch": S, "fanouts": SAMPLE_FANOUTS,
+        "rng_seed": SAMPLE_RNG, "instances_per_batch": inst / args.steps,
+        "unique_per_batch": uniq / args.steps,
+        "e2e": {"value": inst / (sum(wall_ms) / 1e3), "unit": "instances/s",
+                "ms_per_batch": statistics.mean(wall_ms), "h2d_bytes_per_step": S * 8,
+                "d2h_bytes_per_step": int(len(first[1]) * 8),
+                "note": "qvb_batch_sample from host seeds (wall clock; first batch also copies "
+                        "the sorted unique ids back)"},
+        "candidates": {"count": info.candidates, "parallel_edges": bool(info.parallel_edges),
+                       "max_row": info.max_candidates, "build_ms": info.build_ms,
+                       "device_bytes": info.device_bytes},
+        "gpu_launches_per_batch": 12 + 8 * len(SAMPLE_FANOUTS),
+    }, first
+
+
+def sampler_cpu(args, cfg, ro, col, w, first):
+    """The reference's OpenMP batch_sample on the same graph and first batch."""
+    from oracle.oracle import Oracle, RefLib
+
+    ref = RefLib() if RefLib.available() else None
+    lib = ref or Oracle()
+    if ro is None:
+        ro, col, w = Oracle().synthetic_graph(cfg["n"], cfg["e"], 7, cfg["weighted"], False)
+    threads = os.cpu_count() or 1
+    seeds = sample_seeds(cfg["n"], args.warmup, args.sample_seeds)
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        res = lib.batch_sample(ro, col, w, seeds, SAMPLE_FANOUTS, SAMPLE_RNG)
+        ts.append(ref.last_ms / 1e3 if ref else time.perf_counter() - t0)
+    same = all((a == b).all() for a, b in zip(res, first[0]))
+    s = min(ts)
+    return {"value": len(res[0]) / s, "unit": "instances/s", "ms_per_batch": s * 1e3,
+            "cores": threads if ref else 1, "kind": "reference" if ref else "port",
+            "sample": f"qv::batch_sample({args.sample_seeds} seeds, {{15, 10}}, 3) on the "
+                      f"{cfg['desc']} graph, best of 3 (transition_view excluded)",
+            "identical_to_gpu": bool(same)}
 
 
 def cpu_baseline(args, cfg, p_host, topo_host, ro, col, w, steps):
@@ -438,6 +528,17 @@ def run_reference(args):
     t0 = time.perf_counter()
     p = ref.access_prob(ro, col, w, cfg["layers"], True) if ref else o.access_prob(ro, col, w, cfg["layers"])
     ap_s = time.perf_counter() - t0
+    sampler = None
+    if args.sample_seeds:  # qv_bench's batch_sample leg (tools/bench.cpp:89-94)
+        seeds = sample_seeds(n, args.warmup, args.sample_seeds)
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            res = lib.batch_sample(ro, col, w, seeds, SAMPLE_FANOUTS, SAMPLE_RNG)
+            ts.append(ref.last_ms / 1e3 if ref else time.perf_counter() - t0)
+        sampler = {"value": len(res[0]) / min(ts), "unit": "instances/s",
+                   "ms_per_batch": min(ts) * 1e3, "seeds_per_batch": args.sample_seeds,
+                   "cores": threads if ref else 1}
     t = topology_defaults(gpus_per_server=1, gpu_feature_capacity=n, host_feature_capacity=n)
     lo, ids = lib.plan_placement(p, t)
     loc, off = lib.build_lookup_table(lo, ids, t, 0)
@@ -469,6 +570,7 @@ def run_reference(args):
         "access_prob": {"value": cfg["e"] * (cfg["layers"] - 1) / ap_s,
                         "unit": "edges/s (input edges)", "seconds": ap_s, "kind": kind,
                         "cores": threads},
+        "sampler": sampler,
     }
     print(json.dumps(line), flush=True)
 
@@ -487,6 +589,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sample-seeds", type=int, default=4096,
+                    help="seeds per batch_sample call of the sampler leg (0: skip)")
     ap.add_argument("--planned", action="store_true", help="location-bucketed, offset-sorted gather (K4 order)")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -218,6 +218,128 @@ FapTable compute_fap(const TransitionView& t, std::uint32_t hops,
 }
 }  // namespace serial
 
+// ---- sampler ------------------------------------------------------------------
+void SamplingConfig::validate() const {
+  if (fanouts.empty()) throw ValidationError("sampling config needs >= 1 hop");
+  for (std::uint32_t l : fanouts)
+    if (l < 1) throw ValidationError("fanouts must be >= 1");
+}
+
+namespace {
+struct SampleHandle {
+  qvb_sample* r = nullptr;
+  ~SampleHandle() {
+    if (r) qvb_sample_destroy(r);
+  }
+};
+
+qvb_sample* run_batch(qvb_sampler* s, std::span<const NodeId> seeds, const SamplingConfig& cfg,
+                      std::uint64_t rng_seed, SampleHandle& h) {
+  cfg.validate();
+  check(qvb_batch_sample(s, seeds.data(), seeds.size(), 0, cfg.fanouts.data(),
+                         static_cast<std::uint32_t>(cfg.fanouts.size()), rng_seed, nullptr, &h.r));
+  return h.r;
+}
+
+// splitmix64 (rng.hpp:10-16) inverted: batch_sample runs seed s under
+// splitmix64(rng ^ s*gamma), so sample_khop(seed, rs) is the one-seed batch
+// with rng = splitmix64^-1(rs) ^ seed*gamma.
+std::uint64_t inv_mul(std::uint64_t c) {
+  std::uint64_t x = c;  // Newton: x <- x(2 - cx) doubles the correct bits
+  for (int i = 0; i < 6; ++i) x *= 2 - c * x;
+  return x;
+}
+std::uint64_t unxorshift(std::uint64_t y, int s) {
+  std::uint64_t x = y;
+  for (int i = 0; i < 64 / s + 1; ++i) x = y ^ (x >> s);
+  return x;
+}
+std::uint64_t unsplitmix64(std::uint64_t z) {
+  z = unxorshift(z, 31);
+  z *= inv_mul(0x94d049bb133111ebULL);
+  z = unxorshift(z, 27);
+  z *= inv_mul(0xbf58476d1ce4e5b9ULL);
+  z = unxorshift(z, 30);
+  return z - 0x9e3779b97f4a7c15ULL;
+}
+}  // namespace
+
+Sampler::Sampler(const Graph& g, int device) {
+  check(qvb_sampler_create(device >= 0 ? device : default_device(), g.node_count, g.edge_count,
+                           g.row_offsets.data(), g.col_indices.data(),
+                           g.edge_weights.empty() ? nullptr : g.edge_weights.data(), nullptr, &s_));
+}
+
+Sampler::~Sampler() {
+  if (s_) qvb_sampler_destroy(s_);
+}
+
+BatchSampleStats Sampler::batch_stats(std::span<const NodeId> seeds, const SamplingConfig& cfg,
+                                      std::uint64_t rng_seed) const {
+  SampleHandle h;
+  run_batch(s_, seeds, cfg, rng_seed, h);
+  qvb_sample_info info;
+  check(qvb_sample_info_get(h.r, &info));
+  BatchSampleStats st;
+  st.total_instances = info.total_instances;
+  st.unique_count = info.unique_count;
+  st.unique_nodes.resize(info.unique_count);
+  check(qvb_sample_copy(h.r, nullptr, nullptr, st.unique_nodes.data()));
+  return st;
+}
+
+BatchSampleResult Sampler::batch_sample(std::span<const NodeId> seeds, const SamplingConfig& cfg,
+                                        std::uint64_t rng_seed) const {
+  SampleHandle h;
+  run_batch(s_, seeds, cfg, rng_seed, h);
+  qvb_sample_info info;
+  check(qvb_sample_info_get(h.r, &info));
+  const std::size_t H = cfg.hops();
+  std::vector<std::uint64_t> nodes(info.total_instances), counts(seeds.size() * (H + 1));
+  BatchSampleResult out;
+  out.stats.total_instances = info.total_instances;
+  out.stats.unique_count = info.unique_count;
+  out.stats.unique_nodes.resize(info.unique_count);
+  check(qvb_sample_copy(h.r, nodes.data(), counts.data(), out.stats.unique_nodes.data()));
+  out.per_seed.resize(seeds.size());
+  std::size_t at = 0;
+  for (std::size_t i = 0; i < seeds.size(); ++i) {
+    SampleResult& r = out.per_seed[i];
+    r.seed = seeds[i];
+    r.frontiers.resize(H + 1);
+    r.instance_counts.resize(H + 1);
+    for (std::size_t k = 0; k <= H; ++k) {
+      const std::uint64_t c = counts[i * (H + 1) + k];
+      r.instance_counts[k] = c;
+      r.frontiers[k].assign(nodes.begin() + at, nodes.begin() + at + c);
+      r.unique_nodes.insert(r.unique_nodes.end(), r.frontiers[k].begin(), r.frontiers[k].end());
+      at += c;
+    }
+    std::sort(r.unique_nodes.begin(), r.unique_nodes.end());
+    r.unique_nodes.erase(std::unique(r.unique_nodes.begin(), r.unique_nodes.end()),
+                         r.unique_nodes.end());
+  }
+  return out;
+}
+
+SampleResult sample_khop(const TransitionView& t, NodeId seed, const SamplingConfig& cfg,
+                         std::uint64_t rng_seed) {
+  cfg.validate();
+  if (seed >= t.node_count())
+    throw ValidationError("sample seed " + std::to_string(seed) + " out of range");
+  const NodeId one[1] = {seed};
+  Sampler s(*t.graph);
+  const std::uint64_t rng = unsplitmix64(rng_seed) ^ (seed * 0x9e3779b97f4a7c15ULL);
+  return std::move(s.batch_sample(one, cfg, rng).per_seed[0]);
+}
+
+BatchSampleResult batch_sample(const TransitionView& t, std::span<const NodeId> seeds,
+                               const SamplingConfig& cfg, std::uint64_t rng_seed) {
+  cfg.validate();
+  Sampler s(*t.graph);
+  return s.batch_sample(seeds, cfg, rng_seed);
+}
+
 // ---- topology -------------------------------------------------------------------
 const char* link_class_name(LinkClass c) {
   static const char* names[] = {"local", "nvlink", "pcie", "upi", "infiniband", "ethernet", "disk"};

@@ -12,6 +12,7 @@
 //   graph.hpp:25-48   Graph / Edge / from_edges / validate
 //   graph.hpp:72-93   in_adjacency (device transpose) / TransitionView
 //   metrics.hpp:32-64 FapTable / AccessProbTable / compute_access_prob_ie
+//   sampler.hpp:11-53 SamplingConfig / SampleResult / sample_khop / batch_sample
 //   topology.hpp:11-54 LinkClass / LinkSpec / ClusterTopology
 //   placement.hpp:14-121 Tier / Location / PlacementPlan / plan_placement /
 //                     FeatureLookupTable / build_lookup_table / ReadPlan /
@@ -29,6 +30,7 @@
 #include <vector>
 
 struct qvb_store;
+struct qvb_sampler;
 
 namespace qv {
 
@@ -128,6 +130,61 @@ AccessProbTable compute_access_prob_ie(const Graph& g, const TransitionView& t,
 FapTable compute_fap(const TransitionView& t, std::uint32_t hops,
                      std::optional<std::span<const double>> seed_dist = {});
 }
+
+// ---- sampler (sampler.hpp:11-53, metrics.hpp:14-19) ----------------------------
+struct SamplingConfig {
+  std::vector<std::uint32_t> fanouts;
+  std::size_t hops() const { return fanouts.size(); }
+  void validate() const;  // metrics.cpp:13-18
+};
+
+struct SampleResult {
+  NodeId seed = 0;
+  std::vector<std::vector<NodeId>> frontiers;  // index 0 is {seed}
+  std::vector<std::uint64_t> instance_counts;  // per hop
+  std::vector<NodeId> unique_nodes;            // sorted, across all hops
+  std::uint64_t total_instances() const {
+    std::uint64_t n = 0;
+    for (std::uint64_t c : instance_counts) n += c;
+    return n;
+  }
+};
+
+struct BatchSampleStats {
+  std::uint64_t total_instances = 0;
+  std::uint64_t unique_count = 0;
+  std::vector<NodeId> unique_nodes;  // sorted union
+};
+
+struct BatchSampleResult {
+  std::vector<SampleResult> per_seed;
+  BatchSampleStats stats;
+};
+
+// The device-resident sampling candidates of one graph (qvb_sampler), for
+// many batches; the free functions below build one per call.
+class Sampler {
+ public:
+  explicit Sampler(const Graph& g, int device = -1);
+  ~Sampler();
+  Sampler(const Sampler&) = delete;
+  Sampler& operator=(const Sampler&) = delete;
+  BatchSampleResult batch_sample(std::span<const NodeId> seeds, const SamplingConfig& cfg,
+                                 std::uint64_t rng_seed) const;
+  // Only the sorted union (what simulator.cpp:250-254 keeps), no per-seed copy.
+  BatchSampleStats batch_stats(std::span<const NodeId> seeds, const SamplingConfig& cfg,
+                               std::uint64_t rng_seed) const;
+
+ private:
+  qvb_sampler* s_ = nullptr;
+};
+
+// sample_khop (sampler.cpp:56-112) / batch_sample (:114-149) on the GPU,
+// identical frontiers.
+SampleResult sample_khop(const TransitionView& t, NodeId seed, const SamplingConfig& cfg,
+                         std::uint64_t rng_seed);
+BatchSampleResult batch_sample(const TransitionView& t, std::span<const NodeId> seeds,
+                               const SamplingConfig& cfg, std::uint64_t rng_seed);
 
 // ---- topology (topology.hpp:11-54) -------------------------------------------
 enum class LinkClass : std::uint8_t { local = 0, nvlink, pcie, upi, infiniband, ethernet, disk };

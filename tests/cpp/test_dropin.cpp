@@ -287,6 +287,62 @@ int main(int argc, char** argv) {
     CHECK_THROWS_AS(store.gather(std::vector<NodeId>{n}), ValidationError, "outside lookup table");
   }
 
+  // --- sampler: test_sampler.cpp:15-150, vs the oracle restatement ------------
+  {
+    Graph g = fig8_graph();
+    TransitionView t = transition_view(g);
+    SampleResult r = sample_khop(t, 4, SamplingConfig{{10, 10}}, 1);
+    CHECK(r.frontiers[0] == std::vector<NodeId>{4});
+    CHECK(r.frontiers[1] == std::vector<NodeId>{0});
+    CHECK((std::set<NodeId>(r.frontiers[2].begin(), r.frontiers[2].end()) == std::set<NodeId>{3, 5}));
+    CHECK(r.total_instances() == 4);
+    Graph c3 = Graph::from_edges(3, std::vector<Edge>{{0, 1, 1.0}, {1, 2, 1.0}});
+    SampleResult c = sample_khop(transition_view(c3), 0, SamplingConfig{{1, 1}}, 99);
+    CHECK(c.frontiers[2] == std::vector<NodeId>{2});
+    CHECK_THROWS_AS(sample_khop(transition_view(c3), 3, SamplingConfig{{1}}, 1), ValidationError,
+                    "out of range");
+    std::vector<NodeId> bad = {0, 7};
+    CHECK_THROWS_AS(batch_sample(transition_view(c3), bad, SamplingConfig{{1}}, 1), ValidationError,
+                    "position 1");
+    CHECK_THROWS_AS(batch_sample(t, bad, SamplingConfig{{}}, 1), ValidationError, ">= 1 hop");
+    std::vector<NodeId> none;
+    BatchSampleResult e = batch_sample(t, none, SamplingConfig{{2, 2}}, 5);
+    CHECK(e.per_seed.empty() && e.stats.total_instances == 0 && e.stats.unique_count == 0);
+    std::vector<NodeId> dup = {0, 0, 3, 0};
+    BatchSampleResult d = batch_sample(t, dup, SamplingConfig{{2, 2}}, 7);
+    CHECK(d.per_seed[0].frontiers == d.per_seed[1].frontiers);
+    CHECK(d.per_seed[0].frontiers == d.per_seed[3].frontiers);
+  }
+  g_state = 0x5A4D;
+  for (int it = 0; it < 20; ++it) {
+    Graph g = random_graph(50, 400, it % 2 == 0);
+    TransitionView t = transition_view(g);
+    SamplingConfig cfg{{static_cast<uint32_t>(1 + below(4)), static_cast<uint32_t>(1 + below(4))}};
+    std::vector<NodeId> seeds(30);
+    for (auto& s : seeds) s = below(g.node_count);
+    const uint64_t rng = 1000 + it;
+    Sampler smp(g);
+    BatchSampleResult r = smp.batch_sample(seeds, cfg, rng);
+    uint64_t total = 0, uc = 0;
+    qvo_batch_sample(g.node_count, g.edge_count, g.row_offsets.data(), g.col_indices.data(),
+                     g.edge_weights.data(), seeds.data(), seeds.size(), cfg.fanouts.data(), 2, rng,
+                     &total, &uc, nullptr, nullptr, nullptr);
+    std::vector<uint64_t> nodes(total), counts(seeds.size() * 3), uniq(uc);
+    qvo_batch_sample(g.node_count, g.edge_count, g.row_offsets.data(), g.col_indices.data(),
+                     g.edge_weights.data(), seeds.data(), seeds.size(), cfg.fanouts.data(), 2, rng,
+                     &total, &uc, nodes.data(), counts.data(), uniq.data());
+    std::vector<uint64_t> flat;
+    for (const SampleResult& sr : r.per_seed)
+      for (const auto& f : sr.frontiers) flat.insert(flat.end(), f.begin(), f.end());
+    CHECK(flat == nodes);
+    CHECK(r.stats.unique_nodes == uniq);
+    CHECK(smp.batch_stats(seeds, cfg, rng).unique_nodes == uniq);
+    // sample_khop(seed, rs) == the seed's part of a batch run under rng
+    const NodeId s0 = seeds[0];
+    const uint64_t rs = qvo_splitmix64(rng ^ (s0 * 0x9e3779b97f4a7c15ULL));
+    CHECK(sample_khop(t, s0, cfg, rs).frontiers == r.per_seed[0].frontiers);
+  }
+
   std::printf("test_dropin: %d checks, %d failed\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }
