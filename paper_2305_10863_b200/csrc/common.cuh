@@ -179,13 +179,19 @@ __device__ __forceinline__ uint64_t ld_stream(const uint64_t* a, uint64_t pol) {
                : "l"(a), "l"(pol));
   return v;
 }
+__device__ __forceinline__ uint32_t ld_hint(const uint32_t* a, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ double ld_hint(const double* a, uint64_t pol) {
   double v;
   asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
   return v;
 }
 // Gather of one operand: mode 0 = ld.global.nc (read-only path, L1 allocate),
-// 1 = ld.global.nc.L1::no_allocate, 2 = ld.global.cg (L2 only), 3 = .L2::evict_last.
+// 1 = ld.global.nc.L1::no_allocate, 2 = ld.global.cg (L2 only), 3 = .L2::evict_last,
+// 9 = timing experiment only (wrong results): every gather hits one 8 KB block.
 __device__ __forceinline__ double ld_gather(const double* a, int mode) {
   double v;
   if (mode == 1) {
@@ -198,6 +204,8 @@ __device__ __forceinline__ double ld_gather(const double* a, int mode) {
         " ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], p;\n}"
         : "=d"(v)
         : "l"(a));
+  } else if (mode == 9) {
+    v = __ldg(reinterpret_cast<const double*>(reinterpret_cast<uint64_t>(a) & ~0x1FF8ull));
   } else {
     v = __ldg(a);
   }

@@ -44,9 +44,14 @@ qvb_graph::~qvb_graph() {
   cudaFree(exc_R);
   cudaFree(inv);
   cudaFree(state);
+  cudaFree(nm_lenf);
+  cudaFree(nm_sbase);
+  cudaFree(nm_col);
+  cudaFree(nm_R);
   for (int i = 0; i < 2; ++i) {
     cudaFree(p[i]);
     cudaFree(y[i]);
+    cudaFree(kcode[i]);
     if (ev[i]) cudaEventDestroy(ev[i]);
   }
   if (prev >= 0) cudaSetDevice(prev);
@@ -453,6 +458,87 @@ T* persist(DevBuf<T>& b) {
   return b.release_ownership();
 }
 
+// ---- node-major segmented layout (graph.cuh "nm") --------------------------
+// Per node: its sources per segment (rows are source-sorted, so one walk),
+// flagged with the first and last pass that touch it. Long rows (> thr) stay
+// 0 everywhere (long path); in-degree-0 nodes finish in pass 0.
+__global__ void k_nm_lens(const uint64_t* __restrict__ uptr, const uint32_t* __restrict__ src,
+                          uint64_t n, uint64_t npad, uint32_t thr, uint64_t seg,
+                          uint8_t* __restrict__ lenf) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = uptr[v], b = uptr[v + 1];
+    if (b - a > thr) continue;
+    if (b == a) {
+      lenf[v] = kNmFirst | kNmLast;
+      continue;
+    }
+    bool first = true;
+    uint64_t u = a;
+    while (u < b) {
+      const uint64_t k = src[u] / seg;
+      uint32_t cnt = 0;
+      while (u < b && src[u] / seg == k) {
+        ++u;
+        ++cnt;
+      }
+      uint8_t f = static_cast<uint8_t>(cnt);
+      if (first) f |= kNmFirst;
+      if (u == b) f |= kNmLast;
+      first = false;
+      lenf[k * npad + v] = f;
+    }
+  }
+}
+
+// Columns of slice (k, s): sum of its 32 lens; entry nseg*S is 0.
+__global__ void k_nm_slice_sums(const uint8_t* __restrict__ lenf, uint64_t S, int nseg,
+                                uint32_t* __restrict__ cnt) {
+  const uint64_t total = S * nseg;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x <= total;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    if (x == total) {
+      cnt[x] = 0;
+      continue;
+    }
+    const uint8_t* l = lenf + x * 32;  // (k, s) -> k*S*32 + s*32 == x*32
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) c += l[i] & kNmLen;
+    cnt[x] = c;
+  }
+}
+
+// One warp per slice: lane = node; pass by pass, the lane's next len sources
+// go to sbase(k, s) + (prefix of the slice's lens).
+__global__ void k_nm_fill(const uint64_t* __restrict__ uptr, const uint32_t* __restrict__ col,
+                          const double* __restrict__ R, const uint8_t* __restrict__ lenf,
+                          const uint64_t* __restrict__ sbase, uint64_t n, uint64_t S, int nseg,
+                          uint32_t* __restrict__ ncol, double* __restrict__ nR) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  for (uint64_t sl = blockIdx.x * (uint64_t)(blockDim.x / 32) + (threadIdx.x >> 5); sl < S;
+       sl += warps) {
+    const uint64_t v = sl * 32 + lane;
+    uint64_t u = v < n ? uptr[v] : 0;
+    for (int k = 0; k < nseg; ++k) {
+      const uint32_t len = lenf[(uint64_t)k * S * 32 + v] & kNmLen;
+      uint32_t incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const uint64_t dst = sbase[(uint64_t)k * S + sl] + (incl - len);
+      for (uint32_t t = 0; t < len; ++t) {
+        ncol[dst + t] = col[u + t];
+        if (R) nR[dst + t] = R[u + t];
+      }
+      u += len;
+    }
+  }
+}
+
 }  // namespace
 
 void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, const double* d_w,
@@ -568,6 +654,89 @@ uint64_t segment_size(uint64_t n) {
   return std::min<uint64_t>(seg, std::max<uint64_t>(n, 1));
 }
 
+// Rows with in-degree above thr: a plain CSR, one warp per row.
+void build_long_rows(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const double* R,
+                     uint32_t thr, cudaStream_t s) {
+  const uint64_t n = g.n;
+  DevBuf<uint8_t> mark(n, s);
+  DevBuf<uint32_t> lidx(n, s);
+  k_long_marks<<<grid_for(n, kBlock), kBlock, 0, s>>>(uptr, n, thr, mark.p);
+  QVB_LAUNCH_CHECK();
+  exclusive_sum_u8_u32(mark.p, lidx.p, n, s);
+  g.nlong = (uint64_t)read_scalar(lidx.p + (n - 1), s) + read_scalar(mark.p + (n - 1), s);
+  if (g.nlong) {
+    const uint64_t L = g.nlong;
+    DevBuf<uint32_t> lnode(L, s), ldeg(L + 1, s);
+    DevBuf<uint64_t> lptr(L + 1, s);
+    k_long_list<<<grid_for(n, kBlock), kBlock, 0, s>>>(mark.p, lidx.p, uptr, n, lnode.p, ldeg.p);
+    QVB_LAUNCH_CHECK();
+    QVB_CUDA(cudaMemsetAsync(ldeg.p + L, 0, sizeof(uint32_t), s));
+    exclusive_sum_u32_u64(ldeg.p, lptr.p, L + 1, s);
+    const uint64_t lsum = read_scalar(lptr.p + L, s);
+    DevBuf<uint32_t> lcol(lsum, s);
+    DevBuf<double> lR;
+    if (R) lR.alloc(lsum, s);
+    k_long_copy<<<static_cast<unsigned>((L * 32 + kBlock - 1) / kBlock), kBlock, 0, s>>>(
+        lnode.p, lptr.p, uptr, col, R, L, lcol.p, lR.p);
+    QVB_LAUNCH_CHECK();
+    g.lnode = persist(lnode);
+    g.lptr = persist(lptr);
+    g.lcol = persist(lcol);
+    g.lR = lR.p ? persist(lR) : nullptr;
+    g.bytes += L * 12 + lsum * (R ? 12 : 4);
+  }
+}
+
+// The nm layout (graph.cuh) for more than one source segment.
+void build_nm(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const uint32_t* src,
+              const double* R, cudaStream_t s) {
+  const uint64_t n = g.n;
+  const uint32_t thr = std::min<uint32_t>(g.long_threshold, kNmLen);
+  g.long_threshold = thr;
+  // compact sweeps gather 4-byte codes: twice the sources per segment, and
+  // by default a 96 MiB code slice (measured best at C4: fewer passes beat
+  // the L2 hit rate lost above ~64 MiB, experiments/l2_capacity.cu)
+  uint64_t seg = R ? g.seg_size : g.seg_size * 2;
+  if (!R && !std::getenv("QVB_SEG_MB") && !std::getenv("QVB_SEG_SOURCES")) seg = (96ull << 20) / 4;
+  seg = std::min<uint64_t>(n, seg);
+  g.seg_size = seg;
+  const int nseg = static_cast<int>((n + seg - 1) / seg);
+  if (nseg > 255) fail(QVB_ERR_UNSUPPORTED, "too many source segments (raise QVB_SEG_MB)");
+  g.seg_slice.assign(nseg + 1, 0);
+  const uint64_t S = (n + 31) / 32, npad = S * 32;
+  DevBuf<uint8_t> lenf(npad * nseg, s);
+  QVB_CUDA(cudaMemsetAsync(lenf.p, 0, npad * nseg, s));
+  k_nm_lens<<<grid_for(n, kBlock), kBlock, 0, s>>>(uptr, src, n, npad, thr, seg, lenf.p);
+  QVB_LAUNCH_CHECK();
+  DevBuf<uint32_t> cnt(S * nseg + 1, s);
+  DevBuf<uint64_t> sbase(S * nseg + 3, s);  // +2: 16-byte bulk-copy windows
+  k_nm_slice_sums<<<grid_for(S * nseg + 1, kBlock), kBlock, 0, s>>>(lenf.p, S, nseg, cnt.p);
+  QVB_LAUNCH_CHECK();
+  exclusive_sum_u32_u64(cnt.p, sbase.p, S * nseg + 1, s);
+  cnt.release();
+  const uint64_t total = read_scalar(sbase.p + S * nseg, s);
+  DevBuf<uint32_t> ncol(total + 4, s);  // +4: 16-byte bulk-copy windows
+  DevBuf<double> nR;
+  if (R) nR.alloc(total ? total : 1, s);
+  k_nm_fill<<<grid_for(S * 32, kBlock), kBlock, 0, s>>>(uptr, col, R, lenf.p, sbase.p, n, S, nseg,
+                                                        ncol.p, nR.p);
+  QVB_LAUNCH_CHECK();
+  QVB_CUDA(cudaMalloc(&g.state, npad * sizeof(double)));  // whole slices: bulk-copied
+  QVB_CUDA(cudaMemsetAsync(sbase.p + S * nseg + 1, 0, 2 * sizeof(uint64_t), s));
+  QVB_CUDA(cudaMemsetAsync(ncol.p + total, 0, 4 * sizeof(uint32_t), s));
+  build_long_rows(g, uptr, col, R, thr, s);
+  g.nm = true;
+  g.nm_S = S;
+  g.nm_cols = total;
+  g.slots = total;
+  g.nslices = 0;
+  g.nm_lenf = persist(lenf);
+  g.nm_sbase = persist(sbase);
+  g.nm_col = persist(ncol);
+  g.nm_R = nR.p ? persist(nR) : nullptr;
+  g.bytes += npad * nseg + (S * nseg + 1) * 8 + total * (R ? 12 : 4) + n * 8;
+}
+
 void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const uint32_t* src,
                   const double* R, cudaStream_t s) {
   const uint64_t n = g.n;
@@ -575,6 +744,11 @@ void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const
   g.long_threshold = static_cast<uint32_t>(std::max<uint64_t>(64, 4 * avg));
   const uint32_t thr = g.long_threshold;
   g.seg_size = g.seg_size ? g.seg_size : segment_size(n);
+  const char* layout_env = std::getenv("QVB_SEG_LAYOUT");
+  if (n > g.seg_size && !(layout_env && std::string(layout_env) == "slices")) {
+    build_nm(g, uptr, col, src, R, s);
+    return;
+  }
   const uint64_t seg = g.seg_size;
   const int nseg = static_cast<int>((n + seg - 1) / seg);
   if (nseg > 255) fail(QVB_ERR_UNSUPPORTED, "too many source segments (raise QVB_SEG_MB)");
@@ -648,34 +822,7 @@ void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const
   QVB_LAUNCH_CHECK();
   if (nseg > 1) QVB_CUDA(cudaMalloc(&g.state, n * sizeof(double)));
 
-  // long rows
-  DevBuf<uint8_t> mark(n, s);
-  DevBuf<uint32_t> lidx(n, s);
-  k_long_marks<<<grid_for(n, kBlock), kBlock, 0, s>>>(uptr, n, thr, mark.p);
-  QVB_LAUNCH_CHECK();
-  exclusive_sum_u8_u32(mark.p, lidx.p, n, s);
-  g.nlong = (uint64_t)read_scalar(lidx.p + (n - 1), s) + read_scalar(mark.p + (n - 1), s);
-  if (g.nlong) {
-    const uint64_t L = g.nlong;
-    DevBuf<uint32_t> lnode(L, s), ldeg(L + 1, s);
-    DevBuf<uint64_t> lptr(L + 1, s);
-    k_long_list<<<grid_for(n, kBlock), kBlock, 0, s>>>(mark.p, lidx.p, uptr, n, lnode.p, ldeg.p);
-    QVB_LAUNCH_CHECK();
-    QVB_CUDA(cudaMemsetAsync(ldeg.p + L, 0, sizeof(uint32_t), s));
-    exclusive_sum_u32_u64(ldeg.p, lptr.p, L + 1, s);
-    const uint64_t lsum = read_scalar(lptr.p + L, s);
-    DevBuf<uint32_t> lcol(lsum, s);
-    DevBuf<double> lR;
-    if (R) lR.alloc(lsum, s);
-    k_long_copy<<<static_cast<unsigned>((L * 32 + kBlock - 1) / kBlock), kBlock, 0, s>>>(
-        lnode.p, lptr.p, uptr, col, R, L, lcol.p, lR.p);
-    QVB_LAUNCH_CHECK();
-    g.lnode = persist(lnode);
-    g.lptr = persist(lptr);
-    g.lcol = persist(lcol);
-    g.lR = lR.p ? persist(lR) : nullptr;
-    g.bytes += L * 12 + lsum * (R ? 12 : 4);
-  }
+  build_long_rows(g, uptr, col, R, thr, s);
   g.perm = persist(perm);
   g.sptr = persist(sptr);
   g.scol = persist(scol);

@@ -33,6 +33,26 @@
 // carried between passes (state), and because each in-row is sorted by
 // source, pass order == the reference's factor order: still bit-exact.
 // Each pass has its own slices built only over the nodes it touches.
+//
+// Node-major passes (nm, default when there is more than one segment). The
+// per-pass slices above re-sort every pass's nodes by degree, so the running
+// product is read and written through a scattered perm word per (node, pass)
+// pair and the warp's chain starts with perm -> state and sptr -> columns.
+// The nm layout keeps node v in lane v%32 of slice v/32 in EVERY pass:
+//   nm_lenf  u8[nseg][S*32]  len | first<<6 | last<<7  (len <= 63)
+//   nm_sbase u64[nseg*S+1]   start of slice (k, s)'s columns in nm_col
+//   nm_col   u32 / nm_R f64  each node's pass-k sources (ascending), nodes
+//                            in id order, no padding
+// so the state, P and y accesses are coalesced and need no perm, and a lane
+// finds its columns by a warp prefix sum of the 32 lens. The compact layout
+// then gathers a 4-byte code instead of y (see kcode), which halves the
+// operand bytes and so the number of passes.
+//
+// kcode: round(1 - y) in fp64 depends on y only through J = rint(y * 2^53)
+// while y <= 1/2: the doubles in [1/2, 1] are the multiples of 2^-53, so
+// __dsub_rn(1, y) == 1 - J * 2^-53 exactly (ties: J even <=> result even).
+// kcode[s] = J when J < 2^32 - 1 (y < 2^-21), else kBigCode and the sweep
+// gathers y itself. Both arrays are written by every sweep epilogue.
 #pragma once
 
 #include <vector>
@@ -66,6 +86,15 @@ struct qvb_graph {
   double* inv = nullptr;
   double* p[2] = {nullptr, nullptr};
   double* y[2] = {nullptr, nullptr};
+  // node-major segmented passes
+  bool nm = false;
+  uint64_t nm_S = 0;   // slices of 32 node ids
+  uint64_t nm_cols = 0;
+  uint8_t* nm_lenf = nullptr;
+  uint64_t* nm_sbase = nullptr;
+  uint32_t* nm_col = nullptr;
+  double* nm_R = nullptr;
+  uint32_t* kcode[2] = {nullptr, nullptr};
   uint64_t bytes = 0;
   double build_ms = 0.0;
   cudaEvent_t ev[2] = {nullptr, nullptr};  // bracket the sweeps of the last run
@@ -83,6 +112,8 @@ constexpr uint32_t kNodeMask = 0x3FFFFFFFu;
 constexpr uint32_t kNoNode = kNodeMask;  // padding slot
 constexpr uint32_t kWindow = 256;  // slots sorted together (one CTA of 8 warps)
 constexpr uint64_t kMaxNodes = (1ull << 30) - 2;
+constexpr uint32_t kBigCode = 0xFFFFFFFFu;  // kcode: gather y instead
+constexpr uint8_t kNmFirst = 0x40, kNmLast = 0x80, kNmLen = 0x3F;
 constexpr uint64_t kMaxEdges = 0xFFFFFFFFull;
 
 // Builds the in-CSR from a device out-CSR. d_w == nullptr means unit weights.

@@ -146,11 +146,14 @@ def test_layouts_exercised(qvb, oracle):
     g.close()
 
 
+@pytest.mark.parametrize("layout", ["nm", "slices"])
 @pytest.mark.parametrize("seg_sources", ["1", "7", "1000", "31337"])
-def test_segmented_passes_bit_exact(qvb, oracle, seg_sources, monkeypatch):
+def test_segmented_passes_bit_exact(qvb, oracle, seg_sources, layout, monkeypatch):
     """Force many source segments (passes carrying the running product in
-    source order) on small graphs: results must stay bit-identical."""
+    source order) on small graphs: results must stay bit-identical, for the
+    node-major passes (default) and the per-pass degree-sorted slices."""
     monkeypatch.setenv("QVB_SEG_SOURCES", seg_sources)
+    monkeypatch.setenv("QVB_SEG_LAYOUT", layout)
     rng = derive_stream(79, int(seg_sources))
     if seg_sources in ("1", "7"):  # <= 255 segments: tiny graphs only
         for _ in range(10):
@@ -172,6 +175,20 @@ def test_segmented_passes_bit_exact(qvb, oracle, seg_sources, monkeypatch):
         for layers in (2, 3):
             assert (bits(g.access_prob(layers)) == bits(oracle.access_prob(ro, col, w, layers))).all()
         g.close()
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_c2_node_major_segments_bit_exact(qvb, oracle, weighted, monkeypatch):
+    """C2 split into several source segments (node-major passes). Unweighted
+    P values straddle the 4-byte code range (y < 2^-22 coded, larger y
+    gathered), so both operand paths run; weighted streams R per edge."""
+    c = CONFIGS["C2"]
+    monkeypatch.setenv("QVB_SEG_MB", "4")
+    ro, col, w = oracle.synthetic_graph(c["n"], c["e"], 7, weighted, False)
+    g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, weighted, False)
+    for layers in (2, 3):
+        assert (bits(g.access_prob(layers)) == bits(oracle.access_prob(ro, col, w, layers))).all()
+    g.close()
 
 
 def test_c3_weighted_bit_exact(qvb, oracle):
