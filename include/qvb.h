@@ -111,6 +111,8 @@ typedef struct qvb_graph_info {
   uint32_t device;
   uint64_t device_bytes;       /* HBM held by the graph                     */
   double build_ms;             /* device time of the in-CSR build           */
+  uint32_t classes;            /* first-sweep out-degree classes (0: the first sweep gathers) */
+  uint32_t segments;           /* source segments (passes) of the later sweeps */
 } qvb_graph_info;
 
 /* Upload an out-CSR (qv::Graph layout, graph.hpp:25-48): row_offsets[n+1],

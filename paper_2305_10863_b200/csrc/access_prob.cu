@@ -102,7 +102,7 @@ __device__ __forceinline__ void long_row(uint64_t i, uint64_t nlong,
                                          const double* __restrict__ opnd,
                                          const double* __restrict__ inv, double* __restrict__ out,
                                          double* __restrict__ yout, uint32_t* __restrict__ kout,
-                                         int gmode, uint64_t pol) {
+                                         int gmode, uint64_t pol, double fbase) {
   const int lane = threadIdx.x & 31;
   if (i >= nlong) return;
   const uint64_t a = lptr[i], b = lptr[i + 1];
@@ -116,7 +116,9 @@ __device__ __forceinline__ void long_row(uint64_t i, uint64_t nlong,
       if (e < b) {
         const uint32_t c = ld_stream(lcol + e, pol);
         const double r = kWeighted ? ld_stream(lR + e, pol) : 0.0;
-        const double v = (!kWeighted && (c & kExcFlag)) ? 0.0 : ld_gather(opnd + c, gmode);
+        // weighted first sweep: P(s,1) = fbase for every source, no gather
+        const double v = (!kWeighted && (c & kExcFlag)) ? 0.0
+                         : (kWeighted && fbase != 0.0) ? fbase : ld_gather(opnd + c, gmode);
         f[u] = factor<kWeighted>(c, v, r, exc_src, exc_R, prev);
       }
     }
@@ -184,16 +186,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
             const uint32_t* __restrict__ exc_src, const double* __restrict__ exc_R,
             const double* __restrict__ prev, const double* __restrict__ yprev,
             const double* __restrict__ inv, double* __restrict__ out, double* __restrict__ yout,
-            int gmode) {
+            int gmode, double fbase) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const uint64_t pol = policy_evict_first();
-  // kWeighted gathers P(s, j-1); compact gathers y(s, j-1)
+  // kWeighted gathers P(s, j-1) (the first sweep: fbase = P(s,1) for every s);
+  // compact gathers y(s, j-1)
   const double* __restrict__ opnd = kWeighted ? prev : yprev;
 
   if (blockIdx.x < long_blocks) {  // ---- long rows: one warp per row
     long_row<kWeighted>((uint64_t)blockIdx.x * kWarpsPerBlock + wib, nlong, lnode, lptr, lcol, lR,
-                        exc_src, exc_R, prev, opnd, inv, out, yout, nullptr, gmode, pol);
+                        exc_src, exc_R, prev, opnd, inv, out, yout, nullptr, gmode, pol, fbase);
     return;
   }
 
@@ -224,7 +227,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const bool in = k + u < len;
-      x[u] = (in && (kWeighted || !(c[u] & kExcFlag))) ? ld_gather(opnd + c[u], gmode) : 0.0;
+      x[u] = (in && (kWeighted || !(c[u] & kExcFlag)))
+                 ? ((kWeighted && fbase != 0.0) ? fbase : ld_gather(opnd + c[u], gmode))
+                 : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u)
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                const double* __restrict__ exc_R, const double* __restrict__ prev,
                const double* __restrict__ yprev, const uint32_t* __restrict__ kprev,
                const double* __restrict__ inv, double* __restrict__ out,
-               double* __restrict__ yout, uint32_t* __restrict__ kout, int gmode) {
+               double* __restrict__ yout, uint32_t* __restrict__ kout, int gmode, double fbase) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const uint64_t pol = policy_evict_first();
@@ -260,7 +265,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   if (blockIdx.x < long_blocks) {
     long_row<kWeighted>((uint64_t)blockIdx.x * kWarpsPerBlock + wib, nlong, lnode, lptr, lcol, lR,
                         exc_src, exc_R, prev, kWeighted ? prev : yprev, inv, out, yout, kout,
-                        gmode, pol);
+                        gmode, pol, fbase);
     return;
   }
   const uint64_t s_block = ((uint64_t)blockIdx.x - long_blocks) * kWarpsPerBlock;
@@ -313,7 +318,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     }
     if constexpr (kWeighted) {
 #pragma unroll
-      for (int u = 0; u < kU; ++u) x[u] = t + u < len ? ld_gather(prev + c[u], gmode) : 0.0;
+      for (int u = 0; u < kU; ++u)
+        x[u] = t + u < len ? (fbase != 0.0 ? fbase : ld_gather(prev + c[u], gmode)) : 0.0;
     } else {
       // all codes in flight first; the rare y fallbacks after (no load waits
       // on a branch over an earlier load)
@@ -343,28 +349,131 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   else if (len) st_stream(state + v, miss, pol);
 }
 
-// ---- node-major passes with TMA-staged streams ----------------------------
-// The same pass as k_sweep_nm, restructured so that a slice's only global
-// reads on the critical path are its operand gathers: a producer warp
-// streams each chunk of kNmChunk slices — their lenf bytes, slice pointers,
-// running products and columns, all contiguous — into a shared-memory stage
-// with cp.async.bulk (mbarrier full/empty pipeline, kNmStages deep), and 8
-// consumer warps work from shared memory.
-constexpr int kNmChunk = 16;       // slices per chunk (512 nodes)
-constexpr int kNmStages = 2;
-constexpr uint32_t kNmColCap = 7680;  // columns per stage; larger chunks read global
-constexpr int kNmConsumers = 8;
-constexpr int kNmThreads = (kNmConsumers + 1) * 32;
+// ---- first sweep over the class stream (graph.cuh "f1") ---------------------
+// P(s,1) = 1/N for every source (metrics.cpp:143), so a regular edge's
+// factor 1 - P(s,1) * (1/row_sum(s)) depends on the source only through its
+// class; the ncls+1 factors (the last 1.0, for padding slots) sit in shared
+// memory and every slot streams a 2-byte class instead of gathering.
+// Exception edges (R != 1/row_sum, e.g. coalesced parallel edges) look their
+// R up by slot: 1 - P(s,1) * R, as metrics.cpp:166.
+__device__ __noinline__ double exc_first(uint64_t at, const uint64_t* __restrict__ xslot,
+                                            const double* __restrict__ xR, uint64_t nx,
+                                            double base) {
+  uint64_t lo = 0, hi = nx;  // the first listed slot >= at (== at)
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (xslot[mid] < at) lo = mid + 1;
+    else hi = mid;
+  }
+  return __dsub_rn(1.0, __dmul_rn(base, xR[lo]));
+}
 
-struct alignas(128) NmStage {
-  double st[kNmChunk * 32];
-  uint32_t col[kNmColCap + 8];
-  uint64_t sb[kNmChunk + 4];
-  uint8_t lenf[kNmChunk * 32];
-  uint64_t col_lo;  // global column index of col[0]; ~0: this chunk reads global
-  uint32_t ns;      // slices in the chunk
-  uint32_t sb_off;  // (k*S + first slice) - index of sb[0]
+__device__ __forceinline__ void finish_first(uint32_t v, double miss, double base,
+                                             const double* __restrict__ inv, double* __restrict__ out,
+                                             double* __restrict__ yout, uint32_t* __restrict__ kout,
+                                             uint64_t pol) {
+  // metrics.cpp:169 with prev[v] = P(v,1) = base
+  const double P = __dadd_rn(base, __dmul_rn(__dsub_rn(1.0, base), __dsub_rn(1.0, miss)));
+  if (!pol) {  // L2-resident outputs: plain stores
+    out[v] = P;
+    if (yout || kout) {
+      const double y = __dmul_rn(P, inv[v]);
+      if (yout) yout[v] = y;
+      if (kout) kout[v] = y_code(y);
+    }
+    return;
+  }
+  st_stream(out + v, P, pol);
+  if (yout || kout) {
+    const double y = __dmul_rn(P, inv[v]);
+    if (yout) st_stream(yout + v, y, pol);
+    if (kout) st_stream(kout + v, y_code(y), pol);
+  }
+}
+
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+
+__device__ __forceinline__ void load_factors(double* fac, uint32_t ncls, double base,
+                                             const double* __restrict__ cls_inv) {
+  // class ncls: padding, exactly 1.0; class ncls+1: exception edges, a NaN
+  // sentinel (no factor is NaN, so a NaN product flags the slice)
+  for (uint32_t c = threadIdx.x; c <= ncls + 1; c += blockDim.x)
+    fac[c] = c < ncls ? __dsub_rn(1.0, __dmul_rn(base, cls_inv[c])) : c == ncls ? 1.0 : __longlong_as_double(0x7ff8000000000000ll);
+  __syncthreads();
+}
+
+// Long rows: one warp per row, 32 factors per step in parallel, one ordered
+// chain (every lane runs it on shuffled factors; lane 0 writes).
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_first_long(uint64_t nlong, double base, uint32_t ncls, const double* __restrict__ cls_inv,
+                 const uint32_t* __restrict__ lnode, const uint64_t* __restrict__ lptr,
+                 const uint32_t* __restrict__ lcol, const uint16_t* __restrict__ lcls,
+                 const double* __restrict__ exc_R, const double* __restrict__ inv,
+                 double* __restrict__ out, double* __restrict__ yout, uint32_t* __restrict__ kout) {
+  extern __shared__ double fac[];
+  load_factors(fac, ncls, base, cls_inv);
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = policy_evict_first();
+  const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
+  for (uint64_t it = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); it < nlong; it += warps) {
+    const uint64_t a = lptr[it], b = lptr[it + 1];
+    double miss = 1.0;
+    for (uint64_t cs = a; cs < b; cs += 32 * kLongU) {
+      double f[kLongU];
+#pragma unroll
+      for (int u = 0; u < kLongU; ++u) {
+        const uint64_t e = cs + u * 32 + lane;
+        f[u] = 1.0;
+        if (e < b) {
+          const uint16_t c = ld_stream(lcls + e, pol);
+          f[u] = c == ncls + 1 ? __dsub_rn(1.0, __dmul_rn(base, exc_R[lcol[e] & ~kExcFlag])) : fac[c];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kLongU; ++u) {
+        const uint64_t b0 = cs + u * 32;
+        const int cnt = b > b0 ? static_cast<int>(b - b0 < 32 ? b - b0 : 32) : 0;
+        for (int j = 0; j < cnt; ++j) miss = __dmul_rn(miss, __shfl_sync(kFull, f[u], j));
+      }
+    }
+    if (lane == 0) finish_first(lnode[it], miss, base, inv, out, yout, kout, pol);
+  }
+}
+
+// Regular rows. The f1 slices come in windows of 8 (256 nodes, sorted by
+// in-degree into the slots, so a window's first slice is its longest); a CTA
+// takes a unit of two windows at a time (16 slices, 512 consecutive regular
+// nodes) and warp w runs slices w and 15 - w, which balances the warps.
+// Lane = node, lane-major classes.
+//
+// The kernel is a pure stream (2 bytes per slot, no gathers), so it is fed by
+// a TMA pipeline: thread 0 bulk-copies (cp.async.bulk, mbarrier complete_tx)
+// each unit's perm words, slice pointers, node range, class stream and
+// 1/row_sum span into a kF1Stages-deep shared-memory ring ahead of the
+// compute, so the compute has no global load on its critical path. The
+// unit's results are staged in shared memory by node and written back
+// coalesced (P, and y / code) instead of 8-byte stores scattered across it.
+constexpr int kF1Slices = kF1Unit;
+constexpr int kStage = 1024;        // node span a unit may stage (long rows interleave)
+#ifndef QVB_F1_STAGES
+#define QVB_F1_STAGES 2
+#endif
+constexpr int kF1Stages = QVB_F1_STAGES;
+constexpr uint32_t kF1Cls = 16384;  // classes a stage holds; larger units stream from global
+constexpr uint32_t kF1Inv = 514;    // 1/row_sum span a stage holds (512 nodes + alignment)
+
+struct alignas(128) F1Stage {
+  uint16_t cls[kF1Cls];
+  uint32_t perm[kF1Slices * 32];
+  uint64_t sptr[kF1Slices + 2];
+  uint64_t urange[2];
+  double inv[kF1Inv];
 };
+constexpr size_t kF1StageBytes = sizeof(F1Stage) * kF1Stages;
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
@@ -381,161 +490,190 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-__global__ void __launch_bounds__(kNmThreads)
-    k_sweep_nm_tma(int k, uint64_t S, uint64_t nchunks, const uint8_t* __restrict__ lenf,
-                   const uint64_t* __restrict__ sbase, const uint32_t* __restrict__ ncol,
-                   double* __restrict__ state, const uint32_t* __restrict__ exc_src,
-                   const double* __restrict__ exc_R, const double* __restrict__ prev,
-                   const double* __restrict__ yprev, const uint32_t* __restrict__ kprev,
-                   const double* __restrict__ inv, double* __restrict__ out,
-                   double* __restrict__ yout, uint32_t* __restrict__ kout, int gmode) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  NmStage* stg = reinterpret_cast<NmStage*>(smem);
-  __shared__ __align__(8) uint64_t full[kNmStages], empty[kNmStages];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// One slice's ordered product over its class stream (staged in shared memory
+// or read from global), exception classes contributing the NaN sentinel.
+template <bool kStaged>
+__device__ __forceinline__ double slice_product(uint32_t len, const uint16_t* __restrict__ cp,
+                                                uint32_t tab, uint32_t ncls, uint64_t pol) {
+  double miss = 1.0;  // metrics.cpp:152
+  uint32_t k = 0;
+  for (; k + kU <= len; k += kU) {
+    uint32_t c[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) c[u] = kStaged ? cp[(k + u) * 32] : ld_stream(cp + (uint64_t)(k + u) * 32, pol);
+    double f[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) f[u] = lds_f64(tab + c[u] * 8);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) miss = __dmul_rn(miss, f[u]);
+  }
+  if (k < len) {
+    uint32_t c[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      c[u] = k + u < len ? (kStaged ? cp[(k + u) * 32] : ld_stream(cp + (uint64_t)(k + u) * 32, pol)) : ncls;
+    double f[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) f[u] = lds_f64(tab + c[u] * 8);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) miss = __dmul_rn(miss, f[u]);  // ncls: exactly 1.0
+  }
+  return miss;
+}
+
+// The slice again, element by element, exceptions with their R (rare).
+__device__ __noinline__ double slice_product_exc(uint32_t len, const uint16_t* __restrict__ gc,
+                                                 uint64_t at0, uint32_t tab, uint32_t ncls,
+                                                 const uint64_t* __restrict__ xslot,
+                                                 const double* __restrict__ xR, uint64_t nx,
+                                                 double base) {
+  double miss = 1.0;
+  for (uint32_t k = 0; k < len; ++k) {
+    const uint32_t c = gc[(uint64_t)k * 32];
+    const double f = c == ncls + 1 ? exc_first(at0 + (uint64_t)k * 32, xslot, xR, nx, base) : lds_f64(tab + c * 8);
+    miss = __dmul_rn(miss, f);
+  }
+  return miss;
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_first(uint64_t nunit, double base, uint32_t ncls, const double* __restrict__ cls_inv,
+            const uint32_t* __restrict__ perm, const uint64_t* __restrict__ sptr,
+            const uint16_t* __restrict__ cls, const uint64_t* __restrict__ urange,
+            const uint64_t* __restrict__ xslot, const double* __restrict__ xR, uint64_t nx,
+            const double* __restrict__ inv, double* __restrict__ out, double* __restrict__ yout,
+            uint32_t* __restrict__ kout) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  F1Stage* stg = reinterpret_cast<F1Stage*>(dsm);
+  double* fac = reinterpret_cast<double*>(dsm + kF1StageBytes);
+  __shared__ double sP[kStage];
+  __shared__ uint32_t sMask[kStage / 32];
+  __shared__ __align__(8) uint64_t full[kF1Stages];
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kNmStages; ++i) {
+    for (int i = 0; i < kF1Stages; ++i)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
           static_cast<uint32_t>(__cvta_generic_to_shared(&full[i]))));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
-                       static_cast<uint32_t>(__cvta_generic_to_shared(&empty[i]))),
-                   "r"(kNmConsumers));
-    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-  const uint64_t mine =
-      blockIdx.x < nchunks ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-
-  if (warp == kNmConsumers) {  // ---- producer
-    if (lane != 0) return;
-    uint64_t c0n = 0, c1n = 0;
-    auto bounds = [&](uint64_t it, uint64_t& i0, uint32_t& ns) {
-      const uint64_t a = (blockIdx.x + it * gridDim.x) * kNmChunk;
-      ns = static_cast<uint32_t>(S - a < kNmChunk ? S - a : kNmChunk);
-      i0 = (uint64_t)k * S + a;
-    };
-    if (mine) {
-      uint64_t i0;
-      uint32_t ns;
-      bounds(0, i0, ns);
-      c0n = sbase[i0];
-      c1n = sbase[i0 + ns];
-    }
-    for (uint64_t it = 0; it < mine; ++it) {
-      const int si = static_cast<int>(it % kNmStages);
-      uint64_t i0;
-      uint32_t ns;
-      bounds(it, i0, ns);
-      const uint64_t c0 = c0n, c1 = c1n;
-      if (it + 1 < mine) {  // next chunk's column range: in flight during the wait
-        uint64_t j0;
-        uint32_t nn;
-        bounds(it + 1, j0, nn);
-        c0n = sbase[j0];
-        c1n = sbase[j0 + nn];
-      }
-      if (it >= kNmStages)
-        mbar_wait(static_cast<uint32_t>(__cvta_generic_to_shared(&empty[si])),
-                  static_cast<uint32_t>((it / kNmStages - 1) & 1));
-      NmStage& st = stg[si];
-      const uint64_t a = i0 - (uint64_t)k * S;
-      const uint64_t sb_lo = i0 & ~1ull, sb_hi = (i0 + ns + 2) & ~1ull;
-      const uint64_t col_lo = c0 & ~3ull, col_hi = (c1 + 3) & ~3ull;
-      const bool cols_in = col_hi - col_lo <= kNmColCap;
-      st.ns = ns;
-      st.sb_off = static_cast<uint32_t>(i0 - sb_lo);
-      st.col_lo = cols_in ? col_lo : ~0ull;
-      const uint32_t b_len = ns * 32, b_sb = static_cast<uint32_t>((sb_hi - sb_lo) * 8);
-      const uint32_t b_st = k > 0 ? ns * 32 * 8 : 0;
-      const uint32_t b_col = cols_in ? static_cast<uint32_t>((col_hi - col_lo) * 4) : 0;
-      const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&full[si]));
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                   "r"(b_len + b_sb + b_st + b_col)
-                   : "memory");
-      bulk_g2s(st.lenf, lenf + i0 * 32, b_len, bar);
-      bulk_g2s(st.sb, sbase + sb_lo, b_sb, bar);
-      if (b_st) bulk_g2s(st.st, state + a * 32, b_st, bar);
-      if (b_col) bulk_g2s(st.col, ncol + col_lo, b_col, bar);
-    }
-    return;
-  }
-
-  // ---- consumers
+  load_factors(fac, ncls, base, cls_inv);  // ends with __syncthreads
+  const uint32_t tab = static_cast<uint32_t>(__cvta_generic_to_shared(fac));
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t pol = policy_evict_first();
-  for (uint64_t it = 0; it < mine; ++it) {
-    const int si = static_cast<int>(it % kNmStages);
-    mbar_wait(static_cast<uint32_t>(__cvta_generic_to_shared(&full[si])),
-              static_cast<uint32_t>((it / kNmStages) & 1));
-    const NmStage& st = stg[si];
-    const uint32_t ns = st.ns;
-    const uint64_t col_lo = st.col_lo;
-    const uint64_t a = (blockIdx.x + it * gridDim.x) * kNmChunk;
-    for (uint32_t q = warp; q < ns; q += kNmConsumers) {
-      const uint64_t v = (a + q) * 32 + lane;
-      const uint32_t lf = st.lenf[q * 32 + lane];
-      if (__ballot_sync(kFull, lf != 0) == 0) continue;
-      const uint32_t len = lf & kNmLen;
-      uint32_t incl = len;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const uint32_t maxlen = __reduce_max_sync(kFull, len);
-      const uint64_t cs = st.sb[st.sb_off + q] + (incl - len);  // global column index
-      const bool last = lf & kNmLast;
-      double pv = 0.0, iv = 0.0;
-      if (last) {  // finish operands early, off the critical path
-        pv = prev[v];
-        if (yout) iv = inv[v];
-      }
-      double miss = (lf != 0 && !(lf & kNmFirst)) ? st.st[q * 32 + lane] : 1.0;
-      for (uint32_t t = 0; t < maxlen; t += kU) {
-        uint32_t c[kU], code[kU];
-        double x[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const bool in = t + u < len;
-          c[u] = !in ? 0u
-                     : (col_lo != ~0ull ? st.col[cs + t + u - col_lo]
-                                        : ld_stream(ncol + cs + t + u, pol));
+  const uint64_t mine = blockIdx.x < nunit ? (nunit - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const bool want_inv = yout || kout;
+
+  // producer state (thread 0): class range and node range of the next unit
+  uint64_t c0n = 0, c1n = 0, urn = 0;
+  auto unit = [&](uint64_t i) { return blockIdx.x + i * gridDim.x; };
+  auto fetch = [&](uint64_t i) {
+    const uint64_t w = unit(i);
+    c0n = sptr[w * kF1Slices];
+    c1n = sptr[w * kF1Slices + kF1Slices];
+    urn = urange[w];
+  };
+  auto issue = [&](uint64_t i) {  // unit i of this block into stage i % kF1Stages
+    const uint64_t w = unit(i);
+    F1Stage& st = stg[i % kF1Stages];
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&full[i % kF1Stages]));
+    const uint64_t c0 = c0n, c1 = c1n, ur = urn;
+    if (i + 1 < mine) fetch(i + 1);  // in flight while this unit lands
+    const uint32_t lo = static_cast<uint32_t>(ur), hi = static_cast<uint32_t>(ur >> 32);
+    const uint32_t lo2 = lo & ~1u;
+    const uint32_t ninv = (hi - lo2 + 2) & ~1u;  // even: 16-byte multiples
+    const uint32_t b_cls = c1 - c0 <= kF1Cls ? static_cast<uint32_t>((c1 - c0) * sizeof(uint16_t)) : 0u;
+    const uint32_t b_perm = kF1Slices * 32 * sizeof(uint32_t);
+    const uint32_t b_sptr = (kF1Slices + 2) * sizeof(uint64_t);
+    const uint32_t b_ur = 2 * sizeof(uint64_t);
+    const uint32_t b_inv = (want_inv && ur && ninv <= kF1Inv) ? ninv * 8u : 0u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"(b_perm + b_sptr + b_ur + b_cls + b_inv)
+                 : "memory");
+    bulk_g2s(st.perm, perm + w * kF1Slices * 32, b_perm, bar);
+    bulk_g2s(st.sptr, sptr + w * kF1Slices, b_sptr, bar);
+    bulk_g2s(st.urange, urange + (w & ~1ull), b_ur, bar);
+    if (b_cls) bulk_g2s(st.cls, cls + c0, b_cls, bar);
+    if (b_inv) bulk_g2s(st.inv, inv + lo2, b_inv, bar);
+  };
+  if (threadIdx.x == 0 && mine) {
+    fetch(0);
+    for (uint64_t i = 0; i < mine && i < kF1Stages - 1; ++i) issue(i);
+  }
+  for (uint64_t i = 0; i < mine; ++i) {
+    // stage (i + kF1Stages - 1) % kF1Stages was consumed in iteration i - 1,
+    // which ended with __syncthreads
+    if (threadIdx.x == 0 && i + kF1Stages - 1 < mine) issue(i + kF1Stages - 1);
+    if (threadIdx.x < kStage / 32) sMask[threadIdx.x] = 0;
+    mbar_wait(static_cast<uint32_t>(__cvta_generic_to_shared(&full[i % kF1Stages])),
+              static_cast<uint32_t>((i / kF1Stages) & 1));
+    __syncthreads();  // sMask reset
+    const F1Stage& st = stg[i % kF1Stages];
+    const uint64_t ur = st.urange[unit(i) & 1];
+    const uint32_t lo = static_cast<uint32_t>(ur), hi = static_cast<uint32_t>(ur >> 32);
+    const uint32_t lo2 = lo & ~1u;
+    const bool inv_staged = ur && ((hi - lo2 + 2) & ~1u) <= kF1Inv;
+    const uint64_t w0 = st.sptr[0];
+    const bool staged = st.sptr[kF1Slices] - w0 <= kF1Cls;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int sl = h ? kF1Slices - 1 - wib : wib;  // a balanced pair of slices
+      const uint32_t v = st.perm[sl * 32 + lane] & kNodeMask;
+      const uint64_t b0 = st.sptr[sl];
+      const uint32_t len = static_cast<uint32_t>((st.sptr[sl + 1] - b0) >> 5);
+      double miss = staged ? slice_product<true>(len, st.cls + (b0 - w0) + lane, tab, ncls, pol)
+                           : slice_product<false>(len, cls + b0 + lane, tab, ncls, pol);
+      if (miss != miss)  // an exception edge in the slice
+        miss = slice_product_exc(len, cls + b0 + lane, b0 + lane, tab, ncls, xslot, xR, nx, base);
+      if (v != kNoNode) {
+        // metrics.cpp:169 with prev[v] = P(v,1) = base
+        const double P = __dadd_rn(base, __dmul_rn(__dsub_rn(1.0, base), __dsub_rn(1.0, miss)));
+        const uint32_t d = v - lo;
+        if (d < kStage) {
+          sP[d] = P;
+          atomicOr(&sMask[d >> 5], 1u << (d & 31));
+        } else {
+          finish_first(v, miss, base, inv, out, yout, kout, pol);
         }
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          code[u] = (t + u < len && !(c[u] & kExcFlag)) ? __ldg(kprev + c[u]) : 0u;
-#pragma unroll
-        for (int u = 0; u < kU; ++u) x[u] = __dmul_rn(static_cast<double>(code[u]), 0x1p-53);
-        bool big = false;
-#pragma unroll
-        for (int u = 0; u < kU; ++u) big |= code[u] == kBigCode;
-        if (big) {
-#pragma unroll
-          for (int u = 0; u < kU; ++u)
-            if (code[u] == kBigCode) x[u] = ld_gather(yprev + c[u], gmode);
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          if (t + u < len) miss = __dmul_rn(miss, factor<false>(c[u], x[u], 0.0, exc_src, exc_R, prev));
-      }
-      if (last) {
-        // metrics.cpp:169, as finish()
-        const double P = __dadd_rn(pv, __dmul_rn(__dsub_rn(1.0, pv), __dsub_rn(1.0, miss)));
-        st_stream(out + v, P, pol);
-        if (yout) {
-          const double y = __dmul_rn(P, iv);
-          st_stream(yout + v, y, pol);
-          if (kout) kout[v] = y_code(y);
-        }
-      } else if (len) {
-        st_stream(state + v, miss, pol);
       }
     }
-    __syncwarp();
-    if (lane == 0)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                       static_cast<uint32_t>(__cvta_generic_to_shared(&empty[si])))
-                   : "memory");
+    __syncthreads();
+    const uint32_t span = ur ? (hi - lo + 1 < kStage ? hi - lo + 1 : kStage) : 0u;
+    for (uint32_t d = threadIdx.x; d < span; d += blockDim.x) {
+      if (!(sMask[d >> 5] >> (d & 31) & 1)) continue;
+      const uint32_t vv = lo + d;
+      const double P = sP[d];
+      st_stream(out + vv, P, pol);
+      if (want_inv) {
+        const double y = __dmul_rn(P, inv_staged ? st.inv[vv - lo2] : inv[vv]);
+        if (yout) st_stream(yout + vv, y, pol);
+        if (kout) st_stream(kout + vv, y_code(y), pol);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Small graphs (P, y and codes L2-resident): one warp per slice, persistent
+// warps, no staging; the scattered per-node stores merge in L2.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_first_small(uint64_t S, double base, uint32_t ncls, const double* __restrict__ cls_inv,
+                  const uint32_t* __restrict__ perm, const uint64_t* __restrict__ sptr,
+                  const uint16_t* __restrict__ cls, const uint64_t* __restrict__ xslot,
+                  const double* __restrict__ xR, uint64_t nx, const double* __restrict__ inv,
+                  double* __restrict__ out, double* __restrict__ yout, uint32_t* __restrict__ kout) {
+  extern __shared__ double fac[];
+  load_factors(fac, ncls, base, cls_inv);
+  const uint32_t tab = static_cast<uint32_t>(__cvta_generic_to_shared(fac));
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = policy_evict_first();
+  const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
+  for (uint64_t sl = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); sl < S; sl += warps) {
+    const uint32_t v = perm[sl * 32 + lane] & kNodeMask;
+    const uint64_t b0 = sptr[sl];
+    const uint32_t len = static_cast<uint32_t>((sptr[sl + 1] - b0) >> 5);
+    double miss = slice_product<false>(len, cls + b0 + lane, tab, ncls, pol);
+    if (miss != miss) miss = slice_product_exc(len, cls + b0 + lane, b0 + lane, tab, ncls, xslot, xR, nx, base);
+    if (v != kNoNode) finish_first(v, miss, base, inv, out, yout, kout, 0);
   }
 }
 
@@ -545,21 +683,22 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
   if (layers < 1) fail(QVB_ERR_VALIDATION, "access probability needs layers >= 1");
   const uint64_t n = g.n;
   const bool compact = g.layout == 0;
+  const bool codes = g.nm && compact;           // nm compact sweeps gather 4-byte codes
+  const bool f1 = compact && g.ncls > 0 && layers >= 2;  // class-stream first sweep
   for (int i = 0; i < 2; ++i) {
     if (!g.p[i]) QVB_CUDA(cudaMalloc(&g.p[i], (n + 1) * sizeof(double)));
     if (compact && !g.y[i]) QVB_CUDA(cudaMalloc(&g.y[i], (n + 1) * sizeof(double)));
+    if (codes && !g.kcode[i]) QVB_CUDA(cudaMalloc(&g.kcode[i], (n + 1) * sizeof(uint32_t)));
+    // entry N is the padding operand of every gathered vector: 0 (factor 1.0)
+    QVB_CUDA(cudaMemsetAsync(g.p[i] + n, 0, sizeof(double), s));
+    if (compact) QVB_CUDA(cudaMemsetAsync(g.y[i] + n, 0, sizeof(double), s));
+    if (codes) QVB_CUDA(cudaMemsetAsync(g.kcode[i] + n, 0, sizeof(uint32_t), s));
   }
-  // both ping-pong buffers carry the zero padding operand at index N
-  const bool codes = g.nm && compact;
-  if (codes)
-    for (int i = 0; i < 2; ++i)
-      if (!g.kcode[i]) QVB_CUDA(cudaMalloc(&g.kcode[i], (n + 1) * sizeof(uint32_t)));
-  k_init<<<grid_for(n + 1, 256), 256, 0, s>>>(n, g.inv, g.p[0], (compact && layers >= 2) ? g.y[0] : nullptr,
-                                             (codes && layers >= 2) ? g.kcode[0] : nullptr);
-  QVB_LAUNCH_CHECK();
-  if (layers >= 3) {
-    QVB_CUDA(cudaMemsetAsync(g.p[1] + n, 0, sizeof(double), s));
-    if (compact) QVB_CUDA(cudaMemsetAsync(g.y[1] + n, 0, sizeof(double), s));
+  const double base = 1.0 / static_cast<double>(n);  // metrics.cpp:143
+  if (!f1) {  // P(n,1) (and, for a gathering first sweep, its operands)
+    k_init<<<grid_for(n + 1, 256), 256, 0, s>>>(n, g.inv, g.p[0], (compact && layers >= 2) ? g.y[0] : nullptr,
+                                               (codes && layers >= 2) ? g.kcode[0] : nullptr);
+    QVB_LAUNCH_CHECK();
   }
   const uint64_t long_blocks = (g.nlong + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int nseg = static_cast<int>(g.seg_slice.size()) - 1;
@@ -567,47 +706,52 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
     if (!e) QVB_CUDA(cudaEventCreate(&e));
   int gmode = 0;
   if (const char* m = std::getenv("QVB_GATHER_MODE")) gmode = std::atoi(m);
-  // L2 lookahead in blocks for the sliced passes (QVB_PF_BLOCKS; 0 = off);
+  // L2 lookahead in blocks for the segmented passes (QVB_PF_BLOCKS; 0 = off);
   // worthwhile only when the streams do not already sit in L2
   uint64_t pf = nseg > 1 ? 512 : 0;
   if (const char* m = std::getenv("QVB_PF_BLOCKS")) pf = std::strtoull(m, nullptr, 10);
-  int persist_mb = 0;
-  if (const char* m = std::getenv("QVB_L2_PERSIST_MB")) persist_mb = std::atoi(m);
-  if (persist_mb > 0) {
-    QVB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)persist_mb << 20));
-  }
-  unsigned tma_grid = 0;  // persistent grid of the TMA-staged node-major kernel
-  const char* nm_kernel = std::getenv("QVB_NM_KERNEL");
-  if (g.nm && compact && nm_kernel && std::string(nm_kernel) == "tma") {
-    const int smem = static_cast<int>(sizeof(NmStage) * kNmStages);
-    QVB_CUDA(cudaFuncSetAttribute(k_sweep_nm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const uint64_t nchunks = (g.nm_S + kNmChunk - 1) / kNmChunk;
-    tma_grid = resident_grid(k_sweep_nm_tma, kNmThreads, smem, nchunks);
-  }
   QVB_CUDA(cudaEventRecord(g.ev[0], s));
   for (uint32_t j = 2; j <= layers; ++j) {
     const int cur = (j - 2) & 1, nxt = cur ^ 1;
+    const bool first = j == 2;
     double* yout = (compact && j < layers) ? g.y[nxt] : nullptr;
-    if (g.nm && compact && tma_grid) {  // node-major passes, TMA-staged
-      uint32_t* kout = (codes && j < layers) ? g.kcode[nxt] : nullptr;
-      const uint64_t nchunks = (g.nm_S + kNmChunk - 1) / kNmChunk;
-      for (int k = 0; k < nseg; ++k) {
-        if (k == 0 && long_blocks) {  // long rows: the warp-per-row path, full rows
-          k_sweep_nm<false><<<static_cast<unsigned>(long_blocks), kWarpsPerBlock * 32, 0, s>>>(
-              0, 0, long_blocks, g.nlong, 0, g.nm_lenf, g.nm_sbase, g.nm_col, nullptr, g.state,
-              g.lnode, g.lptr, g.lcol, nullptr, g.exc_src, g.exc_R, g.p[cur], g.y[cur],
-              g.kcode[cur], g.inv, g.p[nxt], yout, kout, gmode);
-          QVB_LAUNCH_CHECK();
-        }
-        k_sweep_nm_tma<<<tma_grid, kNmThreads, sizeof(NmStage) * kNmStages, s>>>(
-            k, g.nm_S, nchunks, g.nm_lenf, g.nm_sbase, g.nm_col, g.state, g.exc_src, g.exc_R,
-            g.p[cur], g.y[cur], g.kcode[cur], g.inv, g.p[nxt], yout, kout, gmode);
+    uint32_t* kout = (codes && j < layers) ? g.kcode[nxt] : nullptr;
+    if (first && f1) {
+      const size_t smem = (g.ncls + 2) * sizeof(double);
+      QVB_CUDA(cudaFuncSetAttribute(k_first_long, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kMaxCls + 2) * 8));
+      if (g.nlong) {
+        const unsigned lg = resident_grid(k_first_long, kWarpsPerBlock * 32, smem,
+                                          (g.nlong + kWarpsPerBlock - 1) / kWarpsPerBlock);
+        k_first_long<<<lg, kWarpsPerBlock * 32, smem, s>>>(g.nlong, base, g.ncls, g.cls_inv, g.lnode,
+                                                           g.lptr, g.lcol, g.lcls, g.exc_R, g.inv,
+                                                           g.p[nxt], yout, kout);
+        QVB_LAUNCH_CHECK();
+      }
+      const uint64_t nwin = (g.f1_S + kF1Slices - 1) / kF1Slices;  // units of 16 slices
+      if (nwin && n * 24 <= (64ull << 20)) {  // outputs L2-resident (half the L2): no write staging
+        QVB_CUDA(cudaFuncSetAttribute(k_first_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kMaxCls + 2) * 8));
+        const unsigned grid = resident_grid(k_first_small, kWarpsPerBlock * 32, smem,
+                                            (g.f1_S + kWarpsPerBlock - 1) / kWarpsPerBlock);
+        k_first_small<<<grid, kWarpsPerBlock * 32, smem, s>>>(
+            g.f1_S, base, g.ncls, g.cls_inv, g.f1_perm, g.f1_sptr, g.f1_cls, g.f1_xslot, g.f1_xR,
+            g.f1_nx, g.inv, g.p[nxt], yout, kout);
+        QVB_LAUNCH_CHECK();
+      } else if (nwin) {
+        const size_t dsm = kF1StageBytes + smem;
+        QVB_CUDA(cudaFuncSetAttribute(k_first, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kF1StageBytes + (kMaxCls + 2) * 8)));
+        const unsigned grid = resident_grid(k_first, kWarpsPerBlock * 32, dsm, nwin);
+        k_first<<<grid, kWarpsPerBlock * 32, dsm, s>>>(nwin, base, g.ncls, g.cls_inv, g.f1_perm,
+                                                       g.f1_sptr, g.f1_cls, g.f1_urange, g.f1_xslot,
+                                                       g.f1_xR, g.f1_nx, g.inv, g.p[nxt], yout, kout);
         QVB_LAUNCH_CHECK();
       }
       continue;
     }
+    const double fbase = (first && !compact) ? base : 0.0;  // weighted first sweep: no gathers
     if (g.nm) {  // node-major passes
-      uint32_t* kout = (codes && j < layers) ? g.kcode[nxt] : nullptr;
       for (int k = 0; k < nseg; ++k) {
         const uint64_t lb = k == 0 ? long_blocks : 0;
         const uint64_t blocks = lb + (g.nm_S + kWarpsPerBlock - 1) / kWarpsPerBlock;
@@ -615,69 +759,31 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
           k_sweep_nm<false><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
               k, g.nm_S, lb, g.nlong, pf, g.nm_lenf, g.nm_sbase, g.nm_col, nullptr, g.state, g.lnode,
               g.lptr, g.lcol, nullptr, g.exc_src, g.exc_R, g.p[cur], g.y[cur], g.kcode[cur],
-              g.inv, g.p[nxt], yout, kout, gmode);
+              g.inv, g.p[nxt], yout, kout, gmode, 0.0);
         else
           k_sweep_nm<true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
               k, g.nm_S, lb, g.nlong, pf, g.nm_lenf, g.nm_sbase, g.nm_col, g.nm_R, g.state, g.lnode,
               g.lptr, g.lcol, g.lR, nullptr, nullptr, g.p[cur], nullptr, nullptr, g.inv,
-              g.p[nxt], nullptr, nullptr, gmode);
+              g.p[nxt], nullptr, nullptr, gmode, fbase);
         QVB_LAUNCH_CHECK();
       }
       continue;
     }
-    // pass k multiplies the factors of source segment k; the long rows ride
-    // along in the first pass's grid (their blocks first)
+    // sliced passes: pass k multiplies the factors of source segment k; the
+    // long rows ride along in the first pass's grid (their blocks first)
     for (int k = 0; k < nseg; ++k) {
       const uint64_t s0 = g.seg_slice[k], s1 = g.seg_slice[k + 1];
       const uint64_t lb = k == 0 ? long_blocks : 0;
       const uint64_t blocks = lb + (s1 - s0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
       if (blocks == 0) continue;
-      if (persist_mb > 0 && nseg > 1) {
-        // experiment: pin this pass's operand slice in the persisting L2 carve-out
-        const double* opnd = compact ? g.y[cur] : g.p[cur];
-        const uint64_t first = (uint64_t)k * g.seg_size;
-        const uint64_t count = std::min<uint64_t>(g.seg_size, n - first);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(static_cast<unsigned>(blocks));
-        cfg.blockDim = dim3(kWarpsPerBlock * 32);
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow.base_ptr = const_cast<double*>(opnd + first);
-        attr[0].val.accessPolicyWindow.num_bytes = count * sizeof(double);
-        attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        if (compact)
-          QVB_CUDA(cudaLaunchKernelEx(&cfg, k_sweep<false>, s0, s1, lb, g.nlong, pf, g.nslices, g.state,
-                                      (const uint32_t*)g.perm, (const uint64_t*)g.sptr,
-                                      (const uint32_t*)g.scol, (const double*)nullptr,
-                                      (const uint32_t*)g.lnode, (const uint64_t*)g.lptr,
-                                      (const uint32_t*)g.lcol, (const double*)nullptr,
-                                      (const uint32_t*)g.exc_src, (const double*)g.exc_R,
-                                      (const double*)g.p[cur], (const double*)g.y[cur],
-                                      (const double*)g.inv, g.p[nxt], yout, gmode));
-        else
-          QVB_CUDA(cudaLaunchKernelEx(&cfg, k_sweep<true>, s0, s1, lb, g.nlong, pf, g.nslices, g.state,
-                                      (const uint32_t*)g.perm, (const uint64_t*)g.sptr,
-                                      (const uint32_t*)g.scol, (const double*)g.sR,
-                                      (const uint32_t*)g.lnode, (const uint64_t*)g.lptr,
-                                      (const uint32_t*)g.lcol, (const double*)g.lR,
-                                      (const uint32_t*)nullptr, (const double*)nullptr,
-                                      (const double*)g.p[cur], (const double*)nullptr,
-                                      (const double*)g.inv, g.p[nxt], (double*)nullptr, gmode));
-        continue;
-      }
       if (compact) {
         k_sweep<false><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
             s0, s1, lb, g.nlong, pf, g.nslices, g.state, g.perm, g.sptr, g.scol, nullptr, g.lnode, g.lptr,
-            g.lcol, nullptr, g.exc_src, g.exc_R, g.p[cur], g.y[cur], g.inv, g.p[nxt], yout, gmode);
+            g.lcol, nullptr, g.exc_src, g.exc_R, g.p[cur], g.y[cur], g.inv, g.p[nxt], yout, gmode, 0.0);
       } else {
         k_sweep<true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
             s0, s1, lb, g.nlong, pf, g.nslices, g.state, g.perm, g.sptr, g.scol, g.sR, g.lnode, g.lptr, g.lcol,
-            g.lR, nullptr, nullptr, g.p[cur], nullptr, g.inv, g.p[nxt], nullptr, gmode);
+            g.lR, nullptr, nullptr, g.p[cur], nullptr, g.inv, g.p[nxt], nullptr, gmode, fbase);
       }
       QVB_LAUNCH_CHECK();
     }

@@ -179,6 +179,16 @@ __device__ __forceinline__ uint64_t ld_stream(const uint64_t* a, uint64_t pol) {
                : "l"(a), "l"(pol));
   return v;
 }
+__device__ __forceinline__ uint16_t ld_stream(const uint16_t* a, uint64_t pol) {
+  uint16_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
+               : "=h"(v)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_stream(uint32_t* a, uint32_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ uint32_t ld_hint(const uint32_t* a, uint64_t pol) {
   uint32_t v;
   asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));

@@ -48,6 +48,14 @@ qvb_graph::~qvb_graph() {
   cudaFree(nm_sbase);
   cudaFree(nm_col);
   cudaFree(nm_R);
+  cudaFree(cls_inv);
+  cudaFree(f1_perm);
+  cudaFree(f1_sptr);
+  cudaFree(f1_cls);
+  cudaFree(f1_urange);
+  cudaFree(f1_xslot);
+  cudaFree(f1_xR);
+  cudaFree(lcls);
   for (int i = 0; i < 2; ++i) {
     cudaFree(p[i]);
     cudaFree(y[i]);
@@ -539,12 +547,131 @@ __global__ void k_nm_fill(const uint64_t* __restrict__ uptr, const uint32_t* __r
   }
 }
 
+
+// ---- first-sweep classes (graph.cuh "f1") ------------------------------------
+__global__ void k_cls_keys(const double* __restrict__ inv, uint64_t n, uint64_t* __restrict__ keys,
+                           uint32_t* __restrict__ vals) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    keys[i] = static_cast<uint64_t>(__double_as_longlong(inv[i]));
+    vals[i] = static_cast<uint32_t>(i);
+  }
+}
+
+__global__ void k_cls_heads(const uint64_t* __restrict__ skeys, uint64_t n, uint8_t* __restrict__ head) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    head[k] = (k == 0 || skeys[k] != skeys[k - 1]) ? 1 : 0;
+}
+
+__global__ void k_cls_assign(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
+                             const uint8_t* __restrict__ head, const uint32_t* __restrict__ cidx,
+                             uint64_t n, uint32_t* __restrict__ cls_of, double* __restrict__ cls_inv) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = cidx[k] + head[k] - 1;
+    cls_of[svals[k]] = c;
+    if (head[k]) cls_inv[c] = __longlong_as_double(static_cast<long long>(skeys[k]));
+  }
+}
+
+// k_fill_slots for the class stream: exceptions get class ncls+1 and are appended
+// (slot, exception index) for a later sort by slot.
+__global__ void k_fill_cls(const uint32_t* __restrict__ slot_pair, const uint32_t* __restrict__ pv,
+                           const uint64_t* __restrict__ pstart, const uint32_t* __restrict__ pdeg,
+                           const uint64_t* __restrict__ sptr, const uint32_t* __restrict__ col,
+                           const uint32_t* __restrict__ cls_of, uint64_t nslices, uint16_t pad,
+                           uint16_t exc_cls,
+                           uint32_t* __restrict__ perm, uint16_t* __restrict__ scls,
+                           unsigned long long* __restrict__ xcount, uint64_t* __restrict__ xslot,
+                           uint32_t* __restrict__ xidx) {
+  const uint64_t slots = nslices * 32;
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < slots;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = p >> 5, lane = p & 31;
+    const uint64_t base = sptr[s];
+    const uint64_t len = (sptr[s + 1] - base) >> 5;
+    const uint32_t i = slot_pair[p];
+    uint64_t r0 = 0, deg = 0;
+    if (i != 0xFFFFFFFFu) {
+      perm[p] = pv[i];
+      r0 = pstart[i];
+      deg = pdeg[i];
+    } else {
+      perm[p] = kNoNode;
+    }
+    for (uint64_t k = 0; k < len; ++k) {
+      const uint64_t at = base + k * 32 + lane;
+      uint16_t c = pad;
+      if (k < deg) {
+        const uint32_t x = col[r0 + k];
+        if (x & kExcFlag) {
+          c = exc_cls;
+          const unsigned long long j = atomicAdd(xcount, 1ull);
+          xslot[j] = at;
+          xidx[j] = x & ~kExcFlag;
+        } else {
+          c = static_cast<uint16_t>(cls_of[x]);
+        }
+      }
+      scls[at] = c;
+    }
+  }
+}
+
+__global__ void k_fill_u64(uint64_t* __restrict__ p, uint64_t n, uint64_t v) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+__global__ void k_fill_u32(uint32_t* __restrict__ p, uint64_t n, uint32_t v) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// Node range of every unit of kF1Unit slices (padding slots skipped).
+__global__ void k_unit_range(const uint32_t* __restrict__ perm, uint64_t nunit,
+                             uint64_t* __restrict__ urange) {
+  const uint64_t u = blockIdx.x * (uint64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  const uint32_t lane = threadIdx.x & 31;
+  if (u >= nunit) return;
+  uint32_t lo = 0xFFFFFFFFu, hi = 0;
+  for (uint32_t i = lane; i < kF1Unit * 32; i += 32) {
+    const uint32_t v = perm[u * kF1Unit * 32 + i] & kNodeMask;
+    if (v != kNoNode) {
+      lo = min(lo, v);
+      hi = max(hi, v);
+    }
+  }
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if (lane == 0) urange[u] = lo > hi ? 0ull : (uint64_t)lo | ((uint64_t)hi << 32);
+}
+
+__global__ void k_x_values(const uint32_t* __restrict__ sidx, const double* __restrict__ exc_R,
+                           uint64_t nx, double* __restrict__ xR) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nx;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    xR[i] = exc_R[sidx[i]];
+}
+
+__global__ void k_long_cls(const uint32_t* __restrict__ lcol, const uint32_t* __restrict__ cls_of,
+                           uint64_t m, uint16_t exc_cls, uint16_t* __restrict__ lcls) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = lcol[i];
+    lcls[i] = (x & kExcFlag) ? exc_cls : static_cast<uint16_t>(cls_of[x]);
+  }
+}
+
 }  // namespace
 
 void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, const double* d_w,
                   const uint32_t* d_src, cudaStream_t s) {
   const uint64_t n = g.n, e = g.e;
-  DevBuf<double> rs(n, s), inv(n, s);
+  DevBuf<double> rs(n, s), inv(n + 2, s);  // +2: 16-byte bulk-copy spans (f1)
+  QVB_CUDA(cudaMemsetAsync(inv.p + n, 0, 2 * sizeof(double), s));
   DevBuf<unsigned long long> flags(1, s);
   QVB_CUDA(cudaMemsetAsync(flags.p, 0xFF, sizeof(unsigned long long), s));
   k_row_sums<<<grid_for(n, kBlock), kBlock, 0, s>>>(d_ro, d_w, n, rs.p, inv.p, flags.p);
@@ -636,6 +763,7 @@ void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, con
     g.exc_R = persist(xR);
     g.bytes = (nexc ? nexc : 1) * 12;
     build_slices(g, uptr.p, col.p, ucol.p, nullptr, s);
+    build_first(g, uptr.p, col.p, inv.p, s);
   } else {
     g.layout = 1;
     uexc.release();
@@ -735,6 +863,139 @@ void build_nm(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const uin
   g.nm_col = persist(ncol);
   g.nm_R = nR.p ? persist(nR) : nullptr;
   g.bytes += npad * nseg + (S * nseg + 1) * 8 + total * (R ? 12 : 4) + n * 8;
+}
+
+void build_first(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const double* inv,
+                 cudaStream_t s) {
+  const char* mode = std::getenv("QVB_FIRST");
+  if (mode && std::string(mode) == "gather") return;
+  const uint64_t n = g.n;
+  if (n == 0 || g.eu == 0 || g.layout != 0) return;
+  // classes: distinct bit patterns of 1/row_sum, by a sort of (inv, node)
+  DevBuf<uint32_t> cls_of(n, s);
+  uint32_t ncls = 0;
+  {
+    DevBuf<uint64_t> keys(n, s), skeys(n, s);
+    DevBuf<uint32_t> vals(n, s), svals(n, s);
+    k_cls_keys<<<grid_for(n, kBlock), kBlock, 0, s>>>(inv, n, keys.p, vals.p);
+    QVB_LAUNCH_CHECK();
+    sort_pairs_u64_u32(keys.p, skeys.p, vals.p, svals.p, n, 0, 64, s);
+    keys.release();
+    vals.release();
+    DevBuf<uint8_t> head(n, s);
+    DevBuf<uint32_t> cidx(n, s);
+    k_cls_heads<<<grid_for(n, kBlock), kBlock, 0, s>>>(skeys.p, n, head.p);
+    QVB_LAUNCH_CHECK();
+    exclusive_sum_u8_u32(head.p, cidx.p, n, s);
+    ncls = read_scalar(cidx.p + (n - 1), s) + read_scalar(head.p + (n - 1), s);
+    if (ncls > kMaxCls) return;  // (ncls+1 must also fit the u16 class stream)
+    DevBuf<double> cinv(ncls, s);
+    k_cls_assign<<<grid_for(n, kBlock), kBlock, 0, s>>>(skeys.p, svals.p, head.p, cidx.p, n, cls_of.p,
+                                                       cinv.p);
+    QVB_LAUNCH_CHECK();
+    g.cls_inv = persist(cinv);
+  }
+  g.ncls = ncls;
+  // one pass over every regular row (in-degree <= long_threshold): pairs are
+  // the rows themselves, in node order
+  const uint32_t thr = g.long_threshold;
+  const uint64_t one = ~0ull;  // a single source segment
+  DevBuf<uint32_t> cnt(n + 1, s);
+  DevBuf<uint64_t> po(n + 1, s);
+  QVB_CUDA(cudaMemsetAsync(cnt.p + n, 0, sizeof(uint32_t), s));
+  k_pair_count<<<grid_for(n, kBlock), kBlock, 0, s>>>(uptr, col, n, thr, one, cnt.p);
+  QVB_LAUNCH_CHECK();
+  exclusive_sum_u32_u64(cnt.p, po.p, n + 1, s);
+  cnt.release();
+  const uint64_t H = read_scalar(po.p + n, s);
+  DevBuf<uint32_t> pk(H ? H : 1, s), pv(H ? H : 1, s), pdeg(H ? H : 1, s), iota(H ? H : 1, s);
+  DevBuf<uint64_t> pstart(H ? H : 1, s);
+  k_pair_emit<<<grid_for(n, kBlock), kBlock, 0, s>>>(uptr, col, n, thr, one, po.p, pk.p, pv.p,
+                                                     pstart.p, pdeg.p);
+  QVB_LAUNCH_CHECK();
+  po.release();
+  pk.release();
+  k_iota<<<grid_for(H, kBlock), kBlock, 0, s>>>(iota.p, H);
+  QVB_LAUNCH_CHECK();
+  const uint64_t groups = (H + kWindow - 1) / kWindow;
+  const uint64_t S = groups * (kWindow / 32);
+  DevBuf<uint64_t> spb(2, s), sgb(2, s);
+  {
+    const uint64_t hb[2] = {0, H}, gb[2] = {0, groups};
+    QVB_CUDA(cudaMemcpyAsync(spb.p, hb, sizeof(hb), cudaMemcpyHostToDevice, s));
+    QVB_CUDA(cudaMemcpyAsync(sgb.p, gb, sizeof(gb), cudaMemcpyHostToDevice, s));
+    QVB_CUDA(cudaStreamSynchronize(s));
+  }
+  DevBuf<uint32_t> slot_pair(S * 32 ? S * 32 : 1, s);
+  if (groups)
+    k_group_sort<<<static_cast<unsigned>(groups), kWindow, 0, s>>>(iota.p, spb.p, sgb.p, 1, pv.p,
+                                                                   pdeg.p, slot_pair.p);
+  QVB_LAUNCH_CHECK();
+  iota.release();
+  DevBuf<uint32_t> len32(S + 1, s);
+  // f1 is read in units of 16 slices with 16-byte bulk copies: sptr and perm
+  // are padded to a whole unit (+2 pointers) with empty slices
+  const uint64_t Sp = (S + kF1Unit - 1) / kF1Unit * kF1Unit;
+  DevBuf<uint64_t> sptr(Sp + 3, s);
+  k_slot_lens<<<grid_for(S + 1, kBlock), kBlock, 0, s>>>(slot_pair.p, pdeg.p, S, len32.p);
+  QVB_LAUNCH_CHECK();
+  exclusive_sum_u32_u64(len32.p, sptr.p, S + 1, s);
+  len32.release();
+  const uint64_t slots = read_scalar(sptr.p + S, s);
+  k_fill_u64<<<grid_for(Sp + 2 - S, kBlock), kBlock, 0, s>>>(sptr.p + S + 1, Sp + 2 - S, slots);
+  QVB_LAUNCH_CHECK();
+  DevBuf<uint32_t> perm(Sp * 32 ? Sp * 32 : 1, s);
+  if (Sp > S) {
+    k_fill_u32<<<grid_for((Sp - S) * 32, kBlock), kBlock, 0, s>>>(perm.p + S * 32, (Sp - S) * 32, kNoNode);
+    QVB_LAUNCH_CHECK();
+  }
+  DevBuf<uint16_t> scls(slots ? slots : 1, s);
+  const uint64_t xcap = g.nexc ? g.nexc : 1;
+  DevBuf<unsigned long long> xcount(1, s);
+  DevBuf<uint64_t> xslot(xcap, s);
+  DevBuf<uint32_t> xidx(xcap, s);
+  QVB_CUDA(cudaMemsetAsync(xcount.p, 0, sizeof(unsigned long long), s));
+  k_fill_cls<<<grid_for(S * 32, kBlock), kBlock, 0, s>>>(slot_pair.p, pv.p, pstart.p, pdeg.p, sptr.p,
+                                                         col, cls_of.p, S,
+                                                         static_cast<uint16_t>(ncls),
+                                                         static_cast<uint16_t>(ncls + 1), perm.p, scls.p,
+                                                         xcount.p, xslot.p, xidx.p);
+  QVB_LAUNCH_CHECK();
+  const uint64_t nx = read_scalar(xcount.p, s);
+  if (nx) {  // exception slots ascending, with their R
+    DevBuf<uint64_t> sslot(nx, s);
+    DevBuf<uint32_t> sidx(nx, s);
+    sort_pairs_u64_u32(xslot.p, sslot.p, xidx.p, sidx.p, nx, 0, bits_for(slots), s);
+    DevBuf<double> xR(nx, s);
+    k_x_values<<<grid_for(nx, kBlock), kBlock, 0, s>>>(sidx.p, g.exc_R, nx, xR.p);
+    QVB_LAUNCH_CHECK();
+    g.f1_xslot = persist(sslot);
+    g.f1_xR = persist(xR);
+  }
+  g.f1_nx = nx;
+  if (g.nlong) {
+    const uint64_t m = read_scalar(g.lptr + g.nlong, s);
+    DevBuf<uint16_t> lc(m ? m : 1, s);
+    k_long_cls<<<grid_for(m, kBlock), kBlock, 0, s>>>(g.lcol, cls_of.p, m,
+                                                      static_cast<uint16_t>(ncls + 1), lc.p);
+    QVB_LAUNCH_CHECK();
+    g.lcls = persist(lc);
+    g.bytes += m * 2;
+  }
+  const uint64_t nunit = Sp / kF1Unit;
+  DevBuf<uint64_t> urange(nunit + 2, s);  // read in aligned pairs by bulk copies
+  QVB_CUDA(cudaMemsetAsync(urange.p, 0, (nunit + 2) * sizeof(uint64_t), s));
+  if (nunit) {
+    k_unit_range<<<static_cast<unsigned>((nunit + 7) / 8), 256, 0, s>>>(perm.p, nunit, urange.p);
+    QVB_LAUNCH_CHECK();
+  }
+  g.f1_urange = persist(urange);
+  g.f1_S = S;
+  g.f1_perm = persist(perm);
+  g.f1_sptr = persist(sptr);
+  g.f1_cls = persist(scls);
+  g.bytes += S * 32 * 4 + (S + 1) * 8 + slots * 2 + nx * 16 + (uint64_t)ncls * 8;
+  QVB_CUDA(cudaStreamSynchronize(s));
 }
 
 void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const uint32_t* src,
@@ -1085,6 +1346,8 @@ extern "C" int qvb_graph_info_get(const qvb_graph* g, qvb_graph_info* info) {
     info->device = static_cast<uint32_t>(g->device);
     info->device_bytes = g->bytes;
     info->build_ms = g->build_ms;
+    info->classes = g->ncls;
+    info->segments = g->seg_slice.empty() ? 1u : static_cast<uint32_t>(g->seg_slice.size() - 1);
   });
 }
 

@@ -48,6 +48,23 @@
 // then gathers a 4-byte code instead of y (see kcode), which halves the
 // operand bytes and so the number of passes.
 //
+// First sweep ("f1"). P(s,1) = 1/N for every s (metrics.cpp:143), so the
+// first sweep's operand P(s,1) * (1/row_sum(s)) depends on the source only
+// through row_sum(s). Sources are grouped into classes of equal 1/row_sum
+// (bitwise), and the first sweep streams a 2-byte class per in-edge instead
+// of gathering: factor = table[class], the table holding
+// 1 - (1/N) * inv(class) in shared memory. It is a one-pass sliced layout
+// (windows of 256 nodes sorted by in-degree, slices of 32, lane-major),
+// built over every regular row whatever the segmentation of later sweeps:
+//   f1_perm u32[S*32], f1_sptr u64[S+1], f1_cls u16[...]
+// Class ncls is padding (factor exactly 1.0). Exception edges
+// (R != 1/row_sum) carry class ncls+1, whose table entry is a NaN sentinel:
+// a slice whose product comes out NaN is recomputed with their R, looked up
+// by slot in the ascending list (f1_xslot, f1_xR). Long rows use lcls next
+// to lcol. The slices come in units of 16 (512 nodes) whose node ranges are
+// f1_urange (lo | hi << 32). Graphs with more than kMaxCls classes keep the
+// gathering sweep.
+//
 // kcode: round(1 - y) in fp64 depends on y only through J = rint(y * 2^53)
 // while y <= 1/2: the doubles in [1/2, 1] are the multiples of 2^-53, so
 // __dsub_rn(1, y) == 1 - J * 2^-53 exactly (ties: J even <=> result even).
@@ -95,6 +112,18 @@ struct qvb_graph {
   uint32_t* nm_col = nullptr;
   double* nm_R = nullptr;
   uint32_t* kcode[2] = {nullptr, nullptr};
+  // first sweep ("f1", see above): out-degree classes and their streams
+  uint32_t ncls = 0;            // 0: no class stream (the first sweep gathers)
+  double* cls_inv = nullptr;    // [ncls] 1/row_sum of each class
+  uint64_t f1_S = 0;            // slices of the one-pass sliced layout
+  uint32_t* f1_perm = nullptr;  // node of each slot (kNoNode: padding)
+  uint64_t* f1_sptr = nullptr;  // slice starts (elements)
+  uint16_t* f1_cls = nullptr;   // class per slot, lane-major; ncls: pad, ncls+1: exception
+  uint64_t* f1_urange = nullptr;  // node range of each unit of 16 slices
+  uint64_t f1_nx = 0;           // exception slots, ascending, with their R
+  uint64_t* f1_xslot = nullptr;
+  double* f1_xR = nullptr;
+  uint16_t* lcls = nullptr;     // class per long-row edge (ncls+1: see lcol)
   uint64_t bytes = 0;
   double build_ms = 0.0;
   cudaEvent_t ev[2] = {nullptr, nullptr};  // bracket the sweeps of the last run
@@ -115,6 +144,8 @@ constexpr uint64_t kMaxNodes = (1ull << 30) - 2;
 constexpr uint32_t kBigCode = 0xFFFFFFFFu;  // kcode: gather y instead
 constexpr uint8_t kNmFirst = 0x40, kNmLast = 0x80, kNmLen = 0x3F;
 constexpr uint64_t kMaxEdges = 0xFFFFFFFFull;
+constexpr uint32_t kMaxCls = 12288;   // shared-memory table of ncls+2 doubles
+constexpr uint32_t kF1Unit = 16;      // f1 slices per unit (two windows)
 
 // Builds the in-CSR from a device out-CSR. d_w == nullptr means unit weights.
 // d_src (nullable): source of every out-CSR edge if already known.
@@ -125,6 +156,10 @@ void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, con
 // col as stored (flagged exceptions), true sources src, R).
 void build_slices(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const uint32_t* src,
                   const double* R, cudaStream_t s);
+// The first-sweep class stream (f1) of a compact graph; no-op when the
+// graph has more than kMaxCls classes or QVB_FIRST=gather.
+void build_first(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const double* inv,
+                 cudaStream_t s);
 // Segment size in sources: QVB_SEG_MB (default 64) MiB of 8-byte operands.
 uint64_t segment_size(uint64_t n);
 

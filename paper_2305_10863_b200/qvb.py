@@ -100,6 +100,8 @@ class GraphInfo(C.Structure):
         ("device", C.c_uint32),
         ("device_bytes", C.c_uint64),
         ("build_ms", C.c_double),
+        ("classes", C.c_uint32),
+        ("segments", C.c_uint32),
     ]
 
 

@@ -218,3 +218,32 @@ def test_c4_segmented_equals_single_pass(qvb, monkeypatch):
     g.close()
     assert (bits(p_seg) == bits(p_one)).all()
     assert (p_one >= p2).all() and (p2 >= 1.0 / c["n"]).all() and (p_one <= 1.0).all()
+
+
+@pytest.mark.parametrize("first", ["classes", "gather"])
+def test_first_sweep_paths_bit_exact(qvb, oracle, first, monkeypatch):
+    """The first sweep streams 2-byte out-degree classes (P(s,1) is uniform,
+    so a factor depends on its source only through 1/row_sum); QVB_FIRST=gather
+    keeps the gathering first sweep. Both bit-identical to the oracle on
+    random graphs with parallel edges (exceptions), unit weights given as a
+    weight array, and C1 (uniform / transposed)."""
+    if first == "gather":
+        monkeypatch.setenv("QVB_FIRST", "gather")
+    rng = derive_stream(61, 1)
+    for trial in range(30):
+        n, s, d, w = random_edges(rng, 60, 300, False)
+        ro, col, ww = _csr(oracle, n, s, d, w)
+        g = qvb.DeviceGraph.upload(ro, col, None if trial % 2 else ww)
+        info = g.info()
+        assert (info.classes > 0) == (first == "classes" and info.layout == 0)
+        for layers in (2, 3):
+            assert (bits(g.access_prob(layers)) == bits(oracle.access_prob(ro, col, ww, layers))).all()
+        g.close()
+    c = CONFIGS["C1"]
+    for transposed in (False, True):
+        ro, col, w = oracle.synthetic_graph(c["n"], c["e"], 7, False, transposed)
+        g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, False, transposed)
+        assert g.info().exception_count > 0
+        for layers in (2, 3):
+            assert (bits(g.access_prob(layers)) == bits(oracle.access_prob(ro, col, w, layers))).all()
+        g.close()
