@@ -27,6 +27,8 @@
 // Their blocks come first in the grid so these chains start immediately.
 #include <cstdlib>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "graph.cuh"
 
@@ -41,6 +43,13 @@ constexpr unsigned kFull = 0xffffffffu;
 // kcode of y (graph.cuh): rint(y * 2^53) while y < 2^-22, else kBigCode.
 __device__ __forceinline__ uint32_t y_code(double y) {
   return y < 0x1p-22 ? static_cast<uint32_t>(__double2ull_rn(__dmul_rn(y, 0x1p53))) : kBigCode;
+}
+
+// The factor of a code J (< 2^52): 1 - J 2^-53 is a multiple of 2^-53 in
+// (1/2, 1], so it is exact, and its bit pattern is 1.0's minus J — one
+// integer subtraction instead of a conversion and an FMA.
+__device__ __forceinline__ double code_to_factor(uint32_t J) {
+  return __longlong_as_double(0x3FF0000000000000ll - static_cast<long long>(J));
 }
 
 __global__ void k_init(uint64_t n, const double* __restrict__ inv, double* __restrict__ p,
@@ -677,6 +686,284 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   }
 }
 
+// ---- node-major passes, edge-parallel gathers (compact layout) -------------
+// Pass k of a later sweep (graph.cuh "nm"): one warp per slice of 32
+// consecutive nodes; the slice's pass-k sources are one contiguous run of
+// M = sum of the 32 lens. The warp gathers them edge-parallel — 32 coalesced
+// column reads and 32 independent 4-byte code gathers per instruction, every
+// lane busy — turns each code into its factor (1 - J 2^-53, exact: one
+// rounding, like the reference's 1 - y) and drops the factors into a
+// per-warp shared-memory chunk; each lane then multiplies its own node's run
+// out of the chunk, in source order (its running product carried between
+// passes in `state`, metrics.cpp:152-168). Codes of kBigCode (y >= 2^-21)
+// fall back to y = P(s) * (1/row_sum(s)), recomputed exactly as the
+// producing sweep formed it; exception edges use their own R.
+constexpr int kPassChunk = 256;  // factors per warp chunk
+
+__device__ __forceinline__ double code_factor(uint32_t c, uint32_t code, const uint32_t* __restrict__ exc_src,
+                                              const double* __restrict__ exc_R,
+                                              const double* __restrict__ prev,
+                                              const double* __restrict__ inv) {
+  if (c & kExcFlag) {
+    const uint32_t x = c & ~kExcFlag;
+    return __dsub_rn(1.0, __dmul_rn(prev[exc_src[x]], exc_R[x]));  // metrics.cpp:166
+  }
+  if (code == kBigCode) return __dsub_rn(1.0, __dmul_rn(prev[c], inv[c]));
+  return code_to_factor(code);  // == 1 - y (the reference's one rounding, see graph.cuh)
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_pass(int k, uint64_t S, uint64_t pf, const uint8_t* __restrict__ lenf,
+           const uint64_t* __restrict__ sbase, const uint32_t* __restrict__ ncol,
+           double* __restrict__ state, const uint32_t* __restrict__ exc_src,
+           const double* __restrict__ exc_R, const double* __restrict__ prev,
+           const uint32_t* __restrict__ kprev, const double* __restrict__ inv,
+           double* __restrict__ out, uint32_t* __restrict__ kout) {
+  __shared__ double fbuf[kWarpsPerBlock][kPassChunk];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t pol = policy_evict_first();
+  const uint64_t keep = policy_evict_last();
+  const uint64_t s_block = (uint64_t)blockIdx.x * kWarpsPerBlock;
+  if (pf && wib == kWarpsPerBlock - 1 && lane == 0) {
+    // L2 lookahead: lens, slice pointers and running products of the block
+    // pf ahead, columns of the block pf/2 ahead
+    const uint64_t sp = s_block + pf * kWarpsPerBlock;
+    if (sp < S) {
+      const uint64_t cnt = S - sp < kWarpsPerBlock ? S - sp : kWarpsPerBlock;
+      prefetch_l2(lenf + ((uint64_t)k * S + sp) * 32, cnt * 32);
+      prefetch_l2(sbase + (uint64_t)k * S + sp, (cnt + 1) * sizeof(uint64_t));
+      if (k > 0) prefetch_l2(state + sp * 32, cnt * 32 * sizeof(double));
+    }
+    const uint64_t sc = s_block + (pf / 2) * kWarpsPerBlock;
+    if (sc < S) {
+      const uint64_t ce = sc + kWarpsPerBlock < S ? sc + kWarpsPerBlock : S;
+      const uint64_t a = sbase[(uint64_t)k * S + sc], b = sbase[(uint64_t)k * S + ce];
+      if (b > a) prefetch_l2(ncol + a, (b - a) * sizeof(uint32_t));
+    }
+  }
+  const uint64_t sl = s_block + wib;
+  if (sl >= S) return;
+  const uint64_t v = sl * 32 + lane;
+  const uint32_t lf = lenf[(uint64_t)k * S * 32 + v];
+  if (__ballot_sync(kFull, lf != 0) == 0) return;  // slice untouched by this pass
+  const uint32_t len = lf & kNmLen;
+  uint32_t incl = len;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const uint32_t M = __shfl_sync(kFull, incl, 31);
+  const uint32_t off = incl - len;
+  const uint64_t base = sbase[(uint64_t)k * S + sl];
+  const bool last = lf & kNmLast;
+  double pv = 0.0, iv = 0.0;
+  if (last) {  // finish operands in flight early
+    pv = ld_stream(prev + v, pol);
+    if (kout) iv = ld_stream(inv + v, pol);
+  }
+  // metrics.cpp:152 starts every product at 1.0; a later pass resumes it
+  double miss = (lf != 0 && !(lf & kNmFirst)) ? ld_stream(state + v, pol) : 1.0;
+  double* fb = fbuf[wib];
+  for (uint32_t c0 = 0; c0 < M; c0 += kPassChunk) {
+    const uint32_t cnt = M - c0 < kPassChunk ? M - c0 : kPassChunk;
+    uint32_t c[kPassChunk / 32], code[kPassChunk / 32];
+#pragma unroll
+    for (int u = 0; u < kPassChunk / 32; ++u) {
+      const uint32_t e = u * 32 + lane;
+      c[u] = e < cnt ? ld_stream(ncol + base + c0 + e, pol) : kExcFlag;
+    }
+#pragma unroll
+    for (int u = 0; u < kPassChunk / 32; ++u)
+      code[u] = (c[u] & kExcFlag) ? 0u : ld_hint(kprev + c[u], keep);
+#pragma unroll
+    for (int u = 0; u < kPassChunk / 32; ++u) {
+      const uint32_t e = u * 32 + lane;
+      if (e < cnt) fb[e] = code_factor(c[u], code[u], exc_src, exc_R, prev, inv);
+    }
+    __syncwarp();
+    // this lane's run [off, off + len) within the chunk [c0, c0 + cnt)
+    const uint32_t a = off > c0 ? off : c0;
+    const uint32_t b = off + len < c0 + cnt ? off + len : c0 + cnt;
+    for (uint32_t t = a; t < b; ++t) miss = __dmul_rn(miss, fb[t - c0]);
+    __syncwarp();
+  }
+  if (last) {
+    // metrics.cpp:169: prev + (1 - prev) * (1 - miss_all)
+    const double P = __dadd_rn(pv, __dmul_rn(__dsub_rn(1.0, pv), __dsub_rn(1.0, miss)));
+    st_stream(out + v, P, pol);
+    if (kout) st_stream(kout + v, y_code(__dmul_rn(P, iv)), pol);
+  } else if (len) {
+    st_stream(state + v, miss, pol);
+  }
+}
+
+// Long rows of a node-major graph (in-degree above kNmLen): one warp per row
+// over the whole row, in the first pass; factors as k_pass.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_pass_long(uint64_t nlong, const uint32_t* __restrict__ lnode, const uint64_t* __restrict__ lptr,
+                const uint32_t* __restrict__ lcol, const uint32_t* __restrict__ exc_src,
+                const double* __restrict__ exc_R, const double* __restrict__ prev,
+                const uint32_t* __restrict__ kprev, const double* __restrict__ inv,
+                double* __restrict__ out, uint32_t* __restrict__ kout) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  if (i >= nlong) return;
+  const uint64_t a = lptr[i], b = lptr[i + 1];
+  double miss = 1.0;
+  for (uint64_t cs = a; cs < b; cs += 32) {
+    const uint64_t e = cs + lane;
+    double f = 1.0;
+    if (e < b) {
+      const uint32_t c = lcol[e];
+      f = code_factor(c, (c & kExcFlag) ? 0u : kprev[c], exc_src, exc_R, prev, inv);
+    }
+    const int cnt = static_cast<int>(b - cs < 32 ? b - cs : 32);
+    for (int j = 0; j < cnt; ++j) miss = __dmul_rn(miss, __shfl_sync(kFull, f, j));
+  }
+  if (lane == 0) {
+    const uint32_t v = lnode[i];
+    const double pv = prev[v];
+    const double P = __dadd_rn(pv, __dmul_rn(__dsub_rn(1.0, pv), __dsub_rn(1.0, miss)));
+    out[v] = P;
+    if (kout) kout[v] = y_code(__dmul_rn(P, inv[v]));
+  }
+}
+
+// ---- later sweeps, decoupled: gather codes, then ordered products ---------
+// A node-major graph's later sweep runs in two kernels instead of
+// state-carrying passes.
+//
+// k_codes (G): every nm_col entry's 4-byte code, gathered into nm_code at the
+// same position. nm_col is laid out pass by pass (source segment by source
+// segment), and the persistent grid walks it in order, so the CTAs in flight
+// gather from one L2-sized code segment at a time (evict_last), while the
+// column and code streams go by evict_first. No per-node work at all: the
+// kernel is bound by the random-gather rate of the L1 (one wavefront per
+// 4-byte gather) and the stream bandwidth.
+//
+// k_products (P): one warp per slice of 32 consecutive nodes, lane = node;
+// for pass 0..K-1 the lane reads its run of codes (its sources ascending
+// inside the pass, passes in source order) and multiplies the factors
+// 1 - J 2^-53 in order — the reference's left-to-right product
+// (metrics.cpp:152-168) with the running product in a register across
+// passes. Exception and big-code entries carry marker codes and are resolved
+// from nm_col (rare).
+constexpr uint32_t kExcCode = 0xFFFFFFFEu;  // nm_code marker: exception edge
+
+constexpr int kCodesPerThread = 8;
+
+__global__ void __launch_bounds__(256)
+    k_codes(uint64_t e0, uint64_t e1, const uint32_t* __restrict__ ncol, const uint32_t* __restrict__ kprev,
+            uint32_t* __restrict__ ncode, int smode) {
+  const uint64_t pol = policy_evict_first();
+  constexpr uint64_t kChunk = 256ull * kCodesPerThread;
+  for (uint64_t c0 = e0 + (uint64_t)blockIdx.x * kChunk; c0 < e1; c0 += (uint64_t)gridDim.x * kChunk) {
+    uint32_t c[kCodesPerThread], code[kCodesPerThread];
+#pragma unroll
+    for (int u = 0; u < kCodesPerThread; ++u) {
+      const uint64_t i = c0 + u * 256 + threadIdx.x;
+      c[u] = i < e1 ? ld_stream(ncol + i, pol) : kExcFlag;
+    }
+#pragma unroll
+    for (int u = 0; u < kCodesPerThread; ++u)
+      code[u] = (c[u] & kExcFlag) ? kExcCode : __ldg(kprev + c[u]);
+#pragma unroll
+    for (int u = 0; u < kCodesPerThread; ++u) {
+      const uint64_t i = c0 + u * 256 + threadIdx.x;
+      if (i < e1) {
+        if (smode == 1) __stcs(ncode + i, code[u]);
+        else if (smode == 2) ncode[i] = code[u];
+        else st_stream(ncode + i, code[u], pol);
+      }
+    }
+  }
+}
+
+__device__ __noinline__ double marker_factor(uint32_t code, uint32_t c, const uint32_t* __restrict__ exc_src,
+                                             const double* __restrict__ exc_R,
+                                             const double* __restrict__ prev,
+                                             const double* __restrict__ inv) {
+  if (code == kExcCode) {
+    const uint32_t x = c & ~kExcFlag;
+    return __dsub_rn(1.0, __dmul_rn(prev[exc_src[x]], exc_R[x]));  // metrics.cpp:166
+  }
+  return __dsub_rn(1.0, __dmul_rn(prev[c], inv[c]));  // kBigCode: y = P(s) * (1/row_sum(s))
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_products(int K, uint64_t S, uint64_t n, const uint8_t* __restrict__ lenf,
+               const uint64_t* __restrict__ sbase, const uint32_t* __restrict__ ncode,
+               const uint32_t* __restrict__ ncol, const uint32_t* __restrict__ exc_src,
+               const double* __restrict__ exc_R, const double* __restrict__ prev,
+               const double* __restrict__ inv, double* __restrict__ out, uint32_t* __restrict__ kout) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t sl = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (sl >= S) return;
+  const uint64_t pol = policy_evict_first();
+  const uint64_t v = sl * 32 + lane;
+  const bool real = v < n;
+  double pv = 0.0, iv = 0.0;
+  if (real) {  // finish operands in flight early
+    pv = ld_stream(prev + v, pol);
+    if (kout) iv = ld_stream(inv + v, pol);
+  }
+  double miss = 1.0;  // metrics.cpp:152
+  bool regular = false;  // long rows have no lens (their own kernel)
+  // passes in groups of kPG: the group's lens and slice pointers are loaded
+  // together up front (one memory round trip), then each pass's run
+  constexpr int kPG = 8;
+  for (int k0 = 0; k0 < K; k0 += kPG) {
+    uint32_t lfs[kPG];
+#pragma unroll
+    for (int j = 0; j < kPG; ++j) lfs[j] = k0 + j < K ? lenf[(uint64_t)(k0 + j) * S * 32 + v] : 0u;
+    const uint64_t sb = lane < kPG && k0 + lane < K ? sbase[(uint64_t)(k0 + lane) * S + sl] : 0ull;
+#pragma unroll
+    for (int j = 0; j < kPG; ++j) {
+      const uint32_t lf = lfs[j];
+      regular |= (lf & kNmFirst) != 0;
+      const uint32_t len = lf & kNmLen;
+      const uint32_t maxlen = __reduce_max_sync(kFull, len);
+      const uint64_t base = __shfl_sync(kFull, sb, j);
+      if (maxlen == 0) continue;  // slice untouched by this pass
+      uint32_t incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const uint32_t* __restrict__ cp = ncode + base + (incl - len);
+      const double m0 = miss;  // the product so far, strictly left to right
+      uint32_t marked = 0;
+      for (uint32_t t = 0; t < maxlen; t += 4) {
+        uint32_t code[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) code[u] = t + u < len ? __ldg(cp + t + u) : 0u;  // past the run: 1.0
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          marked |= code[u] >= kExcCode;
+          miss = __dmul_rn(miss, code_to_factor(code[u]));
+        }
+      }
+      if (marked) {  // rare: an exception or big-code entry in the lane's run: redo it
+        miss = m0;
+        const uint64_t q = cp - ncode;
+        for (uint32_t t = 0; t < len; ++t) {
+          const uint32_t code = cp[t];
+          miss = __dmul_rn(miss, code < kExcCode ? code_to_factor(code)
+                                                : marker_factor(code, ncol[q + t], exc_src, exc_R, prev, inv));
+        }
+      }
+    }
+  }
+  if (real && regular) {
+    // metrics.cpp:169: prev + (1 - prev) * (1 - miss_all)
+    const double P = __dadd_rn(pv, __dmul_rn(__dsub_rn(1.0, pv), __dsub_rn(1.0, miss)));
+    st_stream(out + v, P, pol);
+    if (kout) st_stream(kout + v, y_code(__dmul_rn(P, iv)), pol);
+  }
+}
+
 }  // namespace
 
 const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
@@ -687,16 +974,16 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
   const bool f1 = compact && g.ncls > 0 && layers >= 2;  // class-stream first sweep
   for (int i = 0; i < 2; ++i) {
     if (!g.p[i]) QVB_CUDA(cudaMalloc(&g.p[i], (n + 1) * sizeof(double)));
-    if (compact && !g.y[i]) QVB_CUDA(cudaMalloc(&g.y[i], (n + 1) * sizeof(double)));
+    if (compact && !g.nm && !g.y[i]) QVB_CUDA(cudaMalloc(&g.y[i], (n + 1) * sizeof(double)));
     if (codes && !g.kcode[i]) QVB_CUDA(cudaMalloc(&g.kcode[i], (n + 1) * sizeof(uint32_t)));
     // entry N is the padding operand of every gathered vector: 0 (factor 1.0)
     QVB_CUDA(cudaMemsetAsync(g.p[i] + n, 0, sizeof(double), s));
-    if (compact) QVB_CUDA(cudaMemsetAsync(g.y[i] + n, 0, sizeof(double), s));
+    if (compact && !g.nm) QVB_CUDA(cudaMemsetAsync(g.y[i] + n, 0, sizeof(double), s));
     if (codes) QVB_CUDA(cudaMemsetAsync(g.kcode[i] + n, 0, sizeof(uint32_t), s));
   }
   const double base = 1.0 / static_cast<double>(n);  // metrics.cpp:143
   if (!f1) {  // P(n,1) (and, for a gathering first sweep, its operands)
-    k_init<<<grid_for(n + 1, 256), 256, 0, s>>>(n, g.inv, g.p[0], (compact && layers >= 2) ? g.y[0] : nullptr,
+    k_init<<<grid_for(n + 1, 256), 256, 0, s>>>(n, g.inv, g.p[0], (compact && !g.nm && layers >= 2) ? g.y[0] : nullptr,
                                                (codes && layers >= 2) ? g.kcode[0] : nullptr);
     QVB_LAUNCH_CHECK();
   }
@@ -714,7 +1001,7 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
   for (uint32_t j = 2; j <= layers; ++j) {
     const int cur = (j - 2) & 1, nxt = cur ^ 1;
     const bool first = j == 2;
-    double* yout = (compact && j < layers) ? g.y[nxt] : nullptr;
+    double* yout = (compact && !g.nm && j < layers) ? g.y[nxt] : nullptr;
     uint32_t* kout = (codes && j < layers) ? g.kcode[nxt] : nullptr;
     if (first && f1) {
       const size_t smem = (g.ncls + 2) * sizeof(double);
@@ -753,18 +1040,63 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
     const double fbase = (first && !compact) ? base : 0.0;  // weighted first sweep: no gathers
     if (g.nm) {  // node-major passes
       for (int k = 0; k < nseg; ++k) {
-        const uint64_t lb = k == 0 ? long_blocks : 0;
-        const uint64_t blocks = lb + (g.nm_S + kWarpsPerBlock - 1) / kWarpsPerBlock;
-        if (compact)
-          k_sweep_nm<false><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
-              k, g.nm_S, lb, g.nlong, pf, g.nm_lenf, g.nm_sbase, g.nm_col, nullptr, g.state, g.lnode,
-              g.lptr, g.lcol, nullptr, g.exc_src, g.exc_R, g.p[cur], g.y[cur], g.kcode[cur],
-              g.inv, g.p[nxt], yout, kout, gmode, 0.0);
-        else
+        if (compact) {
+          if (k > 0) continue;  // one G + P pair covers every pass
+          if (g.nlong) {
+            k_pass_long<<<static_cast<unsigned>((g.nlong * 32 + 255) / 256), 256, 0, s>>>(
+                g.nlong, g.lnode, g.lptr, g.lcol, g.exc_src, g.exc_R, g.p[cur], g.kcode[cur], g.inv,
+                g.p[nxt], kout);
+            QVB_LAUNCH_CHECK();
+          }
+          if (!g.nm_code) QVB_CUDA(cudaMalloc(&g.nm_code, (g.nm_cols ? g.nm_cols : 1) * sizeof(uint32_t)));
+          int smode = 0;
+          if (const char* m = std::getenv("QVB_G_STORE")) smode = std::atoi(m);
+          size_t persist = 0;  // QVB_G_PERSIST_MB: pin each region's code segment in L2
+          if (const char* m = std::getenv("QVB_G_PERSIST_MB")) persist = (size_t)std::atoi(m) << 20;
+          if (persist) {
+            int maxp = 0;
+            QVB_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, g.device));
+            persist = std::min(persist, (size_t)maxp);
+            QVB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
+          }
+          const std::vector<uint64_t>& sb = g.nm_region;
+          for (int kk = 0; kk < nseg; ++kk) {
+            const uint64_t e0 = sb[kk], e1 = sb[kk + 1];
+            if (e1 <= e0) continue;
+            const unsigned cg = resident_grid(k_codes, 256, 0, (e1 - e0 + 2047) / 2048);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(cg);
+            cfg.blockDim = dim3(256);
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            if (persist) {
+              const uint64_t first = (uint64_t)kk * g.seg_size;
+              const uint64_t count = std::min<uint64_t>(g.seg_size, n - first);
+              attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+              attr[0].val.accessPolicyWindow.base_ptr = g.kcode[cur] + first;
+              attr[0].val.accessPolicyWindow.num_bytes = std::min<size_t>(count * sizeof(uint32_t), persist);
+              attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+              attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+              attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+              cfg.attrs = attr;
+              cfg.numAttrs = 1;
+            }
+            QVB_CUDA(cudaLaunchKernelEx(&cfg, k_codes, e0, e1, (const uint32_t*)g.nm_col,
+                                        (const uint32_t*)g.kcode[cur], g.nm_code, smode));
+          }
+          if (persist) QVB_CUDA(cudaCtxResetPersistingL2Cache());
+          k_products<<<static_cast<unsigned>((g.nm_S + kWarpsPerBlock - 1) / kWarpsPerBlock),
+                       kWarpsPerBlock * 32, 0, s>>>(nseg, g.nm_S, n, g.nm_lenf, g.nm_sbase, g.nm_code,
+                                                    g.nm_col, g.exc_src, g.exc_R, g.p[cur], g.inv,
+                                                    g.p[nxt], kout);
+        } else {
+          const uint64_t lb = k == 0 ? long_blocks : 0;
+          const uint64_t blocks = lb + (g.nm_S + kWarpsPerBlock - 1) / kWarpsPerBlock;
           k_sweep_nm<true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
               k, g.nm_S, lb, g.nlong, pf, g.nm_lenf, g.nm_sbase, g.nm_col, g.nm_R, g.state, g.lnode,
               g.lptr, g.lcol, g.lR, nullptr, nullptr, g.p[cur], nullptr, nullptr, g.inv,
               g.p[nxt], nullptr, nullptr, gmode, fbase);
+        }
         QVB_LAUNCH_CHECK();
       }
       continue;

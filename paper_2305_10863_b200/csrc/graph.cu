@@ -47,6 +47,7 @@ qvb_graph::~qvb_graph() {
   cudaFree(nm_lenf);
   cudaFree(nm_sbase);
   cudaFree(nm_col);
+  cudaFree(nm_code);
   cudaFree(nm_R);
   cudaFree(cls_inv);
   cudaFree(f1_perm);
@@ -843,6 +844,8 @@ void build_nm(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const uin
   exclusive_sum_u32_u64(cnt.p, sbase.p, S * nseg + 1, s);
   cnt.release();
   const uint64_t total = read_scalar(sbase.p + S * nseg, s);
+  g.nm_region.resize(nseg + 1);
+  for (int k = 0; k <= nseg; ++k) g.nm_region[k] = read_scalar(sbase.p + S * k, s);
   DevBuf<uint32_t> ncol(total + 4, s);  // +4: 16-byte bulk-copy windows
   DevBuf<double> nR;
   if (R) nR.alloc(total ? total : 1, s);

@@ -110,6 +110,8 @@ struct qvb_graph {
   uint8_t* nm_lenf = nullptr;
   uint64_t* nm_sbase = nullptr;
   uint32_t* nm_col = nullptr;
+  uint32_t* nm_code = nullptr;
+  std::vector<uint64_t> nm_region;  // host: start of each pass's columns in nm_col (nseg + 1)  // compact: the gathered code of every nm_col entry (per sweep)
   double* nm_R = nullptr;
   uint32_t* kcode[2] = {nullptr, nullptr};
   // first sweep ("f1", see above): out-degree classes and their streams
