@@ -122,6 +122,91 @@ def bytes_per_sweep(eu: int, n: int, weighted: bool) -> int:
     return eu * (20 if weighted else 12) + n * (24 if weighted else 32)
 
 
+# measured random 4-byte gather rate from an L2-resident vector on this pool's
+# B200s (experiments/die_split.cu, experiments/gather_paths.cu: 273-288 G/s):
+# one L1 wavefront per random gather, ~1 per SM per clock
+GATHER_CEILING = 286e9
+
+
+def access_prob_line(cfg, info, layers, ap_call, ap_sweep, phases, pk):
+    """The P(n,j) leg of the bench line. ``roofline`` is the call's dominant
+    phase against its own algorithmic bytes; ``survey_model`` is the north-star
+    statement (every sweep moves 12 B per coalesced edge and 32 B
+    per node, T_roof = bytes / HBM peak) as the ratio T_roof / T_call. The
+    first sweep streams 2-byte out-degree classes instead of gathering
+    (P(s,1) is uniform), so it moves fewer bytes than that model assumes."""
+    n, eu = cfg["n"], info.unique_edge_count
+    sweeps = layers - 1
+    ap_ms = statistics.mean(ap_call)
+    sweep_ms = statistics.mean(ap_sweep)
+    ph = {k: statistics.mean(p[k] for p in phases) for k in ("first", "gather", "products", "other")}
+    launches = phases[-1]["launches"]
+    later = sweeps - 1 if ph["first"] > 0 else sweeps
+    cols = info.segment_columns
+    nseg = info.segments
+    # algorithmic bytes per phase (all sweeps of one call)
+    alg = {
+        # classes 2 B/slot, perm 4 B/node, P out 8 B/node; for a later sweep
+        # also its 1/row_sum in and its 4-byte code out
+        "first": info.first_slots * 2 + n * (4 + 8 + (12 if layers > 2 else 0)),
+        # per later sweep: column in + code out per edge, plus the code
+        # segment once (the gathers themselves are L2 hits)
+        "gather": later * (cols * 8 + n * 4),
+        # per later sweep: codes in, lens per pass, P(j-1) and 1/row_sum in,
+        # P out (+ code out if another sweep follows)
+        "products": sum(cols * 4 + n * nseg + n * 24 + (n * 4 if j < sweeps - 1 else 0)
+                        for j in range(later)),
+    }
+    kernels = {}
+    for k, name in (("first", "k_first"), ("gather", "k_codes"), ("products", "k_products")):
+        if ph[k] > 0:
+            a = alg[k] / (ph[k] / 1e3) / 1e9
+            kernels[name] = {"ms_per_call": ph[k], "algorithmic_bytes": alg[k], "achieved_gbs": a,
+                             "frac_hbm": a / pk["hbm_gbs"]}
+    if ph["gather"] > 0:
+        gps = later * cols / (ph["gather"] / 1e3)
+        kernels["k_codes"].update({"gathers_per_s": gps, "gather_ceiling_per_s": GATHER_CEILING,
+                                   "frac_gather_ceiling": gps / GATHER_CEILING})
+    if ph["other"] > 0:
+        kernels["k_sweep"] = {"ms_per_call": ph["other"]}
+    survey_bytes = bytes_per_sweep(eu, n, info.layout == 1) * sweeps
+    t_roof = survey_bytes / (pk["hbm_gbs"] * 1e9) * 1e3
+    dom = max(kernels, key=lambda k: kernels[k]["ms_per_call"]) if kernels else None
+    if dom in ("k_first", "k_codes", "k_products"):
+        d = kernels[dom]
+        roof = {"bound": "hbm", "kernel": dom, "traffic": None, "algorithmic_bytes": d["algorithmic_bytes"],
+                "achieved": d["achieved_gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": d["frac_hbm"], "per_launch_ms": d["ms_per_call"], "peak_source": pk["source"]}
+    else:  # sliced sweeps: the SURVEY per-sweep model, except that a weighted
+        # first sweep does not gather (P(s,1) is uniform): 12 B/edge there
+        w = info.layout == 1
+        sb = survey_bytes - (eu * 8 if w and sweeps >= 1 else 0)
+        a = sb / (sweep_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": "k_sweep", "traffic": None, "algorithmic_bytes": sb,
+                "achieved": a, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": a / pk["hbm_gbs"],
+                "peak_source": pk["source"]}
+    return {
+        "metric": "access-prob edges/s (coalesced in-edges x sweeps / device time of the P call)",
+        "value": eu * sweeps / (ap_ms / 1e3),
+        "unit": "edges/s",
+        "ms_per_call": ap_ms,
+        "sweep_ms": sweep_ms,
+        "layers": layers,
+        "graph": {"nodes": n, "edges": cfg["e"], "unique_edges": eu,
+                  "exceptions": info.exception_count,
+                  "layout": "weighted" if info.layout else "compact",
+                  "first_sweep_classes": info.classes, "source_segments": nseg,
+                  "in_csr_build_ms": info.build_ms, "device_bytes": info.device_bytes},
+        "roofline": roof,
+        "kernels": kernels,
+        "survey_model": {"bytes": survey_bytes, "t_roof_ms": t_roof, "ms": ap_ms,
+                         "frac": t_roof / ap_ms,
+                         "note": "SURVEY §8(d) per-sweep bytes (12 B/edge + 32 B/node) at the HBM peak, "
+                                 "over the measured call time: the north-star 'P pass vs HBM roofline'"},
+        "gpu_launches": launches * len(ap_call),
+    }
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -146,7 +231,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         g.access_prob(layers, out=p_dev, stream=stream)
     torch.cuda.synchronize(dev)
-    ap_call, ap_sweep = [], []
+    ap_call, ap_sweep, phases = [], [], []
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     for _ in range(args.steps):
         ev[0].record(stream)
@@ -155,29 +240,9 @@ def run_ours(args):
         ev[1].synchronize()
         ap_call.append(ev[0].elapsed_time(ev[1]))
         ap_sweep.append(g.last_sweep_ms())
+        phases.append(g.phase_ms())
     p_host = p_dev.cpu().numpy()
-    sweeps = layers - 1
-    ap_bytes = bytes_per_sweep(info.unique_edge_count, n, info.layout == 1) * sweeps
-    ap_ms = statistics.mean(ap_call)
-    sweep_ms = statistics.mean(ap_sweep)
-    access_prob = {
-        "metric": "access-prob edges/s (coalesced in-edges x sweeps / device time of the P call)",
-        "value": info.unique_edge_count * sweeps / (ap_ms / 1e3),
-        "unit": "edges/s",
-        "ms_per_call": ap_ms,
-        "sweep_ms": sweep_ms,
-        "layers": layers,
-        "graph": {"nodes": n, "edges": e, "unique_edges": info.unique_edge_count,
-                  "exceptions": info.exception_count,
-                  "layout": "weighted" if info.layout else "compact",
-                  "in_csr_build_ms": info.build_ms, "device_bytes": info.device_bytes},
-        "roofline": {"bound": "hbm", "kernel": "k_sweep", "traffic": None,
-                     "algorithmic_bytes": ap_bytes,
-                     "achieved": ap_bytes / (sweep_ms / 1e3) / 1e9, "peak": pk["hbm_gbs"],
-                     "unit": "GB/s", "frac": ap_bytes / (sweep_ms / 1e3) / 1e9 / pk["hbm_gbs"],
-                     "peak_source": pk["source"]},
-        "gpu_launches": args.steps * (1 + sweeps),
-    }
+    access_prob = access_prob_line(cfg, info, layers, ap_call, ap_sweep, phases, pk)
     g.close()
 
     # ---- K0 sampler: qv_bench's batch_sample (tools/bench.cpp:89-94) ----------
@@ -291,7 +356,7 @@ def run_ours(args):
                                    timings=tm)
         wall = time.perf_counter() - t0
         access_prob["e2e"] = {
-            "value": info.unique_edge_count * sweeps / wall, "unit": "edges/s",
+            "value": info.unique_edge_count * (layers - 1) / wall, "unit": "edges/s",
             "wall_s": wall, "upload_build_ms": tm[0], "sweeps_ms": tm[1], "download_ms": tm[2],
             "h2d_bytes": int(ro.nbytes + col.nbytes + (w.nbytes if cfg["weighted"] else 0)),
             "d2h_bytes": n * 8,
@@ -354,8 +419,9 @@ def run_ours(args):
             if "k_gather" in tr:
                 line["roofline"]["traffic"] = tr["k_gather"]["bytes_per_launch"]
                 line["roofline"]["traffic_batch"] = tr["k_gather"].get("batch")
-            if "k_sweep" in tr:
-                access_prob["roofline"]["traffic"] = tr["k_sweep"]["bytes_per_launch"]
+            kname = access_prob["roofline"]["kernel"]
+            if kname in tr:
+                access_prob["roofline"]["traffic"] = tr[kname]["bytes_per_launch"]
         except Exception:  # noqa: BLE001
             pass
     store.close()

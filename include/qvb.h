@@ -113,6 +113,8 @@ typedef struct qvb_graph_info {
   double build_ms;             /* device time of the in-CSR build           */
   uint32_t classes;            /* first-sweep out-degree classes (0: the first sweep gathers) */
   uint32_t segments;           /* source segments (passes) of the later sweeps */
+  uint64_t first_slots;        /* padded slots of the first sweep's class stream */
+  uint64_t segment_columns;    /* columns of the node-major segmented layout (0: sliced) */
 } qvb_graph_info;
 
 /* Upload an out-CSR (qv::Graph layout, graph.hpp:25-48): row_offsets[n+1],
@@ -144,6 +146,10 @@ int qvb_graph_info_get(const qvb_graph* g, qvb_graph_info* info);
 /* Device time (ms, CUDA events on the call's stream) of the P sweeps of the
  * last qvb_access_prob on g. */
 int qvb_graph_last_sweep_ms(const qvb_graph* g, double* ms);
+/* Per-phase device time (ms) of the last qvb_access_prob on g: ms[0] first
+ * sweep over the class stream, ms[1] code gathers, ms[2] ordered products,
+ * ms[3] other sweep kernels; *launches (nullable) = kernels launched. */
+int qvb_graph_phase_ms(const qvb_graph* g, double* ms, uint32_t* launches);
 int qvb_graph_destroy(qvb_graph* g);
 
 /* ---- K1: access probability P(n,j) (metrics.cpp:134-173) ---------------- */

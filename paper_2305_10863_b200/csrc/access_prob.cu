@@ -686,20 +686,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   }
 }
 
-// ---- node-major passes, edge-parallel gathers (compact layout) -------------
-// Pass k of a later sweep (graph.cuh "nm"): one warp per slice of 32
-// consecutive nodes; the slice's pass-k sources are one contiguous run of
-// M = sum of the 32 lens. The warp gathers them edge-parallel — 32 coalesced
-// column reads and 32 independent 4-byte code gathers per instruction, every
-// lane busy — turns each code into its factor (1 - J 2^-53, exact: one
-// rounding, like the reference's 1 - y) and drops the factors into a
-// per-warp shared-memory chunk; each lane then multiplies its own node's run
-// out of the chunk, in source order (its running product carried between
-// passes in `state`, metrics.cpp:152-168). Codes of kBigCode (y >= 2^-21)
-// fall back to y = P(s) * (1/row_sum(s)), recomputed exactly as the
-// producing sweep formed it; exception edges use their own R.
-constexpr int kPassChunk = 256;  // factors per warp chunk
-
+// ---- node-major graphs, compact layout: shared factor helpers --------------
+// Codes of kBigCode (y >= 2^-21) fall back to y = P(s) * (1/row_sum(s)),
+// recomputed exactly as the producing sweep formed it; exception edges use
+// their own R.
 __device__ __forceinline__ double code_factor(uint32_t c, uint32_t code, const uint32_t* __restrict__ exc_src,
                                               const double* __restrict__ exc_R,
                                               const double* __restrict__ prev,
@@ -712,94 +702,8 @@ __device__ __forceinline__ double code_factor(uint32_t c, uint32_t code, const u
   return code_to_factor(code);  // == 1 - y (the reference's one rounding, see graph.cuh)
 }
 
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    k_pass(int k, uint64_t S, uint64_t pf, const uint8_t* __restrict__ lenf,
-           const uint64_t* __restrict__ sbase, const uint32_t* __restrict__ ncol,
-           double* __restrict__ state, const uint32_t* __restrict__ exc_src,
-           const double* __restrict__ exc_R, const double* __restrict__ prev,
-           const uint32_t* __restrict__ kprev, const double* __restrict__ inv,
-           double* __restrict__ out, uint32_t* __restrict__ kout) {
-  __shared__ double fbuf[kWarpsPerBlock][kPassChunk];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t pol = policy_evict_first();
-  const uint64_t keep = policy_evict_last();
-  const uint64_t s_block = (uint64_t)blockIdx.x * kWarpsPerBlock;
-  if (pf && wib == kWarpsPerBlock - 1 && lane == 0) {
-    // L2 lookahead: lens, slice pointers and running products of the block
-    // pf ahead, columns of the block pf/2 ahead
-    const uint64_t sp = s_block + pf * kWarpsPerBlock;
-    if (sp < S) {
-      const uint64_t cnt = S - sp < kWarpsPerBlock ? S - sp : kWarpsPerBlock;
-      prefetch_l2(lenf + ((uint64_t)k * S + sp) * 32, cnt * 32);
-      prefetch_l2(sbase + (uint64_t)k * S + sp, (cnt + 1) * sizeof(uint64_t));
-      if (k > 0) prefetch_l2(state + sp * 32, cnt * 32 * sizeof(double));
-    }
-    const uint64_t sc = s_block + (pf / 2) * kWarpsPerBlock;
-    if (sc < S) {
-      const uint64_t ce = sc + kWarpsPerBlock < S ? sc + kWarpsPerBlock : S;
-      const uint64_t a = sbase[(uint64_t)k * S + sc], b = sbase[(uint64_t)k * S + ce];
-      if (b > a) prefetch_l2(ncol + a, (b - a) * sizeof(uint32_t));
-    }
-  }
-  const uint64_t sl = s_block + wib;
-  if (sl >= S) return;
-  const uint64_t v = sl * 32 + lane;
-  const uint32_t lf = lenf[(uint64_t)k * S * 32 + v];
-  if (__ballot_sync(kFull, lf != 0) == 0) return;  // slice untouched by this pass
-  const uint32_t len = lf & kNmLen;
-  uint32_t incl = len;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += t;
-  }
-  const uint32_t M = __shfl_sync(kFull, incl, 31);
-  const uint32_t off = incl - len;
-  const uint64_t base = sbase[(uint64_t)k * S + sl];
-  const bool last = lf & kNmLast;
-  double pv = 0.0, iv = 0.0;
-  if (last) {  // finish operands in flight early
-    pv = ld_stream(prev + v, pol);
-    if (kout) iv = ld_stream(inv + v, pol);
-  }
-  // metrics.cpp:152 starts every product at 1.0; a later pass resumes it
-  double miss = (lf != 0 && !(lf & kNmFirst)) ? ld_stream(state + v, pol) : 1.0;
-  double* fb = fbuf[wib];
-  for (uint32_t c0 = 0; c0 < M; c0 += kPassChunk) {
-    const uint32_t cnt = M - c0 < kPassChunk ? M - c0 : kPassChunk;
-    uint32_t c[kPassChunk / 32], code[kPassChunk / 32];
-#pragma unroll
-    for (int u = 0; u < kPassChunk / 32; ++u) {
-      const uint32_t e = u * 32 + lane;
-      c[u] = e < cnt ? ld_stream(ncol + base + c0 + e, pol) : kExcFlag;
-    }
-#pragma unroll
-    for (int u = 0; u < kPassChunk / 32; ++u)
-      code[u] = (c[u] & kExcFlag) ? 0u : ld_hint(kprev + c[u], keep);
-#pragma unroll
-    for (int u = 0; u < kPassChunk / 32; ++u) {
-      const uint32_t e = u * 32 + lane;
-      if (e < cnt) fb[e] = code_factor(c[u], code[u], exc_src, exc_R, prev, inv);
-    }
-    __syncwarp();
-    // this lane's run [off, off + len) within the chunk [c0, c0 + cnt)
-    const uint32_t a = off > c0 ? off : c0;
-    const uint32_t b = off + len < c0 + cnt ? off + len : c0 + cnt;
-    for (uint32_t t = a; t < b; ++t) miss = __dmul_rn(miss, fb[t - c0]);
-    __syncwarp();
-  }
-  if (last) {
-    // metrics.cpp:169: prev + (1 - prev) * (1 - miss_all)
-    const double P = __dadd_rn(pv, __dmul_rn(__dsub_rn(1.0, pv), __dsub_rn(1.0, miss)));
-    st_stream(out + v, P, pol);
-    if (kout) st_stream(kout + v, y_code(__dmul_rn(P, iv)), pol);
-  } else if (len) {
-    st_stream(state + v, miss, pol);
-  }
-}
-
 // Long rows of a node-major graph (in-degree above kNmLen): one warp per row
-// over the whole row, in the first pass; factors as k_pass.
+// over the whole row (gathers span every segment; few rows).
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     k_pass_long(uint64_t nlong, const uint32_t* __restrict__ lnode, const uint64_t* __restrict__ lptr,
                 const uint32_t* __restrict__ lcol, const uint32_t* __restrict__ exc_src,
@@ -853,11 +757,22 @@ constexpr uint32_t kExcCode = 0xFFFFFFFEu;  // nm_code marker: exception edge
 
 constexpr int kCodesPerThread = 8;
 
+// A factor f in (1/2, 1] is 1 - J 2^-53 for the integer J = bits(1.0) -
+// bits(f): the code whose code_to_factor is f bit for bit. Factors outside
+// that range, or whose J does not fit below the markers, keep a marker.
+__device__ __forceinline__ uint32_t factor_to_code(double f) {
+  const long long j = 0x3FF0000000000000ll - __double_as_longlong(f);
+  return (f > 0.5 && j >= 0 && j < kExcCode) ? static_cast<uint32_t>(j) : kExcCode;
+}
+
 __global__ void __launch_bounds__(256)
     k_codes(uint64_t e0, uint64_t e1, const uint32_t* __restrict__ ncol, const uint32_t* __restrict__ kprev,
-            uint32_t* __restrict__ ncode, int smode) {
+            const uint32_t* __restrict__ exc_src, const double* __restrict__ exc_R,
+            const double* __restrict__ prev, const double* __restrict__ inv,
+            uint32_t* __restrict__ ncode, uint32_t* __restrict__ marked) {
   const uint64_t pol = policy_evict_first();
   constexpr uint64_t kChunk = 256ull * kCodesPerThread;
+  uint32_t any = 0;
   for (uint64_t c0 = e0 + (uint64_t)blockIdx.x * kChunk; c0 < e1; c0 += (uint64_t)gridDim.x * kChunk) {
     uint32_t c[kCodesPerThread], code[kCodesPerThread];
 #pragma unroll
@@ -871,24 +786,63 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int u = 0; u < kCodesPerThread; ++u) {
       const uint64_t i = c0 + u * 256 + threadIdx.x;
-      if (i < e1) {
-        if (smode == 1) __stcs(ncode + i, code[u]);
-        else if (smode == 2) ncode[i] = code[u];
-        else st_stream(ncode + i, code[u], pol);
+      if (i >= e1) continue;
+      if (code[u] >= kExcCode) {  // rare: exception edge or y >= 2^-21: the exact factor's code
+        double f;
+        if (c[u] & kExcFlag) {
+          const uint32_t x = c[u] & ~kExcFlag;
+          f = __dsub_rn(1.0, __dmul_rn(prev[exc_src[x]], exc_R[x]));  // metrics.cpp:166
+        } else {
+          f = __dsub_rn(1.0, __dmul_rn(prev[c[u]], inv[c[u]]));  // y = P(s) * (1/row_sum(s))
+        }
+        code[u] = factor_to_code(f);
+        any |= code[u] == kExcCode;
       }
+      st_stream(ncode + i, code[u], pol);
     }
   }
+  if (__any_sync(kFull, any) && (threadIdx.x & 31) == 0) atomicOr(marked, 1u);
 }
 
 __device__ __noinline__ double marker_factor(uint32_t code, uint32_t c, const uint32_t* __restrict__ exc_src,
                                              const double* __restrict__ exc_R,
                                              const double* __restrict__ prev,
                                              const double* __restrict__ inv) {
-  if (code == kExcCode) {
+  if (c & kExcFlag) {
     const uint32_t x = c & ~kExcFlag;
     return __dsub_rn(1.0, __dmul_rn(prev[exc_src[x]], exc_R[x]));  // metrics.cpp:166
   }
-  return __dsub_rn(1.0, __dmul_rn(prev[c], inv[c]));  // kBigCode: y = P(s) * (1/row_sum(s))
+  return __dsub_rn(1.0, __dmul_rn(prev[c], inv[c]));  // y = P(s) * (1/row_sum(s))
+}
+
+// The lane's product over every pass with marker codes resolved (rare: only
+// when some factor of the sweep had no code, see k_codes).
+__device__ __noinline__ double products_markers(int K, uint64_t S, uint64_t sl, int lane,
+                                                const uint8_t* __restrict__ lenf,
+                                                const uint64_t* __restrict__ sbase,
+                                                const uint32_t* __restrict__ ncode,
+                                                const uint32_t* __restrict__ ncol,
+                                                const uint32_t* __restrict__ exc_src,
+                                                const double* __restrict__ exc_R,
+                                                const double* __restrict__ prev,
+                                                const double* __restrict__ inv) {
+  const uint64_t v = sl * 32 + lane;
+  double miss = 1.0;
+  for (int k = 0; k < K; ++k) {
+    const uint32_t len = lenf[(uint64_t)k * S * 32 + v] & kNmLen;
+    uint32_t incl = len;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const uint64_t q = sbase[(uint64_t)k * S + sl] + (incl - len);
+    for (uint32_t t = 0; t < len; ++t) {
+      const uint32_t code = ncode[q + t];
+      miss = __dmul_rn(miss, code < kExcCode ? code_to_factor(code)
+                                            : marker_factor(code, ncol[q + t], exc_src, exc_R, prev, inv));
+    }
+  }
+  return miss;
 }
 
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
@@ -896,7 +850,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                const uint64_t* __restrict__ sbase, const uint32_t* __restrict__ ncode,
                const uint32_t* __restrict__ ncol, const uint32_t* __restrict__ exc_src,
                const double* __restrict__ exc_R, const double* __restrict__ prev,
-               const double* __restrict__ inv, double* __restrict__ out, uint32_t* __restrict__ kout) {
+               const double* __restrict__ inv, double* __restrict__ out, uint32_t* __restrict__ kout,
+               const uint32_t* __restrict__ marked) {
   const int lane = threadIdx.x & 31;
   const uint64_t sl = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (sl >= S) return;
@@ -909,54 +864,36 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     if (kout) iv = ld_stream(inv + v, pol);
   }
   double miss = 1.0;  // metrics.cpp:152
-  bool regular = false;  // long rows have no lens (their own kernel)
-  // passes in groups of kPG: the group's lens and slice pointers are loaded
-  // together up front (one memory round trip), then each pass's run
-  constexpr int kPG = 8;
-  for (int k0 = 0; k0 < K; k0 += kPG) {
-    uint32_t lfs[kPG];
+  uint32_t any = 0;   // a first-pass flag: regular row (long rows have their own kernel)
+  const uint8_t* __restrict__ lp = lenf + v;
+  const uint64_t* __restrict__ sp = sbase + sl;
+  const uint64_t lstep = S * 32;
+  for (int k = 0; k < K; ++k, lp += lstep, sp += S) {
+    const uint32_t lf = *lp;
+    const uint64_t sb = *sp;
+    any |= lf;
+    const uint32_t len = lf & kNmLen;
+    const uint32_t maxlen = __reduce_max_sync(kFull, len);
+    if (maxlen == 0) continue;  // slice untouched by this pass
+    uint32_t incl = len;
 #pragma unroll
-    for (int j = 0; j < kPG; ++j) lfs[j] = k0 + j < K ? lenf[(uint64_t)(k0 + j) * S * 32 + v] : 0u;
-    const uint64_t sb = lane < kPG && k0 + lane < K ? sbase[(uint64_t)(k0 + lane) * S + sl] : 0ull;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const uint32_t* __restrict__ cp = ncode + sb + (incl - len);
+    for (uint32_t t = 0; t < maxlen; t += 4) {
+      uint32_t code[4];
 #pragma unroll
-    for (int j = 0; j < kPG; ++j) {
-      const uint32_t lf = lfs[j];
-      regular |= (lf & kNmFirst) != 0;
-      const uint32_t len = lf & kNmLen;
-      const uint32_t maxlen = __reduce_max_sync(kFull, len);
-      const uint64_t base = __shfl_sync(kFull, sb, j);
-      if (maxlen == 0) continue;  // slice untouched by this pass
-      uint32_t incl = len;
+      for (int u = 0; u < 4; ++u) code[u] = __ldg(cp + t + u);  // ncode is padded past its end
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const uint32_t* __restrict__ cp = ncode + base + (incl - len);
-      const double m0 = miss;  // the product so far, strictly left to right
-      uint32_t marked = 0;
-      for (uint32_t t = 0; t < maxlen; t += 4) {
-        uint32_t code[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) code[u] = t + u < len ? __ldg(cp + t + u) : 0u;  // past the run: 1.0
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          marked |= code[u] >= kExcCode;
-          miss = __dmul_rn(miss, code_to_factor(code[u]));
-        }
-      }
-      if (marked) {  // rare: an exception or big-code entry in the lane's run: redo it
-        miss = m0;
-        const uint64_t q = cp - ncode;
-        for (uint32_t t = 0; t < len; ++t) {
-          const uint32_t code = cp[t];
-          miss = __dmul_rn(miss, code < kExcCode ? code_to_factor(code)
-                                                : marker_factor(code, ncol[q + t], exc_src, exc_R, prev, inv));
-        }
-      }
+      for (int u = 0; u < 4; ++u)
+        miss = __dmul_rn(miss, code_to_factor(t + u < len ? code[u] : 0u));  // past the run: 1.0
     }
   }
-  if (real && regular) {
+  if (*marked)  // uniform and rare: redo with the marker codes resolved
+    miss = products_markers(K, S, sl, lane, lenf, sbase, ncode, ncol, exc_src, exc_R, prev, inv);
+  if (real && (any & kNmFirst)) {
     // metrics.cpp:169: prev + (1 - prev) * (1 - miss_all)
     const double P = __dadd_rn(pv, __dmul_rn(__dsub_rn(1.0, pv), __dsub_rn(1.0, miss)));
     st_stream(out + v, P, pol);
@@ -966,11 +903,43 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 
 }  // namespace
 
+namespace {
+
+// Phase brackets of one run (graph.cuh PhaseEv), events pooled in the graph.
+struct PhaseTimer {
+  qvb_graph& g;
+  cudaStream_t s;
+  int open = -1;
+  PhaseTimer(qvb_graph& gr, cudaStream_t st) : g(gr), s(st) {
+    g.phase_used = 0;
+    g.launches = 0;
+  }
+  void begin(int phase) {
+    if (g.phase_used == g.phase_ev.size()) {
+      qvb_graph::PhaseEv pe{phase, nullptr, nullptr};
+      QVB_CUDA(cudaEventCreate(&pe.a));
+      QVB_CUDA(cudaEventCreate(&pe.b));
+      g.phase_ev.push_back(pe);
+    }
+    auto& pe = g.phase_ev[g.phase_used];
+    pe.phase = phase;
+    QVB_CUDA(cudaEventRecord(pe.a, s));
+    open = static_cast<int>(g.phase_used);
+  }
+  void end(uint32_t launched) {
+    QVB_CUDA(cudaEventRecord(g.phase_ev[open].b, s));
+    ++g.phase_used;
+    g.launches += launched;
+  }
+};
+
+}  // namespace
+
 const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
   if (layers < 1) fail(QVB_ERR_VALIDATION, "access probability needs layers >= 1");
   const uint64_t n = g.n;
   const bool compact = g.layout == 0;
-  const bool codes = g.nm && compact;           // nm compact sweeps gather 4-byte codes
+  const bool codes = g.nm && compact;                    // nm compact sweeps gather 4-byte codes
   const bool f1 = compact && g.ncls > 0 && layers >= 2;  // class-stream first sweep
   for (int i = 0; i < 2; ++i) {
     if (!g.p[i]) QVB_CUDA(cudaMalloc(&g.p[i], (n + 1) * sizeof(double)));
@@ -981,16 +950,23 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
     if (compact && !g.nm) QVB_CUDA(cudaMemsetAsync(g.y[i] + n, 0, sizeof(double), s));
     if (codes) QVB_CUDA(cudaMemsetAsync(g.kcode[i] + n, 0, sizeof(uint32_t), s));
   }
+  if (codes && !g.nm_code) {  // +128: k_products reads whole 4-code groups past a run's end
+    QVB_CUDA(cudaMalloc(&g.nm_code, (g.nm_cols + 128) * sizeof(uint32_t)));
+    QVB_CUDA(cudaMalloc(&g.marked, sizeof(uint32_t)));
+  }
+  for (auto& e : g.ev)
+    if (!e) QVB_CUDA(cudaEventCreate(&e));
+  PhaseTimer pt(g, s);
   const double base = 1.0 / static_cast<double>(n);  // metrics.cpp:143
   if (!f1) {  // P(n,1) (and, for a gathering first sweep, its operands)
-    k_init<<<grid_for(n + 1, 256), 256, 0, s>>>(n, g.inv, g.p[0], (compact && !g.nm && layers >= 2) ? g.y[0] : nullptr,
+    k_init<<<grid_for(n + 1, 256), 256, 0, s>>>(n, g.inv, g.p[0],
+                                               (compact && !g.nm && layers >= 2) ? g.y[0] : nullptr,
                                                (codes && layers >= 2) ? g.kcode[0] : nullptr);
     QVB_LAUNCH_CHECK();
+    ++g.launches;
   }
   const uint64_t long_blocks = (g.nlong + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const int nseg = static_cast<int>(g.seg_slice.size()) - 1;
-  for (auto& e : g.ev)
-    if (!e) QVB_CUDA(cudaEventCreate(&e));
   int gmode = 0;
   if (const char* m = std::getenv("QVB_GATHER_MODE")) gmode = std::atoi(m);
   // L2 lookahead in blocks for the segmented passes (QVB_PF_BLOCKS; 0 = off);
@@ -1003,20 +979,28 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
     const bool first = j == 2;
     double* yout = (compact && !g.nm && j < layers) ? g.y[nxt] : nullptr;
     uint32_t* kout = (codes && j < layers) ? g.kcode[nxt] : nullptr;
-    if (first && f1) {
+
+    if (first && f1) {  // ---- first sweep over the class stream
+      pt.begin(0);
+      uint32_t launched = 0;
       const size_t smem = (g.ncls + 2) * sizeof(double);
-      QVB_CUDA(cudaFuncSetAttribute(k_first_long, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kMaxCls + 2) * 8));
       if (g.nlong) {
+        QVB_CUDA(cudaFuncSetAttribute(k_first_long, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kMaxCls + 2) * 8));
         const unsigned lg = resident_grid(k_first_long, kWarpsPerBlock * 32, smem,
                                           (g.nlong + kWarpsPerBlock - 1) / kWarpsPerBlock);
         k_first_long<<<lg, kWarpsPerBlock * 32, smem, s>>>(g.nlong, base, g.ncls, g.cls_inv, g.lnode,
                                                            g.lptr, g.lcol, g.lcls, g.exc_R, g.inv,
                                                            g.p[nxt], yout, kout);
         QVB_LAUNCH_CHECK();
+        ++launched;
       }
-      const uint64_t nwin = (g.f1_S + kF1Slices - 1) / kF1Slices;  // units of 16 slices
-      if (nwin && n * 24 <= (64ull << 20)) {  // outputs L2-resident (half the L2): no write staging
+      const uint64_t nunit = (g.f1_S + kF1Slices - 1) / kF1Slices;  // units of 16 slices
+      const char* f1k = std::getenv("QVB_F1_KERNEL");
+      // outputs L2-resident (half the L2): the scattered per-node stores merge
+      // in L2, no write staging
+      const bool small = f1k ? std::string(f1k) == "small" : n * 24 <= (64ull << 20);
+      if (nunit && small) {
         QVB_CUDA(cudaFuncSetAttribute(k_first_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(kMaxCls + 2) * 8));
         const unsigned grid = resident_grid(k_first_small, kWarpsPerBlock * 32, smem,
@@ -1025,100 +1009,93 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
             g.f1_S, base, g.ncls, g.cls_inv, g.f1_perm, g.f1_sptr, g.f1_cls, g.f1_xslot, g.f1_xR,
             g.f1_nx, g.inv, g.p[nxt], yout, kout);
         QVB_LAUNCH_CHECK();
-      } else if (nwin) {
+        ++launched;
+      } else if (nunit) {
         const size_t dsm = kF1StageBytes + smem;
         QVB_CUDA(cudaFuncSetAttribute(k_first, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(kF1StageBytes + (kMaxCls + 2) * 8)));
-        const unsigned grid = resident_grid(k_first, kWarpsPerBlock * 32, dsm, nwin);
-        k_first<<<grid, kWarpsPerBlock * 32, dsm, s>>>(nwin, base, g.ncls, g.cls_inv, g.f1_perm,
+        const unsigned grid = resident_grid(k_first, kWarpsPerBlock * 32, dsm, nunit);
+        k_first<<<grid, kWarpsPerBlock * 32, dsm, s>>>(nunit, base, g.ncls, g.cls_inv, g.f1_perm,
                                                        g.f1_sptr, g.f1_cls, g.f1_urange, g.f1_xslot,
                                                        g.f1_xR, g.f1_nx, g.inv, g.p[nxt], yout, kout);
         QVB_LAUNCH_CHECK();
+        ++launched;
       }
+      pt.end(launched);
       continue;
     }
-    const double fbase = (first && !compact) ? base : 0.0;  // weighted first sweep: no gathers
-    if (g.nm) {  // node-major passes
+
+    if (codes) {  // ---- node-major compact graph: code gathers, then products
+      uint32_t launched = 0;
+      pt.begin(1);
+      QVB_CUDA(cudaMemsetAsync(g.marked, 0, sizeof(uint32_t), s));
+      if (g.nlong) {  // long rows: whole rows, one warp each
+        k_pass_long<<<static_cast<unsigned>((g.nlong * 32 + 255) / 256), 256, 0, s>>>(
+            g.nlong, g.lnode, g.lptr, g.lcol, g.exc_src, g.exc_R, g.p[cur], g.kcode[cur], g.inv,
+            g.p[nxt], kout);
+        QVB_LAUNCH_CHECK();
+        ++launched;
+      }
+      // one launch per source segment: the CTAs in flight gather from one
+      // L2-resident code segment
       for (int k = 0; k < nseg; ++k) {
+        const uint64_t e0 = g.nm_region[k], e1 = g.nm_region[k + 1];
+        if (e1 <= e0) continue;
+        const unsigned cg = resident_grid(k_codes, 256, 0, (e1 - e0 + 2047) / 2048);
+        k_codes<<<cg, 256, 0, s>>>(e0, e1, g.nm_col, g.kcode[cur], g.exc_src, g.exc_R, g.p[cur], g.inv,
+                                  g.nm_code, g.marked);
+        QVB_LAUNCH_CHECK();
+        ++launched;
+      }
+      pt.end(launched);
+      pt.begin(2);
+      k_products<<<static_cast<unsigned>((g.nm_S + kWarpsPerBlock - 1) / kWarpsPerBlock),
+                   kWarpsPerBlock * 32, 0, s>>>(nseg, g.nm_S, n, g.nm_lenf, g.nm_sbase, g.nm_code,
+                                                g.nm_col, g.exc_src, g.exc_R, g.p[cur], g.inv,
+                                                g.p[nxt], kout, g.marked);
+      QVB_LAUNCH_CHECK();
+      pt.end(1);
+      continue;
+    }
+
+    const double fbase = (first && !compact) ? base : 0.0;  // weighted first sweep: no gathers
+    pt.begin(3);
+    uint32_t launched = 0;
+    if (g.nm) {  // node-major weighted passes, carrying the running products
+      for (int k = 0; k < nseg; ++k) {
+        const uint64_t lb = k == 0 ? long_blocks : 0;
+        const uint64_t blocks = lb + (g.nm_S + kWarpsPerBlock - 1) / kWarpsPerBlock;
+        k_sweep_nm<true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
+            k, g.nm_S, lb, g.nlong, pf, g.nm_lenf, g.nm_sbase, g.nm_col, g.nm_R, g.state, g.lnode,
+            g.lptr, g.lcol, g.lR, nullptr, nullptr, g.p[cur], nullptr, nullptr, g.inv, g.p[nxt],
+            nullptr, nullptr, gmode, fbase);
+        QVB_LAUNCH_CHECK();
+        ++launched;
+      }
+    } else {
+      // sliced passes: pass k multiplies the factors of source segment k; the
+      // long rows ride along in the first pass's grid (their blocks first)
+      for (int k = 0; k < nseg; ++k) {
+        const uint64_t s0 = g.seg_slice[k], s1 = g.seg_slice[k + 1];
+        const uint64_t lb = k == 0 ? long_blocks : 0;
+        const uint64_t blocks = lb + (s1 - s0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
+        if (blocks == 0) continue;
         if (compact) {
-          if (k > 0) continue;  // one G + P pair covers every pass
-          if (g.nlong) {
-            k_pass_long<<<static_cast<unsigned>((g.nlong * 32 + 255) / 256), 256, 0, s>>>(
-                g.nlong, g.lnode, g.lptr, g.lcol, g.exc_src, g.exc_R, g.p[cur], g.kcode[cur], g.inv,
-                g.p[nxt], kout);
-            QVB_LAUNCH_CHECK();
-          }
-          if (!g.nm_code) QVB_CUDA(cudaMalloc(&g.nm_code, (g.nm_cols ? g.nm_cols : 1) * sizeof(uint32_t)));
-          int smode = 0;
-          if (const char* m = std::getenv("QVB_G_STORE")) smode = std::atoi(m);
-          size_t persist = 0;  // QVB_G_PERSIST_MB: pin each region's code segment in L2
-          if (const char* m = std::getenv("QVB_G_PERSIST_MB")) persist = (size_t)std::atoi(m) << 20;
-          if (persist) {
-            int maxp = 0;
-            QVB_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, g.device));
-            persist = std::min(persist, (size_t)maxp);
-            QVB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
-          }
-          const std::vector<uint64_t>& sb = g.nm_region;
-          for (int kk = 0; kk < nseg; ++kk) {
-            const uint64_t e0 = sb[kk], e1 = sb[kk + 1];
-            if (e1 <= e0) continue;
-            const unsigned cg = resident_grid(k_codes, 256, 0, (e1 - e0 + 2047) / 2048);
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(cg);
-            cfg.blockDim = dim3(256);
-            cfg.stream = s;
-            cudaLaunchAttribute attr[1];
-            if (persist) {
-              const uint64_t first = (uint64_t)kk * g.seg_size;
-              const uint64_t count = std::min<uint64_t>(g.seg_size, n - first);
-              attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-              attr[0].val.accessPolicyWindow.base_ptr = g.kcode[cur] + first;
-              attr[0].val.accessPolicyWindow.num_bytes = std::min<size_t>(count * sizeof(uint32_t), persist);
-              attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-              attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-              attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-              cfg.attrs = attr;
-              cfg.numAttrs = 1;
-            }
-            QVB_CUDA(cudaLaunchKernelEx(&cfg, k_codes, e0, e1, (const uint32_t*)g.nm_col,
-                                        (const uint32_t*)g.kcode[cur], g.nm_code, smode));
-          }
-          if (persist) QVB_CUDA(cudaCtxResetPersistingL2Cache());
-          k_products<<<static_cast<unsigned>((g.nm_S + kWarpsPerBlock - 1) / kWarpsPerBlock),
-                       kWarpsPerBlock * 32, 0, s>>>(nseg, g.nm_S, n, g.nm_lenf, g.nm_sbase, g.nm_code,
-                                                    g.nm_col, g.exc_src, g.exc_R, g.p[cur], g.inv,
-                                                    g.p[nxt], kout);
+          k_sweep<false><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
+              s0, s1, lb, g.nlong, pf, g.nslices, g.state, g.perm, g.sptr, g.scol, nullptr, g.lnode,
+              g.lptr, g.lcol, nullptr, g.exc_src, g.exc_R, g.p[cur], g.y[cur], g.inv, g.p[nxt], yout,
+              gmode, 0.0);
         } else {
-          const uint64_t lb = k == 0 ? long_blocks : 0;
-          const uint64_t blocks = lb + (g.nm_S + kWarpsPerBlock - 1) / kWarpsPerBlock;
-          k_sweep_nm<true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
-              k, g.nm_S, lb, g.nlong, pf, g.nm_lenf, g.nm_sbase, g.nm_col, g.nm_R, g.state, g.lnode,
-              g.lptr, g.lcol, g.lR, nullptr, nullptr, g.p[cur], nullptr, nullptr, g.inv,
-              g.p[nxt], nullptr, nullptr, gmode, fbase);
+          k_sweep<true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
+              s0, s1, lb, g.nlong, pf, g.nslices, g.state, g.perm, g.sptr, g.scol, g.sR, g.lnode,
+              g.lptr, g.lcol, g.lR, nullptr, nullptr, g.p[cur], nullptr, g.inv, g.p[nxt], nullptr,
+              gmode, fbase);
         }
         QVB_LAUNCH_CHECK();
+        ++launched;
       }
-      continue;
     }
-    // sliced passes: pass k multiplies the factors of source segment k; the
-    // long rows ride along in the first pass's grid (their blocks first)
-    for (int k = 0; k < nseg; ++k) {
-      const uint64_t s0 = g.seg_slice[k], s1 = g.seg_slice[k + 1];
-      const uint64_t lb = k == 0 ? long_blocks : 0;
-      const uint64_t blocks = lb + (s1 - s0 + kWarpsPerBlock - 1) / kWarpsPerBlock;
-      if (blocks == 0) continue;
-      if (compact) {
-        k_sweep<false><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
-            s0, s1, lb, g.nlong, pf, g.nslices, g.state, g.perm, g.sptr, g.scol, nullptr, g.lnode, g.lptr,
-            g.lcol, nullptr, g.exc_src, g.exc_R, g.p[cur], g.y[cur], g.inv, g.p[nxt], yout, gmode, 0.0);
-      } else {
-        k_sweep<true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
-            s0, s1, lb, g.nlong, pf, g.nslices, g.state, g.perm, g.sptr, g.scol, g.sR, g.lnode, g.lptr, g.lcol,
-            g.lR, nullptr, nullptr, g.p[cur], nullptr, g.inv, g.p[nxt], nullptr, gmode, fbase);
-      }
-      QVB_LAUNCH_CHECK();
-    }
+    pt.end(launched);
   }
   QVB_CUDA(cudaEventRecord(g.ev[1], s));
   return g.p[(layers - 1) & 1];

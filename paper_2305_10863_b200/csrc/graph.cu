@@ -48,6 +48,7 @@ qvb_graph::~qvb_graph() {
   cudaFree(nm_sbase);
   cudaFree(nm_col);
   cudaFree(nm_code);
+  cudaFree(marked);
   cudaFree(nm_R);
   cudaFree(cls_inv);
   cudaFree(f1_perm);
@@ -57,6 +58,10 @@ qvb_graph::~qvb_graph() {
   cudaFree(f1_xslot);
   cudaFree(f1_xR);
   cudaFree(lcls);
+  for (auto& pe : phase_ev) {
+    cudaEventDestroy(pe.a);
+    cudaEventDestroy(pe.b);
+  }
   for (int i = 0; i < 2; ++i) {
     cudaFree(p[i]);
     cudaFree(y[i]);
@@ -823,10 +828,12 @@ void build_nm(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const uin
   const uint32_t thr = std::min<uint32_t>(g.long_threshold, kNmLen);
   g.long_threshold = thr;
   // compact sweeps gather 4-byte codes: twice the sources per segment, and
-  // by default a 96 MiB code slice (measured best at C4: fewer passes beat
-  // the L2 hit rate lost above ~64 MiB, experiments/l2_capacity.cu)
+  // by default a 64 MiB code slice — the per-segment code gathers (k_codes)
+  // stay L2-resident up to about that size next to their column and code
+  // streams (C4: 48 MiB 7.2 ms, 64 MiB 7.5 ms, 96 MiB 11.6 ms), and fewer
+  // segments mean fewer runs per node for k_products (48: 5.0, 64: 4.1 ms)
   uint64_t seg = R ? g.seg_size : g.seg_size * 2;
-  if (!R && !std::getenv("QVB_SEG_MB") && !std::getenv("QVB_SEG_SOURCES")) seg = (96ull << 20) / 4;
+  if (!R && !std::getenv("QVB_SEG_MB") && !std::getenv("QVB_SEG_SOURCES")) seg = (64ull << 20) / 4;
   seg = std::min<uint64_t>(n, seg);
   g.seg_size = seg;
   const int nseg = static_cast<int>((n + seg - 1) / seg);
@@ -994,6 +1001,7 @@ void build_first(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const 
   }
   g.f1_urange = persist(urange);
   g.f1_S = S;
+  g.f1_slots = slots;
   g.f1_perm = persist(perm);
   g.f1_sptr = persist(sptr);
   g.f1_cls = persist(scls);
@@ -1337,6 +1345,22 @@ extern "C" int qvb_graph_last_sweep_ms(const qvb_graph* g, double* ms) {
   });
 }
 
+extern "C" int qvb_graph_phase_ms(const qvb_graph* g, double* ms, uint32_t* launches) {
+  return guarded([&] {
+    if (!g || !ms) fail(QVB_ERR_VALIDATION, "null argument");
+    for (int i = 0; i < 4; ++i) ms[i] = 0.0;
+    DeviceGuard dg(g->device);
+    for (size_t i = 0; i < g->phase_used; ++i) {
+      const auto& pe = g->phase_ev[i];
+      QVB_CUDA(cudaEventSynchronize(pe.b));
+      float f = 0;
+      QVB_CUDA(cudaEventElapsedTime(&f, pe.a, pe.b));
+      ms[pe.phase] += f;
+    }
+    if (launches) *launches = g->launches;
+  });
+}
+
 extern "C" int qvb_graph_info_get(const qvb_graph* g, qvb_graph_info* info) {
   return guarded([&] {
     if (!g || !info) fail(QVB_ERR_VALIDATION, "null argument");
@@ -1351,6 +1375,8 @@ extern "C" int qvb_graph_info_get(const qvb_graph* g, qvb_graph_info* info) {
     info->build_ms = g->build_ms;
     info->classes = g->ncls;
     info->segments = g->seg_slice.empty() ? 1u : static_cast<uint32_t>(g->seg_slice.size() - 1);
+    info->first_slots = g->f1_slots;
+    info->segment_columns = g->nm ? g->nm_cols : 0;
   });
 }
 

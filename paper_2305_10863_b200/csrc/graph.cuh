@@ -111,13 +111,15 @@ struct qvb_graph {
   uint64_t* nm_sbase = nullptr;
   uint32_t* nm_col = nullptr;
   uint32_t* nm_code = nullptr;
-  std::vector<uint64_t> nm_region;  // host: start of each pass's columns in nm_col (nseg + 1)  // compact: the gathered code of every nm_col entry (per sweep)
+  std::vector<uint64_t> nm_region;
+  uint32_t* marked = nullptr;  // device flag: a sweep's codes kept a marker (see k_codes)  // host: start of each pass's columns in nm_col (nseg + 1)  // compact: the gathered code of every nm_col entry (per sweep)
   double* nm_R = nullptr;
   uint32_t* kcode[2] = {nullptr, nullptr};
   // first sweep ("f1", see above): out-degree classes and their streams
   uint32_t ncls = 0;            // 0: no class stream (the first sweep gathers)
   double* cls_inv = nullptr;    // [ncls] 1/row_sum of each class
   uint64_t f1_S = 0;            // slices of the one-pass sliced layout
+  uint64_t f1_slots = 0;        // f1_sptr[f1_S]
   uint32_t* f1_perm = nullptr;  // node of each slot (kNoNode: padding)
   uint64_t* f1_sptr = nullptr;  // slice starts (elements)
   uint16_t* f1_cls = nullptr;   // class per slot, lane-major; ncls: pad, ncls+1: exception
@@ -129,6 +131,13 @@ struct qvb_graph {
   uint64_t bytes = 0;
   double build_ms = 0.0;
   cudaEvent_t ev[2] = {nullptr, nullptr};  // bracket the sweeps of the last run
+  // per-phase brackets of the last run: (phase, start, end); phase 0 = first
+  // sweep (class stream), 1 = code gather (k_codes), 2 = ordered products,
+  // 3 = any other sweep kernel
+  struct PhaseEv { int phase; cudaEvent_t a, b; };
+  std::vector<PhaseEv> phase_ev;
+  size_t phase_used = 0;
+  uint32_t launches = 0;  // kernels launched by the last run
   ~qvb_graph();
 };
 

@@ -102,6 +102,8 @@ class GraphInfo(C.Structure):
         ("build_ms", C.c_double),
         ("classes", C.c_uint32),
         ("segments", C.c_uint32),
+        ("first_slots", C.c_uint64),
+        ("segment_columns", C.c_uint64),
     ]
 
 
@@ -164,6 +166,7 @@ _SIGNATURES = {
     "qvb_synthetic_csr": (i32, [i32, u64, u64, u64, i32, i32, vp, vp, vp]),
     "qvb_in_adjacency": (i32, [i32, u64, u64, vp, vp, vp, vp, vp, vp]),
     "qvb_graph_last_sweep_ms": (i32, [vp, P(C.c_double)]),
+    "qvb_graph_phase_ms": (i32, [vp, P(C.c_double), P(C.c_uint32)]),
     "qvb_graph_destroy": (i32, [vp]),
     "qvb_access_prob": (i32, [vp, u32, vp, i32, vp]),
     "qvb_compute_access_prob_ie": (i32, [i32, u64, u64, vp, vp, vp, u32, vp, vp]),
@@ -313,6 +316,16 @@ class DeviceGraph:
         ms = C.c_double(0)
         _check(_lib().qvb_graph_last_sweep_ms(self._h, C.byref(ms)))
         return ms.value
+
+    def phase_ms(self):
+        """Device ms of the last access_prob call by phase: first sweep (class
+        stream), code gathers, ordered products, other sweep kernels; and the
+        number of kernels it launched."""
+        ms = (C.c_double * 4)()
+        n = C.c_uint32()
+        _check(_lib().qvb_graph_phase_ms(self._h, ms, C.byref(n)))
+        return {"first": ms[0], "gather": ms[1], "products": ms[2], "other": ms[3],
+                "launches": n.value}
 
     def close(self):
         if self._h:
