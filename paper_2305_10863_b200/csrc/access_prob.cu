@@ -49,7 +49,12 @@ __device__ __forceinline__ uint32_t y_code(double y) {
 // (1/2, 1], so it is exact, and its bit pattern is 1.0's minus J — one
 // integer subtraction instead of a conversion and an FMA.
 __device__ __forceinline__ double code_to_factor(uint32_t J) {
-  return __longlong_as_double(0x3FF0000000000000ll - static_cast<long long>(J));
+  double f;  // {lo, hi} = {-J, 0x3FF00000 - borrow}
+  asm("{\n .reg .u32 lo, hi;\n sub.cc.u32 lo, 0, %1;\n subc.u32 hi, 1072693248, 0;\n"
+      " mov.b64 %0, {lo, hi};\n}"
+      : "=d"(f)
+      : "r"(J));
+  return f;
 }
 
 __global__ void k_init(uint64_t n, const double* __restrict__ inv, double* __restrict__ p,
@@ -845,7 +850,7 @@ __device__ __noinline__ double products_markers(int K, uint64_t S, uint64_t sl, 
   return miss;
 }
 
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
     k_products(int K, uint64_t S, uint64_t n, const uint8_t* __restrict__ lenf,
                const uint64_t* __restrict__ sbase, const uint32_t* __restrict__ ncode,
                const uint32_t* __restrict__ ncol, const uint32_t* __restrict__ exc_src,
@@ -868,9 +873,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   const uint8_t* __restrict__ lp = lenf + v;
   const uint64_t* __restrict__ sp = sbase + sl;
   const uint64_t lstep = S * 32;
-  for (int k = 0; k < K; ++k, lp += lstep, sp += S) {
-    const uint32_t lf = *lp;
-    const uint64_t sb = *sp;
+  uint32_t lf_next = K > 0 ? *lp : 0u;  // software-pipelined: pass k+1's len and base
+  uint64_t sb_next = K > 0 ? *sp : 0ull;  // are in flight during pass k
+  for (int k = 0; k < K; ++k) {
+    const uint32_t lf = lf_next;
+    const uint64_t sb = sb_next;
+    lp += lstep;
+    sp += S;
+    if (k + 1 < K) {
+      lf_next = *lp;
+      sb_next = *sp;
+    }
     any |= lf;
     const uint32_t len = lf & kNmLen;
     const uint32_t maxlen = __reduce_max_sync(kFull, len);
