@@ -458,52 +458,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   }
 }
 
-// Regular rows. The f1 slices come in windows of 8 (256 nodes, sorted by
-// in-degree into the slots, so a window's first slice is its longest); a CTA
-// takes a unit of two windows at a time (16 slices, 512 consecutive regular
-// nodes) and warp w runs slices w and 15 - w, which balances the warps.
-// Lane = node, lane-major classes.
-//
-// The kernel is a pure stream (2 bytes per slot, no gathers), so it is fed by
-// a TMA pipeline: thread 0 bulk-copies (cp.async.bulk, mbarrier complete_tx)
-// each unit's perm words, slice pointers, node range, class stream and
-// 1/row_sum span into a kF1Stages-deep shared-memory ring ahead of the
-// compute, so the compute has no global load on its critical path. The
-// unit's results are staged in shared memory by node and written back
-// coalesced (P, and y / code) instead of 8-byte stores scattered across it.
-constexpr int kF1Slices = kF1Unit;
-constexpr int kStage = 1024;        // node span a unit may stage (long rows interleave)
-#ifndef QVB_F1_STAGES
-#define QVB_F1_STAGES 2
-#endif
-constexpr int kF1Stages = QVB_F1_STAGES;
-constexpr uint32_t kF1Cls = 16384;  // classes a stage holds; larger units stream from global
-constexpr uint32_t kF1Inv = 514;    // 1/row_sum span a stage holds (512 nodes + alignment)
-
-struct alignas(128) F1Stage {
-  uint16_t cls[kF1Cls];
-  uint32_t perm[kF1Slices * 32];
-  uint64_t sptr[kF1Slices + 2];
-  uint64_t urange[2];
-  double inv[kF1Inv];
-};
-constexpr size_t kF1StageBytes = sizeof(F1Stage) * kF1Stages;
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra W_%=;\n}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-
 // One slice's ordered product over its class stream (staged in shared memory
 // or read from global), exception classes contributing the NaN sentinel.
 template <bool kStaged>
@@ -550,127 +504,15 @@ __device__ __noinline__ double slice_product_exc(uint32_t len, const uint16_t* _
   return miss;
 }
 
+// Regular rows: persistent warps, one slice of 32 nodes at a time, lane =
+// node, lane-major classes (one coalesced 64-byte line per step). For graphs
+// whose per-node outputs exceed half the L2, the slices are built without
+// in-degree sorting across slices (graph.cu build_first, window 32), so a
+// warp's stores of P / y / code cover its own 32 consecutive nodes and stay
+// whole sectors; small graphs sort windows of 256 (less padding) and their
+// scattered stores merge in L2.
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    k_first(uint64_t nunit, double base, uint32_t ncls, const double* __restrict__ cls_inv,
-            const uint32_t* __restrict__ perm, const uint64_t* __restrict__ sptr,
-            const uint16_t* __restrict__ cls, const uint64_t* __restrict__ urange,
-            const uint64_t* __restrict__ xslot, const double* __restrict__ xR, uint64_t nx,
-            const double* __restrict__ inv, double* __restrict__ out, double* __restrict__ yout,
-            uint32_t* __restrict__ kout) {
-  extern __shared__ __align__(128) unsigned char dsm[];
-  F1Stage* stg = reinterpret_cast<F1Stage*>(dsm);
-  double* fac = reinterpret_cast<double*>(dsm + kF1StageBytes);
-  __shared__ double sP[kStage];
-  __shared__ uint32_t sMask[kStage / 32];
-  __shared__ __align__(8) uint64_t full[kF1Stages];
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kF1Stages; ++i)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
-          static_cast<uint32_t>(__cvta_generic_to_shared(&full[i]))));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  load_factors(fac, ncls, base, cls_inv);  // ends with __syncthreads
-  const uint32_t tab = static_cast<uint32_t>(__cvta_generic_to_shared(fac));
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint64_t pol = policy_evict_first();
-  const uint64_t mine = blockIdx.x < nunit ? (nunit - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const bool want_inv = yout || kout;
-
-  // producer state (thread 0): class range and node range of the next unit
-  uint64_t c0n = 0, c1n = 0, urn = 0;
-  auto unit = [&](uint64_t i) { return blockIdx.x + i * gridDim.x; };
-  auto fetch = [&](uint64_t i) {
-    const uint64_t w = unit(i);
-    c0n = sptr[w * kF1Slices];
-    c1n = sptr[w * kF1Slices + kF1Slices];
-    urn = urange[w];
-  };
-  auto issue = [&](uint64_t i) {  // unit i of this block into stage i % kF1Stages
-    const uint64_t w = unit(i);
-    F1Stage& st = stg[i % kF1Stages];
-    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&full[i % kF1Stages]));
-    const uint64_t c0 = c0n, c1 = c1n, ur = urn;
-    if (i + 1 < mine) fetch(i + 1);  // in flight while this unit lands
-    const uint32_t lo = static_cast<uint32_t>(ur), hi = static_cast<uint32_t>(ur >> 32);
-    const uint32_t lo2 = lo & ~1u;
-    const uint32_t ninv = (hi - lo2 + 2) & ~1u;  // even: 16-byte multiples
-    const uint32_t b_cls = c1 - c0 <= kF1Cls ? static_cast<uint32_t>((c1 - c0) * sizeof(uint16_t)) : 0u;
-    const uint32_t b_perm = kF1Slices * 32 * sizeof(uint32_t);
-    const uint32_t b_sptr = (kF1Slices + 2) * sizeof(uint64_t);
-    const uint32_t b_ur = 2 * sizeof(uint64_t);
-    const uint32_t b_inv = (want_inv && ur && ninv <= kF1Inv) ? ninv * 8u : 0u;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                 "r"(b_perm + b_sptr + b_ur + b_cls + b_inv)
-                 : "memory");
-    bulk_g2s(st.perm, perm + w * kF1Slices * 32, b_perm, bar);
-    bulk_g2s(st.sptr, sptr + w * kF1Slices, b_sptr, bar);
-    bulk_g2s(st.urange, urange + (w & ~1ull), b_ur, bar);
-    if (b_cls) bulk_g2s(st.cls, cls + c0, b_cls, bar);
-    if (b_inv) bulk_g2s(st.inv, inv + lo2, b_inv, bar);
-  };
-  if (threadIdx.x == 0 && mine) {
-    fetch(0);
-    for (uint64_t i = 0; i < mine && i < kF1Stages - 1; ++i) issue(i);
-  }
-  for (uint64_t i = 0; i < mine; ++i) {
-    // stage (i + kF1Stages - 1) % kF1Stages was consumed in iteration i - 1,
-    // which ended with __syncthreads
-    if (threadIdx.x == 0 && i + kF1Stages - 1 < mine) issue(i + kF1Stages - 1);
-    if (threadIdx.x < kStage / 32) sMask[threadIdx.x] = 0;
-    mbar_wait(static_cast<uint32_t>(__cvta_generic_to_shared(&full[i % kF1Stages])),
-              static_cast<uint32_t>((i / kF1Stages) & 1));
-    __syncthreads();  // sMask reset
-    const F1Stage& st = stg[i % kF1Stages];
-    const uint64_t ur = st.urange[unit(i) & 1];
-    const uint32_t lo = static_cast<uint32_t>(ur), hi = static_cast<uint32_t>(ur >> 32);
-    const uint32_t lo2 = lo & ~1u;
-    const bool inv_staged = ur && ((hi - lo2 + 2) & ~1u) <= kF1Inv;
-    const uint64_t w0 = st.sptr[0];
-    const bool staged = st.sptr[kF1Slices] - w0 <= kF1Cls;
-#pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      const int sl = h ? kF1Slices - 1 - wib : wib;  // a balanced pair of slices
-      const uint32_t v = st.perm[sl * 32 + lane] & kNodeMask;
-      const uint64_t b0 = st.sptr[sl];
-      const uint32_t len = static_cast<uint32_t>((st.sptr[sl + 1] - b0) >> 5);
-      double miss = staged ? slice_product<true>(len, st.cls + (b0 - w0) + lane, tab, ncls, pol)
-                           : slice_product<false>(len, cls + b0 + lane, tab, ncls, pol);
-      if (miss != miss)  // an exception edge in the slice
-        miss = slice_product_exc(len, cls + b0 + lane, b0 + lane, tab, ncls, xslot, xR, nx, base);
-      if (v != kNoNode) {
-        // metrics.cpp:169 with prev[v] = P(v,1) = base
-        const double P = __dadd_rn(base, __dmul_rn(__dsub_rn(1.0, base), __dsub_rn(1.0, miss)));
-        const uint32_t d = v - lo;
-        if (d < kStage) {
-          sP[d] = P;
-          atomicOr(&sMask[d >> 5], 1u << (d & 31));
-        } else {
-          finish_first(v, miss, base, inv, out, yout, kout, pol);
-        }
-      }
-    }
-    __syncthreads();
-    const uint32_t span = ur ? (hi - lo + 1 < kStage ? hi - lo + 1 : kStage) : 0u;
-    for (uint32_t d = threadIdx.x; d < span; d += blockDim.x) {
-      if (!(sMask[d >> 5] >> (d & 31) & 1)) continue;
-      const uint32_t vv = lo + d;
-      const double P = sP[d];
-      st_stream(out + vv, P, pol);
-      if (want_inv) {
-        const double y = __dmul_rn(P, inv_staged ? st.inv[vv - lo2] : inv[vv]);
-        if (yout) st_stream(yout + vv, y, pol);
-        if (kout) st_stream(kout + vv, y_code(y), pol);
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// Small graphs (P, y and codes L2-resident): one warp per slice, persistent
-// warps, no staging; the scattered per-node stores merge in L2.
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    k_first_small(uint64_t S, double base, uint32_t ncls, const double* __restrict__ cls_inv,
+    k_first(uint64_t S, double base, uint32_t ncls, const double* __restrict__ cls_inv,
                   const uint32_t* __restrict__ perm, const uint64_t* __restrict__ sptr,
                   const uint16_t* __restrict__ cls, const uint64_t* __restrict__ xslot,
                   const double* __restrict__ xR, uint64_t nx, const double* __restrict__ inv,
@@ -1008,29 +850,14 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
         QVB_LAUNCH_CHECK();
         ++launched;
       }
-      const uint64_t nunit = (g.f1_S + kF1Slices - 1) / kF1Slices;  // units of 16 slices
-      const char* f1k = std::getenv("QVB_F1_KERNEL");
-      // outputs L2-resident (half the L2): the scattered per-node stores merge
-      // in L2, no write staging
-      const bool small = f1k ? std::string(f1k) == "small" : n * 24 <= (64ull << 20);
-      if (nunit && small) {
-        QVB_CUDA(cudaFuncSetAttribute(k_first_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kMaxCls + 2) * 8));
-        const unsigned grid = resident_grid(k_first_small, kWarpsPerBlock * 32, smem,
-                                            (g.f1_S + kWarpsPerBlock - 1) / kWarpsPerBlock);
-        k_first_small<<<grid, kWarpsPerBlock * 32, smem, s>>>(
-            g.f1_S, base, g.ncls, g.cls_inv, g.f1_perm, g.f1_sptr, g.f1_cls, g.f1_xslot, g.f1_xR,
-            g.f1_nx, g.inv, g.p[nxt], yout, kout);
-        QVB_LAUNCH_CHECK();
-        ++launched;
-      } else if (nunit) {
-        const size_t dsm = kF1StageBytes + smem;
+      if (g.f1_S) {
         QVB_CUDA(cudaFuncSetAttribute(k_first, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kF1StageBytes + (kMaxCls + 2) * 8)));
-        const unsigned grid = resident_grid(k_first, kWarpsPerBlock * 32, dsm, nunit);
-        k_first<<<grid, kWarpsPerBlock * 32, dsm, s>>>(nunit, base, g.ncls, g.cls_inv, g.f1_perm,
-                                                       g.f1_sptr, g.f1_cls, g.f1_urange, g.f1_xslot,
-                                                       g.f1_xR, g.f1_nx, g.inv, g.p[nxt], yout, kout);
+                                      static_cast<int>(kMaxCls + 2) * 8));
+        const unsigned grid = resident_grid(k_first, kWarpsPerBlock * 32, smem,
+                                            (g.f1_S + kWarpsPerBlock - 1) / kWarpsPerBlock);
+        k_first<<<grid, kWarpsPerBlock * 32, smem, s>>>(g.f1_S, base, g.ncls, g.cls_inv, g.f1_perm,
+                                                        g.f1_sptr, g.f1_cls, g.f1_xslot, g.f1_xR,
+                                                        g.f1_nx, g.inv, g.p[nxt], yout, kout);
         QVB_LAUNCH_CHECK();
         ++launched;
       }

@@ -54,7 +54,6 @@ qvb_graph::~qvb_graph() {
   cudaFree(f1_perm);
   cudaFree(f1_sptr);
   cudaFree(f1_cls);
-  cudaFree(f1_urange);
   cudaFree(f1_xslot);
   cudaFree(f1_xR);
   cudaFree(lcls);
@@ -305,17 +304,18 @@ __global__ void k_pair_emit(const uint64_t* __restrict__ uptr, const uint32_t* _
 // One CTA per group of up to 256 pairs of one pass: order them by degree
 // (descending, node id ascending) into the group's 256 slots, so each slice
 // of 32 holds similar row lengths and pads little.
-__global__ void __launch_bounds__(kWindow)
+template <uint32_t W = kWindow>
+__global__ void __launch_bounds__(W)
     k_group_sort(const uint32_t* __restrict__ sorted_idx, const uint64_t* __restrict__ seg_pair_begin,
                  const uint64_t* __restrict__ seg_group_begin, int nseg,
                  const uint32_t* __restrict__ pv, const uint32_t* __restrict__ pdeg,
                  uint32_t* __restrict__ slot_pair) {
-  __shared__ uint32_t sdeg[kWindow];
-  __shared__ uint32_t snode[kWindow];
+  __shared__ uint32_t sdeg[W];
+  __shared__ uint32_t snode[W];
   const uint64_t grp = blockIdx.x;
   int k = 0;
   while (k + 1 < nseg && seg_group_begin[k + 1] <= grp) ++k;
-  const uint64_t q0 = seg_pair_begin[k] + (grp - seg_group_begin[k]) * kWindow;
+  const uint64_t q0 = seg_pair_begin[k] + (grp - seg_group_begin[k]) * W;
   const uint64_t q1 = seg_pair_begin[k + 1];
   const uint32_t t = threadIdx.x;
   const bool real = q0 + t < q1;
@@ -328,16 +328,16 @@ __global__ void __launch_bounds__(kWindow)
   sdeg[t] = real ? d : 0u;
   snode[t] = real ? node : 0xFFFFFFFFu;
   __syncthreads();
-  const uint32_t cnt = static_cast<uint32_t>(q1 - q0 < kWindow ? q1 - q0 : kWindow);
+  const uint32_t cnt = static_cast<uint32_t>(q1 - q0 < W ? q1 - q0 : W);
   if (real) {
     uint32_t rank = 0;
     for (uint32_t j = 0; j < cnt; ++j) {
       const uint32_t dj = sdeg[j], nj = snode[j];
       rank += (dj > d) || (dj == d && nj < node);
     }
-    slot_pair[grp * kWindow + rank] = idx;
+    slot_pair[grp * W + rank] = idx;
   } else {
-    slot_pair[grp * kWindow + t] = 0xFFFFFFFFu;
+    slot_pair[grp * W + t] = 0xFFFFFFFFu;
   }
 }
 
@@ -625,36 +625,6 @@ __global__ void k_fill_cls(const uint32_t* __restrict__ slot_pair, const uint32_
   }
 }
 
-__global__ void k_fill_u64(uint64_t* __restrict__ p, uint64_t n, uint64_t v) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    p[i] = v;
-}
-__global__ void k_fill_u32(uint32_t* __restrict__ p, uint64_t n, uint32_t v) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    p[i] = v;
-}
-
-// Node range of every unit of kF1Unit slices (padding slots skipped).
-__global__ void k_unit_range(const uint32_t* __restrict__ perm, uint64_t nunit,
-                             uint64_t* __restrict__ urange) {
-  const uint64_t u = blockIdx.x * (uint64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
-  const uint32_t lane = threadIdx.x & 31;
-  if (u >= nunit) return;
-  uint32_t lo = 0xFFFFFFFFu, hi = 0;
-  for (uint32_t i = lane; i < kF1Unit * 32; i += 32) {
-    const uint32_t v = perm[u * kF1Unit * 32 + i] & kNodeMask;
-    if (v != kNoNode) {
-      lo = min(lo, v);
-      hi = max(hi, v);
-    }
-  }
-  lo = __reduce_min_sync(0xffffffffu, lo);
-  hi = __reduce_max_sync(0xffffffffu, hi);
-  if (lane == 0) urange[u] = lo > hi ? 0ull : (uint64_t)lo | ((uint64_t)hi << 32);
-}
-
 __global__ void k_x_values(const uint32_t* __restrict__ sidx, const double* __restrict__ exc_R,
                            uint64_t nx, double* __restrict__ xR) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nx;
@@ -927,8 +897,16 @@ void build_first(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const 
   pk.release();
   k_iota<<<grid_for(H, kBlock), kBlock, 0, s>>>(iota.p, H);
   QVB_LAUNCH_CHECK();
-  const uint64_t groups = (H + kWindow - 1) / kWindow;
-  const uint64_t S = groups * (kWindow / 32);
+  // Nodes are sorted by in-degree into slices inside windows of W nodes:
+  // wider windows pad less, but scatter a warp's per-node stores across the
+  // window. Those merge in L2 while the outputs (24 B per node) fit half of
+  // it; beyond that W = 32 keeps every warp's stores whole sectors (C4: the
+  // first sweep 2.7 ms at W = 256 with 2x the DRAM reads, 1.8 ms at W = 32).
+  uint32_t W = n * 24 <= (64ull << 20) ? 256 : 32;
+  if (const char* m = std::getenv("QVB_F1_WINDOW")) W = static_cast<uint32_t>(std::atoi(m));
+  if (W != 32 && W != 64 && W != 128) W = 256;
+  const uint64_t groups = (H + W - 1) / W;
+  const uint64_t S = groups * (W / 32);
   DevBuf<uint64_t> spb(2, s), sgb(2, s);
   {
     const uint64_t hb[2] = {0, H}, gb[2] = {0, groups};
@@ -938,27 +916,29 @@ void build_first(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const 
   }
   DevBuf<uint32_t> slot_pair(S * 32 ? S * 32 : 1, s);
   if (groups)
-    k_group_sort<<<static_cast<unsigned>(groups), kWindow, 0, s>>>(iota.p, spb.p, sgb.p, 1, pv.p,
-                                                                   pdeg.p, slot_pair.p);
+    switch (W) {
+      case 32:
+        k_group_sort<32><<<static_cast<unsigned>(groups), 32, 0, s>>>(iota.p, spb.p, sgb.p, 1, pv.p, pdeg.p, slot_pair.p);
+        break;
+      case 64:
+        k_group_sort<64><<<static_cast<unsigned>(groups), 64, 0, s>>>(iota.p, spb.p, sgb.p, 1, pv.p, pdeg.p, slot_pair.p);
+        break;
+      case 128:
+        k_group_sort<128><<<static_cast<unsigned>(groups), 128, 0, s>>>(iota.p, spb.p, sgb.p, 1, pv.p, pdeg.p, slot_pair.p);
+        break;
+      default:
+        k_group_sort<256><<<static_cast<unsigned>(groups), 256, 0, s>>>(iota.p, spb.p, sgb.p, 1, pv.p, pdeg.p, slot_pair.p);
+    }
   QVB_LAUNCH_CHECK();
   iota.release();
   DevBuf<uint32_t> len32(S + 1, s);
-  // f1 is read in units of 16 slices with 16-byte bulk copies: sptr and perm
-  // are padded to a whole unit (+2 pointers) with empty slices
-  const uint64_t Sp = (S + kF1Unit - 1) / kF1Unit * kF1Unit;
-  DevBuf<uint64_t> sptr(Sp + 3, s);
+  DevBuf<uint64_t> sptr(S + 1, s);
   k_slot_lens<<<grid_for(S + 1, kBlock), kBlock, 0, s>>>(slot_pair.p, pdeg.p, S, len32.p);
   QVB_LAUNCH_CHECK();
   exclusive_sum_u32_u64(len32.p, sptr.p, S + 1, s);
   len32.release();
   const uint64_t slots = read_scalar(sptr.p + S, s);
-  k_fill_u64<<<grid_for(Sp + 2 - S, kBlock), kBlock, 0, s>>>(sptr.p + S + 1, Sp + 2 - S, slots);
-  QVB_LAUNCH_CHECK();
-  DevBuf<uint32_t> perm(Sp * 32 ? Sp * 32 : 1, s);
-  if (Sp > S) {
-    k_fill_u32<<<grid_for((Sp - S) * 32, kBlock), kBlock, 0, s>>>(perm.p + S * 32, (Sp - S) * 32, kNoNode);
-    QVB_LAUNCH_CHECK();
-  }
+  DevBuf<uint32_t> perm(S * 32 ? S * 32 : 1, s);
   DevBuf<uint16_t> scls(slots ? slots : 1, s);
   const uint64_t xcap = g.nexc ? g.nexc : 1;
   DevBuf<unsigned long long> xcount(1, s);
@@ -992,14 +972,6 @@ void build_first(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const 
     g.lcls = persist(lc);
     g.bytes += m * 2;
   }
-  const uint64_t nunit = Sp / kF1Unit;
-  DevBuf<uint64_t> urange(nunit + 2, s);  // read in aligned pairs by bulk copies
-  QVB_CUDA(cudaMemsetAsync(urange.p, 0, (nunit + 2) * sizeof(uint64_t), s));
-  if (nunit) {
-    k_unit_range<<<static_cast<unsigned>((nunit + 7) / 8), 256, 0, s>>>(perm.p, nunit, urange.p);
-    QVB_LAUNCH_CHECK();
-  }
-  g.f1_urange = persist(urange);
   g.f1_S = S;
   g.f1_slots = slots;
   g.f1_perm = persist(perm);

@@ -54,16 +54,15 @@
 // (bitwise), and the first sweep streams a 2-byte class per in-edge instead
 // of gathering: factor = table[class], the table holding
 // 1 - (1/N) * inv(class) in shared memory. It is a one-pass sliced layout
-// (windows of 256 nodes sorted by in-degree, slices of 32, lane-major),
-// built over every regular row whatever the segmentation of later sweeps:
+// (windows of 256 nodes — 32 for large graphs — sorted by in-degree, slices
+// of 32, lane-major), built over every regular row whatever the segmentation
+// of later sweeps:
 //   f1_perm u32[S*32], f1_sptr u64[S+1], f1_cls u16[...]
 // Class ncls is padding (factor exactly 1.0). Exception edges
 // (R != 1/row_sum) carry class ncls+1, whose table entry is a NaN sentinel:
 // a slice whose product comes out NaN is recomputed with their R, looked up
 // by slot in the ascending list (f1_xslot, f1_xR). Long rows use lcls next
-// to lcol. The slices come in units of 16 (512 nodes) whose node ranges are
-// f1_urange (lo | hi << 32). Graphs with more than kMaxCls classes keep the
-// gathering sweep.
+// to lcol. Graphs with more than kMaxCls classes keep the gathering sweep.
 //
 // kcode: round(1 - y) in fp64 depends on y only through J = rint(y * 2^53)
 // while y <= 1/2: the doubles in [1/2, 1] are the multiples of 2^-53, so
@@ -123,7 +122,6 @@ struct qvb_graph {
   uint32_t* f1_perm = nullptr;  // node of each slot (kNoNode: padding)
   uint64_t* f1_sptr = nullptr;  // slice starts (elements)
   uint16_t* f1_cls = nullptr;   // class per slot, lane-major; ncls: pad, ncls+1: exception
-  uint64_t* f1_urange = nullptr;  // node range of each unit of 16 slices
   uint64_t f1_nx = 0;           // exception slots, ascending, with their R
   uint64_t* f1_xslot = nullptr;
   double* f1_xR = nullptr;
@@ -156,7 +154,6 @@ constexpr uint32_t kBigCode = 0xFFFFFFFFu;  // kcode: gather y instead
 constexpr uint8_t kNmFirst = 0x40, kNmLast = 0x80, kNmLen = 0x3F;
 constexpr uint64_t kMaxEdges = 0xFFFFFFFFull;
 constexpr uint32_t kMaxCls = 12288;   // shared-memory table of ncls+2 doubles
-constexpr uint32_t kF1Unit = 16;      // f1 slices per unit (two windows)
 
 // Builds the in-CSR from a device out-CSR. d_w == nullptr means unit weights.
 // d_src (nullable): source of every out-CSR edge if already known.
