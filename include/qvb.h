@@ -150,6 +150,13 @@ int qvb_graph_last_sweep_ms(const qvb_graph* g, double* ms);
  * sweep over the class stream, ms[1] code gathers, ms[2] ordered products,
  * ms[3] other sweep kernels; *launches (nullable) = kernels launched. */
 int qvb_graph_phase_ms(const qvb_graph* g, double* ms, uint32_t* launches);
+/* Diagnostics / size-independent parity: the coalesced in-row of each listed
+ * node as the sweeps multiply it — sources ascending, R = w_sum / row_sum(s)
+ * (metrics.cpp:157-166). Fills row_ptr[count+1]; src and R receive
+ * row_ptr[count] entries unless NULL (call once with NULL to size them).
+ * Node-major (segmented) graphs only. */
+int qvb_graph_in_rows(const qvb_graph* g, const uint64_t* nodes, uint64_t count,
+                      uint64_t* row_ptr, uint32_t* src, double* R);
 int qvb_graph_destroy(qvb_graph* g);
 
 /* ---- K1: access probability P(n,j) (metrics.cpp:134-173) ---------------- */

@@ -822,6 +822,7 @@ void build_nm(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const uin
   cnt.release();
   const uint64_t total = read_scalar(sbase.p + S * nseg, s);
   g.nm_region.resize(nseg + 1);
+  g.nm_region_count = nseg;
   for (int k = 0; k <= nseg; ++k) g.nm_region[k] = read_scalar(sbase.p + S * k, s);
   DevBuf<uint32_t> ncol(total + 4, s);  // +4: 16-byte bulk-copy windows
   DevBuf<double> nR;
@@ -1304,6 +1305,113 @@ extern "C" int qvb_synthetic_csr(int device, uint64_t n, uint64_t e, uint64_t se
     QVB_CUDA(cudaStreamSynchronize(s));
   });
 }
+
+namespace qvb {
+namespace {
+
+// qvb_graph_in_rows: one thread per listed node walks its runs of the
+// node-major layout (pass by pass = ascending source) or its long row; with
+// src == nullptr it only counts.
+struct InRowsView {  // the device arrays k_in_rows reads
+  uint32_t layout;
+  uint64_t nlong, nm_S, nm_region_count;
+  const uint32_t *lnode, *lcol, *exc_src, *nm_col;
+  const uint64_t *lptr, *nm_sbase;
+  const double *lR, *exc_R, *inv, *nm_R;
+  const uint8_t* nm_lenf;
+};
+
+__global__ void k_in_rows(const InRowsView g, const uint64_t* __restrict__ nodes, uint64_t count,
+                          const uint64_t* __restrict__ row_ptr, uint32_t* __restrict__ src,
+                          double* __restrict__ R, uint64_t* __restrict__ lens) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint64_t v = nodes[i];
+  uint64_t at = src ? row_ptr[i] : 0, m = 0;
+  auto emit = [&](uint32_t c, double r_weighted, bool weighted) {
+    if (src) {
+      uint32_t s = c;
+      double r;
+      if (weighted) {
+        r = r_weighted;
+      } else if (c & kExcFlag) {
+        s = g.exc_src[c & ~kExcFlag];
+        r = g.exc_R[c & ~kExcFlag];
+      } else {
+        r = g.inv[c];
+      }
+      src[at] = s;
+      R[at] = r;
+      ++at;
+    }
+    ++m;
+  };
+  const bool weighted = g.layout == 1;
+  // long row?
+  uint64_t lo = 0, hi = g.nlong;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (g.lnode[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < g.nlong && g.lnode[lo] == v) {
+    for (uint64_t e = g.lptr[lo]; e < g.lptr[lo + 1]; ++e) emit(g.lcol[e], weighted ? g.lR[e] : 0.0, weighted);
+  } else {
+    const uint64_t S = g.nm_S, sl = v / 32, lane = v % 32;
+    const int nseg = static_cast<int>(g.nm_region_count);
+    for (int k = 0; k < nseg; ++k) {
+      const uint8_t* lf = g.nm_lenf + (uint64_t)k * S * 32 + sl * 32;
+      uint64_t off = 0;
+      for (uint64_t l = 0; l < lane; ++l) off += lf[l] & kNmLen;
+      const uint64_t len = lf[lane] & kNmLen;
+      const uint64_t b = g.nm_sbase[(uint64_t)k * S + sl] + off;
+      for (uint64_t t = 0; t < len; ++t) emit(g.nm_col[b + t], weighted ? g.nm_R[b + t] : 0.0, weighted);
+    }
+  }
+  if (!src) lens[i] = m;
+}
+
+}  // namespace
+}  // namespace qvb
+
+extern "C" int qvb_graph_in_rows(const qvb_graph* g, const uint64_t* nodes, uint64_t count,
+                                 uint64_t* row_ptr, uint32_t* src, double* R) {
+  return guarded([&] {
+    if (!g || (count && (!nodes || !row_ptr))) fail(QVB_ERR_VALIDATION, "null argument");
+    if (!g->nm) fail(QVB_ERR_UNSUPPORTED, "in_rows needs the node-major (segmented) layout");
+    DeviceGuard dg(g->device);
+    cudaStream_t s = nullptr;
+    for (uint64_t i = 0; i < count; ++i)
+      if (nodes[i] >= g->n) fail(QVB_ERR_VALIDATION, "node " + std::to_string(nodes[i]) + " out of range");
+    DevBuf<uint64_t> dn(count ? count : 1, s), dl(count ? count : 1, s), dp(count + 1, s);
+    QVB_CUDA(cudaMemcpyAsync(dn.p, nodes, count * 8, cudaMemcpyHostToDevice, s));
+    const InRowsView gv{g->layout, g->nlong, g->nm_S, g->nm_region_count, g->lnode, g->lcol,
+                        g->exc_src, g->nm_col, g->lptr, g->nm_sbase, g->lR, g->exc_R, g->inv,
+                        g->nm_R, g->nm_lenf};
+    const unsigned blocks = static_cast<unsigned>((count + 127) / 128);
+    std::vector<uint64_t> lens(count);
+    if (count) {
+      k_in_rows<<<blocks, 128, 0, s>>>(gv, dn.p, count, nullptr, nullptr, nullptr, dl.p);
+      QVB_LAUNCH_CHECK();
+      QVB_CUDA(cudaMemcpyAsync(lens.data(), dl.p, count * 8, cudaMemcpyDeviceToHost, s));
+      QVB_CUDA(cudaStreamSynchronize(s));
+    }
+    row_ptr[0] = 0;
+    for (uint64_t i = 0; i < count; ++i) row_ptr[i + 1] = row_ptr[i] + lens[i];
+    if (src && R && count) {
+      const uint64_t tot = row_ptr[count];
+      DevBuf<uint32_t> ds(tot ? tot : 1, s);
+      DevBuf<double> dr(tot ? tot : 1, s);
+      QVB_CUDA(cudaMemcpyAsync(dp.p, row_ptr, (count + 1) * 8, cudaMemcpyHostToDevice, s));
+      k_in_rows<<<blocks, 128, 0, s>>>(gv, dn.p, count, dp.p, ds.p, dr.p, nullptr);
+      QVB_LAUNCH_CHECK();
+      QVB_CUDA(cudaMemcpyAsync(src, ds.p, tot * 4, cudaMemcpyDeviceToHost, s));
+      QVB_CUDA(cudaMemcpyAsync(R, dr.p, tot * 8, cudaMemcpyDeviceToHost, s));
+      QVB_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
 
 extern "C" int qvb_graph_last_sweep_ms(const qvb_graph* g, double* ms) {
   return guarded([&] {

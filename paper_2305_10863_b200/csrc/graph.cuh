@@ -109,9 +109,10 @@ struct qvb_graph {
   uint8_t* nm_lenf = nullptr;
   uint64_t* nm_sbase = nullptr;
   uint32_t* nm_col = nullptr;
-  uint32_t* nm_code = nullptr;
-  std::vector<uint64_t> nm_region;
-  uint32_t* marked = nullptr;  // device flag: a sweep's codes kept a marker (see k_codes)  // host: start of each pass's columns in nm_col (nseg + 1)  // compact: the gathered code of every nm_col entry (per sweep)
+  uint32_t* nm_code = nullptr;      // compact: the gathered code of every nm_col entry (per sweep)
+  std::vector<uint64_t> nm_region;  // host: start of each pass's columns in nm_col (nseg + 1)
+  uint64_t nm_region_count = 0;     // passes (nseg) of the node-major layout
+  uint32_t* marked = nullptr;       // device flag: a sweep's codes kept a marker (see k_codes)
   double* nm_R = nullptr;
   uint32_t* kcode[2] = {nullptr, nullptr};
   // first sweep ("f1", see above): out-degree classes and their streams

@@ -167,6 +167,7 @@ _SIGNATURES = {
     "qvb_in_adjacency": (i32, [i32, u64, u64, vp, vp, vp, vp, vp, vp]),
     "qvb_graph_last_sweep_ms": (i32, [vp, P(C.c_double)]),
     "qvb_graph_phase_ms": (i32, [vp, P(C.c_double), P(C.c_uint32)]),
+    "qvb_graph_in_rows": (i32, [vp, vp, u64, vp, vp, vp]),
     "qvb_graph_destroy": (i32, [vp]),
     "qvb_access_prob": (i32, [vp, u32, vp, i32, vp]),
     "qvb_compute_access_prob_ie": (i32, [i32, u64, u64, vp, vp, vp, u32, vp, vp]),
@@ -326,6 +327,17 @@ class DeviceGraph:
         _check(_lib().qvb_graph_phase_ms(self._h, ms, C.byref(n)))
         return {"first": ms[0], "gather": ms[1], "products": ms[2], "other": ms[3],
                 "launches": n.value}
+
+    def in_rows(self, nodes):
+        """The coalesced in-rows the sweeps multiply for ``nodes``: (row_ptr,
+        sources ascending, R = w_sum / row_sum(source)). Node-major graphs."""
+        nd = np.ascontiguousarray(nodes, np.uint64)
+        rp = np.zeros(len(nd) + 1, np.uint64)
+        _check(_lib().qvb_graph_in_rows(self._h, _ptr(nd), len(nd), _ptr(rp), None, None))
+        src = np.zeros(max(int(rp[-1]), 1), np.uint32)
+        R = np.zeros(max(int(rp[-1]), 1), np.float64)
+        _check(_lib().qvb_graph_in_rows(self._h, _ptr(nd), len(nd), _ptr(rp), _ptr(src), _ptr(R)))
+        return rp, src[: int(rp[-1])], R[: int(rp[-1])]
 
     def close(self):
         if self._h:

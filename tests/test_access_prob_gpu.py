@@ -247,3 +247,73 @@ def test_first_sweep_paths_bit_exact(qvb, oracle, first, monkeypatch):
         for layers in (2, 3):
             assert (bits(g.access_prob(layers)) == bits(oracle.access_prob(ro, col, w, layers))).all()
         g.close()
+
+
+def _coalesced_rows(oracle, ro, col, w, nodes):
+    """The reference's per-node factor list (metrics.cpp:152-166): in-row of
+    the transpose, parallel edges merged in order, R = w_sum / row_sum(s)."""
+    tro, tcol, tw = oracle.in_adjacency(ro, col, w)
+    rs = oracle.row_sums(ro, w)
+    out = []
+    for v in nodes:
+        a, b = int(tro[v]), int(tro[v + 1])
+        row, k = [], a
+        while k < b:
+            s, wt = int(tcol[k]), tw[k]
+            k += 1
+            while k < b and int(tcol[k]) == s:
+                wt += tw[k]
+                k += 1
+            row.append((s, wt / rs[s]))
+        out.append(row)
+    return out
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_in_rows_match_reference_rows(qvb, oracle, weighted, monkeypatch):
+    """qvb_graph_in_rows (the rows the node-major sweeps multiply) equals the
+    reference's coalesced in-rows, sources and R bit for bit, on C1 forced
+    into many source segments."""
+    monkeypatch.setenv("QVB_SEG_SOURCES", "9000")
+    c = CONFIGS["C1"]
+    ro, col, w = oracle.synthetic_graph(c["n"], c["e"], 7, weighted, False)
+    g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, weighted, False)
+    assert g.info().segments > 1
+    rng = np.random.default_rng(5)
+    nodes = np.unique(np.concatenate([rng.integers(0, c["n"], 3000), [0, c["n"] - 1]]))
+    rp, src, R = g.in_rows(nodes)
+    exp = _coalesced_rows(oracle, ro, col, w, nodes)
+    for i, row in enumerate(exp):
+        a, b = int(rp[i]), int(rp[i + 1])
+        assert [int(x) for x in src[a:b]] == [s for s, _ in row]
+        assert (bits(R[a:b]) == bits(np.array([r for _, r in row]))).all()
+    g.close()
+
+
+def test_c4_sampled_against_oracle(qvb, oracle):
+    """C4 at full size (111M nodes, 1.6B edges, 3 layers) against the oracle's
+    restatement on a sample of 20,000 nodes, layer by layer: P(v,2) from the
+    uniform P(.,1), and P(v,3) from the device's P(.,2) (itself checked on the
+    sample), each over the in-row the device multiplies — bit for bit. This
+    checks the first sweep (class stream), the per-segment code gathers and
+    the ordered products at the configuration they are built for."""
+    c = CONFIGS["C4"]
+    n = c["n"]
+    g = qvb.DeviceGraph.synthetic(n, c["e"], 7, False, False)
+    assert g.info().segments > 1 and g.info().classes > 0
+    p2 = g.access_prob(2)
+    p3 = g.access_prob(3)
+    rng = np.random.default_rng(11)
+    nodes = np.unique(np.concatenate([rng.integers(0, n, 20000), [0, 1, n // 2, n - 1]]))
+    rp, src, R = g.in_rows(nodes)
+    g.close()
+    tro = np.zeros(n + 1, np.uint64)
+    tro[nodes.astype(np.int64) + 1] = np.diff(rp)
+    np.cumsum(tro, out=tro)
+    assert int(tro[-1]) == len(src)
+    ones = np.ones(n, np.float64)
+    base = np.full(n, 1.0 / n)
+    exp2 = oracle.sweep_nodes(tro, src.astype(np.uint64), R, ones, base, nodes)
+    assert (bits(p2[nodes]) == bits(exp2)).all()
+    exp3 = oracle.sweep_nodes(tro, src.astype(np.uint64), R, ones, p2, nodes)
+    assert (bits(p3[nodes]) == bits(exp3)).all()
