@@ -215,6 +215,7 @@ def run_ours(args):
     from paper_2305_10863_b200 import qvb
 
     rank, world, local = D.init()
+    local = D.device_index(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)

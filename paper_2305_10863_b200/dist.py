@@ -21,11 +21,24 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
+def shared_gpu() -> bool:
+    """QVB_SHARE_GPU=1 (testing on a one-GPU box): every rank runs on the
+    same device; peers are still separate processes mapped with CUDA IPC, and
+    the setup collectives go over gloo (NCCL refuses two ranks on one GPU)."""
+    return os.environ.get("QVB_SHARE_GPU", "0") == "1"
+
+
+def device_index(local_rank: int) -> int:
+    if shared_gpu() and torch.cuda.is_available():
+        return local_rank % torch.cuda.device_count()
+    return local_rank
+
+
 def init(backend: str | None = None):
     rank, world, local = env_rank()
     if world > 1 and not dist.is_initialized():
         if backend is None:
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            backend = "nccl" if torch.cuda.is_available() and not shared_gpu() else "gloo"
         kw = {}
         if backend == "nccl":
             torch.cuda.set_device(local)
