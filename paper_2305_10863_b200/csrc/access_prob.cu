@@ -254,39 +254,33 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   else st_stream(state + v, miss, pol);
 }
 
-// Node-major segmented pass k (graph.cuh "nm"): one warp per slice of 32
-// consecutive node ids, lane = node in every pass, so the running product,
-// P, y and the code are read and written coalesced and without a perm word;
-// the lane's pass-k sources start at sbase(k, slice) + the prefix of the
-// slice's lens. Compact sweeps gather the 4-byte code of y (exact, see
-// graph.cuh) and fall back to y for kBigCode sources.
-template <bool kWeighted>
+// Node-major segmented pass k of a weighted graph (graph.cuh "nm"): one warp
+// per slice of 32 consecutive node ids, lane = node in every pass, so the
+// running product (carried between passes in `state`) and P are read and
+// written coalesced; the lane's pass-k sources (and R) start at
+// sbase(k, slice) + the prefix of the slice's lens. The first sweep gathers
+// nothing (fbase = P(s,1)). Compact node-major graphs use k_codes/k_products.
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     k_sweep_nm(int k, uint64_t S, uint64_t long_blocks, uint64_t nlong, uint64_t pf,
                const uint8_t* __restrict__ lenf, const uint64_t* __restrict__ sbase,
                const uint32_t* __restrict__ ncol, const double* __restrict__ nR,
                double* __restrict__ state, const uint32_t* __restrict__ lnode,
                const uint64_t* __restrict__ lptr, const uint32_t* __restrict__ lcol,
-               const double* __restrict__ lR, const uint32_t* __restrict__ exc_src,
-               const double* __restrict__ exc_R, const double* __restrict__ prev,
-               const double* __restrict__ yprev, const uint32_t* __restrict__ kprev,
-               const double* __restrict__ inv, double* __restrict__ out,
-               double* __restrict__ yout, uint32_t* __restrict__ kout, int gmode, double fbase) {
+               const double* __restrict__ lR, const double* __restrict__ prev,
+               const double* __restrict__ inv, double* __restrict__ out, int gmode, double fbase) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const uint64_t pol = policy_evict_first();
-  const uint64_t keep = policy_evict_last();
   if (blockIdx.x < long_blocks) {
-    long_row<kWeighted>((uint64_t)blockIdx.x * kWarpsPerBlock + wib, nlong, lnode, lptr, lcol, lR,
-                        exc_src, exc_R, prev, kWeighted ? prev : yprev, inv, out, yout, kout,
-                        gmode, pol, fbase);
+    long_row<true>((uint64_t)blockIdx.x * kWarpsPerBlock + wib, nlong, lnode, lptr, lcol, lR, nullptr,
+                   nullptr, prev, prev, inv, out, nullptr, nullptr, gmode, pol, fbase);
     return;
   }
   const uint64_t s_block = ((uint64_t)blockIdx.x - long_blocks) * kWarpsPerBlock;
   const uint64_t sl = s_block + wib;
   if (pf && wib == kWarpsPerBlock - 1 && lane == 0) {
     // L2 lookahead (see prefetch_ahead): lens, slice pointers and running
-    // products of the block pf ahead, columns (and R) of the block pf/2 ahead
+    // products of the block pf ahead, columns and R of the block pf/2 ahead
     const uint64_t sp = s_block + pf * kWarpsPerBlock;
     if (sp < S) {
       const uint64_t cnt = S - sp < kWarpsPerBlock ? S - sp : kWarpsPerBlock;
@@ -300,7 +294,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
       const uint64_t a = sbase[(uint64_t)k * S + sc], b = sbase[(uint64_t)k * S + ce];
       if (b > a) {
         prefetch_l2(ncol + a, (b - a) * sizeof(uint32_t));
-        if constexpr (kWeighted) prefetch_l2(nR + a, (b - a) * sizeof(double));
+        prefetch_l2(nR + a, (b - a) * sizeof(double));
       }
     }
   }
@@ -327,39 +321,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     for (int u = 0; u < kU; ++u) {
       const bool in = t + u < len;
       c[u] = in ? ld_stream(ncol + off + t + u, pol) : 0u;
-      if constexpr (kWeighted) r[u] = in ? ld_stream(nR + off + t + u, pol) : 0.0;
-      else r[u] = 0.0;
-    }
-    if constexpr (kWeighted) {
-#pragma unroll
-      for (int u = 0; u < kU; ++u)
-        x[u] = t + u < len ? (fbase != 0.0 ? fbase : ld_gather(prev + c[u], gmode)) : 0.0;
-    } else {
-      // all codes in flight first; the rare y fallbacks after (no load waits
-      // on a branch over an earlier load)
-      uint32_t code[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u)
-        code[u] = (t + u < len && !(c[u] & kExcFlag))
-                      ? (gmode == 3 ? ld_hint(kprev + c[u], keep) : __ldg(kprev + c[u]))
-                      : 0u;
-#pragma unroll
-      for (int u = 0; u < kU; ++u)  // J * 2^-53 is exact; 1 - it rounds like 1 - y
-        x[u] = __dmul_rn(static_cast<double>(code[u]), 0x1p-53);
-      bool big = false;
-#pragma unroll
-      for (int u = 0; u < kU; ++u) big |= code[u] == kBigCode;
-      if (big) {
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          if (code[u] == kBigCode) x[u] = ld_gather(yprev + c[u], gmode);
-      }
+      r[u] = in ? ld_stream(nR + off + t + u, pol) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u)
-      if (t + u < len) miss = __dmul_rn(miss, factor<kWeighted>(c[u], x[u], r[u], exc_src, exc_R, prev));
+      x[u] = t + u < len ? (fbase != 0.0 ? fbase : ld_gather(prev + c[u], gmode)) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (t + u < len) miss = __dmul_rn(miss, factor<true>(c[u], x[u], r[u], nullptr, nullptr, prev));
   }
-  if (lf & kNmLast) finish<kWeighted>(static_cast<uint32_t>(v), miss, prev, inv, out, yout, kout, pol);
+  if (lf & kNmLast) finish<true>(static_cast<uint32_t>(v), miss, prev, inv, out, nullptr, nullptr, pol);
   else if (len) st_stream(state + v, miss, pol);
 }
 
@@ -458,9 +429,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   }
 }
 
-// One slice's ordered product over its class stream (staged in shared memory
-// or read from global), exception classes contributing the NaN sentinel.
-template <bool kStaged>
+// One slice's ordered product over its lane-major class stream, exception
+// classes contributing the NaN sentinel.
 __device__ __forceinline__ double slice_product(uint32_t len, const uint16_t* __restrict__ cp,
                                                 uint32_t tab, uint32_t ncls, uint64_t pol) {
   double miss = 1.0;  // metrics.cpp:152
@@ -468,7 +438,7 @@ __device__ __forceinline__ double slice_product(uint32_t len, const uint16_t* __
   for (; k + kU <= len; k += kU) {
     uint32_t c[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) c[u] = kStaged ? cp[(k + u) * 32] : ld_stream(cp + (uint64_t)(k + u) * 32, pol);
+    for (int u = 0; u < kU; ++u) c[u] = ld_stream(cp + (uint64_t)(k + u) * 32, pol);
     double f[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) f[u] = lds_f64(tab + c[u] * 8);
@@ -479,7 +449,7 @@ __device__ __forceinline__ double slice_product(uint32_t len, const uint16_t* __
     uint32_t c[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u)
-      c[u] = k + u < len ? (kStaged ? cp[(k + u) * 32] : ld_stream(cp + (uint64_t)(k + u) * 32, pol)) : ncls;
+      c[u] = k + u < len ? ld_stream(cp + (uint64_t)(k + u) * 32, pol) : ncls;
     double f[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) f[u] = lds_f64(tab + c[u] * 8);
@@ -527,7 +497,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     const uint32_t v = perm[sl * 32 + lane] & kNodeMask;
     const uint64_t b0 = sptr[sl];
     const uint32_t len = static_cast<uint32_t>((sptr[sl + 1] - b0) >> 5);
-    double miss = slice_product<false>(len, cls + b0 + lane, tab, ncls, pol);
+    double miss = slice_product(len, cls + b0 + lane, tab, ncls, pol);
     if (miss != miss) miss = slice_product_exc(len, cls + b0 + lane, b0 + lane, tab, ncls, xslot, xR, nx, base);
     if (v != kNoNode) finish_first(v, miss, base, inv, out, yout, kout, 0);
   }
@@ -905,10 +875,9 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
       for (int k = 0; k < nseg; ++k) {
         const uint64_t lb = k == 0 ? long_blocks : 0;
         const uint64_t blocks = lb + (g.nm_S + kWarpsPerBlock - 1) / kWarpsPerBlock;
-        k_sweep_nm<true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
+        k_sweep_nm<<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
             k, g.nm_S, lb, g.nlong, pf, g.nm_lenf, g.nm_sbase, g.nm_col, g.nm_R, g.state, g.lnode,
-            g.lptr, g.lcol, g.lR, nullptr, nullptr, g.p[cur], nullptr, nullptr, g.inv, g.p[nxt],
-            nullptr, nullptr, gmode, fbase);
+            g.lptr, g.lcol, g.lR, g.p[cur], g.inv, g.p[nxt], gmode, fbase);
         QVB_LAUNCH_CHECK();
         ++launched;
       }
