@@ -278,14 +278,16 @@ __global__ void k_row_stats(const uint64_t* __restrict__ cro, const double* __re
 }
 
 // ---- one hop --------------------------------------------------------------
-__global__ void k_hop_count(const uint32_t* __restrict__ pn, uint64_t P, uint32_t fanout,
-                            const uint64_t* __restrict__ cro, const uint32_t* __restrict__ cpos,
-                            uint32_t* __restrict__ m_out, uint32_t* __restrict__ large,
-                            unsigned long long* __restrict__ nlarge) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= P;
+__global__ void k_hop_count(const uint32_t* __restrict__ pn, const uint64_t* __restrict__ Pp, uint64_t ub,
+                            uint32_t fanout, const uint64_t* __restrict__ cro,
+                            const uint32_t* __restrict__ cpos, uint32_t* __restrict__ m_out,
+                            uint32_t* __restrict__ large, unsigned long long* __restrict__ nlarge) {
+  // entries [P, ub] are 0, so the scan over ub + 1 entries ends in the total
+  const uint64_t P = *Pp;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= ub;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    if (i == P) {
-      m_out[P] = 0;
+    if (i >= P) {
+      m_out[i] = 0;
       continue;
     }
     const uint32_t p = pn[i];
@@ -300,7 +302,7 @@ __global__ void k_hop_count(const uint32_t* __restrict__ pn, uint64_t P, uint32_
 struct HopArgs {
   const uint32_t* pn;  // parents: node, seed slot
   const uint32_t* ps;
-  uint64_t P;
+  const uint64_t* P;  // parent count (device: the previous frontier's size)
   const uint64_t* ss_prev;  // seed starts of the parents' frontier
   const uint64_t* O;        // child offsets
   // derive_prefix(splitmix64(rng ^ seed*gamma), hop) per seed: the part of
@@ -411,7 +413,8 @@ __global__ void __launch_bounds__(kBlock) k_hop_sample(HopArgs a) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lt_mask = lanemask_lt();
   const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
-  for (uint64_t i = blockIdx.x * (uint64_t)kWarpsPerBlock + (threadIdx.x >> 5); i < a.P;
+  const uint64_t P = *a.P;
+  for (uint64_t i = blockIdx.x * (uint64_t)kWarpsPerBlock + (threadIdx.x >> 5); i < P;
        i += warps) {
     const uint32_t p = a.pn[i], s = a.ps[i];
     const uint64_t c0 = a.cro[p];
@@ -646,9 +649,10 @@ __global__ void k_instance_counts(const uint64_t* __restrict__ ss, uint64_t nsee
 
 // Frontier k -> flattened seed-major/hop-major position; marks the bitmap.
 __global__ void k_flatten(const uint32_t* __restrict__ fn, const uint32_t* __restrict__ fs,
-                          uint64_t count, const uint64_t* __restrict__ ssk,
+                          const uint64_t* __restrict__ countp, const uint64_t* __restrict__ ssk,
                           const uint64_t* __restrict__ flat_off, uint32_t H, uint32_t k,
                           uint64_t* __restrict__ nodes, uint32_t* __restrict__ bitmap) {
+  const uint64_t count = *countp;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < count;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t v = fn[j], s = fs[j];
@@ -912,38 +916,58 @@ extern "C" int qvb_batch_sample(qvb_sampler* sp, const uint64_t* seeds, uint64_t
     } events{{&ea, &eb, &fork, &join}};
     QVB_CUDA(cudaEventRecord(ea, s));
 
+    // Frontier sizes live on the device (frontier k's size = its sentinel
+    // seed start ss[k][nseeds]); every kernel reads them there, so the hops
+    // run without host round trips when the buffers can be sized by the
+    // upper bound |frontier k| <= |frontier k-1| * fanout. Past kSyncFreeMax
+    // instances the exact sizes are read back per hop instead.
+    constexpr uint64_t kSyncFreeMax = 1ull << 28;
+    std::vector<uint64_t> ub(H + 1);
+    ub[0] = nseeds;
+    bool sync_free = true;
+    uint64_t ub_total = nseeds;
+    for (uint32_t k = 1; k <= H; ++k) {
+      const uint64_t f = fanouts[k - 1];
+      ub[k] = ub[k - 1] > kSyncFreeMax / f ? kSyncFreeMax + 1 : ub[k - 1] * f;
+      ub_total += ub[k];
+      if (ub[k] > kSyncFreeMax || ub_total > kSyncFreeMax) sync_free = false;
+    }
     // seed starts of every frontier, [H+1][nseeds+1]
     DevBuf<uint64_t> ss((H + 1) * (nseeds + 1), s);
     std::vector<DevBuf<uint32_t>> fn(H + 1), fs(H + 1);
-    std::vector<uint64_t> fsize(H + 1, 0);
+    std::vector<uint64_t> fcap(H + 1, 0);  // allocated capacity of each frontier
     fn[0].alloc(nseeds ? nseeds : 1, s);
     fs[0].alloc(nseeds ? nseeds : 1, s);
-    fsize[0] = nseeds;
+    fcap[0] = nseeds;
     k_hop0<<<grid_for(nseeds + 1, kBlock), kBlock, 0, s>>>(dseeds.p, nseeds, fn[0].p, fs[0].p, ss.p);
     QVB_LAUNCH_CHECK();
     DevBuf<unsigned long long> nlarge(1, s);
     DevBuf<uint64_t> hop_state(nseeds ? nseeds : 1, s);
     for (uint32_t k = 1; k <= H; ++k) {
-      const uint64_t P = fsize[k - 1];
-      DevBuf<uint32_t> m(P + 1, s), large(P ? P : 1, s);
-      DevBuf<uint64_t> O(P + 1, s);
+      const uint64_t Pub = fcap[k - 1];  // parents: at most the previous capacity
+      const uint64_t* Pd = ss.p + (uint64_t)(k - 1) * (nseeds + 1) + nseeds;
+      DevBuf<uint32_t> m(Pub + 1, s), large(Pub ? Pub : 1, s);
+      DevBuf<uint64_t> O(Pub + 1, s);
       QVB_CUDA(cudaMemsetAsync(nlarge.p, 0, sizeof(unsigned long long), s));
-      k_hop_count<<<grid_for(P + 1, kBlock), kBlock, 0, s>>>(fn[k - 1].p, P, fanouts[k - 1], sp->cro,
-                                                             sp->cpos, m.p, large.p, nlarge.p);
+      k_hop_count<<<grid_for(Pub + 1, kBlock), kBlock, 0, s>>>(fn[k - 1].p, Pd, Pub, fanouts[k - 1], sp->cro,
+                                                               sp->cpos, m.p, large.p, nlarge.p);
       QVB_LAUNCH_CHECK();
-      exclusive_sum_u32_u64(m.p, O.p, P + 1, s);
+      exclusive_sum_u32_u64(m.p, O.p, Pub + 1, s);
       uint64_t* ssk = ss.p + (uint64_t)k * (nseeds + 1);
       k_seed_starts<<<grid_for(nseeds + 1, kBlock), kBlock, 0, s>>>(
           ss.p + (uint64_t)(k - 1) * (nseeds + 1), O.p, nseeds, ssk, dseeds.p, rng_seed, k,
           hop_state.p);
       QVB_LAUNCH_CHECK();
-      const uint64_t C = read_scalar(O.p + P, s);
-      if (C >= 0xFFFFFFFFull) fail(QVB_ERR_UNSUPPORTED, "frontier exceeds 2^32 instances");
-      fsize[k] = C;
+      uint64_t C = ub[k];
+      if (!sync_free) {
+        C = read_scalar(ssk + nseeds, s);
+        if (C >= 0xFFFFFFFFull) fail(QVB_ERR_UNSUPPORTED, "frontier exceeds 2^32 instances");
+      }
+      fcap[k] = C;
       fn[k].alloc(C ? C : 1, s);
       fs[k].alloc(C ? C : 1, s);
-      if (P == 0) continue;
-      HopArgs a{fn[k - 1].p, fs[k - 1].p, P,         ss.p + (uint64_t)(k - 1) * (nseeds + 1),
+      if (Pub == 0) continue;
+      HopArgs a{fn[k - 1].p, fs[k - 1].p, Pd,        ss.p + (uint64_t)(k - 1) * (nseeds + 1),
                 O.p,         hop_state.p, k,
                 fanouts[k - 1], sp->cro,  sp->ccol,  sp->cw,
                 sp->cpos,    fn[k].p,     fs[k].p};
@@ -955,9 +979,10 @@ extern "C" int qvb_batch_sample(qvb_sampler* sp, const uint64_t* seeds, uint64_t
         QVB_LAUNCH_CHECK();
         QVB_CUDA(cudaEventRecord(join, sp->side));
       }
-      k_hop_sample<<<warp_grid(P), kBlock, 0, s>>>(a);
+      k_hop_sample<<<warp_grid(Pub), kBlock, 0, s>>>(a);
       QVB_LAUNCH_CHECK();
       if (sp->scratch) QVB_CUDA(cudaStreamWaitEvent(s, join, 0));
+      // m, large and O are freed stream-ordered after this hop's kernels
     }
     // flatten: instance_counts (seed-major) -> offsets -> scatter
     const uint64_t ncounts = nseeds * (H + 1);
@@ -966,18 +991,18 @@ extern "C" int qvb_batch_sample(qvb_sampler* sp, const uint64_t* seeds, uint64_t
     k_instance_counts<<<grid_for(ncounts + 1, kBlock), kBlock, 0, s>>>(ss.p, nseeds, H, cnt.p);
     QVB_LAUNCH_CHECK();
     exclusive_sum_u32_u64(cnt.p, flat_off.p, ncounts + 1, s);
-    uint64_t total = 0;
-    for (uint32_t k = 0; k <= H; ++k) total += fsize[k];
-    DevBuf<uint64_t> nodes(total ? total : 1, s), counts(ncounts ? ncounts : 1, s);
+    uint64_t cap_total = 0;
+    for (uint32_t k = 0; k <= H; ++k) cap_total += fcap[k];
+    DevBuf<uint64_t> nodes(cap_total ? cap_total : 1, s), counts(ncounts ? ncounts : 1, s);
     const uint64_t words = (sp->n + 31) / 32;
     DevBuf<uint32_t> bitmap(words, s), pc(words + 1, s);
     DevBuf<uint64_t> woff(words + 1, s);
     QVB_CUDA(cudaMemsetAsync(bitmap.p, 0, words * 4, s));
     for (uint32_t k = 0; k <= H; ++k) {
-      if (!fsize[k]) continue;
-      k_flatten<<<grid_for(fsize[k], kBlock), kBlock, 0, s>>>(
-          fn[k].p, fs[k].p, fsize[k], ss.p + (uint64_t)k * (nseeds + 1), flat_off.p, H, k, nodes.p,
-          bitmap.p);
+      if (!fcap[k]) continue;
+      k_flatten<<<grid_for(fcap[k], kBlock), kBlock, 0, s>>>(
+          fn[k].p, fs[k].p, ss.p + (uint64_t)k * (nseeds + 1) + nseeds, ss.p + (uint64_t)k * (nseeds + 1),
+          flat_off.p, H, k, nodes.p, bitmap.p);
       QVB_LAUNCH_CHECK();
     }
     if (ncounts) {
@@ -987,17 +1012,23 @@ extern "C" int qvb_batch_sample(qvb_sampler* sp, const uint64_t* seeds, uint64_t
     k_popc_words<<<grid_for(words + 1, kBlock), kBlock, 0, s>>>(bitmap.p, words, pc.p);
     QVB_LAUNCH_CHECK();
     exclusive_sum_u32_u64(pc.p, woff.p, words + 1, s);
-    const uint64_t uc = read_scalar(woff.p + words, s);
-    DevBuf<uint64_t> unique(uc ? uc : 1, s);
+    const uint64_t ucap = std::min<uint64_t>(sp->n, cap_total);
+    DevBuf<uint64_t> unique(ucap ? ucap : 1, s);
     k_emit_unique<<<grid_for(words, kBlock), kBlock, 0, s>>>(bitmap.p, words, woff.p, unique.p);
     QVB_LAUNCH_CHECK();
+    // the batch's two sizes (unique nodes, instances), read back once
+    DevBuf<uint64_t> sizes(2, s);
+    QVB_CUDA(cudaMemcpyAsync(sizes.p, woff.p + words, 8, cudaMemcpyDeviceToDevice, s));
+    QVB_CUDA(cudaMemcpyAsync(sizes.p + 1, flat_off.p + ncounts, 8, cudaMemcpyDeviceToDevice, s));
+    uint64_t hsz[2] = {0, 0};
+    QVB_CUDA(cudaMemcpyAsync(hsz, sizes.p, sizeof hsz, cudaMemcpyDeviceToHost, s));
     QVB_CUDA(cudaEventRecord(eb, s));
     QVB_CUDA(cudaEventSynchronize(eb));
     float ms = 0;
     QVB_CUDA(cudaEventElapsedTime(&ms, ea, eb));
     r->ms = ms;
-    r->total = total;
-    r->unique_count = uc;
+    r->total = hsz[1];
+    r->unique_count = hsz[0];
     r->nodes = to_device_owned(nodes);
     r->counts = to_device_owned(counts);
     r->unique = to_device_owned(unique);
