@@ -38,44 +38,54 @@ struct Bases {
 
 template <int VEC>
 struct Vec;
+// Row reads and writes are a stream (each row moves once per gather): L2
+// evict_first, so they do not push out the lookup table, whose lines are
+// reused by several requests of a batch (C2: 8 entries per 64-byte line,
+// 1M lookups into 2.4M entries).
 template <>
 struct Vec<16> {
   using T = uint4;
-  static __device__ __forceinline__ T load(const char* p) {
+  static __device__ __forceinline__ T load(const char* p, uint64_t pol) {
     T r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
+                 : "l"(p), "l"(pol));
     return r;
   }
-  static __device__ __forceinline__ void store(char* p, const T& v) {
-    *reinterpret_cast<T*>(p) = v;
+  static __device__ __forceinline__ void store(char* p, const T& v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+                 : "memory");
   }
 };
 template <>
 struct Vec<8> {
   using T = uint2;
-  static __device__ __forceinline__ T load(const char* p) {
+  static __device__ __forceinline__ T load(const char* p, uint64_t pol) {
     T r;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
                  : "=r"(r.x), "=r"(r.y)
-                 : "l"(p));
+                 : "l"(p), "l"(pol));
     return r;
   }
-  static __device__ __forceinline__ void store(char* p, const T& v) {
-    *reinterpret_cast<T*>(p) = v;
+  static __device__ __forceinline__ void store(char* p, const T& v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1,%2}, %3;" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "l"(pol)
+                 : "memory");
   }
 };
 template <>
 struct Vec<4> {
   using T = uint32_t;
-  static __device__ __forceinline__ T load(const char* p) {
+  static __device__ __forceinline__ T load(const char* p, uint64_t pol) {
     T r;
-    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(r)
+                 : "l"(p), "l"(pol));
     return r;
   }
-  static __device__ __forceinline__ void store(char* p, const T& v) {
-    *reinterpret_cast<T*>(p) = v;
+  static __device__ __forceinline__ void store(char* p, const T& v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
   }
 };
 
@@ -89,6 +99,7 @@ __global__ void __launch_bounds__(kGatherBlock)
              Bases bases, uint64_t stride, uint32_t cpr, uint32_t row_bytes, uint64_t n,
              char* __restrict__ out, uint64_t row_base, unsigned long long* err) {
   using V = Vec<VEC>;
+  const uint64_t pol = policy_evict_first();  // rows: a stream
   const uint32_t total = rows * cpr;
   const uint32_t nthreads = gridDim.x * blockDim.x;
   for (uint32_t c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < total; c0 += nthreads * kUnroll) {
@@ -109,14 +120,14 @@ __global__ void __launch_bounds__(kGatherBlock)
         } else {
           const uint64_t e = __ldg(lut + f);
           const char* src = bases.p[e >> kOffsetBits] + (e & kOffsetMask) * stride + k * VEC;
-          v[u] = V::load(src);
+          v[u] = V::load(src, pol);
           dst[u] = (uint64_t)i * row_bytes + (uint64_t)k * VEC;
         }
       }
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
-      if (ok[u]) V::store(out + dst[u], v[u]);
+      if (ok[u]) V::store(out + dst[u], v[u], pol);
   }
 }
 
@@ -136,6 +147,7 @@ __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
                   uint32_t row_bytes, uint64_t n, char* __restrict__ out,
                   unsigned long long* err) {
   using V = Vec<VEC>;
+  const uint64_t pol = policy_evict_first();  // rows: a stream
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -177,7 +189,7 @@ __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
         const uint32_t c = c0 + u * 32;
         const uint64_t s = __shfl_sync(0xffffffffu, src, row < 32 ? row : 31);
         ok[u] = c < tot && s != 0;
-        if (ok[u]) v[u] = V::load(reinterpret_cast<const char*>(s) + (uint64_t)k * VEC);
+        if (ok[u]) v[u] = V::load(reinterpret_cast<const char*>(s) + (uint64_t)k * VEC, pol);
         row += q32;
         k += r32;
         if (k >= cpr) {
@@ -187,7 +199,7 @@ __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u)
-        if (ok[u]) V::store(dst0 + (uint64_t)(c0 + u * 32) * VEC, v[u]);
+        if (ok[u]) V::store(dst0 + (uint64_t)(c0 + u * 32) * VEC, v[u], pol);
     }
     src = src_next;
   }
@@ -204,6 +216,7 @@ __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
                     uint32_t row_bytes, uint64_t n, char* __restrict__ out,
                     unsigned long long* err) {
   using V = Vec<16>;
+  const uint64_t pol = policy_evict_first();  // rows: a stream
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -245,7 +258,7 @@ __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
         ok[u] = c < tot && s != 0;
         half[u] = (k + 1) * 16 > row_bytes;
         dst[u] = (uint64_t)row * row_bytes + (uint64_t)k * 16;
-        if (ok[u]) v[u] = V::load(reinterpret_cast<const char*>(s) + (uint64_t)k * 16);
+        if (ok[u]) v[u] = V::load(reinterpret_cast<const char*>(s) + (uint64_t)k * 16, pol);
         row += q32;
         k += r32;
         if (k >= cpr) {
@@ -461,6 +474,7 @@ __global__ void __launch_bounds__(kGatherBlock)
                     uint32_t rows, Bases bases, uint64_t stride, uint32_t cpr, uint32_t row_bytes,
                     char* __restrict__ out) {
   using V = Vec<VEC>;
+  const uint64_t pol = policy_evict_first();  // rows: a stream
   const uint32_t total = rows * cpr;
   const uint32_t nthreads = gridDim.x * blockDim.x;
   for (uint32_t c0 = blockIdx.x * blockDim.x + threadIdx.x; c0 < total; c0 += nthreads * kUnroll) {
@@ -476,13 +490,13 @@ __global__ void __launch_bounds__(kGatherBlock)
         const uint32_t k = c - j * cpr;
         const uint64_t e = __ldg(keys + j);
         const uint32_t i = __ldg(order + j);
-        v[u] = V::load(bases.p[e >> kOffsetBits] + (e & kOffsetMask) * stride + k * VEC);
+        v[u] = V::load(bases.p[e >> kOffsetBits] + (e & kOffsetMask) * stride + k * VEC, pol);
         dst[u] = (uint64_t)i * row_bytes + (uint64_t)k * VEC;
       }
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
-      if (ok[u]) V::store(out + dst[u], v[u]);
+      if (ok[u]) V::store(out + dst[u], v[u], pol);
   }
 }
 
