@@ -145,9 +145,11 @@ __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
     k_gather_rows(const uint64_t* __restrict__ ids, uint64_t rows,
                   const uint64_t* __restrict__ lut, Bases bases, uint64_t stride, uint32_t cpr,
                   uint32_t row_bytes, uint64_t n, char* __restrict__ out,
-                  unsigned long long* err) {
+                  unsigned long long* err, int lut_keep) {
   using V = Vec<VEC>;
   const uint64_t pol = policy_evict_first();  // rows: a stream
+  // a lookup table that fits L2 comfortably is kept there across the batch
+  const uint64_t lpol = lut_keep ? policy_evict_last() : policy_evict_normal();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
       atomicMin(err, (unsigned long long)r);
       return 0;
     }
-    const uint64_t e = __ldg(lut + f);
+    const uint64_t e = ld_hint(lut + f, lpol);
     return reinterpret_cast<uint64_t>(bases.p[e >> kOffsetBits]) + (e & kOffsetMask) * stride;
   };
 
@@ -593,6 +595,12 @@ struct qvb_store {
   }
 
   int vec() const { return row_bytes % 16 == 0 ? 16 : (row_bytes % 8 == 0 ? 8 : 4); }
+  // keep the lookup table in L2 (evict_last) while it is at most a quarter of it
+  int lut_keep_flag() const {
+    const char* m = std::getenv("QVB_LUT_KEEP");
+    if (m) return std::atoi(m);
+    return n * 8 <= (32ull << 20) ? 1 : 0;
+  }
 
   void launch_gather(const uint64_t* ids, uint64_t b, char* out, cudaStream_t s) {
     check_attached();
@@ -722,13 +730,14 @@ struct qvb_store {
 
   template <int V, int U, int MB>
   void launch_rows_u(const uint64_t* ids, uint64_t rows, uint32_t cpr, char* o, cudaStream_t s) {
+    const int lut_keep = lut_keep_flag();
     static unsigned full = 0;
     if (!full) full = resident_grid(k_gather_rows<V, U, MB>, kGatherBlock, 0, ~0ull);
     const uint64_t warps_needed = (rows + 31) / 32;
     const uint64_t blocks = (warps_needed + kGatherBlock / 32 - 1) / (kGatherBlock / 32);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(full, blocks));
     k_gather_rows<V, U, MB><<<grid, kGatherBlock, 0, s>>>(ids, rows, lut, bases, stride, cpr,
-                                                          row_bytes, n, o, err);
+                                                          row_bytes, n, o, err, lut_keep);
     QVB_LAUNCH_CHECK();
   }
 
