@@ -57,6 +57,24 @@ __device__ __forceinline__ double code_to_factor(uint32_t J) {
   return f;
 }
 
+// Inclusive warp scan of x: shfl.up's validity predicate guards the add
+// (two instructions a step instead of shuffle + lane test + select + add).
+template <int O>
+__device__ __forceinline__ void scan_step(uint32_t& x) {
+  asm("{\n .reg .pred p;\n .reg .u32 t;\n shfl.sync.up.b32 t|p, %0, %1, 0, -1;\n"
+      " @p add.u32 %0, %0, t;\n}"
+      : "+r"(x)
+      : "n"(O));
+}
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+  scan_step<1>(x);
+  scan_step<2>(x);
+  scan_step<4>(x);
+  scan_step<8>(x);
+  scan_step<16>(x);
+  return x;
+}
+
 __global__ void k_init(uint64_t n, const double* __restrict__ inv, double* __restrict__ p,
                        double* __restrict__ y, uint32_t* __restrict__ kc) {
   const double base = __ddiv_rn(1.0, static_cast<double>(n));  // metrics.cpp:143
@@ -700,12 +718,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
     const uint32_t len = lf & kNmLen;
     const uint32_t maxlen = __reduce_max_sync(kFull, len);
     if (maxlen == 0) continue;  // slice untouched by this pass
-    uint32_t incl = len;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += t;
-    }
+    const uint32_t incl = warp_incl_scan(len);
     const uint32_t* __restrict__ cp = ncode + sb + (incl - len);
     for (uint32_t t = 0; t < maxlen; t += 4) {
       uint32_t code[4];
