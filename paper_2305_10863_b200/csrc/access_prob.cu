@@ -773,20 +773,27 @@ struct PhaseTimer {
 
 }  // namespace
 
-const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
+const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, double* final_out) {
   if (layers < 1) fail(QVB_ERR_VALIDATION, "access probability needs layers >= 1");
   const uint64_t n = g.n;
   const bool compact = g.layout == 0;
   const bool codes = g.nm && compact;                    // nm compact sweeps gather 4-byte codes
   const bool f1 = compact && g.ncls > 0 && layers >= 2;  // class-stream first sweep
+  // entry N of every gathered vector is the padding operand: 0 (factor 1.0);
+  // set once when the buffer is made (sweeps write entries < N only)
   for (int i = 0; i < 2; ++i) {
-    if (!g.p[i]) QVB_CUDA(cudaMalloc(&g.p[i], (n + 1) * sizeof(double)));
-    if (compact && !g.nm && !g.y[i]) QVB_CUDA(cudaMalloc(&g.y[i], (n + 1) * sizeof(double)));
-    if (codes && !g.kcode[i]) QVB_CUDA(cudaMalloc(&g.kcode[i], (n + 1) * sizeof(uint32_t)));
-    // entry N is the padding operand of every gathered vector: 0 (factor 1.0)
-    QVB_CUDA(cudaMemsetAsync(g.p[i] + n, 0, sizeof(double), s));
-    if (compact && !g.nm) QVB_CUDA(cudaMemsetAsync(g.y[i] + n, 0, sizeof(double), s));
-    if (codes) QVB_CUDA(cudaMemsetAsync(g.kcode[i] + n, 0, sizeof(uint32_t), s));
+    if (!g.p[i]) {
+      QVB_CUDA(cudaMalloc(&g.p[i], (n + 1) * sizeof(double)));
+      QVB_CUDA(cudaMemsetAsync(g.p[i] + n, 0, sizeof(double), s));
+    }
+    if (compact && !g.nm && !g.y[i]) {
+      QVB_CUDA(cudaMalloc(&g.y[i], (n + 1) * sizeof(double)));
+      QVB_CUDA(cudaMemsetAsync(g.y[i] + n, 0, sizeof(double), s));
+    }
+    if (codes && !g.kcode[i]) {
+      QVB_CUDA(cudaMalloc(&g.kcode[i], (n + 1) * sizeof(uint32_t)));
+      QVB_CUDA(cudaMemsetAsync(g.kcode[i] + n, 0, sizeof(uint32_t), s));
+    }
   }
   if (codes && !g.nm_code) {  // +128: k_products reads whole 4-code groups past a run's end
     QVB_CUDA(cudaMalloc(&g.nm_code, (g.nm_cols + 128) * sizeof(uint32_t)));
@@ -816,6 +823,8 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
     const int cur = (j - 2) & 1, nxt = cur ^ 1;
     const bool first = j == 2;
     double* yout = (compact && !g.nm && j < layers) ? g.y[nxt] : nullptr;
+    // the last sweep writes straight into the caller's device buffer
+    double* const pout = (j == layers && final_out) ? final_out : g.p[nxt];
     uint32_t* kout = (codes && j < layers) ? g.kcode[nxt] : nullptr;
 
     if (first && f1) {  // ---- first sweep over the class stream
@@ -829,18 +838,21 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
                                           (g.nlong + kWarpsPerBlock - 1) / kWarpsPerBlock);
         k_first_long<<<lg, kWarpsPerBlock * 32, smem, s>>>(g.nlong, base, g.ncls, g.cls_inv, g.lnode,
                                                            g.lptr, g.lcol, g.lcls, g.exc_R, g.inv,
-                                                           g.p[nxt], yout, kout);
+                                                           pout, yout, kout);
         QVB_LAUNCH_CHECK();
         ++launched;
       }
       if (g.f1_S) {
-        QVB_CUDA(cudaFuncSetAttribute(k_first, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kMaxCls + 2) * 8));
-        const unsigned grid = resident_grid(k_first, kWarpsPerBlock * 32, smem,
-                                            (g.f1_S + kWarpsPerBlock - 1) / kWarpsPerBlock);
+        if (!g.f1_grid) {  // once per graph: host API calls between launches idle the GPU
+          QVB_CUDA(cudaFuncSetAttribute(k_first, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kMaxCls + 2) * 8));
+          g.f1_grid = resident_grid(k_first, kWarpsPerBlock * 32, smem,
+                                    (g.f1_S + kWarpsPerBlock - 1) / kWarpsPerBlock);
+        }
+        const unsigned grid = g.f1_grid;
         k_first<<<grid, kWarpsPerBlock * 32, smem, s>>>(g.f1_S, base, g.ncls, g.cls_inv, g.f1_perm,
                                                         g.f1_sptr, g.f1_cls, g.f1_xslot, g.f1_xR,
-                                                        g.f1_nx, g.inv, g.p[nxt], yout, kout);
+                                                        g.f1_nx, g.inv, pout, yout, kout);
         QVB_LAUNCH_CHECK();
         ++launched;
       }
@@ -855,7 +867,7 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
       if (g.nlong) {  // long rows: whole rows, one warp each
         k_pass_long<<<static_cast<unsigned>((g.nlong * 32 + 255) / 256), 256, 0, s>>>(
             g.nlong, g.lnode, g.lptr, g.lcol, g.exc_src, g.exc_R, g.p[cur], g.kcode[cur], g.inv,
-            g.p[nxt], kout);
+            pout, kout);
         QVB_LAUNCH_CHECK();
         ++launched;
       }
@@ -864,7 +876,8 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
       for (int k = 0; k < nseg; ++k) {
         const uint64_t e0 = g.nm_region[k], e1 = g.nm_region[k + 1];
         if (e1 <= e0) continue;
-        const unsigned cg = resident_grid(k_codes, 256, 0, (e1 - e0 + 2047) / 2048);
+        if (!g.codes_grid) g.codes_grid = resident_grid(k_codes, 256, 0, ~0ull);
+        const unsigned cg = static_cast<unsigned>(std::min<uint64_t>(g.codes_grid, (e1 - e0 + 2047) / 2048));
         k_codes<<<cg, 256, 0, s>>>(e0, e1, g.nm_col, g.kcode[cur], g.exc_src, g.exc_R, g.p[cur], g.inv,
                                   g.nm_code, g.marked);
         QVB_LAUNCH_CHECK();
@@ -875,7 +888,7 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
       k_products<<<static_cast<unsigned>((g.nm_S + kWarpsPerBlock - 1) / kWarpsPerBlock),
                    kWarpsPerBlock * 32, 0, s>>>(nseg, g.nm_S, n, g.nm_lenf, g.nm_sbase, g.nm_code,
                                                 g.nm_col, g.exc_src, g.exc_R, g.p[cur], g.inv,
-                                                g.p[nxt], kout, g.marked);
+                                                pout, kout, g.marked);
       QVB_LAUNCH_CHECK();
       pt.end(1);
       continue;
@@ -890,7 +903,7 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
         const uint64_t blocks = lb + (g.nm_S + kWarpsPerBlock - 1) / kWarpsPerBlock;
         k_sweep_nm<<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
             k, g.nm_S, lb, g.nlong, pf, g.nm_lenf, g.nm_sbase, g.nm_col, g.nm_R, g.state, g.lnode,
-            g.lptr, g.lcol, g.lR, g.p[cur], g.inv, g.p[nxt], gmode, fbase);
+            g.lptr, g.lcol, g.lR, g.p[cur], g.inv, pout, gmode, fbase);
         QVB_LAUNCH_CHECK();
         ++launched;
       }
@@ -905,12 +918,12 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
         if (compact) {
           k_sweep<false><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
               s0, s1, lb, g.nlong, pf, g.nslices, g.state, g.perm, g.sptr, g.scol, nullptr, g.lnode,
-              g.lptr, g.lcol, nullptr, g.exc_src, g.exc_R, g.p[cur], g.y[cur], g.inv, g.p[nxt], yout,
+              g.lptr, g.lcol, nullptr, g.exc_src, g.exc_R, g.p[cur], g.y[cur], g.inv, pout, yout,
               gmode, 0.0);
         } else {
           k_sweep<true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, s>>>(
               s0, s1, lb, g.nlong, pf, g.nslices, g.state, g.perm, g.sptr, g.scol, g.sR, g.lnode,
-              g.lptr, g.lcol, g.lR, nullptr, nullptr, g.p[cur], nullptr, g.inv, g.p[nxt], nullptr,
+              g.lptr, g.lcol, g.lR, nullptr, nullptr, g.p[cur], nullptr, g.inv, pout, nullptr,
               gmode, fbase);
         }
         QVB_LAUNCH_CHECK();
@@ -920,7 +933,11 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s) {
     pt.end(launched);
   }
   QVB_CUDA(cudaEventRecord(g.ev[1], s));
-  return g.p[(layers - 1) & 1];
+  if (final_out && layers == 1) {
+    QVB_CUDA(cudaMemcpyAsync(final_out, g.p[0], n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return final_out;
+  }
+  return final_out ? final_out : g.p[(layers - 1) & 1];
 }
 
 }  // namespace qvb
@@ -934,10 +951,13 @@ extern "C" int qvb_access_prob(qvb_graph* g, uint32_t layers, double* out, int o
     if (layers < 1) fail(QVB_ERR_VALIDATION, "access probability needs layers >= 1");
     DeviceGuard dg(g->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const double* p = run_access_prob(*g, layers, s);
-    QVB_CUDA(cudaMemcpyAsync(out, p, g->n * sizeof(double),
-                             out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
-    if (!out_on_device) QVB_CUDA(cudaStreamSynchronize(s));
+    if (out_on_device) {  // the last sweep writes the caller's buffer itself
+      run_access_prob(*g, layers, s, out);
+    } else {
+      const double* p = run_access_prob(*g, layers, s);
+      QVB_CUDA(cudaMemcpyAsync(out, p, g->n * sizeof(double), cudaMemcpyDeviceToHost, s));
+      QVB_CUDA(cudaStreamSynchronize(s));
+    }
   });
 }
 

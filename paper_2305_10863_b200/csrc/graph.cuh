@@ -137,6 +137,7 @@ struct qvb_graph {
   std::vector<PhaseEv> phase_ev;
   size_t phase_used = 0;
   uint32_t launches = 0;  // kernels launched by the last run
+  unsigned f1_grid = 0, codes_grid = 0;  // resident grids, computed on first use
   ~qvb_graph();
 };
 
@@ -194,7 +195,9 @@ void generate_out_csr(uint64_t n, uint64_t e, uint64_t seed, int weighted, int t
                       cudaStream_t s, DevBuf<uint64_t>& ro, DevBuf<uint32_t>& col,
                       DevBuf<double>& w, DevBuf<uint32_t>& ssrc);
 
-// Runs layers-1 sweeps; returns the device buffer holding P_layers.
-const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s);
+// Runs layers-1 sweeps; returns the device buffer holding P_layers
+// (final_out, when given: the last sweep writes it directly).
+const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s,
+                              double* final_out = nullptr);
 
 }  // namespace qvb
