@@ -210,8 +210,7 @@ __device__ __forceinline__ double ld_hint(const double* a, uint64_t pol) {
   return v;
 }
 // Gather of one operand: mode 0 = ld.global.nc (read-only path, L1 allocate),
-// 1 = ld.global.nc.L1::no_allocate, 2 = ld.global.cg (L2 only), 3 = .L2::evict_last,
-// 9 = timing experiment only (wrong results): every gather hits one 8 KB block.
+// 1 = ld.global.nc.L1::no_allocate, 2 = ld.global.cg (L2 only), 3 = .L2::evict_last.
 __device__ __forceinline__ double ld_gather(const double* a, int mode) {
   double v;
   if (mode == 1) {
@@ -224,8 +223,6 @@ __device__ __forceinline__ double ld_gather(const double* a, int mode) {
         " ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], p;\n}"
         : "=d"(v)
         : "l"(a));
-  } else if (mode == 9) {
-    v = __ldg(reinterpret_cast<const double*>(reinterpret_cast<uint64_t>(a) & ~0x1FF8ull));
   } else {
     v = __ldg(a);
   }
