@@ -1,4 +1,4 @@
 OUT=gpurun_out
 timeout 900 python -m pytest tests/test_access_prob_gpu.py -q -x > $OUT/t1.log 2>&1; tail -3 $OUT/t1.log
-timeout 600 python bench.py --steps 20 --no-cpu-baseline --sample-seeds 0 > $OUT/b2.json 2> $OUT/b2.err
-timeout 900 python bench.py --config C4 --steps 10 --no-cpu-baseline --no-e2e --sample-seeds 0 > $OUT/b4.json 2> $OUT/b4.err
+timeout 300 python experiments/ap_bench.py C4 >> $OUT/ap4.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,smsp__inst_executed.sum --clock-control none --csv -k regex:"k_first|k_codes|k_products" --log-file $OUT/c4_gp.csv python experiments/ap_bench.py C4 > /dev/null 2>&1

@@ -600,40 +600,91 @@ __device__ __forceinline__ uint32_t factor_to_code(double f) {
   return (f > 0.5 && j >= 0 && j < kExcCode) ? static_cast<uint32_t>(j) : kExcCode;
 }
 
+__device__ __forceinline__ uint32_t code_of(uint32_t c, uint32_t code, const uint32_t* __restrict__ exc_src,
+                                           const double* __restrict__ exc_R,
+                                           const double* __restrict__ prev,
+                                           const double* __restrict__ inv, uint32_t& any) {
+  if (code < kExcCode) return code;
+  // rare: exception edge or y >= 2^-21: the exact factor's code
+  double f;
+  if (c & kExcFlag) {
+    const uint32_t x = c & ~kExcFlag;
+    f = __dsub_rn(1.0, __dmul_rn(prev[exc_src[x]], exc_R[x]));  // metrics.cpp:166
+  } else {
+    f = __dsub_rn(1.0, __dmul_rn(prev[c], inv[c]));  // y = P(s) * (1/row_sum(s))
+  }
+  const uint32_t j = factor_to_code(f);
+  any |= j == kExcCode;
+  return j;
+}
+
+// Each thread owns groups of 4 consecutive entries: 16-byte column loads and
+// code stores (a quarter of the memory instructions of 4-byte ones); the
+// region's unaligned head and tail go element by element.
 __global__ void __launch_bounds__(256)
     k_codes(uint64_t e0, uint64_t e1, const uint32_t* __restrict__ ncol, const uint32_t* __restrict__ kprev,
             const uint32_t* __restrict__ exc_src, const double* __restrict__ exc_R,
             const double* __restrict__ prev, const double* __restrict__ inv,
             uint32_t* __restrict__ ncode, uint32_t* __restrict__ marked) {
   const uint64_t pol = policy_evict_first();
-  constexpr uint64_t kChunk = 256ull * kCodesPerThread;
   uint32_t any = 0;
-  for (uint64_t c0 = e0 + (uint64_t)blockIdx.x * kChunk; c0 < e1; c0 += (uint64_t)gridDim.x * kChunk) {
-    uint32_t c[kCodesPerThread], code[kCodesPerThread];
-#pragma unroll
-    for (int u = 0; u < kCodesPerThread; ++u) {
-      const uint64_t i = c0 + u * 256 + threadIdx.x;
-      c[u] = i < e1 ? ld_stream(ncol + i, pol) : kExcFlag;
+  const uint64_t a0 = (e0 + 3) & ~3ull, a1 = e1 & ~3ull;  // 16-byte aligned body [a0, a1)
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (a0 >= a1) {  // tiny region: element by element
+    for (uint64_t i = e0 + tid; i < e1; i += (uint64_t)gridDim.x * blockDim.x) {
+      const uint32_t c = ncol[i];
+      ncode[i] = code_of(c, (c & kExcFlag) ? kExcCode : __ldg(kprev + c), exc_src, exc_R, prev, inv, any);
     }
+  } else {
+    if (tid < a0 - e0) {
+      const uint64_t i = e0 + tid;
+      const uint32_t c = ncol[i];
+      ncode[i] = code_of(c, (c & kExcFlag) ? kExcCode : __ldg(kprev + c), exc_src, exc_R, prev, inv, any);
+    }
+    if (tid < e1 - a1) {
+      const uint64_t i = a1 + tid;
+      const uint32_t c = ncol[i];
+      ncode[i] = code_of(c, (c & kExcFlag) ? kExcCode : __ldg(kprev + c), exc_src, exc_R, prev, inv, any);
+    }
+    const uint4* __restrict__ col4 = reinterpret_cast<const uint4*>(ncol + a0);
+    uint4* __restrict__ out4 = reinterpret_cast<uint4*>(ncode + a0);
+    const uint64_t g4 = (a1 - a0) / 4;
+    constexpr int kG = kCodesPerThread / 4;  // 4-entry groups per thread per step
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g0 = tid; g0 < g4; g0 += stride * kG) {
+      uint4 c[kG];
 #pragma unroll
-    for (int u = 0; u < kCodesPerThread; ++u)
-      code[u] = (c[u] & kExcFlag) ? kExcCode : __ldg(kprev + c[u]);
-#pragma unroll
-    for (int u = 0; u < kCodesPerThread; ++u) {
-      const uint64_t i = c0 + u * 256 + threadIdx.x;
-      if (i >= e1) continue;
-      if (code[u] >= kExcCode) {  // rare: exception edge or y >= 2^-21: the exact factor's code
-        double f;
-        if (c[u] & kExcFlag) {
-          const uint32_t x = c[u] & ~kExcFlag;
-          f = __dsub_rn(1.0, __dmul_rn(prev[exc_src[x]], exc_R[x]));  // metrics.cpp:166
+      for (int u = 0; u < kG; ++u) {
+        const uint64_t g = g0 + u * stride;
+        if (g < g4) {
+          asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                       : "=r"(c[u].x), "=r"(c[u].y), "=r"(c[u].z), "=r"(c[u].w)
+                       : "l"(col4 + g), "l"(pol));
         } else {
-          f = __dsub_rn(1.0, __dmul_rn(prev[c[u]], inv[c[u]]));  // y = P(s) * (1/row_sum(s))
+          c[u] = make_uint4(kExcFlag, kExcFlag, kExcFlag, kExcFlag);
         }
-        code[u] = factor_to_code(f);
-        any |= code[u] == kExcCode;
       }
-      st_stream(ncode + i, code[u], pol);
+      uint4 k[kG];
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        k[u].x = (c[u].x & kExcFlag) ? kExcCode : __ldg(kprev + c[u].x);
+        k[u].y = (c[u].y & kExcFlag) ? kExcCode : __ldg(kprev + c[u].y);
+        k[u].z = (c[u].z & kExcFlag) ? kExcCode : __ldg(kprev + c[u].z);
+        k[u].w = (c[u].w & kExcFlag) ? kExcCode : __ldg(kprev + c[u].w);
+      }
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        const uint64_t g = g0 + u * stride;
+        if (g >= g4) continue;
+        uint4 o;
+        o.x = code_of(c[u].x, k[u].x, exc_src, exc_R, prev, inv, any);
+        o.y = code_of(c[u].y, k[u].y, exc_src, exc_R, prev, inv, any);
+        o.z = code_of(c[u].z, k[u].z, exc_src, exc_R, prev, inv, any);
+        o.w = code_of(c[u].w, k[u].w, exc_src, exc_R, prev, inv, any);
+        asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(out4 + g), "r"(o.x),
+                     "r"(o.y), "r"(o.z), "r"(o.w), "l"(pol)
+                     : "memory");
+      }
     }
   }
   if (__any_sync(kFull, any) && (threadIdx.x & 31) == 0) atomicOr(marked, 1u);
