@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 // from nm_col (rare).
 constexpr uint32_t kExcCode = 0xFFFFFFFEu;  // nm_code marker: exception edge
 
-constexpr int kCodesPerThread = 8;
+constexpr int kCodesPerThread = 16;
 
 // A factor f in (1/2, 1] is 1 - J 2^-53 for the integer J = bits(1.0) -
 // bits(f): the code whose code_to_factor is f bit for bit. Factors outside
