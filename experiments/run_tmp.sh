@@ -1,5 +1,5 @@
 OUT=gpurun_out
-cp experiments/libs/libqvb_c32.so paper_2305_10863_b200/libqvb.so
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:"k_codes" --log-file $OUT/kc_32.csv python experiments/ap_bench.py C4 > /dev/null 2>&1
-cp experiments/libs/libqvb_c16.so paper_2305_10863_b200/libqvb.so
-for mb in 56 64 72 80; do echo "SEG_MB=$mb" >> $OUT/ap5.log; QVB_SEG_MB=$mb timeout 300 python experiments/ap_bench.py C4 >> $OUT/ap5.log 2>&1; done
+timeout 900 python -m pytest tests/test_access_prob_gpu.py tests/test_cpp_dropin_gpu.py -q -x > $OUT/t1.log 2>&1; tail -3 $OUT/t1.log
+for c in C2 C4; do timeout 300 python experiments/ap_bench.py $c >> $OUT/ap4.log 2>&1; done
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,smsp__inst_executed.sum --clock-control none --csv -k regex:"k_first|k_codes|k_products" --log-file $OUT/c4_gp.csv python experiments/ap_bench.py C4 > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:"k_first" --log-file $OUT/c2_gp.csv python experiments/ap_bench.py C2 > /dev/null 2>&1

@@ -449,51 +449,49 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 
 // One slice's ordered product over its lane-major class stream, exception
 // classes contributing the NaN sentinel.
+// One slice's ordered product over its class stream (lane-major quads: the
+// lane's 4 steps in one 8-byte load), exception classes contributing the NaN
+// sentinel. len is a multiple of 4 (padding: class ncls, factor 1.0).
 __device__ __forceinline__ double slice_product(uint32_t len, const uint16_t* __restrict__ cp,
                                                 uint32_t tab, uint32_t ncls, uint64_t pol) {
   double miss = 1.0;  // metrics.cpp:152
-  uint32_t k = 0;
-  for (; k + kU <= len; k += kU) {
+  for (uint32_t k = 0; k < len; k += kU) {
     uint32_t c[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) c[u] = ld_stream(cp + (uint64_t)(k + u) * 32, pol);
+    for (int q = 0; q < kU / 4; ++q) {
+      uint64_t w = 0;
+      if (k + 4 * q < len) w = ld_stream(reinterpret_cast<const uint64_t*>(cp + (uint64_t)((k >> 2) + q) * 128), pol);
+      else w = 0x0001000100010001ull * ncls;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) c[4 * q + r] = static_cast<uint32_t>(w >> (16 * r)) & 0xFFFFu;
+    }
     double f[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) f[u] = lds_f64(tab + c[u] * 8);
 #pragma unroll
     for (int u = 0; u < kU; ++u) miss = __dmul_rn(miss, f[u]);
   }
-  if (k < len) {
-    uint32_t c[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u)
-      c[u] = k + u < len ? ld_stream(cp + (uint64_t)(k + u) * 32, pol) : ncls;
-    double f[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) f[u] = lds_f64(tab + c[u] * 8);
-#pragma unroll
-    for (int u = 0; u < kU; ++u) miss = __dmul_rn(miss, f[u]);  // ncls: exactly 1.0
-  }
   return miss;
 }
 
 // The slice again, element by element, exceptions with their R (rare).
-__device__ __noinline__ double slice_product_exc(uint32_t len, const uint16_t* __restrict__ gc,
-                                                 uint64_t at0, uint32_t tab, uint32_t ncls,
+__device__ __noinline__ double slice_product_exc(uint32_t len, const uint16_t* __restrict__ cp,
+                                                 uint64_t b0, uint32_t lane, uint32_t tab, uint32_t ncls,
                                                  const uint64_t* __restrict__ xslot,
                                                  const double* __restrict__ xR, uint64_t nx,
                                                  double base) {
   double miss = 1.0;
   for (uint32_t k = 0; k < len; ++k) {
-    const uint32_t c = gc[(uint64_t)k * 32];
-    const double f = c == ncls + 1 ? exc_first(at0 + (uint64_t)k * 32, xslot, xR, nx, base) : lds_f64(tab + c * 8);
+    const uint64_t at = f1_slot(b0, k, lane);
+    const uint32_t c = cp[at];
+    const double f = c == ncls + 1 ? exc_first(at, xslot, xR, nx, base) : lds_f64(tab + c * 8);
     miss = __dmul_rn(miss, f);
   }
   return miss;
 }
 
 // Regular rows: persistent warps, one slice of 32 nodes at a time, lane =
-// node, lane-major classes (one coalesced 64-byte line per step). For graphs
+// node, lane-major quads of classes (one coalesced 256-byte load per 4 steps). For graphs
 // whose per-node outputs exceed half the L2, the slices are built without
 // in-degree sorting across slices (graph.cu build_first, window 32), so a
 // warp's stores of P / y / code cover its own 32 consecutive nodes and stay
@@ -515,8 +513,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     const uint32_t v = perm[sl * 32 + lane] & kNodeMask;
     const uint64_t b0 = sptr[sl];
     const uint32_t len = static_cast<uint32_t>((sptr[sl + 1] - b0) >> 5);
-    double miss = slice_product(len, cls + b0 + lane, tab, ncls, pol);
-    if (miss != miss) miss = slice_product_exc(len, cls + b0 + lane, b0 + lane, tab, ncls, xslot, xR, nx, base);
+    double miss = slice_product(len, cls + b0 + lane * 4, tab, ncls, pol);
+    if (miss != miss)  // an exception edge in the slice
+      miss = slice_product_exc(len, cls, b0, lane, tab, ncls, xslot, xR, nx, base);
     if (v != kNoNode) finish_first(v, miss, base, inv, out, yout, kout, 0);
   }
 }

@@ -342,13 +342,14 @@ __global__ void __launch_bounds__(W)
 }
 
 __global__ void k_slot_lens(const uint32_t* __restrict__ slot_pair, const uint32_t* __restrict__ pdeg,
-                            uint64_t nslices, uint32_t* __restrict__ len32) {
+                            uint64_t nslices, uint32_t* __restrict__ len32, uint32_t quantum = 1) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= nslices;
        j += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t len = 0;
     if (j < nslices) {
       const uint32_t i = slot_pair[j * 32];  // first slot holds the slice maximum
       len = i == 0xFFFFFFFFu ? 0u : pdeg[i];
+      len = (len + quantum - 1) / quantum * quantum;
     }
     len32[j] = 32u * len;
   }
@@ -581,7 +582,8 @@ __global__ void k_cls_assign(const uint64_t* __restrict__ skeys, const uint32_t*
   }
 }
 
-// k_fill_slots for the class stream: exceptions get class ncls+1 and are appended
+// k_fill_slots for the class stream (lane-major quads, f1_slot): exceptions
+// get class ncls+1 and are appended
 // (slot, exception index) for a later sort by slot.
 __global__ void k_fill_cls(const uint32_t* __restrict__ slot_pair, const uint32_t* __restrict__ pv,
                            const uint64_t* __restrict__ pstart, const uint32_t* __restrict__ pdeg,
@@ -607,7 +609,7 @@ __global__ void k_fill_cls(const uint32_t* __restrict__ slot_pair, const uint32_
       perm[p] = kNoNode;
     }
     for (uint64_t k = 0; k < len; ++k) {
-      const uint64_t at = base + k * 32 + lane;
+      const uint64_t at = f1_slot(base, k, lane);
       uint16_t c = pad;
       if (k < deg) {
         const uint32_t x = col[r0 + k];
@@ -934,7 +936,8 @@ void build_first(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const 
   iota.release();
   DevBuf<uint32_t> len32(S + 1, s);
   DevBuf<uint64_t> sptr(S + 1, s);
-  k_slot_lens<<<grid_for(S + 1, kBlock), kBlock, 0, s>>>(slot_pair.p, pdeg.p, S, len32.p);
+  // slices padded to a multiple of 4 steps: lane-major quads (graph.cuh)
+  k_slot_lens<<<grid_for(S + 1, kBlock), kBlock, 0, s>>>(slot_pair.p, pdeg.p, S, len32.p, 4);
   QVB_LAUNCH_CHECK();
   exclusive_sum_u32_u64(len32.p, sptr.p, S + 1, s);
   len32.release();

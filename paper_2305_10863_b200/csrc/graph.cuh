@@ -55,8 +55,8 @@
 // of gathering: factor = table[class], the table holding
 // 1 - (1/N) * inv(class) in shared memory. It is a one-pass sliced layout
 // (windows of 256 nodes — 32 for large graphs — sorted by in-degree, slices
-// of 32, lane-major), built over every regular row whatever the segmentation
-// of later sweeps:
+// of 32 padded to a multiple of 4 steps, lane-major quads: f1_slot), built
+// over every regular row whatever the segmentation of later sweeps:
 //   f1_perm u32[S*32], f1_sptr u64[S+1], f1_cls u16[...]
 // Class ncls is padding (factor exactly 1.0). Exception edges
 // (R != 1/row_sum) carry class ncls+1, whose table entry is a NaN sentinel:
@@ -156,6 +156,12 @@ constexpr uint32_t kBigCode = 0xFFFFFFFFu;  // kcode: gather y instead
 constexpr uint8_t kNmFirst = 0x40, kNmLast = 0x80, kNmLen = 0x3F;
 constexpr uint64_t kMaxEdges = 0xFFFFFFFFull;
 constexpr uint32_t kMaxCls = 12288;   // shared-memory table of ncls+2 doubles
+// f1 slot of step k of the lane's node in the slice starting at `base`:
+// lane-major quads, so a lane reads 4 consecutive steps with one 8-byte load
+// and a warp's 32 loads cover 256 contiguous bytes
+__host__ __device__ __forceinline__ uint64_t f1_slot(uint64_t base, uint64_t k, uint64_t lane) {
+  return base + (k >> 2) * 128 + lane * 4 + (k & 3);
+}
 
 // Builds the in-CSR from a device out-CSR. d_w == nullptr means unit weights.
 // d_src (nullable): source of every out-CSR edge if already known.
