@@ -478,8 +478,10 @@ T* persist(DevBuf<T>& b) {
 // flagged with the first and last pass that touch it. Long rows (> thr) stay
 // 0 everywhere (long path); in-degree-0 nodes finish in pass 0.
 __global__ void k_nm_lens(const uint64_t* __restrict__ uptr, const uint32_t* __restrict__ src,
-                          uint64_t n, uint64_t npad, uint32_t thr, uint64_t seg,
+                          uint64_t n, uint64_t npad, uint32_t thr, uint64_t seg0, uint64_t seg,
                           uint8_t* __restrict__ lenf) {
+  // source segment: [0, seg0), then every seg sources
+  auto segment = [&](uint64_t x) -> uint64_t { return x < seg0 ? 0 : 1 + (x - seg0) / seg; };
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
        v += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t a = uptr[v], b = uptr[v + 1];
@@ -491,9 +493,9 @@ __global__ void k_nm_lens(const uint64_t* __restrict__ uptr, const uint32_t* __r
     bool first = true;
     uint64_t u = a;
     while (u < b) {
-      const uint64_t k = src[u] / seg;
+      const uint64_t k = segment(src[u]);
       uint32_t cnt = 0;
-      while (u < b && src[u] / seg == k) {
+      while (u < b && segment(src[u]) == k) {
         ++u;
         ++cnt;
       }
@@ -808,13 +810,19 @@ void build_nm(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const uin
   if (!R && !std::getenv("QVB_SEG_MB") && !std::getenv("QVB_SEG_SOURCES")) seg = (64ull << 20) / 4;
   seg = std::min<uint64_t>(n, seg);
   g.seg_size = seg;
-  const int nseg = static_cast<int>((n + seg - 1) / seg);
+  // the first segment may be wider (QVB_SEG0_MB of codes): its sources are
+  // the hottest, so its gathers keep hitting L2 over a larger range
+  uint64_t seg0 = seg;
+  if (const char* m = std::getenv("QVB_SEG0_MB")) seg0 = std::max<uint64_t>(1, (std::strtoull(m, nullptr, 10) << 20) / 4);
+  seg0 = std::min<uint64_t>(n, std::max<uint64_t>(seg0, 1));
+  g.seg0_size = seg0;
+  const int nseg = n <= seg0 ? 1 : 1 + static_cast<int>((n - seg0 + seg - 1) / seg);
   if (nseg > 255) fail(QVB_ERR_UNSUPPORTED, "too many source segments (raise QVB_SEG_MB)");
   g.seg_slice.assign(nseg + 1, 0);
   const uint64_t S = (n + 31) / 32, npad = S * 32;
   DevBuf<uint8_t> lenf(npad * nseg, s);
   QVB_CUDA(cudaMemsetAsync(lenf.p, 0, npad * nseg, s));
-  k_nm_lens<<<grid_for(n, kBlock), kBlock, 0, s>>>(uptr, src, n, npad, thr, seg, lenf.p);
+  k_nm_lens<<<grid_for(n, kBlock), kBlock, 0, s>>>(uptr, src, n, npad, thr, seg0, seg, lenf.p);
   QVB_LAUNCH_CHECK();
   DevBuf<uint32_t> cnt(S * nseg + 1, s);
   DevBuf<uint64_t> sbase(S * nseg + 3, s);  // +2: 16-byte bulk-copy windows

@@ -82,6 +82,7 @@ struct qvb_graph {
   // source segments: sweep pass k multiplies the factors whose source lies
   // in [k*seg_size, (k+1)*seg_size); its slices are seg_slice[k]..seg_slice[k+1]
   uint64_t seg_size = 0;
+  uint64_t seg0_size = 0;  // node-major layout: sources of the first segment
   std::vector<uint64_t> seg_slice;  // host, nseg + 1
   double* state = nullptr;          // running products between passes (nseg > 1)
   uint64_t pairs = 0;               // (node, segment) pairs with slots
