@@ -395,9 +395,14 @@ def run_ours(args):
             "host_fraction": args.host_frac,
             "fractions": {"local": f_l, "peer": f_p, "host": f_h},
             "placement_s": plan_s,
-            "l2": "inputs larger than L2 (feature table %.0f MB, %.0f MB of rows per step)" % (
-                n * row_bytes / 1e6, B * row_bytes / 1e6),
+            "l2": "inputs larger than L2 (feature table %.0f MB, %.0f MB of rows per step); rows and "
+                  "outputs stream with L2 evict_first, the %.0f MB lookup table is%s kept with evict_last" % (
+                n * row_bytes / 1e6, B * row_bytes / 1e6, n * 8 / 1e6, "" if n * 8 <= (32 << 20) else " not"),
             "parallelism": f"feature-partitioned x{world}, one process per GPU",
+            **({"shared_gpu": "QVB_SHARE_GPU=1: every rank on one GPU to exercise the multi-rank "
+                              "path (IPC peers, setup collectives); the ranks time-slice the GPU, "
+                              "so these timings are not a performance measurement"}
+               if D.shared_gpu() and world > 1 else {}),
         },
         "roofline": {"bound": bound, "kernel": "k_gather_rows", "achieved": achieved,
                      "peak": link_peak, "unit": "GB/s", "frac": achieved / link_peak,
