@@ -498,7 +498,7 @@ __device__ __noinline__ double slice_product_exc(uint32_t len, const uint16_t* _
 // whole sectors; small graphs sort windows of 256 (less padding) and their
 // scattered stores merge in L2.
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    k_first(uint64_t S, double base, uint32_t ncls, const double* __restrict__ cls_inv,
+    k_first(uint64_t S, uint64_t n, double base, uint32_t ncls, const double* __restrict__ cls_inv,
                   const uint32_t* __restrict__ perm, const uint64_t* __restrict__ sptr,
                   const uint16_t* __restrict__ cls, const uint64_t* __restrict__ xslot,
                   const double* __restrict__ xR, uint64_t nx, const double* __restrict__ inv,
@@ -510,7 +510,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   const uint64_t pol = policy_evict_first();
   const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
   for (uint64_t sl = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); sl < S; sl += warps) {
-    const uint32_t v = perm[sl * 32 + lane] & kNodeMask;
+    // node order (f1_ident): the slot names the node, no perm word to read
+    const uint32_t v = perm ? (perm[sl * 32 + lane] & kNodeMask)
+                            : (sl * 32 + lane < n ? static_cast<uint32_t>(sl * 32 + lane) : kNoNode);
     const uint64_t b0 = sptr[sl];
     const uint32_t len = static_cast<uint32_t>((sptr[sl + 1] - b0) >> 5);
     double miss = slice_product(len, cls + b0 + lane * 4, tab, ncls, pol);
@@ -900,7 +902,8 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, dou
                                     (g.f1_S + kWarpsPerBlock - 1) / kWarpsPerBlock);
         }
         const unsigned grid = g.f1_grid;
-        k_first<<<grid, kWarpsPerBlock * 32, smem, s>>>(g.f1_S, base, g.ncls, g.cls_inv, g.f1_perm,
+        k_first<<<grid, kWarpsPerBlock * 32, smem, s>>>(g.f1_S, n, base, g.ncls, g.cls_inv,
+                                                        g.f1_ident ? nullptr : g.f1_perm,
                                                         g.f1_sptr, g.f1_cls, g.f1_xslot, g.f1_xR,
                                                         g.f1_nx, g.inv, pout, yout, kout);
         QVB_LAUNCH_CHECK();

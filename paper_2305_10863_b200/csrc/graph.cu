@@ -342,13 +342,20 @@ __global__ void __launch_bounds__(W)
 }
 
 __global__ void k_slot_lens(const uint32_t* __restrict__ slot_pair, const uint32_t* __restrict__ pdeg,
-                            uint64_t nslices, uint32_t* __restrict__ len32, uint32_t quantum = 1) {
+                            uint64_t nslices, uint32_t* __restrict__ len32, uint32_t quantum = 1,
+                            bool sorted = true) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= nslices;
        j += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t len = 0;
     if (j < nslices) {
       const uint32_t i = slot_pair[j * 32];  // first slot holds the slice maximum
-      len = i == 0xFFFFFFFFu ? 0u : pdeg[i];
+        len = i == 0xFFFFFFFFu ? 0u : pdeg[i];
+      if (!sorted) {  // unsorted slices: the longest of the 32 rows
+        for (int l = 1; l < 32; ++l) {
+          const uint32_t il = slot_pair[j * 32 + l];
+          if (il != 0xFFFFFFFFu && pdeg[il] > len) len = pdeg[il];
+        }
+      }
       len = (len + quantum - 1) / quantum * quantum;
     }
     len32[j] = 32u * len;
@@ -926,7 +933,13 @@ void build_first(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const 
     QVB_CUDA(cudaStreamSynchronize(s));
   }
   DevBuf<uint32_t> slot_pair(S * 32 ? S * 32 : 1, s);
-  if (groups)
+  // windows of 32 are single slices: sorting them cannot pad less, so their
+  // nodes keep node order (k_first then derives the node from the slot)
+  const bool ident = W == 32;
+  if (groups && ident) {
+    QVB_CUDA(cudaMemsetAsync(slot_pair.p, 0xFF, S * 32 * sizeof(uint32_t), s));
+    QVB_CUDA(cudaMemcpyAsync(slot_pair.p, iota.p, H * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+  } else if (groups)
     switch (W) {
       case 32:
         k_group_sort<32><<<static_cast<unsigned>(groups), 32, 0, s>>>(iota.p, spb.p, sgb.p, 1, pv.p, pdeg.p, slot_pair.p);
@@ -945,7 +958,7 @@ void build_first(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const 
   DevBuf<uint32_t> len32(S + 1, s);
   DevBuf<uint64_t> sptr(S + 1, s);
   // slices padded to a multiple of 4 steps: lane-major quads (graph.cuh)
-  k_slot_lens<<<grid_for(S + 1, kBlock), kBlock, 0, s>>>(slot_pair.p, pdeg.p, S, len32.p, 4);
+  k_slot_lens<<<grid_for(S + 1, kBlock), kBlock, 0, s>>>(slot_pair.p, pdeg.p, S, len32.p, 4, !ident);
   QVB_LAUNCH_CHECK();
   exclusive_sum_u32_u64(len32.p, sptr.p, S + 1, s);
   len32.release();
@@ -986,6 +999,7 @@ void build_first(qvb_graph& g, const uint64_t* uptr, const uint32_t* col, const 
   }
   g.f1_S = S;
   g.f1_slots = slots;
+  g.f1_ident = ident && g.nlong == 0;  // slot (s, l) is node 32 s + l
   g.f1_perm = persist(perm);
   g.f1_sptr = persist(sptr);
   g.f1_cls = persist(scls);

@@ -121,6 +121,7 @@ struct qvb_graph {
   double* cls_inv = nullptr;    // [ncls] 1/row_sum of each class
   uint64_t f1_S = 0;            // slices of the one-pass sliced layout
   uint64_t f1_slots = 0;        // f1_sptr[f1_S]
+  bool f1_ident = false;        // unsorted slices and no long rows: slot (s, l) is node 32 s + l
   uint32_t* f1_perm = nullptr;  // node of each slot (kNoNode: padding)
   uint64_t* f1_sptr = nullptr;  // slice starts (elements)
   uint16_t* f1_cls = nullptr;   // class per slot, lane-major; ncls: pad, ncls+1: exception

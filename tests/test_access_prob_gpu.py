@@ -220,7 +220,7 @@ def test_c4_segmented_equals_single_pass(qvb, monkeypatch):
     assert (p_one >= p2).all() and (p2 >= 1.0 / c["n"]).all() and (p_one <= 1.0).all()
 
 
-@pytest.mark.parametrize("first", ["classes", "gather"])
+@pytest.mark.parametrize("first", ["classes", "gather", "classes-w32"])
 def test_first_sweep_paths_bit_exact(qvb, oracle, first, monkeypatch):
     """The first sweep streams 2-byte out-degree classes (P(s,1) is uniform,
     so a factor depends on its source only through 1/row_sum); QVB_FIRST=gather
@@ -229,13 +229,15 @@ def test_first_sweep_paths_bit_exact(qvb, oracle, first, monkeypatch):
     weight array, and C1 (uniform / transposed)."""
     if first == "gather":
         monkeypatch.setenv("QVB_FIRST", "gather")
+    if first == "classes-w32":  # unsorted slices of 32 in node order (the large-graph layout)
+        monkeypatch.setenv("QVB_F1_WINDOW", "32")
     rng = derive_stream(61, 1)
     for trial in range(30):
         n, s, d, w = random_edges(rng, 60, 300, False)
         ro, col, ww = _csr(oracle, n, s, d, w)
         g = qvb.DeviceGraph.upload(ro, col, None if trial % 2 else ww)
         info = g.info()
-        assert (info.classes > 0) == (first == "classes" and info.layout == 0)
+        assert (info.classes > 0) == (first != "gather" and info.layout == 0)
         for layers in (2, 3):
             assert (bits(g.access_prob(layers)) == bits(oracle.access_prob(ro, col, ww, layers))).all()
         g.close()
