@@ -1,2 +1,3 @@
 OUT=gpurun_out
-timeout 900 python bench.py --config C4 --no-cpu-baseline --no-e2e --steps 20 --sample-seeds 0 > $OUT/b4.json 2> $OUT/b4.err
+timeout 1800 python -m pytest tests -q -m gpu > $OUT/tall.log 2>&1; tail -2 $OUT/tall.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; tail -2 $OUT/smoke.log
