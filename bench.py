@@ -47,7 +47,7 @@ CONFIGS = {
 }
 META_BYTES = 24  # 8 B id + 16 B reference-layout lookup row per request
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
-PCIE_GBS = 64.0  # PCIe Gen5 x16 per direction, nominal
+PCIE_GBS = 51.4  # measured: random 512-byte row reads of pinned host memory (profiles/r01k_host_tier.txt)
 
 
 def peaks():
@@ -329,7 +329,7 @@ def run_ours(args):
     hbm_per_id = META_BYTES + row_bytes * (1 + f_l + f_p)
     links = {"hbm": (B * hbm_per_id, pk["hbm_gbs"], pk["source"]),
              "nvlink": (B * row_bytes * f_p, NVLINK_GBS, "measured peer copy (B200_PROFILING.md)"),
-             "pcie": (B * row_bytes * f_h, PCIE_GBS, "nominal Gen5 x16")}
+             "pcie": (B * row_bytes * f_h, PCIE_GBS, "measured random-row PCIe reads, experiments/host_tier.cu")}
     bound = max(links, key=lambda k: links[k][0] / links[k][1])
     alg, link_peak, link_src = links[bound]
     achieved = alg / (per_launch_ms / 1e3) / 1e9

@@ -57,6 +57,12 @@ __device__ __forceinline__ double code_to_factor(uint32_t J) {
   return f;
 }
 
+// The same factor from its low word L = -J mod 2^32 (the form k_codes
+// stores): J in [1, 2^32) has high word 0x3FEFFFFF, J = 0 is 1.0 exactly.
+__device__ __forceinline__ double low_to_factor(uint32_t L) {
+  return __hiloint2double(L ? 0x3FEFFFFF : 0x3FF00000, static_cast<int>(L));
+}
+
 // Inclusive warp scan of x: shfl.up's validity predicate guards the add
 // (two instructions a step instead of shuffle + lane test + select + add).
 template <int O>
@@ -589,7 +595,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 // (metrics.cpp:152-168) with the running product in a register across
 // passes. Exception and big-code entries carry marker codes and are resolved
 // from nm_col (rare).
-constexpr uint32_t kExcCode = 0xFFFFFFFEu;  // nm_code marker: exception edge
+constexpr uint32_t kExcCode = 0xFFFFFFFEu;  // code marker: exception edge
+// nm_code holds each factor's low word L = -J (low_to_factor): one compare and
+// select rebuild the factor. The marker's low word is 2 (-kExcCode); no code
+// below kExcCode maps there.
+constexpr uint32_t kExcLow = 0u - kExcCode;
 
 constexpr int kCodesPerThread = 16;
 
@@ -634,18 +644,18 @@ __global__ void __launch_bounds__(256)
   if (a0 >= a1) {  // tiny region: element by element
     for (uint64_t i = e0 + tid; i < e1; i += (uint64_t)gridDim.x * blockDim.x) {
       const uint32_t c = ncol[i];
-      ncode[i] = code_of(c, (c & kExcFlag) ? kExcCode : __ldg(kprev + c), exc_src, exc_R, prev, inv, any);
+      ncode[i] = 0u - code_of(c, (c & kExcFlag) ? kExcCode : __ldg(kprev + c), exc_src, exc_R, prev, inv, any);
     }
   } else {
     if (tid < a0 - e0) {
       const uint64_t i = e0 + tid;
       const uint32_t c = ncol[i];
-      ncode[i] = code_of(c, (c & kExcFlag) ? kExcCode : __ldg(kprev + c), exc_src, exc_R, prev, inv, any);
+      ncode[i] = 0u - code_of(c, (c & kExcFlag) ? kExcCode : __ldg(kprev + c), exc_src, exc_R, prev, inv, any);
     }
     if (tid < e1 - a1) {
       const uint64_t i = a1 + tid;
       const uint32_t c = ncol[i];
-      ncode[i] = code_of(c, (c & kExcFlag) ? kExcCode : __ldg(kprev + c), exc_src, exc_R, prev, inv, any);
+      ncode[i] = 0u - code_of(c, (c & kExcFlag) ? kExcCode : __ldg(kprev + c), exc_src, exc_R, prev, inv, any);
     }
     const uint4* __restrict__ col4 = reinterpret_cast<const uint4*>(ncol + a0);
     uint4* __restrict__ out4 = reinterpret_cast<uint4*>(ncode + a0);
@@ -678,10 +688,10 @@ __global__ void __launch_bounds__(256)
         const uint64_t g = g0 + u * stride;
         if (g >= g4) continue;
         uint4 o;
-        o.x = code_of(c[u].x, k[u].x, exc_src, exc_R, prev, inv, any);
-        o.y = code_of(c[u].y, k[u].y, exc_src, exc_R, prev, inv, any);
-        o.z = code_of(c[u].z, k[u].z, exc_src, exc_R, prev, inv, any);
-        o.w = code_of(c[u].w, k[u].w, exc_src, exc_R, prev, inv, any);
+        o.x = 0u - code_of(c[u].x, k[u].x, exc_src, exc_R, prev, inv, any);
+        o.y = 0u - code_of(c[u].y, k[u].y, exc_src, exc_R, prev, inv, any);
+        o.z = 0u - code_of(c[u].z, k[u].z, exc_src, exc_R, prev, inv, any);
+        o.w = 0u - code_of(c[u].w, k[u].w, exc_src, exc_R, prev, inv, any);
         asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(out4 + g), "r"(o.x),
                      "r"(o.y), "r"(o.z), "r"(o.w), "l"(pol)
                      : "memory");
@@ -691,7 +701,7 @@ __global__ void __launch_bounds__(256)
   if (__any_sync(kFull, any) && (threadIdx.x & 31) == 0) atomicOr(marked, 1u);
 }
 
-__device__ __noinline__ double marker_factor(uint32_t code, uint32_t c, const uint32_t* __restrict__ exc_src,
+__device__ __noinline__ double marker_factor(uint32_t c, const uint32_t* __restrict__ exc_src,
                                              const double* __restrict__ exc_R,
                                              const double* __restrict__ prev,
                                              const double* __restrict__ inv) {
@@ -724,9 +734,9 @@ __device__ __noinline__ double products_markers(int K, uint64_t S, uint64_t sl, 
     }
     const uint64_t q = sbase[(uint64_t)k * S + sl] + (incl - len);
     for (uint32_t t = 0; t < len; ++t) {
-      const uint32_t code = ncode[q + t];
-      miss = __dmul_rn(miss, code < kExcCode ? code_to_factor(code)
-                                            : marker_factor(code, ncol[q + t], exc_src, exc_R, prev, inv));
+      const uint32_t low = ncode[q + t];
+      miss = __dmul_rn(miss, low != kExcLow ? low_to_factor(low)
+                                            : marker_factor(ncol[q + t], exc_src, exc_R, prev, inv));
     }
   }
   return miss;
@@ -773,12 +783,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
     const uint32_t incl = warp_incl_scan(len);
     const uint32_t* __restrict__ cp = ncode + sb + (incl - len);
     for (uint32_t t = 0; t < maxlen; t += 4) {
+      const int rem = static_cast<int>(len - t);  // this lane's entries left in the run
       uint32_t code[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) code[u] = __ldg(cp + t + u);  // ncode is padded past its end
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        miss = __dmul_rn(miss, code_to_factor(t + u < len ? code[u] : 0u));  // past the run: 1.0
+        miss = __dmul_rn(miss, low_to_factor(u < rem ? code[u] : 0u));  // past the run: 1.0
     }
   }
   if (*marked)  // uniform and rare: redo with the marker codes resolved

@@ -24,9 +24,14 @@ def plan(qvb, n, gpus=1, cap=None, rep=0, host=None):
     return t, lo, ids
 
 
+@pytest.mark.parametrize("kernel", ["flat", "rows"])
 @pytest.mark.parametrize("dim", [128, 100, 602, 3, 1, 33])
-def test_local_gather_bit_exact(qvb, oracle, dim):
+def test_local_gather_bit_exact(qvb, oracle, dim, kernel, monkeypatch):
+    """Both batch-size paths: the flat (request, chunk) kernel small batches
+    take, and the row-group kernels (forced with QVB_GATHER_SMALL=0)."""
     import torch
+
+    monkeypatch.setenv("QVB_GATHER_SMALL", "0" if kernel == "rows" else "1000000")
 
     n = 5000
     t, lo, ids = plan(qvb, n)
@@ -47,7 +52,9 @@ def test_local_gather_bit_exact(qvb, oracle, dim):
     st.close()
 
 
-def test_host_tier_zero_copy(qvb, oracle):
+@pytest.mark.parametrize("kernel", ["flat", "rows"])
+def test_host_tier_zero_copy(qvb, oracle, kernel, monkeypatch):
+    monkeypatch.setenv("QVB_GATHER_SMALL", "0" if kernel == "rows" else "1000000")
     n, dim = 20000, 128
     t, lo, ids = plan(qvb, n, cap=n // 4, host=n)
     st = qvb.FeatureStore(lo, ids, dim, t, reader=0)
