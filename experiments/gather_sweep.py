@@ -11,7 +11,10 @@ Python-loop time per call is reported beside it), payload GB/s, and the fraction
 mixed HBM / PCIe roofline bench.py uses (24 B metadata + 2 row moves per
 device row; host rows bounded by PCIe). One JSON object per cell on stdout.
 
-  python experiments/gather_sweep.py [C2|C4]
+  python experiments/gather_sweep.py [C2|C3|C4] [planned]
+
+`planned` times qvb_gather_planned instead (requests bucketed by location
+and sorted by shard offset before the copy, the K4 order).
 """
 import json
 import os
@@ -28,6 +31,7 @@ from paper_2305_10863_b200 import qvb  # noqa: E402
 
 def main():
     cname = sys.argv[1] if len(sys.argv) > 1 else "C2"
+    planned = len(sys.argv) > 2 and sys.argv[2] == "planned"
     cfg = bench.CONFIGS[cname]
     n, e, dim, layers = cfg["n"], cfg["e"], cfg["dim"], cfg["layers"]
     rb = 4 * dim
@@ -63,12 +67,12 @@ def main():
         for sname, req in streams.items():
             for b in (1 << 10, 1 << 12, 1 << 14, 1 << 16, 1 << 18, 1 << 20):
                 for k in range(2):
-                    store.gather(req[k, :b], out[:b], stream=st)
+                    store.gather(req[k, :b], out[:b], stream=st, planned=planned)
                 torch.cuda.synchronize()
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
                 ev[0].record(st)
                 for k in range(reps):
-                    store.gather(req[k + 2, :b], out[:b], stream=st)
+                    store.gather(req[k + 2, :b], out[:b], stream=st, planned=planned)
                 ev[1].record(st)
                 ev[1].synchronize()
                 store.check_error()
@@ -81,7 +85,7 @@ def main():
                     cs = torch.cuda.Stream()
                     with torch.cuda.graph(cg, stream=cs):
                         for k in range(reps):
-                            store.gather(req[k + 2, :b], out[:b], stream=cs)
+                            store.gather(req[k + 2, :b], out[:b], stream=cs, planned=planned)
                     cg.replay()
                     torch.cuda.synchronize()
                     ev[0].record()
@@ -98,7 +102,7 @@ def main():
                 pcie = b * rb * f_h / bench.PCIE_GBS / 1e9
                 t_roof = max(hbm, pcie)
                 print(json.dumps({
-                    "config": cname, "host_fraction": h, "stream": sname, "batch": b,
+                    "config": cname, "planned": planned, "host_fraction": h, "stream": sname, "batch": b,
                     "host_rows": f_h, "us_per_launch": ms * 1e3, "us_per_call_python_loop": ms_loop * 1e3,
                     "payload_gbs": b * rb / (ms / 1e3) / 1e9,
                     "bound": "pcie" if pcie > hbm else "hbm",

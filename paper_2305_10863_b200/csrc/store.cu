@@ -469,12 +469,15 @@ __global__ void __launch_bounds__(256)
 }
 
 // Planned gather: sorted (location, offset) keys with the request index as
-// payload (K4 order); no lookup-table read in the copy loop.
-template <int VEC>
+// payload (K4 order); no lookup-table read in the copy loop. A key is
+// loc << ob | offset: the packed lookup entry (ob = 48), or its 32-bit
+// repacking when offsets and locations fit (fewer radix passes).
+template <int VEC, typename K>
 __global__ void __launch_bounds__(kGatherBlock)
-    k_gather_sorted(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ order,
+    k_gather_sorted(const K* __restrict__ keys, const uint32_t* __restrict__ order,
                     uint32_t rows, Bases bases, uint64_t stride, uint32_t cpr, uint32_t row_bytes,
-                    char* __restrict__ out) {
+                    char* __restrict__ out, int ob) {
+  const uint64_t omask = (1ull << ob) - 1;
   using V = Vec<VEC>;
   const uint64_t pol = policy_evict_first();  // rows: a stream
   const uint32_t total = rows * cpr;
@@ -492,13 +495,29 @@ __global__ void __launch_bounds__(kGatherBlock)
         const uint32_t k = c - j * cpr;
         const uint64_t e = __ldg(keys + j);
         const uint32_t i = __ldg(order + j);
-        v[u] = V::load(bases.p[e >> kOffsetBits] + (e & kOffsetMask) * stride + k * VEC, pol);
+        v[u] = V::load(bases.p[e >> ob] + (e & omask) * stride + k * VEC, pol);
         dst[u] = (uint64_t)i * row_bytes + (uint64_t)k * VEC;
       }
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
       if (ok[u]) V::store(out + dst[u], v[u], pol);
+  }
+}
+
+// 32-bit planned keys: loc << ob | offset, from the packed lookup entry.
+__global__ void k_plan_keys32(const uint64_t* __restrict__ ids, uint64_t b,
+                              const uint64_t* __restrict__ lut, uint64_t n, int ob,
+                              uint32_t* __restrict__ keys, uint32_t* __restrict__ idx,
+                              unsigned long long* err) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < b;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t f = ids[i];
+    uint64_t e = 0;
+    if (f >= n) atomicMin(err, (unsigned long long)i);
+    else e = lut[f];
+    keys[i] = static_cast<uint32_t>(((e >> kOffsetBits) << ob) | (e & kOffsetMask));
+    idx[i] = static_cast<uint32_t>(i);
   }
 }
 
@@ -750,14 +769,14 @@ struct qvb_store {
     QVB_LAUNCH_CHECK();
   }
 
-  template <int V>
-  void launch_sorted(const uint64_t* keys, const uint32_t* order, uint32_t rows, uint32_t cpr,
-                     char* o, cudaStream_t s) {
+  template <int V, typename K>
+  void launch_sorted(const K* keys, const uint32_t* order, uint32_t rows, uint32_t cpr, char* o,
+                     int ob, cudaStream_t s) {
     static unsigned full = 0;
-    if (!full) full = resident_grid(k_gather_sorted<V>, kGatherBlock, 0, ~0ull);
+    if (!full) full = resident_grid(k_gather_sorted<V, K>, kGatherBlock, 0, ~0ull);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(full, work_blocks((uint64_t)rows * cpr)));
-    k_gather_sorted<V><<<grid, kGatherBlock, 0, s>>>(keys, order, rows, bases, stride, cpr,
-                                                     row_bytes, o);
+    k_gather_sorted<V, K><<<grid, kGatherBlock, 0, s>>>(keys, order, rows, bases, stride, cpr,
+                                                        row_bytes, o, ob);
     QVB_LAUNCH_CHECK();
   }
 
@@ -767,16 +786,27 @@ struct qvb_store {
     const int V = vec();
     const uint32_t cpr = row_bytes / V;
     if ((uint64_t)b * cpr >= 0xFFFFFFFFull) fail(QVB_ERR_UNSUPPORTED, "planned batch too large");
-    DevBuf<uint64_t> keys(b, s), skeys(b, s);
     DevBuf<uint32_t> idx(b, s), order(b, s);
+    const int loc_bits = bits_for(static_cast<uint64_t>(nloc - 1));
+    const int ob = bits_for(n);  // every shard offset is below n
+    const uint32_t rows = static_cast<uint32_t>(b);
+    if (ob + loc_bits <= 32) {  // 32-bit keys: ob + loc_bits radix bits, half the key bytes
+      DevBuf<uint32_t> keys(b, s), skeys(b, s);
+      k_plan_keys32<<<grid_for(b, 256), 256, 0, s>>>(ids, b, lut, n, ob, keys.p, idx.p, err);
+      QVB_LAUNCH_CHECK();
+      sort_pairs_u32_u32(keys.p, skeys.p, idx.p, order.p, b, 0, ob + loc_bits, s);
+      if (V == 16) launch_sorted<16>(skeys.p, order.p, rows, cpr, out, ob, s);
+      else if (V == 8) launch_sorted<8>(skeys.p, order.p, rows, cpr, out, ob, s);
+      else launch_sorted<4>(skeys.p, order.p, rows, cpr, out, ob, s);
+      return;
+    }
+    DevBuf<uint64_t> keys(b, s), skeys(b, s);
     k_plan_keys_packed<<<grid_for(b, 256), 256, 0, s>>>(ids, b, lut, n, keys.p, idx.p, err);
     QVB_LAUNCH_CHECK();
-    const int loc_bits = bits_for(static_cast<uint64_t>(nloc - 1));
     sort_pairs_u64_u32(keys.p, skeys.p, idx.p, order.p, b, 0, kOffsetBits + loc_bits, s);
-    const uint32_t rows = static_cast<uint32_t>(b);
-    if (V == 16) launch_sorted<16>(skeys.p, order.p, rows, cpr, out, s);
-    else if (V == 8) launch_sorted<8>(skeys.p, order.p, rows, cpr, out, s);
-    else launch_sorted<4>(skeys.p, order.p, rows, cpr, out, s);
+    if (V == 16) launch_sorted<16>(skeys.p, order.p, rows, cpr, out, kOffsetBits, s);
+    else if (V == 8) launch_sorted<8>(skeys.p, order.p, rows, cpr, out, kOffsetBits, s);
+    else launch_sorted<4>(skeys.p, order.p, rows, cpr, out, kOffsetBits, s);
   }
 
   ~qvb_store() {
