@@ -274,12 +274,15 @@ int qvb_store_destroy(qvb_store* s);
  * ValidationError (checked on device; reported at the next synchronising
  * call or by qvb_store_check_error). */
 int qvb_gather(qvb_store* s, const uint64_t* ids, uint64_t b, float* out, void* stream);
-/* Bucketed variant: requests are first grouped by location and sorted by
- * offset (plan_reads order) and each location class is served by its own
- * CTAs, so host (PCIe) reads never stall HBM/NVLink reads. */
+/* K4-order variant: requests are first sorted by (location, shard offset),
+ * the plan_reads order, and the rows are copied in that order. Faster than
+ * qvb_gather only when a large host tier is read with big batches (ascending
+ * host offsets walk the pinned pages in order: 1.46x on a 14 GB host tier at
+ * 1M ids); slower elsewhere (profiles/r01m_gather_sweep.md). */
 int qvb_gather_planned(qvb_store* s, const uint64_t* ids, uint64_t b, float* out, void* stream);
 /* End-to-end collect from HOST buffers: copies ids host->device, gathers,
- * copies rows device->host, and synchronises. */
+ * copies rows device->host, and synchronises. Calls on one store from several
+ * threads are serialised (they share the store's staging buffers). */
 int qvb_gather_host(qvb_store* s, const uint64_t* ids, uint64_t b, float* out, void* stream);
 /* Reports (and clears) a device-side id range error of earlier gathers. */
 int qvb_store_check_error(qvb_store* s);

@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -589,7 +590,10 @@ struct qvb_store {
   void* peer[kMaxLocations] = {};
   uint64_t used_mask = 0;
   unsigned long long* err = nullptr;
-  // e2e / planned scratch
+  // e2e scratch; host_mu serialises qvb_gather_host calls on one store (the
+  // scratch and the error slot are shared), device-side qvb_gather calls on
+  // different streams stay concurrent
+  std::mutex host_mu;
   uint64_t* d_ids = nullptr;
   char* d_out = nullptr;
   uint64_t cap_b = 0;
@@ -1044,6 +1048,7 @@ extern "C" int qvb_gather_host(qvb_store* s, const uint64_t* ids, uint64_t b, fl
     if (!ids || !out) fail(QVB_ERR_VALIDATION, "null argument");
     DeviceGuard dg(s->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lock(s->host_mu);
     s->ensure_scratch(b);
     QVB_CUDA(cudaMemcpyAsync(s->d_ids, ids, b * 8, cudaMemcpyHostToDevice, st));
     s->launch_gather(s->d_ids, b, s->d_out, st);

@@ -66,6 +66,36 @@ def test_host_tier_zero_copy(qvb, oracle, kernel, monkeypatch):
     st.close()
 
 
+def test_concurrent_gather_host_threads(qvb, oracle):
+    """qvb_gather_host from several threads on one store (ctypes drops the
+    GIL): every caller gets its own rows, with batch sizes that regrow the
+    shared staging buffers mid-run."""
+    import threading
+
+    import torch
+
+    n, dim = 20000, 64
+    t, lo, ids = plan(qvb, n, cap=n // 2, host=n)
+    st = qvb.FeatureStore(lo, ids, dim, t, reader=0)
+    x = oracle.features(n, dim)
+    bad = []
+
+    def work(tid):
+        s = torch.cuda.Stream()
+        for k in range(20):
+            req = oracle.request_ids(11, 1000 * tid + k, n, 500 + 700 * ((tid + k) % 5))
+            if not (st.gather_host(req, stream=s) == oracle.gather(x, req)).all():
+                bad.append((tid, k))
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for h in th:
+        h.start()
+    for h in th:
+        h.join()
+    st.close()
+    assert not bad
+
+
 def test_host_features_input(qvb, oracle):
     n, dim = 3000, 100
     t, lo, ids = plan(qvb, n, cap=n // 2, host=n)
