@@ -1015,11 +1015,16 @@ extern "C" int qvb_access_prob(qvb_graph* g, uint32_t layers, double* out, int o
     if (layers < 1) fail(QVB_ERR_VALIDATION, "access probability needs layers >= 1");
     DeviceGuard dg(g->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lock(g->run_mu);
+    if (!g->done) QVB_CUDA(cudaEventCreateWithFlags(&g->done, cudaEventDisableTiming));
+    QVB_CUDA(cudaStreamWaitEvent(s, g->done, 0));  // the previous call's buffers are free
     if (out_on_device) {  // the last sweep writes the caller's buffer itself
       run_access_prob(*g, layers, s, out);
+      QVB_CUDA(cudaEventRecord(g->done, s));
     } else {
       const double* p = run_access_prob(*g, layers, s);
       QVB_CUDA(cudaMemcpyAsync(out, p, g->n * sizeof(double), cudaMemcpyDeviceToHost, s));
+      QVB_CUDA(cudaEventRecord(g->done, s));
       QVB_CUDA(cudaStreamSynchronize(s));
     }
   });

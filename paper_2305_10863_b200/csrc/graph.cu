@@ -32,6 +32,7 @@ qvb_graph::~qvb_graph() {
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   cudaDeviceSynchronize();
+  if (done) cudaEventDestroy(done);
   cudaFree(perm);
   cudaFree(sptr);
   cudaFree(scol);

@@ -71,6 +71,7 @@
 // gathers y itself. Both arrays are written by every sweep epilogue.
 #pragma once
 
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -140,6 +141,11 @@ struct qvb_graph {
   size_t phase_used = 0;
   uint32_t launches = 0;  // kernels launched by the last run
   unsigned f1_grid = 0, codes_grid = 0;  // resident grids, computed on first use
+  // qvb_access_prob reuses the buffers above: calls are serialised on the
+  // host (run_mu) and, across streams, on the device (each call's stream
+  // waits for the previous call's done event)
+  std::mutex run_mu;
+  cudaEvent_t done = nullptr;
   ~qvb_graph();
 };
 

@@ -133,6 +133,41 @@ def test_c2_bit_exact(qvb, oracle):
     g.close()
 
 
+def test_concurrent_calls_on_one_graph(qvb):
+    """qvb_access_prob from several threads, each on its own stream, into
+    device buffers on one graph (it reuses its sweep buffers): every result
+    equals the serial one bit for bit."""
+    import threading
+
+    import torch
+
+    c = CONFIGS["C2"]
+    g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, False, False)
+    ref = g.access_prob(3)
+    outs = {}
+
+    def work(tid):
+        s = torch.cuda.Stream()
+        res = []
+        for k in range(6):
+            o = torch.empty(c["n"], dtype=torch.float64, device="cuda")
+            g.access_prob(2 + (tid + k) % 2, out=o, stream=s)
+            res.append((2 + (tid + k) % 2, o))
+        s.synchronize()
+        outs[tid] = res
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(3)]
+    for h in th:
+        h.start()
+    for h in th:
+        h.join()
+    ref2 = g.access_prob(2)
+    g.close()
+    for res in outs.values():
+        for layers, o in res:
+            assert (bits(o.cpu().numpy()) == bits(ref if layers == 3 else ref2)).all()
+
+
 def test_layouts_exercised(qvb, oracle):
     # unit weights with parallel edges -> compact layout with exceptions;
     # real weights -> weighted layout
