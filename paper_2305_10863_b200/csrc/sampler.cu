@@ -32,6 +32,7 @@
 // doubles order like their bit patterns) and then take keys < T plus the
 // first keys == T in candidate order — exactly the reference's
 // nth_element over (key, idx) pairs followed by the sort by idx.
+#include <mutex>
 #include <algorithm>
 #include <memory>
 #include <vector>
@@ -51,6 +52,9 @@ struct qvb_sampler {
   uint32_t large_ctas = 0;
   cudaStream_t side = nullptr;  // long-row kernel runs beside the warp kernel
   double build_ms = 0.0;
+  // qvb_batch_sample shares scratch and the side stream, and returns only
+  // after its batch completed: calls on one sampler are serialised here
+  std::mutex mu;
   ~qvb_sampler() {
     int prev = -1;
     cudaGetDevice(&prev);
@@ -880,6 +884,7 @@ extern "C" int qvb_batch_sample(qvb_sampler* sp, const uint64_t* seeds, uint64_t
                                        std::to_string(seeds[i]) + ") out of range");
     DeviceGuard dg(sp->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lock(sp->mu);
     auto r = std::make_unique<qvb_sample>();
     r->device = sp->device;
     r->nseeds = nseeds;

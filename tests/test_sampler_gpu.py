@@ -125,6 +125,53 @@ def test_sampler_long_rows_vs_oracle(qvb, oracle):
                 assert x.tolist() == y.tolist(), (fan, weighted)
 
 
+def test_sampler_concurrent_threads(qvb, oracle):
+    """batch_sample from several threads on one sampler, each on its own
+    stream, over a graph with long rows (shared scratch slabs and side
+    stream): every batch equals the serial one."""
+    import threading
+
+    import torch
+
+    rng = derive_stream(224, 1)
+    n = 3000
+    src, dst, w = [], [], []
+    for i in range(40):
+        for _ in range(300 + rng.below(1500)):
+            src.append(i)
+            dst.append(rng.below(n))
+            w.append(0.5 + rng.uniform())
+    for _ in range(20000):
+        src.append(rng.below(n))
+        dst.append(rng.below(n))
+        w.append(0.5 + rng.uniform())
+    ro, col, ww = oracle.build_csr(n, src, dst, w)
+    seeds = np.array([rng.below(40) for _ in range(200)] + [rng.below(n) for _ in range(200)], np.uint64)
+    with qvb.Sampler.upload(ro, col, ww) as sp:
+        def one(seed, stream=None):
+            r = sp.batch_sample(seeds, [20, 5], seed, stream=stream)
+            try:
+                return [a.tolist() for a in r.arrays()]
+            finally:
+                r.close()
+
+        exp = {k: one(k) for k in range(8)}
+        bad = []
+
+        def work(tid):
+            st = torch.cuda.Stream()
+            for k in range(8):
+                if one((k + tid) % 8, st) != exp[(k + tid) % 8]:
+                    bad.append((tid, k))
+
+        th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+        for h in th:
+            h.start()
+        for h in th:
+            h.join()
+    assert not bad
+
+
 def test_sampler_c2_vs_oracle(qvb, oracle):
     """Full-size C2 graph (hubs of 40K out-edges), 8192 seeds, {15, 10}."""
     c = CONFIGS["C2"]
