@@ -598,6 +598,14 @@ struct qvb_store {
   char* d_out = nullptr;
   uint64_t cap_b = 0;
 
+  cudaStream_t hs[2] = {nullptr, nullptr};  // qvb_gather_host chunk streams
+  cudaEvent_t hev[3] = {nullptr, nullptr, nullptr};
+  void ensure_host_streams() {
+    if (hs[0]) return;
+    for (int q = 0; q < 2; ++q) QVB_CUDA(cudaStreamCreateWithFlags(&hs[q], cudaStreamNonBlocking));
+    for (int q = 0; q < 3; ++q) QVB_CUDA(cudaEventCreateWithFlags(&hev[q], cudaEventDisableTiming));
+  }
+
   void ensure_scratch(uint64_t b) {
     if (b <= cap_b) return;
     cudaFree(d_ids);
@@ -826,6 +834,10 @@ struct qvb_store {
     cudaFree(err);
     cudaFree(d_ids);
     cudaFree(d_out);
+    for (auto q : hs)
+      if (q) cudaStreamDestroy(q);
+    for (auto e : hev)
+      if (e) cudaEventDestroy(e);
     if (prev >= 0) cudaSetDevice(prev);
   }
 };
@@ -1050,15 +1062,46 @@ extern "C" int qvb_gather_host(qvb_store* s, const uint64_t* ids, uint64_t b, fl
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     std::lock_guard<std::mutex> lock(s->host_mu);
     s->ensure_scratch(b);
-    QVB_CUDA(cudaMemcpyAsync(s->d_ids, ids, b * 8, cudaMemcpyHostToDevice, st));
-    s->launch_gather(s->d_ids, b, s->d_out, st);
-    QVB_CUDA(cudaMemcpyAsync(out, s->d_out, b * (uint64_t)s->row_bytes, cudaMemcpyDeviceToHost, st));
+    const uint64_t rb = s->row_bytes;
+    // Large batches go in chunks alternating over two internal streams, so
+    // one chunk's rows travel device->host while the next chunk is gathered
+    // (the copy engines and the SMs overlap; the D2H of the rows bounds it).
+    const char* ce = std::getenv("QVB_HOST_CHUNKS");
+    const uint64_t want = ce ? std::max<uint64_t>(1, std::strtoull(ce, nullptr, 10)) : 8;
+    const uint64_t chunks = b >= want * 16384 ? want : 1;
+    if (chunks == 1) {
+      QVB_CUDA(cudaMemcpyAsync(s->d_ids, ids, b * 8, cudaMemcpyHostToDevice, st));
+      s->launch_gather(s->d_ids, b, s->d_out, st);
+      QVB_CUDA(cudaMemcpyAsync(out, s->d_out, b * rb, cudaMemcpyDeviceToHost, st));
+    } else {
+      s->ensure_host_streams();
+      QVB_CUDA(cudaEventRecord(s->hev[2], st));
+      for (int q = 0; q < 2; ++q) QVB_CUDA(cudaStreamWaitEvent(s->hs[q], s->hev[2], 0));
+      const uint64_t per = (b + chunks - 1) / chunks;
+      for (uint64_t c = 0; c < chunks; ++c) {
+        const uint64_t a = c * per, len = std::min(per, b - a);
+        if (a >= b) break;
+        cudaStream_t q = s->hs[c & 1];
+        QVB_CUDA(cudaMemcpyAsync(s->d_ids + a, ids + a, len * 8, cudaMemcpyHostToDevice, q));
+        s->launch_gather(s->d_ids + a, len, s->d_out + a * rb, q);
+        QVB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(out) + a * rb, s->d_out + a * rb, len * rb,
+                                 cudaMemcpyDeviceToHost, q));
+      }
+      for (int q = 0; q < 2; ++q) {
+        QVB_CUDA(cudaEventRecord(s->hev[q], s->hs[q]));
+        QVB_CUDA(cudaStreamWaitEvent(st, s->hev[q], 0));
+      }
+    }
     QVB_CUDA(cudaStreamSynchronize(st));
     unsigned long long e = 0;
     QVB_CUDA(cudaMemcpy(&e, s->err, sizeof e, cudaMemcpyDeviceToHost));
     if (e != ~0ull) {
       QVB_CUDA(cudaMemset(s->err, 0xFF, sizeof(unsigned long long)));
-      fail(QVB_ERR_VALIDATION, "feature id " + std::to_string(ids[e]) + " outside lookup table");
+      // chunked launches report chunk-relative indices: name the first bad id
+      uint64_t i = 0;
+      while (i < b && ids[i] < s->n) ++i;
+      fail(QVB_ERR_VALIDATION, "feature id " + std::to_string(i < b ? ids[i] : ids[e]) +
+                                   " outside lookup table");
     }
   });
 }

@@ -96,6 +96,20 @@ def test_concurrent_gather_host_threads(qvb, oracle):
     assert not bad
 
 
+@pytest.mark.parametrize("chunks", ["1", "3", "8"])
+def test_gather_host_chunked(qvb, oracle, chunks, monkeypatch):
+    """qvb_gather_host's pipelined chunks (two internal streams) return the
+    same rows as one launch, including a ragged last chunk and host rows."""
+    monkeypatch.setenv("QVB_HOST_CHUNKS", chunks)
+    n, dim = 50000, 100
+    t, lo, ids = plan(qvb, n, cap=n // 2, host=n)
+    st = qvb.FeatureStore(lo, ids, dim, t, reader=0)
+    x = oracle.features(n, dim)
+    req = oracle.request_ids(11, 3, n, 8 * 16384 + 12345)
+    assert (st.gather_host(req) == oracle.gather(x, req)).all()
+    st.close()
+
+
 def test_host_features_input(qvb, oracle):
     n, dim = 3000, 100
     t, lo, ids = plan(qvb, n, cap=n // 2, host=n)
@@ -141,6 +155,11 @@ def test_gather_errors(qvb, oracle):
     with pytest.raises(qvb.ValidationError, match="feature id 1000 outside"):
         st.gather_host(np.array([1, 2, 1000, 3], np.uint64))
     assert st.gather_host(np.array([], np.uint64)).shape == (0, dim)
+    # a chunked (pipelined) host call names the first bad id too
+    big = np.random.default_rng(2).integers(0, n, 300_000).astype(np.uint64)
+    big[200_001] = n + 7
+    with pytest.raises(qvb.ValidationError, match=f"feature id {n + 7} outside"):
+        st.gather_host(big)
     st.close()
     dt = qvb.Topology.with_defaults(gpus_per_server=1, gpu_feature_capacity=10,
                                     host_feature_capacity=10, disk_feature_capacity=n)
