@@ -21,8 +21,11 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <memory>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "graph.cuh"
@@ -82,21 +85,6 @@ __global__ void k_check_ro(const uint64_t* __restrict__ ro, uint64_t n,
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
     if (ro[i + 1] < ro[i]) atomicMin(bad_mono, (unsigned long long)i);
-}
-
-// col u64 -> u32 with the range check of graph.cpp:78-81 (edge-level code 1).
-__global__ void k_col_to_u32(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
-                             uint64_t count, uint64_t base, uint64_t n,
-                             unsigned long long* bad_edge) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t v = in[i];
-    if (v >= n) {
-      atomicMin(bad_edge, (unsigned long long)(((base + i) << 2) | 1));
-      v = 0;
-    }
-    out[i] = static_cast<uint32_t>(v);
-  }
 }
 
 // graph.cpp:82-85 (edge-level code 2).
@@ -1167,6 +1155,100 @@ void finish_build(qvb_graph* g, cudaEvent_t a, cudaEvent_t b, cudaStream_t s) {
 
 namespace qvb {
 
+// Columns host -> device as u32, with the range check of graph.cpp:78-81
+// (edge-level code 1): host threads narrow (and range-check) the
+// caller's u64 columns chunk by chunk into pinned staging slots, each chunk
+// DMA'd on the thread's stream as soon as it is written — half the PCIe bytes
+// of shipping u64, at pinned rather than pageable speed, with the narrowing
+// overlapped with the copies. The slots are kept for the process (the first
+// call pays for pinning them). Returns the first out-of-range column index
+// as (i << 2) | 1, or kNone.
+struct ColStage {
+  std::mutex mu;
+  uint32_t* pinned = nullptr;  // threads * 2 slots of kChunk entries
+  unsigned threads = 0;
+  static constexpr uint64_t kChunk = 1ull << 21;
+};
+ColStage& col_stage() {
+  static ColStage c;
+  return c;
+}
+
+unsigned long long upload_columns(const uint64_t* col, uint64_t e, uint64_t n, uint32_t* dcol,
+                                  cudaStream_t s) {
+  constexpr unsigned long long kNoBad = ~0ull;
+  ColStage& cs = col_stage();
+  std::lock_guard<std::mutex> lock(cs.mu);
+  if (!cs.pinned) {
+    const char* te = std::getenv("QVB_UPLOAD_THREADS");
+    unsigned t = te ? static_cast<unsigned>(std::atoi(te)) : std::thread::hardware_concurrency();
+    cs.threads = std::max(1u, std::min(16u, t));
+    QVB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&cs.pinned),
+                           cs.threads * 2 * ColStage::kChunk * sizeof(uint32_t), cudaHostAllocPortable));
+  }
+  const uint64_t nchunks = (e + ColStage::kChunk - 1) / ColStage::kChunk;
+  const unsigned T = static_cast<unsigned>(std::min<uint64_t>(cs.threads, nchunks));
+  cudaEvent_t start;
+  QVB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  QVB_CUDA(cudaEventRecord(start, s));  // dcol is allocated in stream order on s
+  std::vector<cudaStream_t> st(T, nullptr);
+  std::vector<cudaEvent_t> ev(2 * T, nullptr), fin(T, nullptr);
+  for (unsigned t = 0; t < T; ++t) {
+    QVB_CUDA(cudaStreamCreateWithFlags(&st[t], cudaStreamNonBlocking));
+    QVB_CUDA(cudaStreamWaitEvent(st[t], start, 0));
+    for (int k = 0; k < 2; ++k) QVB_CUDA(cudaEventCreateWithFlags(&ev[2 * t + k], cudaEventDisableTiming));
+    QVB_CUDA(cudaEventCreateWithFlags(&fin[t], cudaEventDisableTiming));
+  }
+  std::vector<unsigned long long> bad(T, kNoBad);
+  std::vector<int> err(T, 0);
+  int dev = 0;
+  QVB_CUDA(cudaGetDevice(&dev));
+  auto work = [&](unsigned t) {
+    cudaSetDevice(dev);
+    uint64_t k = 0;
+    for (uint64_t c = t; c < nchunks; c += T, ++k) {
+      uint32_t* slot = cs.pinned + (2 * t + (k & 1)) * ColStage::kChunk;
+      if (k >= 2 && cudaEventSynchronize(ev[2 * t + (k & 1)]) != cudaSuccess) { err[t] = 1; return; }
+      const uint64_t a = c * ColStage::kChunk, len = std::min(ColStage::kChunk, e - a);
+      const uint64_t* in = col + a;
+      for (uint64_t i = 0; i < len; ++i) {
+        const uint64_t v = in[i];
+        if (v >= n && bad[t] == kNoBad) bad[t] = ((a + i) << 2) | 1;
+        slot[i] = static_cast<uint32_t>(v < n ? v : 0);
+      }
+      if (cudaMemcpyAsync(dcol + a, slot, len * sizeof(uint32_t), cudaMemcpyHostToDevice, st[t]) !=
+              cudaSuccess ||
+          cudaEventRecord(ev[2 * t + (k & 1)], st[t]) != cudaSuccess) {
+        err[t] = 1;
+        return;
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < T; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+  int failed = 0;
+  for (unsigned t = 0; t < T; ++t) {
+    failed |= err[t];
+    QVB_CUDA(cudaEventRecord(fin[t], st[t]));
+    QVB_CUDA(cudaStreamWaitEvent(s, fin[t], 0));
+  }
+  // the slots are reused by the next call: this one's copies must be done
+  for (unsigned t = 0; t < T; ++t) QVB_CUDA(cudaStreamSynchronize(st[t]));
+  for (unsigned t = 0; t < T; ++t) {
+    cudaStreamDestroy(st[t]);
+    cudaEventDestroy(ev[2 * t]);
+    cudaEventDestroy(ev[2 * t + 1]);
+    cudaEventDestroy(fin[t]);
+  }
+  cudaEventDestroy(start);
+  if (failed) fail(QVB_ERR_CUDA, "column upload failed");
+  unsigned long long first = kNoBad;
+  for (auto b : bad) first = std::min(first, b);
+  return first;
+}
+
 // Host out-CSR -> device (row offsets u64, columns u32, weights f64 or none)
 // with Graph::validate's checks and messages (graph.cpp:58-93); the
 // all-zero-weights row check runs with the row sums (k_row_sums).
@@ -1190,16 +1272,9 @@ void upload_out_csr(uint64_t n, uint64_t e, const uint64_t* row_offsets, const u
     fail(QVB_ERR_VALIDATION, "row_offsets not non-decreasing at node " + std::to_string(bad_mono));
 
   dcol.alloc(e, s);
+  unsigned long long bad_col = kNone;
   if (e) {
-    const uint64_t chunk = 1ull << 25;  // 256 MiB of u64 per staging round
-    DevBuf<uint64_t> stage(std::min(e, chunk), s);
-    for (uint64_t base = 0; base < e; base += chunk) {
-      const uint64_t c = std::min(chunk, e - base);
-      QVB_CUDA(cudaMemcpyAsync(stage.p, col + base, c * 8, cudaMemcpyHostToDevice, s));
-      k_col_to_u32<<<grid_for(c, kBlock), kBlock, 0, s>>>(stage.p, dcol.p + base, c, base, n,
-                                                          flags.p + 1);
-      QVB_LAUNCH_CHECK();
-    }
+    bad_col = upload_columns(col, e, n, dcol.p, s);
     if (weights) {
       dw.alloc(e, s);
       QVB_CUDA(cudaMemcpyAsync(dw.p, weights, e * 8, cudaMemcpyHostToDevice, s));
@@ -1207,7 +1282,7 @@ void upload_out_csr(uint64_t n, uint64_t e, const uint64_t* row_offsets, const u
       QVB_LAUNCH_CHECK();
     }
   }
-  unsigned long long bad_edge = read_scalar(flags.p + 1, s);
+  unsigned long long bad_edge = std::min(read_scalar(flags.p + 1, s), bad_col);
   if (bad_edge != kNone) {
     // The first failing edge names its row (graph.cpp:75-91 walks rows in
     // order; a zero-weight row before it would be reported first).
