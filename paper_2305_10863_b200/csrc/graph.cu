@@ -22,6 +22,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -1332,9 +1334,19 @@ extern "C" int qvb_graph_upload(int device, uint64_t n, uint64_t e, const uint64
     DevBuf<uint64_t> ro;
     DevBuf<uint32_t> dcol;
     DevBuf<double> dw;
+    const bool trace = std::getenv("QVB_TRACE_UPLOAD") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
     upload_out_csr(n, e, row_offsets, col, weights, s, ro, dcol, dw);
+    if (trace) QVB_CUDA(cudaStreamSynchronize(s));
+    auto t1 = std::chrono::steady_clock::now();
     build_in_csr(*g, ro.p, dcol.p, dw.p, nullptr, s);
+    if (trace) QVB_CUDA(cudaStreamSynchronize(s));
+    auto t2 = std::chrono::steady_clock::now();
     finish_build(g.get(), ea, eb, s);
+    if (trace)
+      std::fprintf(stderr, "qvb_graph_upload: upload %.2f ms, in-CSR build %.2f ms (host clock)\n",
+                   std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                   std::chrono::duration<double, std::milli>(t2 - t1).count());
     cudaEventDestroy(ea);
     cudaEventDestroy(eb);
     *out = g.release();
