@@ -658,11 +658,12 @@ struct qvb_store {
     // batch of a few hundred groups leaves most of the GPU idle behind a chain
     // of sequential copy rounds; the flat kernel spreads (request, chunk)
     // pairs over every thread, one id -> entry -> row chain deep
-    // (profiles/r01l_gather_sweep.md: 1K ids 9.9 -> 7.5 us at 400-byte rows,
-    // 44.6 -> 7.6 us at 2408-byte rows). QVB_GATHER_SMALL overrides the
-    // request-count threshold.
+    // (1K ids: 9.9 -> 7.5 us at 400-byte rows, 44.6 -> 7.6 us at 2408-byte
+    // rows; ~40K ids: 11.4 -> 9.8 and 62.6 -> 52.0 us; at 64K ids the row-group
+    // kernel is ahead again — profiles/r01m_gather_sweep.md). QVB_GATHER_SMALL
+    // overrides the request-count threshold.
     const char* sm = std::getenv("QVB_GATHER_SMALL");
-    const uint64_t small_rows = sm ? std::strtoull(sm, nullptr, 10) : 32768ull;
+    const uint64_t small_rows = sm ? std::strtoull(sm, nullptr, 10) : 49152ull;
     if (kind != 1 && b > small_rows) {
       if (V == 16) launch_rows<16>(ids, b, cpr, out, s);
       else if (V == 8 && stride % 16 == 0) launch_rows_wide(ids, b, out, s);
