@@ -1176,18 +1176,85 @@ ColStage& col_stage() {
   return c;
 }
 
+void ensure_pinned(ColStage& cs) {  // with cs.mu held
+  if (cs.pinned) return;
+  const char* te = std::getenv("QVB_UPLOAD_THREADS");
+  unsigned t = te ? static_cast<unsigned>(std::atoi(te)) : std::thread::hardware_concurrency();
+  cs.threads = std::max(1u, std::min(16u, t));
+  QVB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&cs.pinned),
+                         cs.threads * 2 * ColStage::kChunk * sizeof(uint32_t), cudaHostAllocPortable));
+}
+
+// Device -> pageable host copy through the same pinned slots: each thread
+// DMAs its chunks into its two slots (one in flight while it copies the
+// other out), instead of the driver's single-threaded pageable staging.
+// Stream-ordered after the work queued on s; returns when the data is in dst.
+void copy_to_host(void* dst, const void* src, uint64_t bytes, cudaStream_t s) {
+  if (bytes == 0) return;
+  constexpr uint64_t kBytes = ColStage::kChunk * sizeof(uint32_t);
+  if (bytes < 4 * kBytes) {  // small: one pageable copy
+    QVB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    QVB_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  ColStage& cs = col_stage();
+  std::lock_guard<std::mutex> lock(cs.mu);
+  ensure_pinned(cs);
+  const uint64_t nchunks = (bytes + kBytes - 1) / kBytes;
+  const unsigned T = static_cast<unsigned>(std::min<uint64_t>(cs.threads, nchunks));
+  cudaEvent_t start;
+  QVB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  QVB_CUDA(cudaEventRecord(start, s));
+  std::vector<cudaStream_t> st(T, nullptr);
+  std::vector<cudaEvent_t> ev(2 * T, nullptr);
+  for (unsigned t = 0; t < T; ++t) {
+    QVB_CUDA(cudaStreamCreateWithFlags(&st[t], cudaStreamNonBlocking));
+    QVB_CUDA(cudaStreamWaitEvent(st[t], start, 0));
+    for (int k = 0; k < 2; ++k) QVB_CUDA(cudaEventCreateWithFlags(&ev[2 * t + k], cudaEventDisableTiming));
+  }
+  std::vector<int> err(T, 0);
+  int dev = 0;
+  QVB_CUDA(cudaGetDevice(&dev));
+  auto work = [&](unsigned t) {
+    cudaSetDevice(dev);
+    auto issue = [&](uint64_t c, uint64_t k) {
+      char* slot = reinterpret_cast<char*>(cs.pinned) + (2 * t + (k & 1)) * kBytes;
+      const uint64_t a = c * kBytes, len = std::min(kBytes, bytes - a);
+      return cudaMemcpyAsync(slot, static_cast<const char*>(src) + a, len, cudaMemcpyDeviceToHost, st[t]) ==
+                 cudaSuccess &&
+             cudaEventRecord(ev[2 * t + (k & 1)], st[t]) == cudaSuccess;
+    };
+    uint64_t k = 0;
+    if (t < nchunks && !issue(t, 0)) { err[t] = 1; return; }
+    for (uint64_t c = t; c < nchunks; c += T, ++k) {
+      if (c + T < nchunks && !issue(c + T, k + 1)) { err[t] = 1; return; }  // next chunk in flight
+      if (cudaEventSynchronize(ev[2 * t + (k & 1)]) != cudaSuccess) { err[t] = 1; return; }
+      const uint64_t a = c * kBytes, len = std::min(kBytes, bytes - a);
+      std::memcpy(static_cast<char*>(dst) + a, reinterpret_cast<char*>(cs.pinned) + (2 * t + (k & 1)) * kBytes, len);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < T; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+  int failed = 0;
+  for (unsigned t = 0; t < T; ++t) {
+    failed |= err[t];
+    cudaStreamSynchronize(st[t]);
+    cudaStreamDestroy(st[t]);
+    cudaEventDestroy(ev[2 * t]);
+    cudaEventDestroy(ev[2 * t + 1]);
+  }
+  cudaEventDestroy(start);
+  if (failed) fail(QVB_ERR_CUDA, "device to host copy failed");
+}
+
 unsigned long long upload_columns(const uint64_t* col, uint64_t e, uint64_t n, uint32_t* dcol,
                                   cudaStream_t s) {
   constexpr unsigned long long kNoBad = ~0ull;
   ColStage& cs = col_stage();
   std::lock_guard<std::mutex> lock(cs.mu);
-  if (!cs.pinned) {
-    const char* te = std::getenv("QVB_UPLOAD_THREADS");
-    unsigned t = te ? static_cast<unsigned>(std::atoi(te)) : std::thread::hardware_concurrency();
-    cs.threads = std::max(1u, std::min(16u, t));
-    QVB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&cs.pinned),
-                           cs.threads * 2 * ColStage::kChunk * sizeof(uint32_t), cudaHostAllocPortable));
-  }
+  ensure_pinned(cs);
   const uint64_t nchunks = (e + ColStage::kChunk - 1) / ColStage::kChunk;
   const unsigned T = static_cast<unsigned>(std::min<uint64_t>(cs.threads, nchunks));
   cudaEvent_t start;

@@ -150,6 +150,12 @@ struct qvb_graph {
 };
 
 namespace qvb {
+// Device -> pageable host copy through pinned staging slots and host threads
+// (graph.cu); stream-ordered after the work queued on s, returns when done.
+void copy_to_host(void* dst, const void* src, uint64_t bytes, cudaStream_t s);
+}  // namespace qvb
+
+namespace qvb {
 
 constexpr uint32_t kExcFlag = 0x80000000u;
 // perm slot = node | kFirst (first pass touching the node: start from 1.0)
