@@ -5,6 +5,8 @@ acceptance.cpp:156-173) and adds the BASELINE configs. The bar is
 bit-identical fp64 (north_star allows 1e-9 relative; SURVEY §0 shows only a
 bit-exact P keeps the placement/LUT exact, so that is what we test).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -354,3 +356,23 @@ def test_c4_sampled_against_oracle(qvb, oracle):
     assert (bits(p2[nodes]) == bits(exp2)).all()
     exp3 = oracle.sweep_nodes(tro, src.astype(np.uint64), R, ones, p2, nodes)
     assert (bits(p3[nodes]) == bits(exp3)).all()
+
+
+@pytest.mark.skipif(os.environ.get("QVB_C4_REFERENCE") != "1",
+                    reason="opt-in: ~3 min and ~90 GB of host RAM (QVB_C4_REFERENCE=1)")
+def test_c4_full_against_reference():
+    """All 111M C4 nodes against the unmodified reference's own
+    compute_access_prob_ie (oracle/_ref, 16 threads), from one host CSR."""
+    from oracle.oracle import RefLib
+
+    if not RefLib.available():
+        pytest.skip("oracle/_ref not built")
+    from paper_2305_10863_b200 import qvb
+
+    c = CONFIGS["C4"]
+    ro, col, w = qvb.synthetic_csr(c["n"], c["e"], 7, False, False)
+    p = qvb.compute_access_prob_ie(ro, col, None, c["layers"]).values
+    ref = RefLib()
+    ref.set_threads(os.cpu_count() or 1)
+    exp = ref.access_prob(ro, col, w, c["layers"], parallel=True)
+    assert (bits(p) == bits(exp)).all()
