@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <numeric>
 #include <string>
+#include <thread>
 
 #include "placement.cuh"
 
@@ -41,6 +42,17 @@ __global__ void k_rank_keys(const double* __restrict__ v, uint64_t n, uint64_t* 
     b = (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // ascending total order
     keys[i] = ~b;                                       // descending
     ids[i] = i;
+  }
+}
+
+// vr[r] = v[ranks[r]], pos[ranks[r]] = r
+__global__ void k_rank_views(const double* __restrict__ v, const uint64_t* __restrict__ ranks, uint64_t n,
+                             double* __restrict__ vr, uint64_t* __restrict__ pos) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t f = ranks[r];
+    vr[r] = v[f];
+    pos[f] = r;
   }
 }
 
@@ -163,20 +175,19 @@ __global__ void __launch_bounds__(kTile)
 }
 
 // LPT over one NUMA group's slots (placement.cpp:100-115).
-void lpt(const double* v, const uint64_t* run, uint64_t len, uint32_t gpn, uint64_t cap,
-         std::vector<uint8_t>& slot) {
+// vr: the run's values in rank order (read sequentially, not through the ids).
+void lpt(const double* vr, uint64_t len, uint32_t gpn, uint64_t cap, std::vector<uint8_t>& slot) {
   std::vector<double> load(gpn, 0.0);
   std::vector<uint64_t> used(gpn, 0);
   slot.resize(len);
   for (uint64_t i = 0; i < len; ++i) {
-    const uint64_t f = run[i];
     uint32_t best = gpn;
     for (uint32_t s = 0; s < gpn; ++s) {
       if (used[s] >= cap) continue;
       if (best == gpn || load[s] < load[best]) best = s;
     }
     if (best == gpn) fail(QVB_ERR_GENERIC, "gpu range exceeds numa group capacity");
-    load[best] += v[f];
+    load[best] += vr[i];
     ++used[best];
     slot[i] = static_cast<uint8_t>(best);
   }
@@ -202,7 +213,9 @@ void rank_desc_device(const double* d_values, uint64_t n, uint64_t* d_ranks, cud
   if (b != ~0ull) fail(QVB_ERR_VALIDATION, "NaN value for feature " + std::to_string(b));
 }
 
-HostPlan plan_from_ranks(const double* v, const uint64_t* ranks, uint64_t n,
+// vr[r] = value of the feature at rank position r; pos[f] = rank position of
+// feature f (both computed on the device, see qvb_plan_placement).
+HostPlan plan_from_ranks(const double* vr, const uint64_t* pos, uint64_t n,
                          const qvb_topology& t) {
   const uint32_t G = t.gpus_per_server, S = t.servers;
   const uint32_t gpn = gpus_per_numa(t);
@@ -219,7 +232,7 @@ HostPlan plan_from_ranks(const double* v, const uint64_t* ranks, uint64_t n,
     const uint64_t len = hi - lo;
     r.g = std::min(len, gpu_range_size);
     r.rep = std::min(r.g, rep_cap);
-    if (G > 0 && nvl) lpt(v, ranks + lo + r.rep, r.g - r.rep, gpn, t.gpu_feature_capacity - rep_cap, r.slot);
+    if (G > 0 && nvl) lpt(vr + lo + r.rep, r.g - r.rep, gpn, t.gpu_feature_capacity - rep_cap, r.slot);
     r.h = std::min(len - r.g, t.host_feature_capacity);
     return r;
   };
@@ -254,8 +267,6 @@ HostPlan plan_from_ranks(const double* v, const uint64_t* ranks, uint64_t n,
     }
   }
 
-  std::vector<uint64_t> pos(n);
-  for (uint64_t r = 0; r < n; ++r) pos[ranks[r]] = r;
   const int64_t stride = (int64_t)G + 2;
 
   // Copies of the feature at rank position r, canonical order (ascending id).
@@ -299,18 +310,60 @@ HostPlan plan_from_ranks(const double* v, const uint64_t* ranks, uint64_t n,
     return c;
   };
 
+  // Every feature's copies depend only on its rank position, so the two
+  // emit passes (copy counts, then the copies) run over feature ranges on
+  // host threads; per-thread location counts are summed afterwards.
   HostPlan plan;
   plan.offsets.assign(n + 1, 0);
-  std::vector<int64_t> buf((size_t)S * (G + 1) + 2);
-  for (uint64_t f = 0; f < n; ++f) plan.offsets[f + 1] = plan.offsets[f] + emit(pos[f], buf.data());
-  plan.ids.resize(plan.offsets[n]);
   const int64_t nloc_all = (int64_t)S * stride;
+  const unsigned T = static_cast<unsigned>(
+      std::max<uint64_t>(1, std::min<uint64_t>(std::min(16u, std::max(1u, std::thread::hardware_concurrency())),
+                                                n / 65536)));
+  const uint64_t per = (n + T - 1) / T;
+  std::vector<uint64_t> part(T + 1, 0);
+  std::vector<std::vector<uint64_t>> tcounts(T, std::vector<uint64_t>(nloc_all, 0));
+  std::vector<uint64_t> missing(T, ~0ull);
+  auto parallel = [&](auto&& body) {
+    std::vector<std::thread> pool;
+    for (unsigned k = 1; k < T; ++k) pool.emplace_back(body, k);
+    body(0u);
+    for (auto& th : pool) th.join();
+  };
+  parallel([&](unsigned k) {  // pass 1: copies per feature, range totals
+    std::vector<int64_t> buf((size_t)S * (G + 1) + 2);
+    const uint64_t a = std::min(n, k * per), b = std::min(n, a + per);
+    uint64_t sum = 0;
+    for (uint64_t f = a; f < b; ++f) {
+      const uint32_t c = emit(pos[f], buf.data());
+      plan.offsets[f + 1] = c;
+      sum += c;
+    }
+    part[k + 1] = sum;
+  });
+  for (unsigned k = 0; k < T; ++k) part[k + 1] += part[k];
+  parallel([&](unsigned k) {  // prefix within the range
+    const uint64_t a = std::min(n, k * per), b = std::min(n, a + per);
+    uint64_t at = part[k];
+    for (uint64_t f = a; f < b; ++f) {
+      at += plan.offsets[f + 1];
+      plan.offsets[f + 1] = at;
+    }
+  });
+  plan.ids.resize(plan.offsets[n]);
+  parallel([&](unsigned k) {  // pass 2: the copies, and the location counts
+    const uint64_t a = std::min(n, k * per), b = std::min(n, a + per);
+    std::vector<uint64_t>& cnt = tcounts[k];
+    for (uint64_t f = a; f < b; ++f) {
+      const uint32_t c = emit(pos[f], plan.ids.data() + plan.offsets[f]);
+      if (c == 0 && missing[k] == ~0ull) missing[k] = f;
+      for (uint32_t q = 0; q < c; ++q) ++cnt[plan.ids[plan.offsets[f] + q]];
+    }
+  });
+  for (unsigned k = 0; k < T; ++k)
+    if (missing[k] != ~0ull) fail(QVB_ERR_GENERIC, "feature " + std::to_string(missing[k]) + " has no location");
   std::vector<uint64_t> counts(nloc_all, 0);
-  for (uint64_t f = 0; f < n; ++f) {
-    const uint32_t c = emit(pos[f], plan.ids.data() + plan.offsets[f]);
-    if (c == 0) fail(QVB_ERR_GENERIC, "feature " + std::to_string(f) + " has no location");
-    for (uint32_t k = 0; k < c; ++k) ++counts[plan.ids[plan.offsets[f] + k]];
-  }
+  for (unsigned k = 0; k < T; ++k)
+    for (int64_t id = 0; id < nloc_all; ++id) counts[id] += tcounts[k][id];
   // PlacementPlan::validate (placement.cpp:53-74)
   static const char* tier_names[3] = {"gpu", "host", "disk"};
   for (int64_t id = 0; id < nloc_all; ++id) {
@@ -437,18 +490,24 @@ extern "C" int qvb_plan_placement(int device, const double* values, uint64_t n,
     if (!values || !loc_offsets || !copies_out) fail(QVB_ERR_VALIDATION, "null argument");
     if (topo->nvlink_within_numa && gpus_per_numa(*topo) > 255)
       fail(QVB_ERR_UNSUPPORTED, "more than 255 GPUs per NUMA group");
-    std::vector<uint64_t> ranks(n);
+    // the device ranks the features and hands the sequential planner its
+    // inputs in the order it walks them: values in rank order and each
+    // feature's rank position (no random host reads over n values)
+    std::vector<double> vr(n);
+    std::vector<uint64_t> pos(n);
     {
       DeviceGuard dg(device);
       cudaStream_t s = nullptr;
-      DevBuf<double> dv(n, s);
-      DevBuf<uint64_t> dr(n, s);
+      DevBuf<double> dv(n, s), dvr(n, s);
+      DevBuf<uint64_t> dr(n, s), dpos(n, s);
       QVB_CUDA(cudaMemcpyAsync(dv.p, values, n * 8, cudaMemcpyHostToDevice, s));
       rank_desc_device(dv.p, n, dr.p, s);
-      QVB_CUDA(cudaMemcpyAsync(ranks.data(), dr.p, n * 8, cudaMemcpyDeviceToHost, s));
-      QVB_CUDA(cudaStreamSynchronize(s));
+      k_rank_views<<<grid_for(n, 256), 256, 0, s>>>(dv.p, dr.p, n, dvr.p, dpos.p);
+      QVB_LAUNCH_CHECK();
+      copy_to_host(vr.data(), dvr.p, n * 8, s);
+      copy_to_host(pos.data(), dpos.p, n * 8, s);
     }
-    HostPlan p = plan_from_ranks(values, ranks.data(), n, *topo);
+    HostPlan p = plan_from_ranks(vr.data(), pos.data(), n, *topo);
     *copies_out = p.ids.size();
     if (p.ids.size() > loc_capacity)
       fail(QVB_ERR_VALIDATION, "loc_capacity " + std::to_string(loc_capacity) + " too small, need " +

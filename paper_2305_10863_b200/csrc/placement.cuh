@@ -22,9 +22,13 @@ struct HostPlan {
   std::vector<int64_t> ids;
 };
 
-// plan_placement (placement.cpp:138-226) given the host ranks.
-HostPlan plan_from_ranks(const double* values, const uint64_t* ranks, uint64_t n,
+// plan_placement (placement.cpp:138-226) given, from the device ranking, the
+// values in rank order (vr) and each feature's rank position (pos).
+HostPlan plan_from_ranks(const double* vr, const uint64_t* pos, uint64_t n,
                          const qvb_topology& t);
+
+// Device -> pageable host copy through pinned slots (graph.cu).
+void copy_to_host(void* dst, const void* src, uint64_t bytes, cudaStream_t s);
 
 // Device-side result of K3 for one reader.
 struct DeviceLut {
