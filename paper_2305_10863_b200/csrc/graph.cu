@@ -174,6 +174,14 @@ __global__ void k_runs(const uint32_t* __restrict__ sdst, const uint32_t* __rest
   }
 }
 
+// Run heads over sorted (destination, source) pairs (unit-weight graphs).
+__global__ void k_heads(const uint32_t* __restrict__ sdst, const uint32_t* __restrict__ ssrc, uint64_t e,
+                        uint8_t* __restrict__ head) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < e;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    head[k] = (k == 0 || sdst[k] != sdst[k - 1] || ssrc[k] != ssrc[k - 1]) ? 1 : 0;
+}
+
 // One thread per run head: coalesce the run (metrics.cpp:157-164), form
 // R = w_sum / row_sum(s) and flag it when it differs bitwise from
 // 1/row_sum(s); also writes the in-row pointers of every destination whose
@@ -690,17 +698,26 @@ void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, con
     d_src = src_buf.p;
   }
 
-  // Transpose: stable sort by destination, payload = out-CSR edge index.
-  DevBuf<uint32_t> sdst(e, s), seid(e, s);
-  {
-    DevBuf<uint32_t> iota(e, s);
-    k_iota<<<grid_for(e, kBlock), kBlock, 0, s>>>(iota.p, e);
-    QVB_LAUNCH_CHECK();
-    sort_pairs_u32_u32(d_col, sdst.p, iota.p, seid.p, e, 0, bits_for(n - 1), s);
-  }
-  DevBuf<uint32_t> ssrc(e, s);
+  // Transpose: stable sort by destination. Weighted graphs carry the
+  // out-CSR edge index (the weights are gathered through it); unit-weight
+  // graphs carry the source itself, so the sorted sources come out of the
+  // sort instead of a random gather per edge (stable over source-major input:
+  // ascending sources within every destination either way).
+  DevBuf<uint32_t> sdst(e, s), seid, ssrc(e, s);
   DevBuf<uint8_t> head(e, s);
-  k_runs<<<grid_for(e, kBlock), kBlock, 0, s>>>(sdst.p, seid.p, d_src, e, ssrc.p, head.p);
+  if (d_w) {
+    seid.alloc(e, s);
+    {
+      DevBuf<uint32_t> iota(e, s);
+      k_iota<<<grid_for(e, kBlock), kBlock, 0, s>>>(iota.p, e);
+      QVB_LAUNCH_CHECK();
+      sort_pairs_u32_u32(d_col, sdst.p, iota.p, seid.p, e, 0, bits_for(n - 1), s);
+    }
+    k_runs<<<grid_for(e, kBlock), kBlock, 0, s>>>(sdst.p, seid.p, d_src, e, ssrc.p, head.p);
+  } else {
+    sort_pairs_u32_u32(d_col, sdst.p, d_src, ssrc.p, e, 0, bits_for(n - 1), s);
+    k_heads<<<grid_for(e, kBlock), kBlock, 0, s>>>(sdst.p, ssrc.p, e, head.p);
+  }
   QVB_LAUNCH_CHECK();
   src_buf.release();
   DevBuf<uint32_t> uidx(e, s);
