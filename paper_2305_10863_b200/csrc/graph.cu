@@ -213,16 +213,31 @@ __global__ void k_coalesce(const uint32_t* __restrict__ sdst, const uint32_t* __
       while (k2 < e && !head[k2]) ++k2;
       W = static_cast<double>(k2 - k);  // sum of ones, exact
     }
-    const double R = __ddiv_rn(W, rs[s]);
     ucol[u] = s;
-    uR[u] = R;
-    uexc[u] = __double_as_longlong(R) != __double_as_longlong(inv[s]) ? 1 : 0;
+    if (!w && k2 == k + 1) {
+      // unit weight, single edge: R = 1/row_sum(s) is inv[s] bit for bit, no
+      // exception; uR is filled by k_fill_unit_R only if the weighted layout
+      // is chosen (the compact layout reads uR of exceptions alone)
+      uexc[u] = 0;
+    } else {
+      const double R = __ddiv_rn(W, rs[s]);
+      uR[u] = R;
+      uexc[u] = __double_as_longlong(R) != __double_as_longlong(inv[s]) ? 1 : 0;
+    }
     const uint32_t d = sdst[k];
     if (k == 0 || sdst[k - 1] != d) {
       const uint64_t d0 = k == 0 ? 0 : (uint64_t)sdst[k - 1] + 1;
       for (uint64_t dd = d0; dd <= d; ++dd) uptr[dd] = u;
     }
   }
+}
+
+// uR of the single unit-weight edges k_coalesce skipped: inv[s].
+__global__ void k_fill_unit_R(const uint32_t* __restrict__ ucol, const uint8_t* __restrict__ uexc,
+                              const double* __restrict__ inv, uint64_t eu, double* __restrict__ uR) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < eu;
+       u += (uint64_t)gridDim.x * blockDim.x)
+    if (!uexc[u]) uR[u] = inv[ucol[u]];
 }
 
 __global__ void k_compact(const uint32_t* __restrict__ ucol, const double* __restrict__ uR,
@@ -761,6 +776,10 @@ void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, con
     build_first(g, uptr.p, col.p, inv.p, s);
   } else {
     g.layout = 1;
+    if (!d_w) {
+      k_fill_unit_R<<<grid_for(eu, kBlock), kBlock, 0, s>>>(ucol.p, uexc.p, inv.p, eu, uR.p);
+      QVB_LAUNCH_CHECK();
+    }
     uexc.release();
     build_slices(g, uptr.p, ucol.p, ucol.p, uR.p, s);
   }

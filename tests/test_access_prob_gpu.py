@@ -183,6 +183,26 @@ def test_layouts_exercised(qvb, oracle):
     g.close()
 
 
+def test_unit_weights_mostly_parallel_take_weighted_layout(qvb, oracle):
+    """Unit weights where most unique edges are coalesced parallel edges:
+    too many exceptions for the compact layout, so the weighted layout is
+    built from unit weights (single edges' R filled from 1/row_sum)."""
+    rng = derive_stream(577, 1)
+    n = 3000
+    src, dst = [], []
+    for _ in range(40000):
+        s, d = rng.below(n), rng.below(n)
+        for _ in range(1 + rng.below(3)):  # 1-3 parallel copies
+            src.append(s)
+            dst.append(d)
+    ro, col, w = oracle.build_csr(n, src, dst, [1.0] * len(src))
+    g = qvb.DeviceGraph.upload(ro, col, None)
+    assert g.info().layout == 1
+    for layers in (2, 3, 4):
+        assert (bits(g.access_prob(layers)) == bits(oracle.access_prob(ro, col, w, layers))).all()
+    g.close()
+
+
 @pytest.mark.parametrize("layout", ["nm", "slices"])
 @pytest.mark.parametrize("seg_sources", ["1", "7", "1000", "31337"])
 def test_segmented_passes_bit_exact(qvb, oracle, seg_sources, layout, monkeypatch):
