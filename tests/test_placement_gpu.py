@@ -188,3 +188,32 @@ def test_c2_rank_and_lut_vs_oracle(qvb, oracle):
     req = oracle.request_ids(11, 3, c["n"], 1 << 20)
     for x, y in zip(qvb.plan_reads(a[0], a[1], req, 8), oracle.plan_reads(b[0], b[1], req, 8)):
         assert (x == y).all()
+
+
+@pytest.mark.skipif(os.environ.get("QVB_C4_REFERENCE") != "1",
+                    reason="opt-in: ~2 min, C4-sized planner runs (QVB_C4_REFERENCE=1)")
+def test_c4_full_placement_against_reference(qvb):
+    """C4 at full size (111M features, 8 GPUs, capacity N/16): plan, lookup
+    table and a 1M-id read plan equal the unmodified reference's own."""
+    from oracle.oracle import Oracle, RefLib
+
+    if not RefLib.available():
+        pytest.skip("oracle/_ref not built")
+    c = CONFIGS["C4"]
+    n = c["n"]
+    g = qvb.DeviceGraph.synthetic(n, c["e"], 7, False, False)
+    p = g.access_prob(c["layers"])
+    g.close()
+    t = qvb.Topology.with_defaults(gpus_per_server=8, nvlink_within_numa=1, gpu_feature_capacity=n // 16,
+                                   host_feature_capacity=n)
+    ot = otopo_from(t)
+    ref = RefLib()
+    lo, ids = qvb.plan_placement(p, t)
+    lo2, ids2 = ref.plan_placement(p, ot)
+    assert (lo == lo2).all() and (ids == ids2).all()
+    loc, off = qvb.build_lookup_table(lo, ids, t, 0)
+    loc2, off2 = ref.build_lookup_table(lo2, ids2, ot, 0)
+    assert (loc == loc2).all() and (off == off2).all()
+    req = Oracle().request_ids(11, 0, n, 1 << 20)
+    for x, y in zip(qvb.plan_reads(loc, off, req, 8), ref.plan_reads(loc2, off2, req, 8)):
+        assert (x == y).all()
