@@ -803,6 +803,245 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
   }
 }
 
+// ---- k_products_tma: the products with every pass's run staged by TMA ------
+// k_products above walks the passes of a slice in lock-step: every pass
+// starts with a dependent code load and a warp scan of the 32 run lengths,
+// and lasts as long as its longest run (Σ_k max_lane len_k ≈ 37 steps per
+// slice at C4 for 14.4 in-edges per node).
+//
+// Here a warp owns a slice at a time. The slice's K code ranges (one
+// contiguous range of nm_code per pass, the lanes' runs back to back) are
+// copied into the warp's shared-memory buffer by cp.async.bulk — one bulk
+// copy per pass, issued by lane k, completing on the buffer's mbarrier — ONE
+// slice ahead of the compute, so every pass's loads are in flight together
+// and overlap the previous slice's multiplies. Each lane then walks its
+// node's whole chain across the passes without lock-step (the warp runs
+// max_lane Σ_k len_k ≈ 23 steps), jumping from run to run through a small
+// per-lane table of (first, end) shared-memory addresses.
+//
+// Everything that places a lane's runs inside the staging buffer is static
+// for the graph and precomputed once (k_build_runs):
+//   desc[s*K + k]  (u64) pass k of slice s: words | staging offset << 11 |
+//                  aligned source word << 22 | the slice's longest chain
+//                  << 54; bit 63: the slice exceeds the buffer (global path)
+//   runs[v]        (2 x u64) node v: its non-empty runs in pass order as
+//                  u16 fields (staged word | len << 10), then sentinels:
+//                  an empty run at the buffer's zero words (whose word says
+//                  whether this kernel finishes the node: kPtSentReg)
+// A lane past its chain keeps reading zero codes, i.e. factor 1.0 — an exact
+// identity. Same factors, same left-to-right order: bit-identical.
+constexpr int kPtWarps = 4;
+constexpr int kPtKMax = 7;            // <= 7 runs + 1 sentinel in the 8 u16 fields
+constexpr uint32_t kPtMaxBufw = 1024;  // words per buffer at most (10-bit run starts)
+constexpr uint64_t kPtBig = 1ull << 63;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// shared memory of one warp: two staging buffers, the run table, 2 mbarriers
+__host__ __device__ __forceinline__ size_t pt_warp_bytes(uint32_t bufw) {
+  return (size_t)2 * bufw * 4 + 8 * 32 * 8 + 16;
+}
+
+// Largest staged size (words, 16-byte aligned ranges) of one slice.
+__global__ void k_stage_words(int K, uint64_t S, const uint64_t* __restrict__ sbase,
+                              unsigned* __restrict__ mx) {
+  unsigned best = 0;
+  for (uint64_t sl = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; sl < S;
+       sl += (uint64_t)gridDim.x * blockDim.x) {
+    unsigned w = 0;
+    for (int k = 0; k < K; ++k) {
+      const uint64_t st = sbase[(uint64_t)k * S + sl], en = sbase[(uint64_t)k * S + sl + 1];
+      if (en > st) w += static_cast<unsigned>(((en + 3) & ~3ull) - (st & ~3ull));
+    }
+    best = max(best, w);
+  }
+  best = __reduce_max_sync(kFull, best);
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, best);
+}
+
+// One warp per slice, lane = node: the static staging layout (see above).
+// zw: zero words at the end of each buffer (>= the longest chain).
+__global__ void k_build_runs(int K, uint64_t S, const uint8_t* __restrict__ lenf,
+                             const uint64_t* __restrict__ sbase, uint32_t bufw, uint32_t zw,
+                             uint64_t* __restrict__ desc, ulonglong2* __restrict__ runs,
+                             unsigned* __restrict__ big) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t zs = bufw - zw;  // sentinel start: the zero words
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t sl = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < S; sl += warps) {
+    uint64_t st = 0, en = 0;
+    if (lane < static_cast<uint32_t>(K)) {
+      st = sbase[(uint64_t)lane * S + sl];
+      en = sbase[(uint64_t)lane * S + sl + 1];
+    }
+    const uint64_t a = st & ~3ull;
+    const uint32_t words = en > st ? static_cast<uint32_t>(((en + 3) & ~3ull) - a) : 0u;
+    const uint32_t incl = warp_incl_scan(words);
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    const bool too_big = total > zs;
+    const uint32_t off = incl - words;                          // staging offset of pass `lane`
+    const uint32_t base = off + static_cast<uint32_t>(st - a);  // staged word of its first code
+    uint64_t f[2] = {0, 0};
+    uint32_t nj = 0, chain = 0, anyf = 0;
+    for (int k = 0; k < K; ++k) {
+      const uint32_t lf = lenf[(uint64_t)k * S * 32 + sl * 32 + lane];
+      anyf |= lf;
+      const uint32_t len = lf & kNmLen;
+      const uint32_t pre = warp_incl_scan(len) - len;
+      const uint32_t start = __shfl_sync(kFull, base, k) + pre;
+      if (len) {
+        f[nj >> 2] |= (uint64_t)((start & 0x3FFu) | (len << 10)) << (16 * (nj & 3));
+        ++nj;
+      }
+      chain += len;
+    }
+    const uint64_t sent = (anyf & kNmFirst) ? zs : zs + 1;  // which sentinel: finish or not
+    for (uint32_t j = nj; j < 8; ++j) f[j >> 2] |= sent << (16 * (j & 3));
+    const uint32_t maxchain = __reduce_max_sync(kFull, chain);
+    if (lane < static_cast<uint32_t>(K))
+      desc[sl * K + lane] = (too_big ? kPtBig : 0ull) | ((uint64_t)maxchain << 54) | (a << 22) |
+                            ((uint64_t)off << 11) | words;
+    runs[sl * 32 + lane] = make_ulonglong2(f[0], f[1]);
+    if (lane == 0 && too_big) atomicAdd(big, 1u);
+  }
+}
+
+__global__ void __launch_bounds__(kPtWarps * 32)
+    k_products_tma(int K, uint64_t S, uint64_t n, const uint8_t* __restrict__ lenf,
+                   const uint64_t* __restrict__ desc, const ulonglong2* __restrict__ runs,
+                   const uint64_t* __restrict__ sbase, const uint32_t* __restrict__ ncode,
+                   const uint32_t* __restrict__ ncol, const uint32_t* __restrict__ exc_src,
+                   const double* __restrict__ exc_R, const double* __restrict__ prev,
+                   const double* __restrict__ inv, double* __restrict__ out,
+                   uint32_t* __restrict__ kout, const uint32_t* __restrict__ marked, uint32_t bufw,
+                   uint32_t zw) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned char* mine = smem + wid * pt_warp_bytes(bufw);
+  uint32_t* const buf = reinterpret_cast<uint32_t*>(mine);  // [2][bufw]
+  uint2* const tab = reinterpret_cast<uint2*>(mine + (size_t)2 * bufw * 4);  // [8][32]
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(mine + (size_t)2 * bufw * 4 + 8 * 32 * 8);
+  for (uint32_t z = lane; z < zw; z += 32) {  // the sentinel runs' zero codes
+    buf[bufw - zw + z] = 0u;
+    buf[2 * bufw - zw + z] = 0u;
+  }
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const bool mk = *marked != 0;  // uniform: some factor kept a marker code
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t pol = policy_evict_first();
+  const uint32_t buf0 = smem_u32(buf);
+  const uint32_t sent_reg = bufw - zw;
+
+  auto load_desc = [&](uint64_t sl) -> uint64_t {
+    return (sl < S && lane < static_cast<uint32_t>(K)) ? ld_stream(desc + sl * K + lane, pol) : 0ull;
+  };
+  // Copies of a slice into buffer b: 0 nothing to copy, 1 in flight on
+  // bars[b], 2 global path (too big for the buffer, or markers).
+  auto issue = [&](uint64_t sl, uint64_t d, int b, uint32_t& maxt) -> uint32_t {
+    const uint32_t hi0 = __shfl_sync(kFull, static_cast<uint32_t>(d >> 32), 0);
+    maxt = (hi0 >> 22) & 0x1FF;
+    if (sl >= S) return 0;
+    if ((hi0 & 0x80000000u) || mk) return 2;
+    const uint32_t words = static_cast<uint32_t>(d & 0x7FF);
+    const uint32_t total = __reduce_add_sync(kFull, words);
+    if (total == 0) return 0;
+    const uint32_t bar = smem_u32(&bars[b]);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(total * 4)
+                   : "memory");
+    __syncwarp();
+    if (words)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              buf0 + 4 * (b * bufw + static_cast<uint32_t>((d >> 11) & 0x7FF))),
+          "l"(ncode + ((d >> 22) & 0xFFFFFFFFull)), "r"(words * 4), "r"(bar)
+          : "memory");
+    return 1;
+  };
+
+  uint64_t sl = gw;
+  uint64_t d1 = load_desc(sl);
+  ulonglong2 rc = sl < S ? runs[sl * 32 + lane] : make_ulonglong2(0, 0);
+  uint32_t maxt_cur, maxt_nxt;
+  uint32_t stat_cur = issue(sl, d1, 0, maxt_cur), stat_nxt;
+  d1 = load_desc(sl + nw);
+  uint32_t par = 0;  // expected parity per buffer
+  for (int i = 0; sl < S; ++i, sl += nw) {
+    const int b = i & 1;
+    const uint64_t v = sl * 32 + lane;
+    const bool real = v < n;
+    double pv = 0.0, iv = 0.0;
+    if (real) {  // finish operands in flight early
+      pv = ld_stream(prev + v, pol);
+      if (kout) iv = ld_stream(inv + v, pol);
+    }
+    // the next slice's copies go into the other buffer: its reads by the
+    // previous iteration have completed (their values were consumed)
+    stat_nxt = issue(sl + nw, d1, b ^ 1, maxt_nxt);
+    const ulonglong2 rn = sl + nw < S ? runs[(sl + nw) * 32 + lane] : make_ulonglong2(0, 0);
+    d1 = load_desc(sl + 2 * nw);
+
+    double miss = 1.0;  // metrics.cpp:152
+    if (stat_cur == 2) {  // rare: the slice's runs exceed the buffer, or markers
+      miss = products_markers(K, S, sl, static_cast<int>(lane), lenf, sbase, ncode, ncol, exc_src,
+                              exc_R, prev, inv);
+    } else {
+      // the lane's (first, end) byte addresses of runs 1..7 (run 0 stays in registers)
+      const uint32_t bb = buf0 + 4 * b * bufw;
+      uint32_t a0 = 0, e0 = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t f = static_cast<uint32_t>(((j < 4 ? rc.x : rc.y) >> (16 * (j & 3))) & 0xFFFF);
+        const uint32_t aa = bb + 4 * (f & 0x3FFu), ee = aa + 4 * (f >> 10);
+        if (j == 0) {
+          a0 = aa;
+          e0 = ee;
+        } else {
+          tab[(j - 1) * 32 + lane] = make_uint2(aa, ee);
+        }
+      }
+      if (stat_cur == 1) {
+        asm volatile(
+            "{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            " @!p bra W_%=;\n}" ::"r"(smem_u32(&bars[b])),
+            "r"((par >> b) & 1u)
+            : "memory");
+        par ^= 1u << b;
+      }
+      uint32_t a = a0, e = e0, ta = smem_u32(tab + lane);
+#pragma unroll 4
+      for (uint32_t t = 0; t < maxt_cur; ++t) {
+        uint32_t c;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(c) : "r"(a));
+        miss = __dmul_rn(miss, low_to_factor(c));
+        a += 4;
+        if (a == e) {  // the lane's next run (or its sentinel)
+          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(a), "=r"(e) : "r"(ta));
+          ta += 256;
+        }
+      }
+    }
+    const uint32_t s7 = static_cast<uint32_t>(rc.y >> 48) & 0x3FFu;  // field 7: always a sentinel
+    if (real && s7 == sent_reg) {
+      // metrics.cpp:169: prev + (1 - prev) * (1 - miss_all)
+      const double P = __dadd_rn(pv, __dmul_rn(__dsub_rn(1.0, pv), __dsub_rn(1.0, miss)));
+      st_stream(out + v, P, pol);
+      if (kout) st_stream(kout + v, y_code(__dmul_rn(P, iv)), pol);
+    }
+    __syncwarp();  // buffer b and the table are read; refilled next iteration
+    rc = rn;
+    stat_cur = stat_nxt;
+    maxt_cur = maxt_nxt;
+  }
+}
+
 }  // namespace
 
 namespace {
@@ -949,11 +1188,50 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, dou
         ++launched;
       }
       pt.end(launched);
+      static const bool old_products = [] {
+        const char* m = std::getenv("QVB_PRODUCTS");
+        return m && std::string(m) == "lockstep";
+      }();
+      if (!g.prod_bufw && nseg <= kPtKMax && g.long_threshold <= 256 && !old_products) {
+        // once per graph: the static staging layout of every slice; buffers
+        // sized to the largest slice plus the zero words (chains <=
+        // long_threshold), capped by the 10-bit run starts
+        g.prod_zw = (std::max<uint32_t>(g.long_threshold, 4) + 3) & ~3u;
+        DevBuf<unsigned> mx(1, s);
+        QVB_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(unsigned), s));
+        k_stage_words<<<grid_for(g.nm_S, 256), 256, 0, s>>>(nseg, g.nm_S, g.nm_sbase, mx.p);
+        QVB_LAUNCH_CHECK();
+        const unsigned most = read_scalar(mx.p, s);
+        g.prod_bufw = std::min<uint32_t>(kPtMaxBufw, (most + g.prod_zw + 31) & ~31u);
+        QVB_CUDA(cudaMalloc(&g.nm_desc, g.nm_S * nseg * sizeof(uint64_t)));
+        QVB_CUDA(cudaMalloc(&g.nm_runs, g.nm_S * 32 * 2 * sizeof(uint64_t)));
+        g.bytes += g.nm_S * nseg * sizeof(uint64_t) + g.nm_S * 32 * 2 * sizeof(uint64_t);
+        DevBuf<unsigned> big(1, s);
+        QVB_CUDA(cudaMemsetAsync(big.p, 0, sizeof(unsigned), s));
+        k_build_runs<<<grid_for(g.nm_S * 32, 256), 256, 0, s>>>(
+            nseg, g.nm_S, g.nm_lenf, g.nm_sbase, g.prod_bufw, g.prod_zw, g.nm_desc,
+            reinterpret_cast<ulonglong2*>(g.nm_runs), big.p);
+        QVB_LAUNCH_CHECK();
+        g.prod_big = read_scalar(big.p, s);
+        const size_t smem = (size_t)kPtWarps * pt_warp_bytes(g.prod_bufw);
+        QVB_CUDA(cudaFuncSetAttribute(k_products_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        g.prod_grid = resident_grid(k_products_tma, kPtWarps * 32, smem,
+                                    (g.nm_S + kPtWarps - 1) / kPtWarps);
+      }
       pt.begin(2);
-      k_products<<<static_cast<unsigned>((g.nm_S + kWarpsPerBlock - 1) / kWarpsPerBlock),
-                   kWarpsPerBlock * 32, 0, s>>>(nseg, g.nm_S, n, g.nm_lenf, g.nm_sbase, g.nm_code,
-                                                g.nm_col, g.exc_src, g.exc_R, g.p[cur], g.inv,
-                                                pout, kout, g.marked);
+      if (g.prod_bufw && !old_products) {
+        const size_t smem = (size_t)kPtWarps * pt_warp_bytes(g.prod_bufw);
+        k_products_tma<<<g.prod_grid, kPtWarps * 32, smem, s>>>(
+            nseg, g.nm_S, n, g.nm_lenf, g.nm_desc, reinterpret_cast<const ulonglong2*>(g.nm_runs),
+            g.nm_sbase, g.nm_code, g.nm_col, g.exc_src, g.exc_R, g.p[cur], g.inv, pout, kout,
+            g.marked, g.prod_bufw, g.prod_zw);
+      } else {
+        k_products<<<static_cast<unsigned>((g.nm_S + kWarpsPerBlock - 1) / kWarpsPerBlock),
+                     kWarpsPerBlock * 32, 0, s>>>(nseg, g.nm_S, n, g.nm_lenf, g.nm_sbase, g.nm_code,
+                                                  g.nm_col, g.exc_src, g.exc_R, g.p[cur], g.inv,
+                                                  pout, kout, g.marked);
+      }
       QVB_LAUNCH_CHECK();
       pt.end(1);
       continue;

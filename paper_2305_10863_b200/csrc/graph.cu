@@ -51,6 +51,8 @@ qvb_graph::~qvb_graph() {
   cudaFree(inv);
   cudaFree(state);
   cudaFree(nm_lenf);
+  cudaFree(nm_desc);
+  cudaFree(nm_runs);
   cudaFree(nm_sbase);
   cudaFree(nm_col);
   cudaFree(nm_code);

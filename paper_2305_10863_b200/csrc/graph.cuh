@@ -141,6 +141,13 @@ struct qvb_graph {
   size_t phase_used = 0;
   uint32_t launches = 0;  // kernels launched by the last run
   unsigned f1_grid = 0, codes_grid = 0;  // resident grids, computed on first use
+  // k_products_tma's static staging layout (access_prob.cu), built on first use
+  uint64_t* nm_desc = nullptr;  // [S][K] bulk-copy descriptor per (slice, pass)
+  uint64_t* nm_runs = nullptr;  // [N pad][2] per node: staged run of every pass
+  uint32_t prod_bufw = 0;       // words per staging buffer (0: not built)
+  uint32_t prod_zw = 0;         // zero words closing each buffer (sentinel runs)
+  uint32_t prod_big = 0;        // slices too large for the buffer (global path)   // k_products_tma: words per staging buffer (0: not sized yet)
+  unsigned prod_grid = 0;
   // qvb_access_prob reuses the buffers above: calls are serialised on the
   // host (run_mu) and, across streams, on the device (each call's stream
   // waits for the previous call's done event)
