@@ -203,11 +203,22 @@ int qvb_plan_placement(int device, const double* values, uint64_t n, const qvb_t
                        uint64_t* loc_offsets, int64_t* loc_ids, uint64_t loc_capacity,
                        uint64_t* copies_out);
 
+/* The same plan held by the library (no caller-side upper bound on the copy
+ * count, which is n x servers x (G+1) in the worst case): create, read its
+ * size, copy it into exactly-sized buffers, destroy. */
+typedef struct qvb_plan qvb_plan;
+int qvb_plan_placement_create(int device, const double* values, uint64_t n,
+                              const qvb_topology* topo, qvb_plan** out);
+int qvb_plan_size(const qvb_plan* plan, uint64_t* n, uint64_t* copies);
+int qvb_plan_copy(const qvb_plan* plan, uint64_t* loc_offsets, int64_t* loc_ids);
+int qvb_plan_destroy(qvb_plan* plan);
+
 /* ---- K3: feature lookup table (placement.cpp:306-342) ------------------- */
 /* qv::build_lookup_table(plan, topo, home_server). Reader = GPU
  * `reader_device` of home_server (0 reproduces the reference's
  * reference_reader, placement.cpp:292-295; >0 is the per-reader extension).
- * Output: location_ids[n], offsets[n] (host). */
+ * Output: location_ids[n], offsets[n] (host). Any number of locations
+ * (servers x (G+2)); a feature without copies gets (-1, 0), as the reference. */
 int qvb_build_lookup_table(int device, const uint64_t* loc_offsets, const int64_t* loc_ids,
                            uint64_t n, const qvb_topology* topo, uint32_t home_server,
                            uint32_t reader_device, int64_t* location_ids, uint64_t* offsets);

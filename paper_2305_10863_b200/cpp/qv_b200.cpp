@@ -409,12 +409,18 @@ void PlacementPlan::validate(const ClusterTopology& topo) const {
 PlacementPlan plan_placement(const FapTable& fap, const ClusterTopology& topo) {
   qvb_topology c = to_c(topo);
   const std::uint64_t n = fap.values.size();
-  const std::uint64_t cap = std::max<std::uint64_t>(1, n * topo.servers * (topo.gpus_per_server + 1));
+  qvb_plan* h = nullptr;
+  check(qvb_plan_placement_create(default_device(), fap.values.data(), n, &c, &h));
+  std::uint64_t nn = 0, copies = 0;
   std::vector<std::uint64_t> lo(n + 1);
-  std::vector<std::int64_t> ids(cap);
-  std::uint64_t copies = 0;
-  check(qvb_plan_placement(default_device(), fap.values.data(), n, &c, lo.data(), ids.data(), cap,
-                           &copies));
+  std::vector<std::int64_t> ids;
+  int rc = qvb_plan_size(h, &nn, &copies);
+  if (rc == QVB_OK) {
+    ids.resize(copies);
+    rc = qvb_plan_copy(h, lo.data(), ids.data());
+  }
+  qvb_plan_destroy(h);
+  check(rc);
   PlacementPlan p;
   p.feature_count = n;
   p.locations.resize(n);

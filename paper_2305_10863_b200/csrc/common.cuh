@@ -7,7 +7,10 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <stdexcept>
+#include <tuple>
 #include <string>
 #include <utility>
 
@@ -136,6 +139,24 @@ inline unsigned resident_grid(Kernel k, int block, size_t smem, uint64_t work_bl
   uint64_t g = static_cast<uint64_t>(sms) * (per_sm > 0 ? per_sm : 1);
   if (work_blocks < g) g = work_blocks;
   return static_cast<unsigned>(g ? g : 1);
+}
+
+// resident_grid(k, block, smem, ~0) of the CURRENT device, cached per
+// (kernel, device, block, smem): launch paths call it every launch, several
+// stores may live on different devices, and first calls may race.
+template <typename Kernel>
+inline unsigned resident_grid_cached(Kernel k, int block, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, size_t>, unsigned> cache;
+  int dev = 0;
+  QVB_CUDA(cudaGetDevice(&dev));
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(k), dev, block, smem);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const unsigned g = resident_grid(k, block, smem, ~0ull);
+  cache.emplace(key, g);
+  return g;
 }
 
 inline unsigned grid_for(uint64_t items, unsigned block, unsigned cap = 148u * 64u) {

@@ -17,6 +17,8 @@
 //       copy is the first of the feature's locations in the reader's
 //       (cost, id) order — the reference's min-cost, lowest-id rule.
 #include <algorithm>
+#include <memory>
+#include <vector>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -172,6 +174,101 @@ __global__ void __launch_bounds__(kTile)
   const uint64_t m = f < n ? masks[f] : 0;
   const uint32_t pre = block_prefix(m, loc, nloc, wcnt);
   if (f < n && ((m >> loc) & 1)) feat_of_row[tile_off[(uint64_t)loc * ntiles + t] + pre] = f;
+}
+
+// ---- K3 for any number of locations (multi-server topologies: S x (G+2)
+// location ids can exceed one 64-bit mask). Copies are listed feature by
+// feature, so a stable sort of copy indices by location id leaves each
+// location's copies in ascending feature order: a copy's offset is its rank
+// inside its location's run — the reference's cursor[loc]++ (placement.cpp:
+// 318-330) computed for all copies at once.
+__global__ void k_copy_keys(const uint64_t* __restrict__ lo, const int64_t* __restrict__ ids,
+                            uint64_t n, int nloc, uint64_t* __restrict__ keys,
+                            uint64_t* __restrict__ idx, unsigned long long* bad) {
+  for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < n;
+       f += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = lo[f], b = lo[f + 1];
+    for (uint64_t k = a; k < b; ++k) {
+      const int64_t id = ids[k];
+      if (id < 0 || id >= nloc) {
+        atomicMin(bad, (unsigned long long)(f << 1));
+        keys[k] = 0;
+      } else {
+        keys[k] = static_cast<uint64_t>(id);  // a repeated location consumes a slot per copy
+      }
+      idx[k] = k;
+    }
+  }
+}
+
+// run starts: first sorted position of every location id present
+__global__ void k_run_starts(const uint64_t* __restrict__ skeys, uint64_t copies,
+                             uint64_t* __restrict__ start) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < copies;
+       p += (uint64_t)gridDim.x * blockDim.x)
+    if (p == 0 || skeys[p] != skeys[p - 1]) start[skeys[p]] = p;
+}
+
+__global__ void k_copy_offsets(const uint64_t* __restrict__ skeys, const uint64_t* __restrict__ sidx,
+                               uint64_t copies, const uint64_t* __restrict__ start,
+                               uint64_t* __restrict__ copy_off) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < copies;
+       p += (uint64_t)gridDim.x * blockDim.x)
+    copy_off[sidx[p]] = p - start[skeys[p]];
+}
+
+// per feature: the copy whose location ranks first in the reader's
+// (cost, id) order (placement.cpp:323-337)
+__global__ void k_choose_general(const uint64_t* __restrict__ lo, const int64_t* __restrict__ ids,
+                                 const uint64_t* __restrict__ copy_off,
+                                 const uint32_t* __restrict__ rank_of_loc, uint64_t n,
+                                 int64_t* __restrict__ out_loc, uint64_t* __restrict__ out_off) {
+  for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < n;
+       f += (uint64_t)gridDim.x * blockDim.x) {
+    int64_t best = -1;
+    uint32_t best_rank = 0xFFFFFFFFu;
+    uint64_t off = 0;
+    for (uint64_t k = lo[f]; k < lo[f + 1]; ++k) {
+      const uint32_t r = rank_of_loc[ids[k]];
+      if (r < best_rank) {
+        best_rank = r;
+        best = ids[k];
+        off = copy_off[k];
+      }
+    }
+    out_loc[f] = best;  // -1, offset 0 for a feature without copies, as the reference
+    out_off[f] = off;
+  }
+}
+
+void lut_build_general(const uint64_t* d_lo, const int64_t* d_ids, uint64_t n, uint64_t copies,
+                       int nloc, const std::vector<int>& order, int64_t* d_loc, uint64_t* d_off,
+                       cudaStream_t s) {
+  DevBuf<unsigned long long> flags(1, s);
+  QVB_CUDA(cudaMemsetAsync(flags.p, 0xFF, sizeof(unsigned long long), s));
+  const uint64_t c = copies ? copies : 1;
+  DevBuf<uint64_t> keys(c, s), skeys(c, s), idx(c, s), sidx(c, s), off(c, s), start(nloc, s);
+  k_copy_keys<<<grid_for(n, 256), 256, 0, s>>>(d_lo, d_ids, n, nloc, keys.p, idx.p, flags.p);
+  QVB_LAUNCH_CHECK();
+  const unsigned long long b = read_scalar(flags.p, s);
+  if (b != ~0ull) {
+    const uint64_t f = b >> 1;
+    if (b & 1) fail(QVB_ERR_VALIDATION, "feature " + std::to_string(f) + " lists a location twice");
+    fail(QVB_ERR_VALIDATION, "unknown location id for feature " + std::to_string(f));
+  }
+  if (copies) {
+    sort_pairs_u64_u64(keys.p, skeys.p, idx.p, sidx.p, copies, 0, bits_for((uint64_t)nloc - 1), s);
+    k_run_starts<<<grid_for(copies, 256), 256, 0, s>>>(skeys.p, copies, start.p);
+    QVB_LAUNCH_CHECK();
+    k_copy_offsets<<<grid_for(copies, 256), 256, 0, s>>>(skeys.p, sidx.p, copies, start.p, off.p);
+    QVB_LAUNCH_CHECK();
+  }
+  std::vector<uint32_t> rank(nloc);
+  for (int i = 0; i < nloc; ++i) rank[order[i]] = static_cast<uint32_t>(i);
+  DevBuf<uint32_t> drank(nloc, s);
+  QVB_CUDA(cudaMemcpyAsync(drank.p, rank.data(), nloc * 4, cudaMemcpyHostToDevice, s));
+  k_choose_general<<<grid_for(n, 256), 256, 0, s>>>(d_lo, d_ids, off.p, drank.p, n, d_loc, d_off);
+  QVB_LAUNCH_CHECK();
 }
 
 // LPT over one NUMA group's slots (placement.cpp:100-115).
@@ -480,34 +577,45 @@ extern "C" int qvb_rank_desc(int device, const double* values, uint64_t n, uint6
   });
 }
 
+struct qvb_plan {
+  HostPlan p;
+};
+
+namespace {
+HostPlan plan_on_device(int device, const double* values, uint64_t n, const qvb_topology* topo) {
+  if (!topo) fail(QVB_ERR_VALIDATION, "null topology");
+  topology_validate(*topo);  // placement.cpp:139
+  if (n == 0) fail(QVB_ERR_VALIDATION, "placement needs at least one feature");
+  if (!values) fail(QVB_ERR_VALIDATION, "null argument");
+  if (topo->nvlink_within_numa && gpus_per_numa(*topo) > 255)
+    fail(QVB_ERR_UNSUPPORTED, "more than 255 GPUs per NUMA group");
+  // the device ranks the features and hands the sequential planner its
+  // inputs in the order it walks them: values in rank order and each
+  // feature's rank position (no random host reads over n values)
+  std::vector<double> vr(n);
+  std::vector<uint64_t> pos(n);
+  {
+    DeviceGuard dg(device);
+    cudaStream_t s = nullptr;
+    DevBuf<double> dv(n, s), dvr(n, s);
+    DevBuf<uint64_t> dr(n, s), dpos(n, s);
+    QVB_CUDA(cudaMemcpyAsync(dv.p, values, n * 8, cudaMemcpyHostToDevice, s));
+    rank_desc_device(dv.p, n, dr.p, s);
+    k_rank_views<<<grid_for(n, 256), 256, 0, s>>>(dv.p, dr.p, n, dvr.p, dpos.p);
+    QVB_LAUNCH_CHECK();
+    copy_to_host(vr.data(), dvr.p, n * 8, s);
+    copy_to_host(pos.data(), dpos.p, n * 8, s);
+  }
+  return plan_from_ranks(vr.data(), pos.data(), n, *topo);
+}
+}  // namespace
+
 extern "C" int qvb_plan_placement(int device, const double* values, uint64_t n,
                                   const qvb_topology* topo, uint64_t* loc_offsets,
                                   int64_t* loc_ids, uint64_t loc_capacity, uint64_t* copies_out) {
   return guarded([&] {
-    if (!topo) fail(QVB_ERR_VALIDATION, "null topology");
-    topology_validate(*topo);  // placement.cpp:139
-    if (n == 0) fail(QVB_ERR_VALIDATION, "placement needs at least one feature");
-    if (!values || !loc_offsets || !copies_out) fail(QVB_ERR_VALIDATION, "null argument");
-    if (topo->nvlink_within_numa && gpus_per_numa(*topo) > 255)
-      fail(QVB_ERR_UNSUPPORTED, "more than 255 GPUs per NUMA group");
-    // the device ranks the features and hands the sequential planner its
-    // inputs in the order it walks them: values in rank order and each
-    // feature's rank position (no random host reads over n values)
-    std::vector<double> vr(n);
-    std::vector<uint64_t> pos(n);
-    {
-      DeviceGuard dg(device);
-      cudaStream_t s = nullptr;
-      DevBuf<double> dv(n, s), dvr(n, s);
-      DevBuf<uint64_t> dr(n, s), dpos(n, s);
-      QVB_CUDA(cudaMemcpyAsync(dv.p, values, n * 8, cudaMemcpyHostToDevice, s));
-      rank_desc_device(dv.p, n, dr.p, s);
-      k_rank_views<<<grid_for(n, 256), 256, 0, s>>>(dv.p, dr.p, n, dvr.p, dpos.p);
-      QVB_LAUNCH_CHECK();
-      copy_to_host(vr.data(), dvr.p, n * 8, s);
-      copy_to_host(pos.data(), dpos.p, n * 8, s);
-    }
-    HostPlan p = plan_from_ranks(vr.data(), pos.data(), n, *topo);
+    if (!loc_offsets || !copies_out) fail(QVB_ERR_VALIDATION, "null argument");
+    HostPlan p = plan_on_device(device, values, n, topo);
     *copies_out = p.ids.size();
     if (p.ids.size() > loc_capacity)
       fail(QVB_ERR_VALIDATION, "loc_capacity " + std::to_string(loc_capacity) + " too small, need " +
@@ -515,6 +623,38 @@ extern "C" int qvb_plan_placement(int device, const double* values, uint64_t n,
     std::copy(p.offsets.begin(), p.offsets.end(), loc_offsets);
     if (!p.ids.empty()) std::copy(p.ids.begin(), p.ids.end(), loc_ids);
   });
+}
+
+extern "C" int qvb_plan_placement_create(int device, const double* values, uint64_t n,
+                                         const qvb_topology* topo, qvb_plan** out) {
+  return guarded([&] {
+    if (!out) fail(QVB_ERR_VALIDATION, "null argument");
+    *out = nullptr;
+    auto h = std::make_unique<qvb_plan>();
+    h->p = plan_on_device(device, values, n, topo);
+    *out = h.release();
+  });
+}
+
+extern "C" int qvb_plan_size(const qvb_plan* plan, uint64_t* n, uint64_t* copies) {
+  return guarded([&] {
+    if (!plan || !n || !copies) fail(QVB_ERR_VALIDATION, "null argument");
+    *n = plan->p.offsets.size() - 1;
+    *copies = plan->p.ids.size();
+  });
+}
+
+extern "C" int qvb_plan_copy(const qvb_plan* plan, uint64_t* loc_offsets, int64_t* loc_ids) {
+  return guarded([&] {
+    if (!plan || !loc_offsets || (!loc_ids && !plan->p.ids.empty()))
+      fail(QVB_ERR_VALIDATION, "null argument");
+    std::copy(plan->p.offsets.begin(), plan->p.offsets.end(), loc_offsets);
+    std::copy(plan->p.ids.begin(), plan->p.ids.end(), loc_ids);
+  });
+}
+
+extern "C" int qvb_plan_destroy(qvb_plan* plan) {
+  return guarded([&] { delete plan; });
 }
 
 extern "C" int qvb_build_lookup_table(int device, const uint64_t* loc_offsets,
@@ -535,11 +675,17 @@ extern "C" int qvb_build_lookup_table(int device, const uint64_t* loc_offsets,
     DevBuf<int64_t> dids(copies ? copies : 1, s);
     QVB_CUDA(cudaMemcpyAsync(dlo.p, loc_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
     if (copies) QVB_CUDA(cudaMemcpyAsync(dids.p, loc_ids, copies * 8, cudaMemcpyHostToDevice, s));
-    DeviceLut L;
-    lut_prepare(L, dlo.p, dids.p, n, nloc, s);
     DevBuf<int64_t> dloc(n, s);
     DevBuf<uint64_t> doff(n, s);
-    lut_choose(L, replica_order(*topo, home_server, reader_device), dloc.p, doff.p, nullptr, s);
+    const char* gen = std::getenv("QVB_LUT_GENERAL");  // tests: force the any-location path
+    if (nloc <= kMaxLocations && !(gen && *gen == '1')) {  // one location mask per feature
+      DeviceLut L;
+      lut_prepare(L, dlo.p, dids.p, n, nloc, s);
+      lut_choose(L, replica_order(*topo, home_server, reader_device), dloc.p, doff.p, nullptr, s);
+    } else {
+      lut_build_general(dlo.p, dids.p, n, copies, nloc, replica_order(*topo, home_server, reader_device),
+                        dloc.p, doff.p, s);
+    }
     QVB_CUDA(cudaMemcpyAsync(location_ids, dloc.p, n * 8, cudaMemcpyDeviceToHost, s));
     QVB_CUDA(cudaMemcpyAsync(offsets, doff.p, n * 8, cudaMemcpyDeviceToHost, s));
     QVB_CUDA(cudaStreamSynchronize(s));

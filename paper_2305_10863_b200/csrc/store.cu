@@ -589,7 +589,8 @@ struct qvb_store {
   Bases bases{};
   void* peer[kMaxLocations] = {};
   uint64_t used_mask = 0;
-  unsigned long long* err = nullptr;
+  unsigned long long* err = nullptr;       // qvb_gather / qvb_gather_planned
+  unsigned long long* err_host = nullptr;  // qvb_gather_host's own slot (under host_mu)
   // e2e scratch; host_mu serialises qvb_gather_host calls on one store (the
   // scratch and the error slot are shared), device-side qvb_gather calls on
   // different streams stay concurrent
@@ -633,7 +634,7 @@ struct qvb_store {
     return n * 8 <= (32ull << 20) ? 1 : 0;
   }
 
-  void launch_gather(const uint64_t* ids, uint64_t b, char* out, cudaStream_t s) {
+  void launch_gather(const uint64_t* ids, uint64_t b, char* out, cudaStream_t s, unsigned long long* err) {
     check_attached();
     if (reinterpret_cast<uintptr_t>(out) % vec() != 0)
       fail(QVB_ERR_VALIDATION, "output buffer is not aligned to the row vector width");
@@ -647,11 +648,11 @@ struct qvb_store {
     }();
     const bool host_used = (used_mask >> (nloc - 2)) & 1;
     if (kind == 3 && row_bytes % 16 == 0 && row_bytes <= 512) {
-      launch_cp(ids, b, out, s);
+      launch_cp(ids, b, out, s, err);
       return;
     }
     if (kind == 2 && row_bytes % 16 == 0 && !host_used) {
-      launch_tma(ids, b, out, s);
+      launch_tma(ids, b, out, s, err);
       return;
     }
     // Small batches: the row-group kernels give each warp 32 requests, so a
@@ -665,19 +666,19 @@ struct qvb_store {
     const char* sm = std::getenv("QVB_GATHER_SMALL");
     const uint64_t small_rows = sm ? std::strtoull(sm, nullptr, 10) : 49152ull;
     if (kind != 1 && b > small_rows) {
-      if (V == 16) launch_rows<16>(ids, b, cpr, out, s);
-      else if (V == 8 && stride % 16 == 0) launch_rows_wide(ids, b, out, s);
-      else if (V == 8) launch_rows<8>(ids, b, cpr, out, s);
-      else launch_rows<4>(ids, b, cpr, out, s);
+      if (V == 16) launch_rows<16>(ids, b, cpr, out, s, err);
+      else if (V == 8 && stride % 16 == 0) launch_rows_wide(ids, b, out, s, err);
+      else if (V == 8) launch_rows<8>(ids, b, cpr, out, s, err);
+      else launch_rows<4>(ids, b, cpr, out, s, err);
       return;
     }
     const uint64_t max_rows = std::max<uint64_t>(1, (0xFFFFFFFFull / cpr) / 2);
     for (uint64_t r0 = 0; r0 < b; r0 += max_rows) {
       const uint32_t rows = static_cast<uint32_t>(std::min(max_rows, b - r0));
       char* o = out + r0 * row_bytes;
-      if (V == 16) launch_direct<16>(ids + r0, rows, cpr, o, r0, s);
-      else if (V == 8) launch_direct<8>(ids + r0, rows, cpr, o, r0, s);
-      else launch_direct<4>(ids + r0, rows, cpr, o, r0, s);
+      if (V == 16) launch_direct<16>(ids + r0, rows, cpr, o, r0, s, err);
+      else if (V == 8) launch_direct<8>(ids + r0, rows, cpr, o, r0, s, err);
+      else launch_direct<4>(ids + r0, rows, cpr, o, r0, s, err);
     }
   }
 
@@ -688,9 +689,8 @@ struct qvb_store {
 
   template <int V>
   void launch_direct(const uint64_t* ids, uint32_t rows, uint32_t cpr, char* o, uint64_t r0,
-                     cudaStream_t s) {
-    static unsigned full = 0;  // resident blocks on this GPU (one wave)
-    if (!full) full = resident_grid(k_gather<V>, kGatherBlock, 0, ~0ull);
+                     cudaStream_t s, unsigned long long* err) {
+    const unsigned full = resident_grid_cached(k_gather<V>, kGatherBlock, 0);  // one resident wave
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(full, work_blocks((uint64_t)rows * cpr)));
     k_gather<V><<<grid, kGatherBlock, 0, s>>>(ids, rows, lut, bases, stride, cpr, row_bytes, n, o,
                                               r0, err);
@@ -698,29 +698,26 @@ struct qvb_store {
   }
 
   template <int V>
-  void launch_rows(const uint64_t* ids, uint64_t rows, uint32_t cpr, char* o, cudaStream_t s) {
+  void launch_rows(const uint64_t* ids, uint64_t rows, uint32_t cpr, char* o, cudaStream_t s, unsigned long long* err) {
     static const int variant = [] {
       const char* u = std::getenv("QVB_GATHER_U");
       return u ? std::atoi(u) : 0;
     }();
-    if (variant == 8) launch_rows_u<V, 8, 1>(ids, rows, cpr, o, s);
-    else if (variant == 4) launch_rows_u<V, 4, 4>(ids, rows, cpr, o, s);
-    else if (variant == 2) launch_rows_u<V, 2, 6>(ids, rows, cpr, o, s);
-    else launch_rows_u<V, 4, 4>(ids, rows, cpr, o, s);
+    if (variant == 8) launch_rows_u<V, 8, 1>(ids, rows, cpr, o, s, err);
+    else if (variant == 4) launch_rows_u<V, 4, 4>(ids, rows, cpr, o, s, err);
+    else if (variant == 2) launch_rows_u<V, 2, 6>(ids, rows, cpr, o, s, err);
+    else launch_rows_u<V, 4, 4>(ids, rows, cpr, o, s, err);
   }
 
-  void launch_cp(const uint64_t* ids, uint64_t rows, char* o, cudaStream_t s) {
+  void launch_cp(const uint64_t* ids, uint64_t rows, char* o, cudaStream_t s, unsigned long long* err) {
     const uint32_t cpr = row_bytes / 16;
     const uint64_t per_warp = 2ull * cpr * 32 * 16;
     const uint32_t warps = static_cast<uint32_t>(
         std::max<uint64_t>(1, std::min<uint64_t>(8, (200u << 10) / per_warp)));
     const size_t smem = warps * per_warp;
-    static size_t configured = 0;
-    if (configured < smem) {
-      QVB_CUDA(cudaFuncSetAttribute(k_gather_cp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-      configured = smem;
-    }
+    // per call: the attribute is per device, and stores may live on several
+    QVB_CUDA(cudaFuncSetAttribute(k_gather_cp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
     int per_sm = 0, dev = 0, sms = 0;
     QVB_CUDA(cudaGetDevice(&dev));
     QVB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -733,18 +730,14 @@ struct qvb_store {
     QVB_LAUNCH_CHECK();
   }
 
-  void launch_tma(const uint64_t* ids, uint64_t rows, char* o, cudaStream_t s) {
+  void launch_tma(const uint64_t* ids, uint64_t rows, char* o, cudaStream_t s, unsigned long long* err) {
     const uint64_t per_warp = (uint64_t)kTmaBuffers * 32 * row_bytes;
     const uint32_t warps = static_cast<uint32_t>(
         std::max<uint64_t>(1, std::min<uint64_t>(8, (200u << 10) / per_warp)));
     const size_t smem = 8 * kTmaBuffers * warps + 128 + (size_t)warps * per_warp;
     if (smem > (227u << 10)) fail(QVB_ERR_UNSUPPORTED, "row too large for the TMA gather");
-    static size_t configured = 0;
-    if (configured < smem) {
-      QVB_CUDA(cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-      configured = smem;
-    }
+    QVB_CUDA(cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
     int per_sm = 0, dev = 0, sms = 0;
     QVB_CUDA(cudaGetDevice(&dev));
     QVB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -757,9 +750,8 @@ struct qvb_store {
     QVB_LAUNCH_CHECK();
   }
 
-  void launch_rows_wide(const uint64_t* ids, uint64_t rows, char* o, cudaStream_t s) {
-    static unsigned full = 0;
-    if (!full) full = resident_grid(k_gather_rows_w<4, 4>, kGatherBlock, 0, ~0ull);
+  void launch_rows_wide(const uint64_t* ids, uint64_t rows, char* o, cudaStream_t s, unsigned long long* err) {
+    const unsigned full = resident_grid_cached(k_gather_rows_w<4, 4>, kGatherBlock, 0);  // one resident wave
     const uint32_t cpr16 = (row_bytes + 15) / 16;
     const uint64_t warps_needed = (rows + 31) / 32;
     const uint64_t blocks = (warps_needed + kGatherBlock / 32 - 1) / (kGatherBlock / 32);
@@ -770,10 +762,9 @@ struct qvb_store {
   }
 
   template <int V, int U, int MB>
-  void launch_rows_u(const uint64_t* ids, uint64_t rows, uint32_t cpr, char* o, cudaStream_t s) {
+  void launch_rows_u(const uint64_t* ids, uint64_t rows, uint32_t cpr, char* o, cudaStream_t s, unsigned long long* err) {
     const int lut_keep = lut_keep_flag();
-    static unsigned full = 0;
-    if (!full) full = resident_grid(k_gather_rows<V, U, MB>, kGatherBlock, 0, ~0ull);
+    const unsigned full = resident_grid_cached(k_gather_rows<V, U, MB>, kGatherBlock, 0);  // one resident wave
     const uint64_t warps_needed = (rows + 31) / 32;
     const uint64_t blocks = (warps_needed + kGatherBlock / 32 - 1) / (kGatherBlock / 32);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(full, blocks));
@@ -784,16 +775,15 @@ struct qvb_store {
 
   template <int V, typename K>
   void launch_sorted(const K* keys, const uint32_t* order, uint32_t rows, uint32_t cpr, char* o,
-                     int ob, cudaStream_t s) {
-    static unsigned full = 0;
-    if (!full) full = resident_grid(k_gather_sorted<V, K>, kGatherBlock, 0, ~0ull);
+                     int ob, cudaStream_t s, unsigned long long* err) {
+    const unsigned full = resident_grid_cached(k_gather_sorted<V, K>, kGatherBlock, 0);  // one resident wave
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(full, work_blocks((uint64_t)rows * cpr)));
     k_gather_sorted<V, K><<<grid, kGatherBlock, 0, s>>>(keys, order, rows, bases, stride, cpr,
                                                         row_bytes, o, ob);
     QVB_LAUNCH_CHECK();
   }
 
-  void launch_planned(const uint64_t* ids, uint64_t b, char* out, cudaStream_t s) {
+  void launch_planned(const uint64_t* ids, uint64_t b, char* out, cudaStream_t s, unsigned long long* err) {
     check_attached();
     if (b >= (1ull << 32)) fail(QVB_ERR_UNSUPPORTED, "batch exceeds 2^32 ids");
     const int V = vec();
@@ -808,18 +798,18 @@ struct qvb_store {
       k_plan_keys32<<<grid_for(b, 256), 256, 0, s>>>(ids, b, lut, n, ob, keys.p, idx.p, err);
       QVB_LAUNCH_CHECK();
       sort_pairs_u32_u32(keys.p, skeys.p, idx.p, order.p, b, 0, ob + loc_bits, s);
-      if (V == 16) launch_sorted<16>(skeys.p, order.p, rows, cpr, out, ob, s);
-      else if (V == 8) launch_sorted<8>(skeys.p, order.p, rows, cpr, out, ob, s);
-      else launch_sorted<4>(skeys.p, order.p, rows, cpr, out, ob, s);
+      if (V == 16) launch_sorted<16>(skeys.p, order.p, rows, cpr, out, ob, s, err);
+      else if (V == 8) launch_sorted<8>(skeys.p, order.p, rows, cpr, out, ob, s, err);
+      else launch_sorted<4>(skeys.p, order.p, rows, cpr, out, ob, s, err);
       return;
     }
     DevBuf<uint64_t> keys(b, s), skeys(b, s);
     k_plan_keys_packed<<<grid_for(b, 256), 256, 0, s>>>(ids, b, lut, n, keys.p, idx.p, err);
     QVB_LAUNCH_CHECK();
     sort_pairs_u64_u32(keys.p, skeys.p, idx.p, order.p, b, 0, kOffsetBits + loc_bits, s);
-    if (V == 16) launch_sorted<16>(skeys.p, order.p, rows, cpr, out, kOffsetBits, s);
-    else if (V == 8) launch_sorted<8>(skeys.p, order.p, rows, cpr, out, kOffsetBits, s);
-    else launch_sorted<4>(skeys.p, order.p, rows, cpr, out, kOffsetBits, s);
+    if (V == 16) launch_sorted<16>(skeys.p, order.p, rows, cpr, out, kOffsetBits, s, err);
+    else if (V == 8) launch_sorted<8>(skeys.p, order.p, rows, cpr, out, kOffsetBits, s, err);
+    else launch_sorted<4>(skeys.p, order.p, rows, cpr, out, kOffsetBits, s, err);
   }
 
   ~qvb_store() {
@@ -833,6 +823,7 @@ struct qvb_store {
     cudaFree(local);
     if (host) cudaFreeHost(host);
     cudaFree(err);
+    cudaFree(err_host);
     cudaFree(d_ids);
     cudaFree(d_out);
     for (auto q : hs)
@@ -912,6 +903,8 @@ extern "C" int qvb_store_create(int device, const uint64_t* loc_offsets, const i
     st->stride = (st->row_bytes + align - 1) / align * align;
     QVB_CUDA(cudaMalloc(&st->err, sizeof(unsigned long long)));
     QVB_CUDA(cudaMemset(st->err, 0xFF, sizeof(unsigned long long)));
+    QVB_CUDA(cudaMalloc(&st->err_host, sizeof(unsigned long long)));
+    QVB_CUDA(cudaMemset(st->err_host, 0xFF, sizeof(unsigned long long)));
 
     const uint64_t copies = loc_offsets[n];
     DevBuf<uint64_t> dlo(n + 1, s);
@@ -1025,7 +1018,7 @@ extern "C" int qvb_gather(qvb_store* s, const uint64_t* ids, uint64_t b, float* 
     if (b == 0) return;
     if (!ids || !out) fail(QVB_ERR_VALIDATION, "null argument");
     DeviceGuard dg(s->device);
-    s->launch_gather(ids, b, reinterpret_cast<char*>(out), static_cast<cudaStream_t>(stream));
+    s->launch_gather(ids, b, reinterpret_cast<char*>(out), static_cast<cudaStream_t>(stream), s->err);
   });
 }
 
@@ -1036,7 +1029,7 @@ extern "C" int qvb_gather_planned(qvb_store* s, const uint64_t* ids, uint64_t b,
     if (b == 0) return;
     if (!ids || !out) fail(QVB_ERR_VALIDATION, "null argument");
     DeviceGuard dg(s->device);
-    s->launch_planned(ids, b, reinterpret_cast<char*>(out), static_cast<cudaStream_t>(stream));
+    s->launch_planned(ids, b, reinterpret_cast<char*>(out), static_cast<cudaStream_t>(stream), s->err);
   });
 }
 
@@ -1072,7 +1065,7 @@ extern "C" int qvb_gather_host(qvb_store* s, const uint64_t* ids, uint64_t b, fl
     const uint64_t chunks = b >= want * 16384 ? want : 1;
     if (chunks == 1) {
       QVB_CUDA(cudaMemcpyAsync(s->d_ids, ids, b * 8, cudaMemcpyHostToDevice, st));
-      s->launch_gather(s->d_ids, b, s->d_out, st);
+      s->launch_gather(s->d_ids, b, s->d_out, st, s->err_host);
       QVB_CUDA(cudaMemcpyAsync(out, s->d_out, b * rb, cudaMemcpyDeviceToHost, st));
     } else {
       s->ensure_host_streams();
@@ -1084,7 +1077,7 @@ extern "C" int qvb_gather_host(qvb_store* s, const uint64_t* ids, uint64_t b, fl
         if (a >= b) break;
         cudaStream_t q = s->hs[c & 1];
         QVB_CUDA(cudaMemcpyAsync(s->d_ids + a, ids + a, len * 8, cudaMemcpyHostToDevice, q));
-        s->launch_gather(s->d_ids + a, len, s->d_out + a * rb, q);
+        s->launch_gather(s->d_ids + a, len, s->d_out + a * rb, q, s->err_host);
         QVB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(out) + a * rb, s->d_out + a * rb, len * rb,
                                  cudaMemcpyDeviceToHost, q));
       }
@@ -1095,14 +1088,14 @@ extern "C" int qvb_gather_host(qvb_store* s, const uint64_t* ids, uint64_t b, fl
     }
     QVB_CUDA(cudaStreamSynchronize(st));
     unsigned long long e = 0;
-    QVB_CUDA(cudaMemcpy(&e, s->err, sizeof e, cudaMemcpyDeviceToHost));
+    QVB_CUDA(cudaMemcpy(&e, s->err_host, sizeof e, cudaMemcpyDeviceToHost));
     if (e != ~0ull) {
-      QVB_CUDA(cudaMemset(s->err, 0xFF, sizeof(unsigned long long)));
+      QVB_CUDA(cudaMemset(s->err_host, 0xFF, sizeof(unsigned long long)));
       // chunked launches report chunk-relative indices: name the first bad id
       uint64_t i = 0;
       while (i < b && ids[i] < s->n) ++i;
-      fail(QVB_ERR_VALIDATION, "feature id " + std::to_string(i < b ? ids[i] : ids[e]) +
-                                   " outside lookup table");
+      if (i < b) fail(QVB_ERR_VALIDATION, "feature id " + std::to_string(ids[i]) + " outside lookup table");
+      fail(QVB_ERR_VALIDATION, "feature id outside lookup table");
     }
   });
 }

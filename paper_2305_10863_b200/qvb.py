@@ -174,6 +174,10 @@ _SIGNATURES = {
     "qvb_compute_fap": (i32, [i32, u64, u64, vp, vp, vp, u32, vp, vp]),
     "qvb_rank_desc": (i32, [i32, vp, u64, vp, i32, vp]),
     "qvb_plan_placement": (i32, [i32, vp, u64, P(Topology), vp, vp, u64, P(u64)]),
+    "qvb_plan_placement_create": (i32, [i32, vp, u64, P(Topology), P(vp)]),
+    "qvb_plan_size": (i32, [vp, P(u64), P(u64)]),
+    "qvb_plan_copy": (i32, [vp, vp, vp]),
+    "qvb_plan_destroy": (i32, [vp]),
     "qvb_build_lookup_table": (i32, [i32, vp, vp, u64, P(Topology), u32, u32, vp, vp]),
     "qvb_page_transitions": (i32, [vp, u64, u64, P(u64)]),
     "qvb_plan_reads": (i32, [i32, vp, vp, u64, vp, u64, u64, vp, vp, vp, P(u64), vp]),
@@ -451,13 +455,18 @@ def plan_placement(values, topo: Topology, device: int = 0):
     loc_ids[loc_offsets[f]:loc_offsets[f+1]], ascending encoded location ids."""
     v = np.ascontiguousarray(values, np.float64)
     n = len(v)
-    cap = max(1, n * topo.servers * (topo.gpus_per_server + 1))
-    lo = np.zeros(n + 1, np.uint64)
-    ids = np.zeros(cap, np.int64)
-    copies = u64(0)
-    _check(_lib().qvb_plan_placement(device, _ptr(v) if n else None, n, C.byref(topo), _ptr(lo),
-                                     _ptr(ids), cap, C.byref(copies)))
-    return lo, ids[: copies.value].copy()
+    h = C.c_void_p()
+    _check(_lib().qvb_plan_placement_create(device, _ptr(v) if n else None, n, C.byref(topo),
+                                            C.byref(h)))
+    try:
+        nn, copies = u64(0), u64(0)
+        _check(_lib().qvb_plan_size(h, C.byref(nn), C.byref(copies)))
+        lo = np.zeros(n + 1, np.uint64)
+        ids = np.zeros(max(1, copies.value), np.int64)
+        _check(_lib().qvb_plan_copy(h, _ptr(lo), _ptr(ids)))
+    finally:
+        _lib().qvb_plan_destroy(h)
+    return lo, ids[: copies.value]
 
 
 def build_lookup_table(loc_offsets, loc_ids, topo: Topology, home_server: int = 0,
@@ -545,20 +554,33 @@ class FeatureStore:
         self._peers = getattr(self, "_peers", []) + [peer]
 
     def gather(self, ids, out, stream=None, planned: bool = False) -> None:
-        """Device gather: ids (uint64) and out (float32, b x dim) are device
-        tensors; stream-ordered, no synchronisation."""
+        """Device gather: ids (uint64/int64) and out (float32, b x dim) are
+        contiguous device tensors; stream-ordered, no synchronisation."""
+        import torch
+
+        b = int(ids.numel())
+        if ids.dtype not in (torch.int64, torch.uint64) or not ids.is_contiguous():
+            raise ValidationError("ids must be a contiguous 64-bit integer tensor")
+        if out.dtype != torch.float32 or not out.is_contiguous() or out.numel() < b * self.dim:
+            raise ValidationError(f"out must be a contiguous float32 tensor of at least "
+                                  f"{b} x {self.dim} values")
+        if not ids.is_cuda or not out.is_cuda:
+            raise ValidationError("ids and out must be device tensors (use gather_host for host buffers)")
         fn = _lib().qvb_gather_planned if planned else _lib().qvb_gather
-        _check(fn(self._h, _ptr(ids), int(ids.numel()), _ptr(out), _stream_ptr(stream)))
+        _check(fn(self._h, _ptr(ids), b, _ptr(out), _stream_ptr(stream)))
 
     def check_error(self) -> None:
         _check(_lib().qvb_store_check_error(self._h))
 
     def gather_host(self, ids, out=None, stream=None) -> np.ndarray:
         """End-to-end collect from host buffers (H2D ids, gather, D2H rows)."""
-        req = ids if isinstance(ids, np.ndarray) and ids.dtype == np.uint64 else \
-            np.ascontiguousarray(ids, np.uint64)
+        req = np.ascontiguousarray(ids, np.uint64)  # copies strided / other-typed ids
         if out is None:
             out = np.zeros((len(req), self.dim), np.float32)
+        elif not (isinstance(out, np.ndarray) and out.dtype == np.float32 and out.flags.c_contiguous
+                  and out.shape == (len(req), self.dim)):
+            raise ValidationError(f"out must be a C-contiguous float32 array of shape "
+                                  f"({len(req)}, {self.dim})")
         _check(_lib().qvb_gather_host(self._h, _ptr(req), len(req), _ptr(out), _stream_ptr(stream)))
         return out
 

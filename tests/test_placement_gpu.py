@@ -115,6 +115,62 @@ def test_random_vs_oracle_with_readers(qvb, oracle):
             assert (x == y).all()
 
 
+@pytest.mark.parametrize("servers,gpus", [(8, 8), (12, 6), (3, 30)])
+def test_lookup_table_beyond_64_locations(qvb, oracle, servers, gpus):
+    """S x (G+2) > 64 location ids (e.g. 8 servers x 8 GPUs = 80): the
+    any-location K3 path, equal to the reference restatement for every home
+    server and a few readers (the mask path stopped at 64)."""
+    rng = derive_stream(163, servers * 100 + gpus)
+    n = 5000
+    v = np.array([float(rng.below(97)) / 97 for _ in range(n)])
+    for ib in (0, 1):
+        t = qvb.Topology.with_defaults(servers=servers, numa_per_server=2, gpus_per_server=gpus,
+                                       gpu_feature_capacity=n // (servers * gpus) + 3,
+                                       host_feature_capacity=n // servers + 1,
+                                       disk_feature_capacity=n, nvlink_within_numa=1, infiniband=ib)
+        ot = otopo_from(t)
+        lo, ids = qvb.plan_placement(v, t)
+        lo2, ids2 = oracle.plan_placement(v, ot)
+        assert (lo == lo2).all() and (ids == ids2).all()
+        assert servers * (gpus + 2) > 64
+        for home in range(servers):
+            for reader in (0, gpus - 1):
+                a = qvb.build_lookup_table(lo, ids, t, home, reader)
+                b = oracle.build_lookup_table(lo2, ids2, ot, home, reader)
+                assert (a[0] == b[0]).all() and (a[1] == b[1]).all()
+        req = np.array([rng.below(n) for _ in range(4096)], np.uint64)
+        for x, y in zip(qvb.plan_reads(a[0], a[1], req, 4), oracle.plan_reads(b[0], b[1], req, 4)):
+            assert (x == y).all()
+
+
+def test_lookup_table_general_path_matches_mask_path(qvb, oracle, monkeypatch):
+    """The any-location K3 path forced on small topologies (QVB_LUT_GENERAL=1)
+    gives the same tables as the mask path and the oracle."""
+    rng = derive_stream(167, 3)
+    for _ in range(12):
+        n = 1 + rng.below(4000)
+        v = np.array([float(rng.below(64)) / 64 for _ in range(n)])
+        t = qvb.Topology.with_defaults(servers=1 + rng.below(3), numa_per_server=1 + rng.below(2))
+        t.gpus_per_server = t.numa_per_server * (1 + rng.below(4))
+        t.gpu_feature_capacity = rng.below(600)
+        t.host_feature_capacity = rng.below(2000)
+        t.disk_feature_capacity = n
+        t.nvlink_within_numa = rng.below(2)
+        t.infiniband = rng.below(2)
+        lo, ids = qvb.plan_placement(v, t)
+        ot = otopo_from(t)
+        for home in range(t.servers):
+            reader = rng.below(t.gpus_per_server)
+            monkeypatch.delenv("QVB_LUT_GENERAL", raising=False)
+            a = qvb.build_lookup_table(lo, ids, t, home, reader)
+            monkeypatch.setenv("QVB_LUT_GENERAL", "1")
+            g = qvb.build_lookup_table(lo, ids, t, home, reader)
+            b = oracle.build_lookup_table(lo, ids, ot, home, reader)
+            assert (a[0] == g[0]).all() and (a[1] == g[1]).all()
+            assert (g[0] == b[0]).all() and (g[1] == b[1]).all()
+    monkeypatch.delenv("QVB_LUT_GENERAL", raising=False)
+
+
 def test_lut_properties(qvb):
     # test_placement.cpp:216-234 dense distinct offsets; :236-275 dominance
     rng = derive_stream(107, 2)
