@@ -5,8 +5,9 @@
 
 A "step" is one collect call: gather one batch of B uniform request ids
 (derive_stream(11, 0x5EED, batch).below(N)) from the placed
-feature table. The workload at N=1 is BASELINE configs[1] (C2,
-ogbn-products-shaped: 2.4M nodes, 62M edges, 100-dim fp32, 2-layer P(n,j)):
+feature table. The workload at N=1 is the north-star configuration, BASELINE
+configs[3] (C4, ogbn-papers100M-shaped: 111M nodes, 1.6B edges, 128-dim fp32,
+3-layer P(n,j)), which fits one B200 (`--config C2` etc. run the others):
 the graph is generated on the device, P(n,j) ranks the features, the
 placement manager partitions them over the N GPUs (hot replication / host
 fraction optional), every rank builds its store and lookup table and serves
@@ -48,6 +49,35 @@ CONFIGS = {
 META_BYTES = 24  # 8 B id + 16 B reference-layout lookup row per request
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 PCIE_GBS = 51.4  # measured: random 512-byte row reads of pinned host memory (profiles/r01k_host_tier.txt)
+
+
+def bench_config(args, cfg, world: int) -> dict:
+    """The line's `config`, built identically by both arms (--impl ours and
+    --impl reference) so the driver can match them."""
+    n, dim, B = cfg["n"], cfg["dim"], args.batch
+    row_bytes = 4 * dim
+    return {
+        "workload": cfg["desc"] + f"; gather batches of {B} uniform ids per GPU",
+        "config": args.config, "batch": B, "dim": dim, "n_features": n, "layers": cfg["layers"],
+        "features_partitioned_over": world, "replicate_fraction": args.replicate,
+        "host_fraction": args.host_frac,
+        "l2": "inputs larger than L2 (feature table %.0f MB, %.0f MB of rows per step)" % (
+            n * row_bytes / 1e6, B * row_bytes / 1e6),
+        "parallelism": f"feature-partitioned x{world}, one process per GPU",
+    }
+
+
+def traffic_key(args, world: int) -> str:
+    return f"{args.config}|b{args.batch}|r{args.replicate:g}|h{args.host_frac:g}|n{world}"
+
+
+def load_traffic(key: str) -> dict:
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            ent = json.load(f).get(key, {})
+        return {k: v["bytes_per_launch"] for k, v in ent.items()}
+    except Exception:  # noqa: BLE001
+        return {}
 
 
 def peaks():
@@ -374,11 +404,13 @@ def run_ours(args):
     # ---- CPU baseline (rank 0, N=1) ---------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu, ap_cpu = cpu_baseline(args, cfg, p_host, topo_host=topo, ro=ro, col=col, w=w,
-                                   steps=min(args.steps, args.cpu_steps))
-        access_prob["cpu_baseline"] = ap_cpu
         if sampler is not None:
             sampler["cpu_baseline"] = sampler_cpu(args, cfg, ro, col, w, sample_first)
+        cpu, ap_cpu = cpu_baseline(
+            args, cfg, p_host, (loc, off), ro, col, w, steps=min(args.steps, args.cpu_steps),
+            req0_plan=lambda r: qvb.plan_reads(loc, off, r, 8))
+        access_prob["cpu_baseline"] = ap_cpu
+    ro = col = w = None
 
     line = {
         "metric": METRIC,
@@ -393,17 +425,11 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "fp32 rows copied bit-exact (P in fp64)",
         "data": "synthetic (bench.cpp generator seed 7; SURVEY §8(d) features and request streams)",
-        "config": {
-            "workload": cfg["desc"] + f"; gather batches of {B} uniform ids per GPU",
-            "config": args.config, "batch": B, "dim": dim, "n_features": n,
-            "features_partitioned_over": world, "replicate_fraction": args.replicate,
-            "host_fraction": args.host_frac,
-            "fractions": {"local": f_l, "peer": f_p, "host": f_h},
-            "placement_s": plan_s,
-            "l2": "inputs larger than L2 (feature table %.0f MB, %.0f MB of rows per step); rows and "
-                  "outputs stream with L2 evict_first, the %.0f MB lookup table is%s kept with evict_last" % (
-                n * row_bytes / 1e6, B * row_bytes / 1e6, n * 8 / 1e6, "" if n * 8 <= (32 << 20) else " not"),
-            "parallelism": f"feature-partitioned x{world}, one process per GPU",
+        "config": bench_config(args, cfg, world),
+        "placement": {
+            "fractions": {"local": f_l, "peer": f_p, "host": f_h}, "placement_s": plan_s,
+            "l2_policy": "rows and outputs stream with L2 evict_first; the %.0f MB lookup table is%s "
+                         "kept with evict_last" % (n * 8 / 1e6, "" if n * 8 <= (32 << 20) else " not"),
             **({"shared_gpu": "QVB_SHARE_GPU=1: every rank on one GPU to exercise the multi-rank "
                               "path (IPC peers, setup collectives); the ranks time-slice the GPU, "
                               "so these timings are not a performance measurement"}
@@ -423,18 +449,12 @@ def run_ours(args):
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
     }
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):  # ncu dram bytes per launch, captured by profiles/run_ncu.sh
-        try:
-            tr = json.load(open(prof)).get(args.config, {})
-            if "k_gather" in tr:
-                line["roofline"]["traffic"] = tr["k_gather"]["bytes_per_launch"]
-                line["roofline"]["traffic_batch"] = tr["k_gather"].get("batch")
-            kname = access_prob["roofline"]["kernel"]
-            if kname in tr:
-                access_prob["roofline"]["traffic"] = tr[kname]["bytes_per_launch"]
-        except Exception:  # noqa: BLE001
-            pass
+    # ncu dram bytes per launch (profiles/make_traffic.py), only from a capture
+    # of exactly this line's workload key; null otherwise
+    tr = load_traffic(traffic_key(args, world))
+    line["roofline"]["traffic"] = tr.get("k_gather_rows")
+    access_prob["roofline"]["traffic"] = tr.get(access_prob["roofline"]["kernel"])
+    line["roofline"]["traffic_key"] = access_prob["roofline"]["traffic_key"] = traffic_key(args, world)
     store.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -520,18 +540,22 @@ def sampler_cpu(args, cfg, ro, col, w, first):
             "identical_to_gpu": bool(same)}
 
 
-def cpu_baseline(args, cfg, p_host, topo_host, ro, col, w, steps):
-    """Reference CPU path on this host (rank 0 only), bounded samples."""
+def cpu_baseline(args, cfg, p_host, lut, ro, col, w, steps, req0_plan):
+    """Reference CPU path on this host (rank 0, N=1): the reference's own
+    compute_access_prob_ie on the full graph (OpenMP, all host threads; also a
+    whole-graph bit-identity check of our P), and per collect step the
+    reference's plan_reads (single-threaded, as written) on the same lookup
+    table plus the row copy it only models (threaded memcpy restatement)."""
     import numpy as np
 
-    from oracle.oracle import Oracle, RefLib, topology_defaults
+    from oracle.oracle import Oracle, RefLib
 
     o = Oracle()
     n, dim = cfg["n"], cfg["dim"]
     threads = os.cpu_count() or 1
     ref = RefLib() if RefLib.available() else None
     if ro is None:
-        ro, col, w = o.synthetic_graph(n, cfg["e"], 7, cfg["weighted"], False)
+        ro, col, w = o.synthetic_graph(n, cfg["e"], 7, cfg["weighted"], False, threads=threads)
     # P(n,j): the reference call itself (OpenMP, includes its transpose)
     if ref is not None:
         ref.set_threads(threads)
@@ -549,48 +573,50 @@ def cpu_baseline(args, cfg, p_host, topo_host, ro, col, w, steps):
           "sample": f"one qv::compute_access_prob_ie call on the full {cfg['desc']} graph "
                     f"(L={cfg['layers']}, includes the reference's per-call transpose)",
           "seconds": ap_s,
+          "bit_identical_nodes": int((p_ref.view(np.uint64) == p_host.view(np.uint64)).sum()),
           "bit_identical_to_gpu": bool((p_ref.view(np.uint64) == p_host.view(np.uint64)).all())}
+    del p_ref
     # collect: the reference's read planner (placement.cpp:355-380) on each
-    # batch + the byte copy it only models, restated as a threaded memcpy
-    t = topology_defaults(gpus_per_server=1, gpu_feature_capacity=n, host_feature_capacity=n)
-    t0 = time.perf_counter()
-    lo, ids = (ref or o).plan_placement(p_host, t)
-    t1 = time.perf_counter()
-    loc, off = (ref or o).build_lookup_table(lo, ids, t, 0)
-    t2 = time.perf_counter()
-    ap["planner_reference"] = {"plan_placement_s": t1 - t0, "build_lookup_table_s": t2 - t1,
-                               "kind": kind, "cores": 1,
-                               "note": "single-threaded reference code (placement.cpp), C2 table"}
-    x = o.features(n, dim)
+    # batch of this rank's lookup table + the byte copy it only models
+    loc, off = lut
+    x = o.features(n, dim, threads=threads)
     plan_s = gather_s = 0.0
     b = args.batch
+    same_plan = None
     for k in range(steps):
         req = o.request_ids(11, k, n, b)
         t0 = time.perf_counter()
-        (ref or o).plan_reads(loc, off, req, 8)
+        rp = (ref or o).plan_reads(loc, off, req, 8)
         t1 = time.perf_counter()
         o.gather(x, req, threads=threads)
         t2 = time.perf_counter()
         plan_s += t1 - t0
         gather_s += t2 - t1
+        if k == 0 and req0_plan is not None:
+            same_plan = all((u == v).all() for u, v in zip(rp, req0_plan(req)))
+    del x
     payload = steps * b * 4 * dim
     cpu = {"value": payload / (plan_s + gather_s) / 1e9, "unit": "GB/s", "cores": threads,
            "kind": "reference" if ref is not None else "port",
-           "sample": f"{steps} batches x {b} uniform ids on the C2 table: qv::plan_reads "
+           "sample": f"{steps} batches x {b} uniform ids on the {args.config} table: qv::plan_reads "
                      f"(the reference's collect call, 1 thread) + the row copy it only models "
                      f"(memcpy restatement, {threads} threads)",
            "plan_reads_s": plan_s, "memcpy_s": gather_s,
-           "memcpy_only_GBps": payload / gather_s / 1e9}
+           "memcpy_only_GBps": payload / gather_s / 1e9,
+           "read_plan_identical_to_gpu": same_plan}
     return cpu, ap
 
 
 def run_reference(args):
-    """--impl reference: the reference's own CPU path, rank 0 only."""
-    import numpy as np
-
+    """--impl reference: the reference's own CPU path (oracle/_ref, the
+    unmodified sources), rank 0 only, on this arm's workload: its
+    compute_access_prob_ie on the full graph, its plan_placement and
+    build_lookup_table for the 1-GPU table, then per step its plan_reads on
+    a batch plus the row copy it only models (threaded memcpy restatement)."""
     from oracle.oracle import Oracle, RefLib, topology_defaults
 
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
@@ -601,7 +627,9 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     if ref:
         ref.set_threads(threads)
-    ro, col, w = o.synthetic_graph(n, cfg["e"], 7, cfg["weighted"], False)
+    t0 = time.perf_counter()
+    ro, col, w = o.synthetic_graph(n, cfg["e"], 7, cfg["weighted"], False, threads=threads)
+    gen_s = time.perf_counter() - t0
     t0 = time.perf_counter()
     p = ref.access_prob(ro, col, w, cfg["layers"], True) if ref else o.access_prob(ro, col, w, cfg["layers"])
     ap_s = time.perf_counter() - t0
@@ -616,10 +644,16 @@ def run_reference(args):
         sampler = {"value": len(res[0]) / min(ts), "unit": "instances/s",
                    "ms_per_batch": min(ts) * 1e3, "seeds_per_batch": args.sample_seeds,
                    "cores": threads if ref else 1}
+    del ro, col, w
     t = topology_defaults(gpus_per_server=1, gpu_feature_capacity=n, host_feature_capacity=n)
+    t0 = time.perf_counter()
     lo, ids = lib.plan_placement(p, t)
+    t1 = time.perf_counter()
     loc, off = lib.build_lookup_table(lo, ids, t, 0)
-    x = o.features(n, dim)
+    t2 = time.perf_counter()
+    plan_s, lut_s = t1 - t0, t2 - t1
+    del lo, ids
+    x = o.features(n, dim, threads=threads)
     reqs = [o.request_ids(11, k, n, B) for k in range(args.warmup + args.steps)]
     for k in range(args.warmup):
         lib.plan_reads(loc, off, reqs[k], 8)
@@ -632,21 +666,22 @@ def run_reference(args):
     value = args.steps * B * 4 * dim / el / 1e9
     kind = "reference" if ref else "port"
     line = {
-        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 rows (P in fp64)",
-        "data": "synthetic (bench.cpp generator seed 7; SURVEY §8(d))",
-        "config": {"workload": cfg["desc"] + f"; gather batches of {B} uniform ids",
-                   "config": args.config, "batch": B, "dim": dim, "n_features": n},
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 rows copied bit-exact (P in fp64)",
+        "data": "synthetic (bench.cpp generator seed 7; SURVEY §8(d) features and request streams)",
+        "config": bench_config(args, cfg, world),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
                          "sample": f"each step: qv::plan_reads on a {B}-id batch (reference "
-                                   f"code, oracle/_ref) + the row copy it only models "
-                                   f"(memcpy restatement, {threads} threads)"},
+                                   f"code, oracle/_ref, 1 thread as written) + the row copy it only "
+                                   f"models (memcpy restatement, {threads} threads)"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "access_prob": {"value": cfg["e"] * (cfg["layers"] - 1) / ap_s,
                         "unit": "edges/s (input edges)", "seconds": ap_s, "kind": kind,
                         "cores": threads},
+        "planner": {"plan_placement_s": plan_s, "build_lookup_table_s": lut_s, "cores": 1,
+                    "graph_generation_s": gen_s},
         "sampler": sampler,
     }
     print(json.dumps(line), flush=True)
@@ -658,7 +693,8 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=list(CONFIGS), default="C2")
+    ap.add_argument("--config", choices=list(CONFIGS), default="C4",
+                    help="workload (default: the north-star C4, which fits one B200)")
     ap.add_argument("--batch", type=int, default=1 << 20)
     ap.add_argument("--replicate", type=float, default=0.0)
     ap.add_argument("--host-frac", type=float, default=0.0)

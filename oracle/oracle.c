@@ -113,6 +113,135 @@ int qvo_synthetic_graph(uint64_t n, uint64_t e, uint64_t seed, int weighted, int
   return rc;
 }
 
+/* The same graph (tools/bench.cpp:22-34 + build_csr, graph.cpp:16-47) built
+ * by `threads` host threads, for papers-scale inputs (1.6B edges) that the
+ * sequential generator takes minutes over. SplitMix64 is counter-based:
+ * draw j of the stream is mix(state0 + (j+1)*GAMMA), so edge i's three draws
+ * (3i, 3i+1, 3i+2) are computed directly. Threads own row ranges and scan
+ * the edges in input order, which keeps build_csr's stable order inside a
+ * row. Output identical to qvo_synthetic_graph (tests/test_oracle.py). */
+static inline uint64_t mix_at(uint64_t st0, uint64_t j) {
+  uint64_t z = st0 + (j + 1) * GAMMA;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+typedef struct {
+  int phase;
+  uint64_t n, e, st0, lo, hi; /* edge range (phase 0) or row range (1, 2) */
+  int weighted, transposed;
+  uint32_t* row_of;
+  uint64_t* ro;     /* phase 1: counts at ro[r+1]; phase 2: cursors */
+  uint64_t* col;
+  double* w;
+} gen_job;
+
+static void* gen_worker(void* arg) {
+  gen_job* j = (gen_job*)arg;
+  if (j->phase == 0) {
+    for (uint64_t i = j->lo; i < j->hi; ++i) {
+      double u = (double)(mix_at(j->st0, 3 * i) >> 11) * 0x1.0p-53;
+      uint64_t s = (uint64_t)(u * u * (double)j->n);
+      if (s > j->n - 1) s = j->n - 1;
+      uint64_t d = (uint64_t)(((unsigned __int128)mix_at(j->st0, 3 * i + 1) * j->n) >> 64);
+      j->row_of[i] = (uint32_t)(j->transposed ? d : s);
+    }
+  } else if (j->phase == 1) {
+    for (uint64_t i = 0; i < j->e; ++i) {
+      uint64_t r = j->row_of[i];
+      if (r >= j->lo && r < j->hi) ++j->ro[r + 1];
+    }
+  } else {
+    for (uint64_t i = 0; i < j->e; ++i) {
+      uint64_t r = j->row_of[i];
+      if (r < j->lo || r >= j->hi) continue;
+      uint64_t at = j->ro[r]++;
+      uint64_t other;
+      if (j->transposed) {
+        double u = (double)(mix_at(j->st0, 3 * i) >> 11) * 0x1.0p-53;
+        other = (uint64_t)(u * u * (double)j->n);
+        if (other > j->n - 1) other = j->n - 1;
+      } else {
+        other = (uint64_t)(((unsigned __int128)mix_at(j->st0, 3 * i + 1) * j->n) >> 64);
+      }
+      j->col[at] = other;
+      j->w[at] = j->weighted ? 1.0 + (double)(mix_at(j->st0, 3 * i + 2) >> 11) * 0x1.0p-53 : 1.0;
+    }
+  }
+  return NULL;
+}
+
+static void run_jobs(gen_job* jobs, int threads) {
+  pthread_t th[256];
+  for (int t = 0; t < threads; ++t) pthread_create(&th[t], NULL, gen_worker, &jobs[t]);
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+}
+
+int qvo_synthetic_graph_mt(uint64_t n, uint64_t e, uint64_t seed, int weighted, int transposed,
+                           int threads, uint64_t* ro, uint64_t* col, double* w) {
+  if (n == 0) return fail(QVB_ERR_VALIDATION, "empty graph: node count is zero%.0llu%.0llu", 0, 0);
+  if (n > 0xFFFFFFFFull) return fail(QVB_ERR_VALIDATION, "threaded generator needs n < 2^32%.0llu%.0llu", 0, 0);
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  uint64_t st0 = qvo_derive_state(seed, 0xBE9C4ULL, 0, 0);
+  uint32_t* row_of = (uint32_t*)malloc((e ? e : 1) * sizeof(uint32_t));
+  if (!row_of) return fail(QVB_ERR_GENERIC, "out of host memory%.0llu%.0llu", 0, 0);
+  gen_job jobs[256];
+  for (int t = 0; t < threads; ++t)
+    jobs[t] = (gen_job){0, n, e, st0, e * t / threads, e * (t + 1) / threads, weighted, transposed,
+                        row_of, ro, col, w};
+  run_jobs(jobs, threads);
+  memset(ro, 0, (n + 1) * sizeof(uint64_t));
+  for (int t = 0; t < threads; ++t) {
+    jobs[t].phase = 1;
+    jobs[t].lo = n * t / threads;
+    jobs[t].hi = n * (t + 1) / threads;
+  }
+  run_jobs(jobs, threads);
+  for (uint64_t i = 0; i < n; ++i) ro[i + 1] += ro[i];
+  /* phase 2 row ranges balanced by edge count; ro[r] serves as row r's
+   * cursor and ends at ro[r+1], so shift it back afterwards */
+  uint64_t r = 0;
+  for (int t = 0; t < threads; ++t) {
+    jobs[t].phase = 2;
+    jobs[t].lo = r;
+    uint64_t target = e * (uint64_t)(t + 1) / threads;
+    while (r < n && ro[r] < target) ++r;
+    if (t == threads - 1) r = n;
+    jobs[t].hi = r;
+  }
+  run_jobs(jobs, threads);
+  for (uint64_t i = n; i > 0; --i) ro[i] = ro[i - 1];
+  ro[0] = 0;
+  free(row_of);
+  return 0;
+}
+
+typedef struct {
+  uint64_t first, lo, hi;
+  uint32_t dim;
+  float* x;
+} feat_job;
+
+static void* feat_worker(void* arg) {
+  feat_job* j = (feat_job*)arg;
+  qvo_features(j->first + j->lo, j->hi - j->lo, j->dim, j->x + j->lo * j->dim);
+  return NULL;
+}
+
+void qvo_features_mt(uint64_t first, uint64_t count, uint32_t dim, float* x, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  feat_job jobs[256];
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = (feat_job){first, count * t / threads, count * (t + 1) / threads, dim, x};
+    pthread_create(&th[t], NULL, feat_worker, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+}
+
 /* Graph::validate (graph.cpp:58-93) */
 int qvo_validate(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col,
                  const double* w) {

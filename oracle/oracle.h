@@ -33,6 +33,8 @@ int qvo_synthetic_edges(uint64_t n, uint64_t e, uint64_t seed, int weighted, int
                         uint64_t* src, uint64_t* dst, double* w);
 int qvo_build_csr(uint64_t n, uint64_t e, const uint64_t* src, const uint64_t* dst,
                   const double* w, uint64_t* row_offsets, uint64_t* col, double* w_out);
+int qvo_synthetic_graph_mt(uint64_t n, uint64_t e, uint64_t seed, int weighted, int transposed,
+                           int threads, uint64_t* ro, uint64_t* col, double* w);
 int qvo_synthetic_graph(uint64_t n, uint64_t e, uint64_t seed, int weighted, int transposed,
                         uint64_t* row_offsets, uint64_t* col, double* w);
 
@@ -89,6 +91,7 @@ int qvo_plan_reads(const int64_t* location_ids, const uint64_t* offsets, uint64_
 
 /* Synthetic inputs of SURVEY §8(d). */
 void qvo_features(uint64_t first, uint64_t count, uint32_t dim, float* x);
+void qvo_features_mt(uint64_t first, uint64_t count, uint32_t dim, float* x, int threads);
 void qvo_request_ids(uint64_t seed, uint64_t batch, uint64_t n, uint64_t* ids, uint64_t b);
 /* Row gather restatement: out[i] = X[ids[i]] with `threads` pthreads. */
 int qvo_gather(const float* x, uint64_t n, uint32_t dim, const uint64_t* ids, uint64_t b,

@@ -108,6 +108,9 @@ class Oracle(_Lib):
         L.qvo_derive_state.argtypes = [C.c_uint64] * 4
         L.qvo_synthetic_graph.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.c_int,
                                           u64p, u64p, f64p]
+        L.qvo_synthetic_graph_mt.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.c_int,
+                                             C.c_int, u64p, u64p, f64p]
+        L.qvo_features_mt.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, f32p, C.c_int]
         L.qvo_build_csr.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, u64p, u64p, f64p]
         L.qvo_validate.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p]
         L.qvo_in_adjacency.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, u64p, u64p, f64p]
@@ -138,14 +141,19 @@ class Oracle(_Lib):
         return self._lib.qvo_derive_state(master, a, b, c)
 
     def synthetic_graph(self, n: int, e: int, seed: int = 7, weighted: bool = False,
-                        transposed: bool = False):
-        """tools/bench.cpp:22-34 -> out-CSR (row_offsets, col, weights)."""
+                        transposed: bool = False, threads: int = 1):
+        """tools/bench.cpp:22-34 -> out-CSR (row_offsets, col, weights).
+        threads > 1: the counter-based threaded build (same bytes)."""
         ro = np.zeros(n + 1, np.uint64)
-        col = np.zeros(max(e, 1), np.uint64)
-        w = np.zeros(max(e, 1), np.float64)
-        self._check(self._lib.qvo_synthetic_graph(n, e, seed, int(weighted), int(transposed),
-                                                  ro, col, w))
-        return ro, col[:e].copy(), w[:e].copy()
+        col = np.empty(max(e, 1), np.uint64)
+        w = np.empty(max(e, 1), np.float64)
+        if threads > 1:
+            self._check(self._lib.qvo_synthetic_graph_mt(n, e, seed, int(weighted), int(transposed),
+                                                         threads, ro, col, w))
+        else:
+            self._check(self._lib.qvo_synthetic_graph(n, e, seed, int(weighted), int(transposed),
+                                                      ro, col, w))
+        return ro, col[:e], w[:e]
 
     def build_csr(self, n: int, src, dst, w):
         e = len(src)
@@ -247,9 +255,12 @@ class Oracle(_Lib):
         return _plan_reads_call(self._lib.qvo_plan_reads, self._check, loc, off, ids, b, page)
 
     # features / requests / gather -------------------------------------------
-    def features(self, n: int, dim: int, first: int = 0):
-        x = np.zeros((n, dim), np.float32)
-        self._lib.qvo_features(first, n, dim, x.reshape(-1))
+    def features(self, n: int, dim: int, first: int = 0, threads: int = 1):
+        x = np.empty((n, dim), np.float32)
+        if threads > 1:
+            self._lib.qvo_features_mt(first, n, dim, x.reshape(-1), threads)
+        else:
+            self._lib.qvo_features(first, n, dim, x.reshape(-1))
         return x
 
     def request_ids(self, seed: int, batch: int, n: int, b: int):

@@ -2,8 +2,12 @@
 dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernels, which
 bench.py reports as roofline.traffic.
 
-    python profiles/make_traffic.py C2 k_gather profiles/rXX_gather.ncu-rep [batch]
-    python profiles/make_traffic.py C2 k_sweep  profiles/rXX_sweep.ncu-rep
+    python profiles/make_traffic.py KEY KERNEL profiles/rXX_gather.ncu-rep
+
+KEY names the exact bench line the capture belongs to,
+"<config>|b<batch>|r<replicate>|h<host_frac>|n<gpus>" (bench.traffic_key), e.g.
+"C4|b1048576|r0|h0|n1"; bench.py reports a traffic number only for a line
+with exactly that key (otherwise null).
 """
 import csv
 import io
@@ -33,13 +37,10 @@ def dram_bytes(rep):
 
 if __name__ == "__main__":
     cfg, kernel, rep = sys.argv[1:4]
-    batch = int(sys.argv[4]) if len(sys.argv) > 4 else None
     path = os.path.join(HERE, "traffic.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
     b = dram_bytes(rep)
     ent = {"bytes_per_launch": sum(b) / len(b), "launches": len(b), "source": os.path.basename(rep)}
-    if batch:
-        ent["batch"] = batch
     data.setdefault(cfg, {})[kernel] = ent
     json.dump(data, open(path, "w"), indent=1, sort_keys=True)
     print(cfg, kernel, ent)

@@ -295,3 +295,17 @@ def test_sampler_matches_reference_random(oracle, ref):
         oracle.batch_sample(ro, col, ww, np.array([0], np.uint64), [], 1)
     with pytest.raises(Exception, match="fanouts must be"):
         oracle.batch_sample(ro, col, ww, np.array([0], np.uint64), [2, 0], 1)
+
+
+@pytest.mark.parametrize("n,e,weighted,transposed", [(100_000, 1_000_000, False, False),
+                                                     (100_000, 1_000_000, True, True),
+                                                     (2_000, 300_000, True, False), (3, 50, False, True)])
+def test_threaded_generator_matches_sequential(oracle, n, e, weighted, transposed):
+    """The threaded bench.cpp generator (used for papers-scale host graphs)
+    writes the same CSR bytes as the sequential one, at several thread counts."""
+    a = oracle.synthetic_graph(n, e, 7, weighted, transposed)
+    for t in (2, 7, 16):
+        b = oracle.synthetic_graph(n, e, 7, weighted, transposed, threads=t)
+        assert all((x.view(np.uint64) == y.view(np.uint64)).all() for x, y in zip(a, b))
+    x = oracle.features(1000, 37, first=5)
+    assert (x == oracle.features(1000, 37, first=5, threads=5)).all()
