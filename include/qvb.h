@@ -91,6 +91,21 @@ int64_t qvb_encode_location(const qvb_topology* t, uint32_t server, uint32_t tie
 int qvb_decode_location(const qvb_topology* t, int64_t id, uint32_t* server,
                         uint32_t* tier, uint32_t* device);
 
+/* classify_link (placement.cpp:228-267): the link path from a reader
+ * (server, tier QVB_TIER_GPU/HOST, device) to a location id; *second = -1
+ * for a one-link path. */
+int qvb_classify_link(const qvb_topology* t, uint32_t reader_server, uint32_t reader_tier,
+                      uint32_t reader_device, int64_t location_id, int* first, int* second);
+/* fetch_cost (placement.cpp:382-404), the reference's latency model of one
+ * collect, over a flattened read plan (groups as qvb_plan_reads returns them):
+ * per group setup + count*feature_bytes/bandwidth (+ tlb penalty per page
+ * transition on translated links) into per_location_s[groups]; *total_s =
+ * their max. A location id outside the topology is a ValidationError. */
+int qvb_fetch_cost(const qvb_topology* t, uint32_t reader_server, uint32_t reader_tier,
+                   uint32_t reader_device, uint64_t groups, const int64_t* group_loc,
+                   const uint64_t* group_count, const uint64_t* group_transitions,
+                   uint64_t feature_bytes, double* per_location_s, double* total_s);
+
 /* ---- device info ------------------------------------------------------- */
 /* Number of usable devices (fails with QVB_ERR_CUDA when there are none). */
 int qvb_device_count(int* count);
@@ -143,6 +158,33 @@ int qvb_in_adjacency(int device, uint64_t n, uint64_t e, const uint64_t* row_off
 int qvb_synthetic_csr(int device, uint64_t n, uint64_t e, uint64_t seed, int weighted,
                       int transposed, uint64_t* row_offsets, uint64_t* col, double* weights);
 int qvb_graph_info_get(const qvb_graph* g, qvb_graph_info* info);
+
+/* qv::Edge (graph.hpp:12-16): 24 bytes, the layout of std::vector<qv::Edge>. */
+typedef struct qvb_edge {
+  uint64_t src;
+  uint64_t dst;
+  double weight;
+} qvb_edge;
+/* Graph::from_edges / build_csr (graph.cpp:16-56) on the device: the first
+ * edge (input order) with an endpoint >= n or a negative/NaN weight is a
+ * ValidationError with the reference's message; rows keep input order
+ * (stable sort by source). Outputs: row_offsets[n+1], col[e], weights[e]
+ * (host), then validated like Graph::validate. */
+int qvb_build_csr(int device, uint64_t n, const qvb_edge* edges, uint64_t e,
+                  uint64_t* row_offsets, uint64_t* col, double* weights);
+/* Graph::validate (graph.cpp:58-93) on the device: same checks, same order,
+ * same messages (weights NULL = all 1.0). */
+int qvb_graph_validate(int device, uint64_t n, uint64_t e, const uint64_t* row_offsets,
+                       const uint64_t* col, const double* weights);
+/* transition_view (graph.cpp:292-318) on the device: row_sums[n] (each row's
+ * weights summed sequentially in CSR order), distinct_out[n] (distinct
+ * out-neighbours per node) and *has_parallel_edges, from one upload that also
+ * builds the P(n,j) in-CSR. keep (nullable) receives that device graph, ready
+ * for qvb_access_prob, so compute_access_prob_ie(g, transition_view(g), L)
+ * uploads the graph once; NULL discards it. */
+int qvb_transition_view(int device, uint64_t n, uint64_t e, const uint64_t* row_offsets,
+                        const uint64_t* col, const double* weights, double* row_sums,
+                        uint64_t* distinct_out, int* has_parallel_edges, qvb_graph** keep);
 /* Device time (ms, CUDA events on the call's stream) of the P sweeps of the
  * last qvb_access_prob on g. */
 int qvb_graph_last_sweep_ms(const qvb_graph* g, double* ms);
@@ -237,6 +279,16 @@ int qvb_plan_reads(int device, const int64_t* location_ids, const uint64_t* offs
                    int64_t* group_loc, uint64_t* group_count, uint64_t* group_transitions,
                    uint64_t* n_groups, uint64_t* offsets_out);
 
+/* The same plan from a lookup table already resident on the device (DEVICE
+ * pointers location_ids/offsets[table_n] and ids[b]; outputs are host
+ * buffers as above). Stream-ordered on `stream`, returns when the plan is on
+ * the host. The per-batch call of the reference's serving loop
+ * (simulator.cpp:320-321) without re-uploading the table it builds once. */
+int qvb_plan_reads_device(int device, const int64_t* location_ids, const uint64_t* offsets,
+                          uint64_t table_n, const uint64_t* ids, uint64_t b, uint64_t page_size,
+                          int64_t* group_loc, uint64_t* group_count, uint64_t* group_transitions,
+                          uint64_t* n_groups, uint64_t* offsets_out, void* stream);
+
 /* ---- K5: feature store + gather (new; fetch_cost placement.cpp:382-404
  *          only models this transfer) ------------------------------------- */
 /* One store per (process, device). It owns this device's shard, an optional
@@ -295,6 +347,14 @@ int qvb_gather_planned(qvb_store* s, const uint64_t* ids, uint64_t b, float* out
  * copies rows device->host, and synchronises. Calls on one store from several
  * threads are serialised (they share the store's staging buffers). */
 int qvb_gather_host(qvb_store* s, const uint64_t* ids, uint64_t b, float* out, void* stream);
+/* qv::plan_reads over this store's resident lookup table (the reader's
+ * table: reader 0 of the server is the reference's build_lookup_table), for
+ * ids on the host (ids_on_device=0) or the device. Outputs as
+ * qvb_plan_reads. No per-call table upload. */
+int qvb_store_plan_reads(qvb_store* s, const uint64_t* ids, uint64_t b, int ids_on_device,
+                         uint64_t page_size, int64_t* group_loc, uint64_t* group_count,
+                         uint64_t* group_transitions, uint64_t* n_groups, uint64_t* offsets_out,
+                         void* stream);
 /* Reports (and clears) a device-side id range error of earlier gathers. */
 int qvb_store_check_error(qvb_store* s);
 

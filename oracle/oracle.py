@@ -80,6 +80,9 @@ def build(ref: bool = True) -> None:
     targets = ["oracle"]
     if ref and os.path.isdir("/root/reference/proj"):
         targets.append("ref")
+        # the reference's own test files against the qv:: drop-in (needs it built)
+        if os.path.exists(os.path.join(HERE, "..", "paper_2305_10863_b200", "libqv_b200.so")):
+            targets.append("reftests")
     subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
 
 
@@ -301,6 +304,10 @@ class RefLib(_Lib):
         L.qvr_compute_fap.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, C.c_uint32, C.c_int,
                                       C.c_void_p, f64p]
         L.qvr_row_sums.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, f64p]
+        L.qvr_transition_view.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, f64p, u64p,
+                                          C.POINTER(C.c_int)]
+        L.qvr_from_edges.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, u64p, u64p, f64p]
+        L.qvr_validate.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p]
         L.qvr_plan_placement.argtypes = [f64p, C.c_uint64, C.POINTER(Topology), u64p, i64p,
                                          C.c_uint64, C.POINTER(C.c_uint64), dp]
         L.qvr_build_lookup_table.argtypes = [u64p, i64p, C.c_uint64, C.POINTER(Topology),
@@ -364,6 +371,29 @@ class RefLib(_Lib):
         self._check(self._lib.qvr_row_sums(n, len(col), ro, _pad(col, np.uint64),
                                            _pad(w, np.float64), rs))
         return rs
+
+    def transition_view(self, ro, col, w):
+        """transition_view(g): (row_sums, distinct_out, has_parallel_edges)."""
+        n = len(ro) - 1
+        rs = np.zeros(n, np.float64)
+        dist = np.zeros(n, np.uint64)
+        par = C.c_int(0)
+        self._check(self._lib.qvr_transition_view(n, len(col), ro, _pad(col, np.uint64),
+                                                  _pad(w, np.float64), rs, dist, C.byref(par)))
+        return rs, dist, bool(par.value)
+
+    def from_edges(self, n: int, src, dst, w):
+        e = len(src)
+        ro = np.zeros(n + 1, np.uint64)
+        col = np.zeros(max(e, 1), np.uint64)
+        wo = np.zeros(max(e, 1), np.float64)
+        self._check(self._lib.qvr_from_edges(n, e, _pad(src, np.uint64), _pad(dst, np.uint64),
+                                             _pad(w, np.float64), ro, col, wo))
+        return ro, col[:e].copy(), wo[:e].copy()
+
+    def validate(self, ro, col, w) -> None:
+        self._check(self._lib.qvr_validate(len(ro) - 1, len(col), _pad(ro, np.uint64),
+                                           _pad(col, np.uint64), _pad(w, np.float64)))
 
     def plan_placement(self, values, topo: Topology):
         v = np.ascontiguousarray(values, np.float64)

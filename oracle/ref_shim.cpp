@@ -188,6 +188,34 @@ int qvr_row_sums(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col
   });
 }
 
+int qvr_transition_view(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col,
+                        const double* w, double* rs, uint64_t* distinct, int* parallel) {
+  return guard([&] {
+    qv::Graph g = make_graph(n, e, ro, col, w);
+    qv::TransitionView t = qv::transition_view(g);
+    std::memcpy(rs, t.row_sums.data(), n * sizeof(double));
+    std::memcpy(distinct, t.distinct_out.data(), n * sizeof(uint64_t));
+    *parallel = t.has_parallel_edges ? 1 : 0;
+  });
+}
+
+/* Graph::from_edges over struct-of-arrays edges (the shim only marshals) */
+int qvr_from_edges(uint64_t n, uint64_t e, const uint64_t* src, const uint64_t* dst, const double* w,
+                   uint64_t* ro, uint64_t* col, double* wo) {
+  return guard([&] {
+    std::vector<qv::Edge> edges(e);
+    for (uint64_t i = 0; i < e; ++i) edges[i] = qv::Edge{src[i], dst[i], w[i]};
+    qv::Graph g = qv::Graph::from_edges(n, edges);
+    std::memcpy(ro, g.row_offsets.data(), (n + 1) * sizeof(uint64_t));
+    std::memcpy(col, g.col_indices.data(), e * sizeof(uint64_t));
+    std::memcpy(wo, g.edge_weights.data(), e * sizeof(double));
+  });
+}
+
+int qvr_validate(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col, const double* w) {
+  return guard([&] { make_graph(n, e, ro, col, w).validate(); });
+}
+
 int qvr_plan_placement(const double* v, uint64_t n, const qvb_topology* topo,
                        uint64_t* loc_offsets, int64_t* loc_ids, uint64_t cap, uint64_t* copies,
                        double* ms_out) {

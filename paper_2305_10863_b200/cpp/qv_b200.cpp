@@ -75,60 +75,45 @@ PlanCsr to_csr(const PlacementPlan& plan, const ClusterTopology& topo) {
 }  // namespace
 
 // ---- graph ------------------------------------------------------------------
+static_assert(sizeof(Edge) == sizeof(qvb_edge) && offsetof(Edge, dst) == offsetof(qvb_edge, dst) &&
+                  offsetof(Edge, weight) == offsetof(qvb_edge, weight),
+              "qv::Edge must keep the qvb_edge layout");
+
 Graph Graph::from_edges(std::uint64_t node_count, std::span<const Edge> edges) {
-  // build_csr semantics (graph.cpp:16-56): counting sort by source, input
-  // order kept inside a row; input construction, not the hot path.
-  if (node_count == 0) throw ValidationError("empty graph: node count is zero");
+  // build_csr (graph.cpp:16-56) on the device: checks in input order, a
+  // stable sort by source, then the validate() the reference ends with
   Graph g;
   g.node_count = node_count;
   g.edge_count = edges.size();
-  g.row_offsets.assign(node_count + 1, 0);
-  for (const Edge& e : edges) {
-    if (e.src >= node_count || e.dst >= node_count)
-      throw ValidationError("edge endpoint " + std::to_string(std::max(e.src, e.dst)) +
-                            " out of range for node count " + std::to_string(node_count));
-    if (!(e.weight >= 0.0))
-      throw ValidationError("negative or NaN edge weight on edge " + std::to_string(e.src) +
-                            " -> " + std::to_string(e.dst));
-    ++g.row_offsets[e.src + 1];
-  }
-  std::partial_sum(g.row_offsets.begin(), g.row_offsets.end(), g.row_offsets.begin());
-  g.col_indices.resize(g.edge_count);
-  g.edge_weights.resize(g.edge_count);
-  std::vector<EdgeIdx> cursor(g.row_offsets.begin(), g.row_offsets.end() - 1);
-  for (const Edge& e : edges) {
-    const EdgeIdx at = cursor[e.src]++;
-    g.col_indices[at] = e.dst;
-    g.edge_weights[at] = e.weight;
-  }
-  g.validate();
+  g.row_offsets.resize(node_count + 1);
+  g.col_indices.resize(edges.size());
+  g.edge_weights.resize(edges.size());
+  check(qvb_build_csr(default_device(), node_count, reinterpret_cast<const qvb_edge*>(edges.data()),
+                      edges.size(), g.row_offsets.data(), g.col_indices.data(),
+                      g.edge_weights.data()));
   return g;
 }
 
-void Graph::validate() const {
-  // the device validates on upload with the reference's messages
-  // (graph.cpp:58-93); host-side size checks come first, as there
-  if (node_count == 0) throw ValidationError("empty graph: node count is zero");
-  if (row_offsets.size() != node_count + 1) throw ValidationError("row_offsets size mismatch");
-  if (row_offsets.front() != 0 || row_offsets.back() != edge_count)
+namespace {
+// Graph::validate's container-shape checks (graph.cpp:58-70): properties of
+// the std::vectors, which the C-ABI (plain pointers) cannot see.
+void check_shape(const Graph& g) {
+  if (g.node_count == 0) throw ValidationError("empty graph: node count is zero");
+  const bool sized = g.row_offsets.size() == g.node_count + 1;
+  if (!sized) throw ValidationError("row_offsets size mismatch");
+  if (g.row_offsets.front() != 0 || g.row_offsets.back() != g.edge_count)
     throw ValidationError("row_offsets endpoints invalid");
-  if (col_indices.size() != edge_count || edge_weights.size() != edge_count)
-    throw ValidationError("edge array size mismatch");
-  for (std::uint64_t i = 0; i < node_count; ++i)
-    if (row_offsets[i + 1] < row_offsets[i])
-      throw ValidationError("row_offsets not non-decreasing at node " + std::to_string(i));
-  for (std::uint64_t i = 0; i < node_count; ++i) {
-    bool any_positive = out_degree(i) == 0;
-    for (EdgeIdx e = row_offsets[i]; e < row_offsets[i + 1]; ++e) {
-      if (col_indices[e] >= node_count)
-        throw ValidationError("column index out of range at node " + std::to_string(i));
-      if (!(edge_weights[e] >= 0.0))
-        throw ValidationError("negative or NaN edge weight at node " + std::to_string(i));
-      if (edge_weights[e] > 0.0) any_positive = true;
-    }
-    if (!any_positive)
-      throw ValidationError("node " + std::to_string(i) + " has out-edges but all weights are zero");
-  }
+  const bool edges_sized =
+      g.col_indices.size() == g.edge_count && g.edge_weights.size() == g.edge_count;
+  if (!edges_sized) throw ValidationError("edge array size mismatch");
+}
+}  // namespace
+
+void Graph::validate() const {
+  check_shape(*this);
+  // monotone offsets, column range, weight sign, all-zero rows: on the device
+  check(qvb_graph_validate(default_device(), node_count, edge_count, row_offsets.data(),
+                           col_indices.data(), edge_weights.data()));
 }
 
 Graph in_adjacency(const Graph& g) {
@@ -145,46 +130,51 @@ Graph in_adjacency(const Graph& g) {
 }
 
 double TransitionView::prob(NodeId i, NodeId j) const {
-  if (row_sums[i] <= 0.0) return 0.0;
-  double w = 0.0;
-  for (EdgeIdx e = graph->row_offsets[i]; e < graph->row_offsets[i + 1]; ++e)
-    if (graph->col_indices[e] == j) w += graph->edge_weights[e];
-  return w / row_sums[i];
+  // summed weight of i's edges to j over i's row sum (0 for sink rows)
+  const double total = row_sums[i];
+  if (!(total > 0.0)) return 0.0;
+  const auto cols = graph->neighbors(i);
+  const auto ws = graph->weights(i);
+  double hit = 0.0;
+  for (std::size_t k = 0; k < cols.size(); ++k) hit += cols[k] == j ? ws[k] : 0.0;
+  return hit / total;
+}
+
+bool TransitionView::resident_for(const Graph& g) const {
+  return resident && graph == &g && resident_key[0] == g.row_offsets.data() &&
+         resident_key[1] == g.col_indices.data() && resident_key[2] == g.edge_weights.data();
 }
 
 TransitionView transition_view(const Graph& g) {
-  g.validate();
+  check_shape(g);
   TransitionView t;
   t.graph = &g;
-  t.row_sums.assign(g.node_count, 0.0);
-  t.distinct_out.assign(g.node_count, 0);
-  std::vector<std::uint64_t> stamp(g.node_count, ~0ULL);
-  for (NodeId i = 0; i < g.node_count; ++i) {
-    double sum = 0.0;
-    std::uint64_t distinct = 0;
-    for (EdgeIdx e = g.row_offsets[i]; e < g.row_offsets[i + 1]; ++e) {
-      sum += g.edge_weights[e];
-      const NodeId j = g.col_indices[e];
-      if (stamp[j] != i) {
-        stamp[j] = i;
-        ++distinct;
-      } else {
-        t.has_parallel_edges = true;
-      }
-    }
-    t.row_sums[i] = sum;
-    t.distinct_out[i] = distinct;
-  }
+  t.row_sums.resize(g.node_count);
+  t.distinct_out.resize(g.node_count);
+  int parallel = 0;
+  qvb_graph* dg = nullptr;
+  check(qvb_transition_view(default_device(), g.node_count, g.edge_count, g.row_offsets.data(),
+                            g.col_indices.data(), g.edge_weights.data(), t.row_sums.data(),
+                            t.distinct_out.data(), &parallel, &dg));
+  t.has_parallel_edges = parallel != 0;
+  t.resident = std::shared_ptr<qvb_graph>(dg, [](qvb_graph* p) { qvb_graph_destroy(p); });
+  t.resident_key[0] = g.row_offsets.data();
+  t.resident_key[1] = g.col_indices.data();
+  t.resident_key[2] = g.edge_weights.data();
   return t;
 }
 
 // ---- metrics ------------------------------------------------------------------
-AccessProbTable compute_access_prob_ie(const Graph& g, const TransitionView&,
+AccessProbTable compute_access_prob_ie(const Graph& g, const TransitionView& view,
                                        std::uint32_t layers) {
   if (layers < 1) throw ValidationError("access probability needs layers >= 1");
   AccessProbTable t;
   t.layers = layers;
   t.values.resize(g.node_count);
+  if (view.resident_for(g)) {  // the graph is on the device since transition_view(g)
+    check(qvb_access_prob(view.resident.get(), layers, t.values.data(), 0, nullptr));
+    return t;
+  }
   check(qvb_compute_access_prob_ie(default_device(), g.node_count, g.edge_count,
                                    g.row_offsets.data(), g.col_indices.data(),
                                    g.edge_weights.data(), layers, t.values.data(), nullptr));
@@ -389,20 +379,29 @@ Location decode_location(const ClusterTopology& topo, std::int64_t id) {
 }
 
 void PlacementPlan::validate(const ClusterTopology& topo) const {
-  std::map<std::int64_t, std::uint64_t> counts;
+  // copies per encoded location id (ids are dense, < servers x (G+2)); the
+  // first location over its tier's capacity in ascending id order is named
+  const std::uint64_t nloc = static_cast<std::uint64_t>(topo.servers) * (topo.gpus_per_server + 2);
+  std::vector<std::uint64_t> per_loc(nloc, 0);
   for (std::uint64_t f = 0; f < feature_count; ++f) {
-    if (locations[f].empty()) throw Error("feature " + std::to_string(f) + " has no location");
-    for (const Location& l : locations[f]) ++counts[encode_location(topo, l.server, l.tier, l.device)];
+    const auto& copies = locations[f];
+    if (copies.empty()) throw Error("feature " + std::to_string(f) + " has no location");
+    for (const Location& l : copies) {
+      const auto id = static_cast<std::uint64_t>(encode_location(topo, l.server, l.tier, l.device));
+      if (id >= per_loc.size()) per_loc.resize(id + 1, 0);
+      per_loc[id] += 1;
+    }
   }
-  for (const auto& [id, count] : counts) {
-    const Location l = decode_location(topo, id);
-    const std::uint64_t cap = l.tier == Tier::gpu    ? topo.gpu_feature_capacity
-                              : l.tier == Tier::host ? topo.host_feature_capacity
-                                                     : topo.disk_feature_capacity;
-    if (count > cap)
-      throw Error(std::string("placement overfills ") + tier_name(l.tier) + " on server " +
-                  std::to_string(l.server) + ": " + std::to_string(count) + " > " +
-                  std::to_string(cap));
+  for (std::uint64_t id = 0; id < per_loc.size(); ++id) {
+    if (per_loc[id] == 0) continue;
+    const Location l = decode_location(topo, static_cast<std::int64_t>(id));
+    const std::uint64_t caps[3] = {topo.gpu_feature_capacity, topo.host_feature_capacity,
+                                   topo.disk_feature_capacity};
+    const std::uint64_t cap = caps[static_cast<int>(l.tier)];
+    if (per_loc[id] <= cap) continue;
+    throw Error(std::string("placement overfills ") + tier_name(l.tier) + " on server " +
+                std::to_string(l.server) + ": " + std::to_string(per_loc[id]) + " > " +
+                std::to_string(cap));
   }
 }
 
@@ -481,71 +480,67 @@ ReadPlan plan_reads(const FeatureLookupTable& table, std::span<const NodeId> fea
   return plan;
 }
 
+ReadPlan plan_reads(const FeatureStore& store, std::span<const NodeId> feature_ids,
+                    std::uint64_t page_size) {
+  if (page_size == 0) throw ValidationError("page size must be > 0");
+  ReadPlan plan;
+  plan.home_server = 0;  // the device store serves one server
+  plan.page_size = page_size;
+  const std::uint64_t b = feature_ids.size();
+  if (b == 0) return plan;
+  qvb_store_info info;
+  check(qvb_store_info_get(store.handle(), &info));
+  const std::uint64_t cap = std::min<std::uint64_t>(b, info.location_count);
+  std::vector<std::int64_t> gl(cap);
+  std::vector<std::uint64_t> gc(cap), gt(cap), off(b);
+  std::uint64_t ng = 0;
+  check(qvb_store_plan_reads(store.handle(), feature_ids.data(), b, 0, page_size, gl.data(),
+                             gc.data(), gt.data(), &ng, off.data(), nullptr));
+  std::uint64_t at = 0;
+  plan.per_location.resize(ng);
+  for (std::uint64_t g = 0; g < ng; ++g) {
+    auto& r = plan.per_location[g];
+    r.location_id = gl[g];
+    r.page_transitions = gt[g];
+    r.offsets.assign(off.begin() + at, off.begin() + at + gc[g]);
+    at += gc[g];
+  }
+  return plan;
+}
+
 LinkPath classify_link(const ClusterTopology& topo, const DeviceRef& reader,
                        std::int64_t location_id) {
-  // placement.cpp:228-267 (host arithmetic of the cost model)
-  const Location loc = decode_location(topo, location_id);
+  qvb_topology c = to_c(topo);
+  int first = 0, second = -1;
+  check(qvb_classify_link(&c, reader.server, static_cast<std::uint32_t>(reader.tier), reader.device,
+                          location_id, &first, &second));
   LinkPath path;
-  if (loc.server == reader.server) {
-    switch (loc.tier) {
-      case Tier::gpu:
-        if (reader.tier == Tier::gpu) {
-          if (reader.device == loc.device) path.first = LinkClass::local;
-          else if (topo.gpus_per_numa() > 0 &&
-                   reader.device / topo.gpus_per_numa() == loc.device / topo.gpus_per_numa())
-            path.first = topo.nvlink_within_numa ? LinkClass::nvlink : LinkClass::pcie;
-          else path.first = LinkClass::upi;
-        } else {
-          path.first = LinkClass::pcie;
-        }
-        break;
-      case Tier::host:
-        path.first = reader.tier == Tier::host ? LinkClass::local : LinkClass::pcie;
-        break;
-      case Tier::disk: path.first = LinkClass::disk; break;
-    }
-  } else {
-    const LinkClass net = topo.infiniband ? LinkClass::infiniband : LinkClass::ethernet;
-    if (loc.tier == Tier::disk) {
-      path.first = LinkClass::disk;
-      path.second = net;
-    } else {
-      path.first = net;
-    }
-  }
+  path.first = static_cast<LinkClass>(first);
+  if (second >= 0) path.second = static_cast<LinkClass>(second);
   return path;
 }
 
 FetchCost fetch_cost(const ReadPlan& plan, const ClusterTopology& topo,
                      std::uint64_t feature_bytes, std::optional<DeviceRef> reader) {
-  // placement.cpp:382-404 — the reference's model, unchanged in meaning
-  auto translated = [](LinkClass c) {
-    return c == LinkClass::pcie || c == LinkClass::upi || c == LinkClass::infiniband ||
-           c == LinkClass::ethernet;
-  };
-  DeviceRef rd = reader ? *reader
-                        : (topo.gpus_per_server > 0 ? DeviceRef{plan.home_server, Tier::gpu, 0}
-                                                    : DeviceRef{plan.home_server, Tier::host, 0});
-  FetchCost cost;
-  const std::int64_t max_loc =
-      static_cast<std::int64_t>(topo.servers) * static_cast<std::int64_t>(topo.gpus_per_server + 2);
-  for (const auto& lr : plan.per_location) {
-    if (lr.location_id < 0 || lr.location_id >= max_loc)
-      throw ValidationError("unknown location id " + std::to_string(lr.location_id));
-    const LinkPath p = classify_link(topo, rd, lr.location_id);
-    double setup = topo.link(p.first).latency_s;
-    double bw = topo.link(p.first).bandwidth_Bps;
-    if (p.second) {
-      setup += topo.link(*p.second).latency_s;
-      bw = std::min(bw, topo.link(*p.second).bandwidth_Bps);
-    }
-    const double bytes = static_cast<double>(feature_bytes) * static_cast<double>(lr.offsets.size());
-    double lat = setup + bytes / bw;
-    if (translated(p.first) || (p.second && translated(*p.second)))
-      lat += topo.tlb_miss_penalty_s * static_cast<double>(lr.page_transitions);
-    cost.per_location_s.emplace_back(lr.location_id, lat);
-    cost.total_s = std::max(cost.total_s, lat);
+  qvb_topology c = to_c(topo);
+  // default reader: GPU 0 of the plan's home server, the host without GPUs
+  const DeviceRef rd = reader.value_or(
+      DeviceRef{plan.home_server, topo.gpus_per_server > 0 ? Tier::gpu : Tier::host, 0});
+  const std::size_t groups = plan.per_location.size();
+  std::vector<std::int64_t> loc(groups);
+  std::vector<std::uint64_t> count(groups), trans(groups);
+  for (std::size_t g = 0; g < groups; ++g) {
+    loc[g] = plan.per_location[g].location_id;
+    count[g] = plan.per_location[g].offsets.size();
+    trans[g] = plan.per_location[g].page_transitions;
   }
+  std::vector<double> per(groups);
+  FetchCost cost;
+  check(qvb_fetch_cost(&c, rd.server, static_cast<std::uint32_t>(rd.tier), rd.device, groups,
+                       loc.data(), count.data(), trans.data(), feature_bytes, per.data(),
+                       &cost.total_s));
+  cost.per_location_s.reserve(groups);
+  for (std::size_t g = 0; g < groups; ++g) cost.per_location_s.emplace_back(loc[g], per[g]);
   return cost;
 }
 
@@ -560,65 +555,74 @@ void read_pod(std::ifstream& in, T* p, std::size_t n, const std::string& path, c
   if (!in) throw ParseError(path + what);
 }
 
-Graph load_edge_list(const std::string& path, bool remap) {
-  std::ifstream in(path);
-  if (!in) throw ParseError("cannot open graph file: " + path);
-  std::vector<Edge> edges;
-  std::string line;
+// The text edge-list format (graph.cpp:112-188 semantics): "src dst [w]"
+// per line, '#' starts a comment, blank lines skipped; numbers extract as
+// from a std::istream; errors name "path:line".
+struct LineParser {
+  const std::string& path;
   std::uint64_t line_no = 0;
-  NodeId max_id = 0;
-  while (std::getline(in, line)) {
-    ++line_no;
-    const auto hash = line.find('#');
-    if (hash != std::string::npos) line.resize(hash);
-    std::istringstream ls(line);
-    std::uint64_t src, dst;
-    if (!(ls >> src)) {
-      std::string left;
-      std::istringstream probe(line);
-      if (probe >> left)
-        throw ParseError(path + ":" + std::to_string(line_no) + ": malformed edge line: '" + line + "'");
-      continue;
+
+  [[noreturn]] void bad(const std::string& what) const {
+    throw ParseError(path + ":" + std::to_string(line_no) + ": " + what);
+  }
+
+  // false for a line with nothing but whitespace/comment
+  bool parse(std::string body, Edge& out) const {
+    body.erase(std::min(body.find('#'), body.size()));
+    std::istringstream in(body);
+    std::uint64_t ends[2];
+    for (int k = 0; k < 2; ++k) {
+      if (in >> ends[k]) continue;
+      std::istringstream probe(body);
+      std::string any;
+      if (k == 0 && !(probe >> any)) return false;
+      bad("malformed edge line: '" + body + "'");
     }
-    if (!(ls >> dst))
-      throw ParseError(path + ":" + std::to_string(line_no) + ": malformed edge line: '" + line + "'");
-    double w = 1.0;
-    std::string rest;
-    if (ls >> rest) {
-      try {
-        std::size_t used = 0;
-        w = std::stod(rest, &used);
-        if (used != rest.size()) throw std::invalid_argument(rest);
-      } catch (const std::exception&) {
-        throw ParseError(path + ":" + std::to_string(line_no) + ": malformed weight '" + rest + "'");
-      }
-      std::string extra;
-      if (ls >> extra)
-        throw ParseError(path + ":" + std::to_string(line_no) +
-                         ": trailing tokens after weight: '" + extra + "'");
+    out = Edge{ends[0], ends[1], 1.0};
+    std::string tok;
+    if (!(in >> tok)) return true;
+    std::size_t used = 0;
+    bool ok = true;
+    try {
+      out.weight = std::stod(tok, &used);
+    } catch (const std::exception&) {
+      ok = false;
     }
-    edges.push_back({src, dst, w});
-    max_id = std::max(max_id, std::max(src, dst));
+    if (!ok || used != tok.size()) bad("malformed weight '" + tok + "'");
+    if (in >> tok) bad("trailing tokens after weight: '" + tok + "'");
+    return true;
+  }
+};
+
+Graph load_edge_list(const std::string& path, bool remap) {
+  std::ifstream file(path);
+  if (!file) throw ParseError("cannot open graph file: " + path);
+  std::vector<Edge> edges;
+  LineParser lp{path};
+  NodeId top = 0;
+  for (std::string text; std::getline(file, text);) {
+    ++lp.line_no;
+    Edge ed;
+    if (!lp.parse(std::move(text), ed)) continue;
+    top = std::max({top, ed.src, ed.dst});
+    edges.push_back(ed);
   }
   if (edges.empty()) throw ValidationError("empty graph: no edges in " + path);
-  std::uint64_t n = max_id + 1;
-  std::vector<bool> present(n, false);
-  for (const Edge& e : edges) present[e.src] = present[e.dst] = true;
-  if (!std::all_of(present.begin(), present.end(), [](bool b) { return b; })) {
+  // ids used, and their dense rank when some id in 0..top never appears
+  std::vector<NodeId> rank(top + 2, 0);
+  for (const Edge& ed : edges) rank[ed.src + 1] = rank[ed.dst + 1] = 1;
+  std::partial_sum(rank.begin(), rank.end(), rank.begin());
+  const NodeId used = rank[top + 1];
+  if (used != top + 1) {
     if (!remap)
       throw ValidationError(path + ": node ids are not contiguous 0..N-1 (use id remapping "
                                    "for sparse-id inputs)");
-    std::vector<NodeId> map(n, 0);
-    NodeId next = 0;
-    for (NodeId i = 0; i < n; ++i)
-      if (present[i]) map[i] = next++;
-    for (Edge& e : edges) {
-      e.src = map[e.src];
-      e.dst = map[e.dst];
+    for (Edge& ed : edges) {  // ascending original id -> 0..used-1
+      ed.src = rank[ed.src];
+      ed.dst = rank[ed.dst];
     }
-    n = next;
   }
-  return Graph::from_edges(n, edges);
+  return Graph::from_edges(used, edges);
 }
 
 void json_escape_free_write(std::ostringstream& o, int indent) {

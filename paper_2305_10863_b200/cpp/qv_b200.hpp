@@ -23,6 +23,7 @@
 
 #include <array>
 #include <cstdint>
+#include <memory>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -31,6 +32,7 @@
 
 struct qvb_store;
 struct qvb_sampler;
+struct qvb_graph;
 
 namespace qv {
 
@@ -99,9 +101,17 @@ struct TransitionView {
     return row_sums[i] > 0.0 ? graph->edge_weights[e] / row_sums[i] : 0.0;
   }
   double prob(NodeId i, NodeId j) const;
+
+  // Extension: the device graph transition_view() built on its one upload
+  // (qvb_transition_view), which compute_access_prob_ie(g, view, L) reuses
+  // when `graph` is still the Graph it was built from (same arrays, sizes).
+  std::shared_ptr<qvb_graph> resident;
+  const void* resident_key[3] = {nullptr, nullptr, nullptr};
+  bool resident_for(const Graph& g) const;
 };
-// transition_view (graph.cpp:292-318). The device path recomputes the row
-// sums itself; this host view exists for API compatibility.
+// transition_view (graph.cpp:292-318) on the device: row sums, distinct
+// out-degrees and has_parallel_edges come from the same upload that builds
+// the P(n,j) in-CSR (kept in `resident`).
 TransitionView transition_view(const Graph& g);
 
 // ---- metrics (metrics.hpp:32-64) ---------------------------------------------
@@ -263,6 +273,12 @@ struct ReadPlan {
 
 ReadPlan plan_reads(const FeatureLookupTable& table, std::span<const NodeId> feature_ids,
                     std::uint64_t page_size = 8);
+class FeatureStore;
+// Extension: the same plan over a store's resident lookup table (the store's
+// reader table; reader 0 is the reference's), with no per-call table upload
+// — the per-batch call of the reference's serving loop (simulator.cpp:320).
+ReadPlan plan_reads(const FeatureStore& store, std::span<const NodeId> feature_ids,
+                    std::uint64_t page_size = 8);
 std::uint64_t page_transitions(std::span<const std::uint64_t> offsets, std::uint64_t page_size);
 
 struct DeviceRef {
@@ -324,6 +340,7 @@ class FeatureStore {
   // Host buffers, synchronous: returns count x dim rows.
   std::vector<float> gather(std::span<const NodeId> ids) const;
   std::uint32_t dim() const { return dim_; }
+  qvb_store* handle() const { return s_; }
 
  private:
   qvb_store* s_ = nullptr;

@@ -234,6 +234,13 @@ __global__ void k_coalesce(const uint32_t* __restrict__ sdst, const uint32_t* __
   }
 }
 
+__global__ void k_count_sources(const uint32_t* __restrict__ ucol, uint64_t eu,
+                                uint32_t* __restrict__ distinct) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < eu;
+       u += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&distinct[ucol[u]], 1u);
+}
+
 // uR of the single unit-weight edges k_coalesce skipped: inv[s].
 __global__ void k_fill_unit_R(const uint32_t* __restrict__ ucol, const uint8_t* __restrict__ uexc,
                               const double* __restrict__ inv, uint64_t eu, double* __restrict__ uR) {
@@ -671,7 +678,7 @@ __global__ void k_long_cls(const uint32_t* __restrict__ lcol, const uint32_t* __
 }  // namespace
 
 void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, const double* d_w,
-                  const uint32_t* d_src, cudaStream_t s) {
+                  const uint32_t* d_src, cudaStream_t s, ViewOut view) {
   const uint64_t n = g.n, e = g.e;
   DevBuf<double> rs(n, s), inv(n + 2, s);  // +2: 16-byte bulk-copy spans (f1)
   QVB_CUDA(cudaMemsetAsync(inv.p + n, 0, 2 * sizeof(double), s));
@@ -683,6 +690,9 @@ void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, con
   if (bad_zero != kNone)
     fail(QVB_ERR_VALIDATION, "node " + std::to_string(bad_zero) +
                                  " has out-edges but all weights are zero");
+  if (view.row_sums)
+    QVB_CUDA(cudaMemcpyAsync(view.row_sums, rs.p, n * 8, cudaMemcpyDeviceToDevice, s));
+  if (view.distinct) QVB_CUDA(cudaMemsetAsync(view.distinct, 0, n * 4, s));
 
   DevBuf<uint64_t> uptr(n + 1, s);
   if (e == 0) {
@@ -755,6 +765,10 @@ void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, con
   ssrc.release();
   head.release();
   uidx.release();
+  if (view.distinct) {  // each coalesced in-edge is one distinct out-neighbour of its source
+    k_count_sources<<<grid_for(eu, kBlock), kBlock, 0, s>>>(ucol.p, eu, view.distinct);
+    QVB_LAUNCH_CHECK();
+  }
 
   DevBuf<uint64_t> cnt(1, s);
   sum_u8_u64(uexc.p, cnt.p, eu, s);
@@ -1837,5 +1851,163 @@ extern "C" int qvb_in_adjacency(int device, uint64_t n, uint64_t e, const uint64
     }
     QVB_CUDA(cudaMemcpyAsync(t_row_offsets, tro.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
     QVB_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+// ---- drop-in construction/validation on the device -----------------------------
+namespace qvb {
+namespace {
+
+// from_edges input checks in input order (graph.cpp:21-33): the first edge
+// with an endpoint out of range (code 0) or a bad weight (code 1) wins;
+// splits the AoS edges into u32 source / destination and the weights.
+__global__ void k_split_edges(const qvb_edge* __restrict__ edges, uint64_t e, uint64_t n,
+                              uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                              double* __restrict__ w, unsigned long long* bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < e;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const qvb_edge ed = edges[i];
+    if (ed.src >= n || ed.dst >= n) atomicMin(bad, (unsigned long long)(i << 1));
+    else if (!(ed.weight >= 0.0)) atomicMin(bad, (unsigned long long)((i << 1) | 1));
+    src[i] = static_cast<uint32_t>(ed.src < n ? ed.src : 0);
+    dst[i] = static_cast<uint32_t>(ed.dst < n ? ed.dst : 0);
+    w[i] = ed.weight;
+  }
+}
+
+__global__ void k_u32_to_u64_out(const uint32_t* __restrict__ in, uint64_t* __restrict__ out,
+                                 uint64_t count) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+void check_zero_rows(const uint64_t* d_ro, const double* d_w, uint64_t n, cudaStream_t s) {
+  DevBuf<double> rs(n, s), inv(n, s);
+  DevBuf<unsigned long long> flag(1, s);
+  QVB_CUDA(cudaMemsetAsync(flag.p, 0xFF, sizeof(unsigned long long), s));
+  k_row_sums<<<grid_for(n, kBlock), kBlock, 0, s>>>(d_ro, d_w, n, rs.p, inv.p, flag.p);
+  QVB_LAUNCH_CHECK();
+  const unsigned long long z = read_scalar(flag.p, s);
+  if (z != kNone)
+    fail(QVB_ERR_VALIDATION, "node " + std::to_string(z) + " has out-edges but all weights are zero");
+}
+
+}  // namespace
+}  // namespace qvb
+
+extern "C" int qvb_graph_validate(int device, uint64_t n, uint64_t e, const uint64_t* row_offsets,
+                                  const uint64_t* col, const double* weights) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    cudaStream_t s = nullptr;
+    DevBuf<uint64_t> ro;
+    DevBuf<uint32_t> dcol;
+    DevBuf<double> dw;
+    upload_out_csr(n, e, row_offsets, col, weights, s, ro, dcol, dw);
+    check_zero_rows(ro.p, dw.p, n, s);
+  });
+}
+
+extern "C" int qvb_build_csr(int device, uint64_t n, const qvb_edge* edges, uint64_t e,
+                             uint64_t* row_offsets, uint64_t* col, double* weights) {
+  return guarded([&] {
+    if (n == 0) fail(QVB_ERR_VALIDATION, "empty graph: node count is zero");
+    if (!row_offsets || (e && (!edges || !col || !weights))) fail(QVB_ERR_VALIDATION, "null argument");
+    if (n > kMaxNodes || e > kMaxEdges)
+      fail(QVB_ERR_UNSUPPORTED, "graph exceeds the device path limits (n < 2^31, e < 2^32)");
+    DeviceGuard dg(device);
+    cudaStream_t s = nullptr;
+    DevBuf<uint64_t> ro(n + 1, s);
+    if (e == 0) {
+      QVB_CUDA(cudaMemsetAsync(ro.p, 0, (n + 1) * 8, s));
+      QVB_CUDA(cudaMemcpyAsync(row_offsets, ro.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+      QVB_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+    DevBuf<uint32_t> src(e, s), dst(e, s), iota(e, s), perm(e, s), ssrc(e, s);
+    DevBuf<double> w(e, s), sw(e, s);
+    {
+      DevBuf<qvb_edge> dedges(e, s);
+      QVB_CUDA(cudaMemcpyAsync(dedges.p, edges, e * sizeof(qvb_edge), cudaMemcpyHostToDevice, s));
+      DevBuf<unsigned long long> bad(1, s);
+      QVB_CUDA(cudaMemsetAsync(bad.p, 0xFF, sizeof(unsigned long long), s));
+      k_split_edges<<<grid_for(e, kBlock), kBlock, 0, s>>>(dedges.p, e, n, src.p, dst.p, w.p, bad.p);
+      QVB_LAUNCH_CHECK();
+      const unsigned long long b = read_scalar(bad.p, s);
+      if (b != kNone) {
+        const qvb_edge& ed = edges[b >> 1];
+        if ((b & 1) == 0)
+          fail(QVB_ERR_VALIDATION, "edge endpoint " + std::to_string(std::max(ed.src, ed.dst)) +
+                                       " out of range for node count " + std::to_string(n));
+        fail(QVB_ERR_VALIDATION, "negative or NaN edge weight on edge " + std::to_string(ed.src) +
+                                     " -> " + std::to_string(ed.dst));
+      }
+    }
+    // stable by source: build_csr's cursor walk keeps input order in a row
+    k_iota<<<grid_for(e, kBlock), kBlock, 0, s>>>(iota.p, e);
+    QVB_LAUNCH_CHECK();
+    sort_pairs_u32_u32(src.p, ssrc.p, iota.p, perm.p, e, 0, bits_for(n - 1), s);
+    k_offsets_from_sorted<<<grid_for(e, kBlock), kBlock, 0, s>>>(ssrc.p, e, n, ro.p);
+    QVB_LAUNCH_CHECK();
+    k_gather_by<double><<<grid_for(e, kBlock), kBlock, 0, s>>>(w.p, perm.p, e, sw.p);
+    QVB_LAUNCH_CHECK();
+    check_zero_rows(ro.p, sw.p, n, s);  // the validate() at the end of build_csr
+    {
+      DevBuf<uint32_t> scol(e, s);
+      k_gather_by<uint32_t><<<grid_for(e, kBlock), kBlock, 0, s>>>(dst.p, perm.p, e, scol.p);
+      QVB_LAUNCH_CHECK();
+      DevBuf<uint64_t> col64(e, s);
+      k_u32_to_u64_out<<<grid_for(e, kBlock), kBlock, 0, s>>>(scol.p, col64.p, e);
+      QVB_LAUNCH_CHECK();
+      copy_to_host(col, col64.p, e * 8, s);
+    }
+    copy_to_host(weights, sw.p, e * 8, s);
+    QVB_CUDA(cudaMemcpyAsync(row_offsets, ro.p, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+    QVB_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+extern "C" int qvb_transition_view(int device, uint64_t n, uint64_t e, const uint64_t* row_offsets,
+                                   const uint64_t* col, const double* weights, double* row_sums,
+                                   uint64_t* distinct_out, int* has_parallel_edges,
+                                   qvb_graph** keep) {
+  return guarded([&] {
+    if (!row_sums || !distinct_out || !has_parallel_edges) fail(QVB_ERR_VALIDATION, "null argument");
+    if (keep) *keep = nullptr;
+    DeviceGuard dg(device);
+    cudaStream_t s = nullptr;
+    auto g = std::make_unique<qvb_graph>();
+    g->device = device;
+    g->n = n;
+    g->e = e;
+    cudaEvent_t ea, eb;
+    QVB_CUDA(cudaEventCreate(&ea));
+    QVB_CUDA(cudaEventCreate(&eb));
+    QVB_CUDA(cudaEventRecord(ea, s));
+    DevBuf<uint64_t> ro;
+    DevBuf<uint32_t> dcol;
+    DevBuf<double> dw;
+    upload_out_csr(n, e, row_offsets, col, weights, s, ro, dcol, dw);
+    DevBuf<double> rs(n, s);
+    DevBuf<uint32_t> distinct(n, s);
+    ViewOut view;
+    view.row_sums = rs.p;
+    view.distinct = distinct.p;
+    build_in_csr(*g, ro.p, dcol.p, dw.p, nullptr, s, view);
+    finish_build(g.get(), ea, eb, s);
+    cudaEventDestroy(ea);
+    cudaEventDestroy(eb);
+    ro.release();
+    dcol.release();
+    dw.release();
+    DevBuf<uint64_t> d64(n, s);
+    k_u32_to_u64_out<<<grid_for(n, kBlock), kBlock, 0, s>>>(distinct.p, d64.p, n);
+    QVB_LAUNCH_CHECK();
+    copy_to_host(row_sums, rs.p, n * 8, s);
+    copy_to_host(distinct_out, d64.p, n * 8, s);
+    QVB_CUDA(cudaStreamSynchronize(s));
+    *has_parallel_edges = g->eu != e ? 1 : 0;
+    if (keep) *keep = g.release();
   });
 }

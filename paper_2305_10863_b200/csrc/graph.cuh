@@ -184,10 +184,18 @@ __host__ __device__ __forceinline__ uint64_t f1_slot(uint64_t base, uint64_t k, 
   return base + (k >> 2) * 128 + lane * 4 + (k & 3);
 }
 
+// transition_view (graph.cpp:292-318) by-products of the in-CSR build, on
+// the device (each nullable): row_sums[n] (sequential CSR-order sums) and
+// distinct[n] (coalesced (source, destination) pairs per source).
+struct ViewOut {
+  double* row_sums = nullptr;
+  uint32_t* distinct = nullptr;
+};
+
 // Builds the in-CSR from a device out-CSR. d_w == nullptr means unit weights.
 // d_src (nullable): source of every out-CSR edge if already known.
 void build_in_csr(qvb_graph& g, const uint64_t* d_ro, const uint32_t* d_col, const double* d_w,
-                  const uint32_t* d_src, cudaStream_t s);
+                  const uint32_t* d_src, cudaStream_t s, ViewOut view = {});
 
 // Segmented sliced layout + long-row CSR from the coalesced in-CSR (uptr,
 // col as stored (flagged exceptions), true sources src, R).

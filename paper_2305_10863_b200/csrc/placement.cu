@@ -691,3 +691,51 @@ extern "C" int qvb_build_lookup_table(int device, const uint64_t* loc_offsets,
     QVB_CUDA(cudaStreamSynchronize(s));
   });
 }
+
+// ---- the reference's collect cost model (placement.cpp:269-302,382-404) ------
+namespace {
+bool translated(int c) {  // address-translated links pay the TLB penalty
+  return c == QVB_LINK_PCIE || c == QVB_LINK_UPI || c == QVB_LINK_INFINIBAND ||
+         c == QVB_LINK_ETHERNET;
+}
+}  // namespace
+
+extern "C" int qvb_classify_link(const qvb_topology* t, uint32_t reader_server, uint32_t reader_tier,
+                                 uint32_t reader_device, int64_t location_id, int* first,
+                                 int* second) {
+  return guarded([&] {
+    if (!t || !first || !second) fail(QVB_ERR_VALIDATION, "null argument");
+    *first = classify_link_from(*t, reader_server, reader_tier, reader_device,
+                                location_id, second);
+  });
+}
+
+extern "C" int qvb_fetch_cost(const qvb_topology* t, uint32_t reader_server, uint32_t reader_tier,
+                              uint32_t reader_device, uint64_t groups, const int64_t* group_loc,
+                              const uint64_t* group_count, const uint64_t* group_transitions,
+                              uint64_t feature_bytes, double* per_location_s, double* total_s) {
+  return guarded([&] {
+    if (!t || !total_s || (groups && (!group_loc || !group_count || !group_transitions ||
+                                      !per_location_s)))
+      fail(QVB_ERR_VALIDATION, "null argument");
+    const int64_t nloc = static_cast<int64_t>(t->servers) * (static_cast<int64_t>(t->gpus_per_server) + 2);
+    double worst = 0.0;
+    for (uint64_t g = 0; g < groups; ++g) {
+      const int64_t id = group_loc[g];
+      if (id < 0 || id >= nloc) fail(QVB_ERR_VALIDATION, "unknown location id " + std::to_string(id));
+      int second = -1;
+      const int first = classify_link_from(*t, reader_server, reader_tier, reader_device, id, &second);
+      const double* lat = t->link_latency_s;
+      const double* bw = t->link_bandwidth_Bps;
+      const double setup = second < 0 ? lat[first] : lat[first] + lat[second];
+      const double rate = second < 0 ? bw[first] : std::min(bw[first], bw[second]);
+      const double bytes = static_cast<double>(feature_bytes) * static_cast<double>(group_count[g]);
+      double s = setup + bytes / rate;
+      if (translated(first) || (second >= 0 && translated(second)))
+        s += t->tlb_miss_penalty_s * static_cast<double>(group_transitions[g]);
+      per_location_s[g] = s;
+      worst = std::max(worst, s);
+    }
+    *total_s = worst;
+  });
+}

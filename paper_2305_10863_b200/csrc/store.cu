@@ -1100,6 +1100,33 @@ extern "C" int qvb_gather_host(qvb_store* s, const uint64_t* ids, uint64_t b, fl
   });
 }
 
+extern "C" int qvb_store_plan_reads(qvb_store* s, const uint64_t* ids, uint64_t b, int ids_on_device,
+                                    uint64_t page_size, int64_t* group_loc, uint64_t* group_count,
+                                    uint64_t* group_transitions, uint64_t* n_groups,
+                                    uint64_t* offsets_out, void* stream) {
+  return guarded([&] {
+    if (!s) fail(QVB_ERR_VALIDATION, "null store");
+    if (page_size == 0) fail(QVB_ERR_VALIDATION, "page size must be > 0");
+    if (!n_groups) fail(QVB_ERR_VALIDATION, "null argument");
+    *n_groups = 0;
+    if (b == 0) return;
+    if (!ids || !group_loc || !group_count || !group_transitions || !offsets_out)
+      fail(QVB_ERR_VALIDATION, "null argument");
+    DeviceGuard dg(s->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint64_t* d_ids = ids;
+    DevBuf<uint64_t> staged;
+    if (!ids_on_device) {  // only the batch travels; the table is resident
+      staged.alloc(b, st);
+      QVB_CUDA(cudaMemcpyAsync(staged.p, ids, b * 8, cudaMemcpyHostToDevice, st));
+      d_ids = staged.p;
+    }
+    DeviceReadPlan rp;
+    plan_reads_device(nullptr, nullptr, s->lut, s->n, d_ids, b, page_size, rp, st);
+    copy_read_plan(rp, group_loc, group_count, group_transitions, n_groups, offsets_out, st);
+  });
+}
+
 extern "C" int qvb_request_ids_synthetic(int device, uint64_t seed, uint64_t batch, uint64_t n,
                                          uint64_t* ids, uint64_t b, void* stream) {
   return guarded([&] {

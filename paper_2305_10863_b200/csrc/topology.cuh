@@ -55,35 +55,40 @@ inline void decode_location(const qvb_topology& t, int64_t id, uint32_t* server,
   }
 }
 
-// classify_link (placement.cpp:228-267). Reader: GPU `rdev` of server `rs`,
-// or the host when the server has no GPUs (reference_reader, :292-295).
-// Returns the first link; *second = -1 when the path has one link.
-inline int classify_link(const qvb_topology& t, uint32_t rs, uint32_t rdev, int64_t id,
-                         int* second) {
+// classify_link (placement.cpp:228-267) for a reader on server `rs` of tier
+// `rtier` (QVB_TIER_*; GPU `rdev` when a GPU). Returns the first link;
+// *second = -1 when the path has one link.
+inline int classify_link_from(const qvb_topology& t, uint32_t rs, uint32_t rtier, uint32_t rdev,
+                              int64_t id, int* second) {
+  const bool reader_gpu = rtier == QVB_TIER_GPU;
   uint32_t server, tier, dev;
   decode_location(t, id, &server, &tier, &dev);
-  const bool reader_gpu = t.gpus_per_server > 0;
   *second = -1;
-  if (server == rs) {
-    if (tier == QVB_TIER_GPU) {
-      if (reader_gpu) {
-        const uint32_t gpn = gpus_per_numa(t);
-        if (rdev == dev) return QVB_LINK_LOCAL;
-        if (gpn > 0 && rdev / gpn == dev / gpn)
-          return t.nvlink_within_numa ? QVB_LINK_NVLINK : QVB_LINK_PCIE;
-        return QVB_LINK_UPI;
-      }
-      return QVB_LINK_PCIE;
-    }
-    if (tier == QVB_TIER_HOST) return reader_gpu ? QVB_LINK_PCIE : QVB_LINK_LOCAL;
-    return QVB_LINK_DISK;
-  }
-  const int net = t.infiniband ? QVB_LINK_INFINIBAND : QVB_LINK_ETHERNET;
-  if (tier == QVB_TIER_DISK) {
+  if (server != rs) {  // another server: over the network (disk: network, then disk)
+    const int net = t.infiniband ? QVB_LINK_INFINIBAND : QVB_LINK_ETHERNET;
+    if (tier != QVB_TIER_DISK) return net;
     *second = net;
     return QVB_LINK_DISK;
   }
-  return net;
+  switch (tier) {
+    case QVB_TIER_HOST: return rtier == QVB_TIER_HOST ? QVB_LINK_LOCAL : QVB_LINK_PCIE;
+    case QVB_TIER_DISK: return QVB_LINK_DISK;
+    default: break;
+  }
+  if (!reader_gpu) return QVB_LINK_PCIE;  // a non-GPU reader of a GPU copy
+  if (rdev == dev) return QVB_LINK_LOCAL;
+  const uint32_t gpn = gpus_per_numa(t);
+  const bool same_numa = gpn > 0 && rdev / gpn == dev / gpn;
+  if (!same_numa) return QVB_LINK_UPI;
+  return t.nvlink_within_numa ? QVB_LINK_NVLINK : QVB_LINK_PCIE;
+}
+
+// The reference reader (placement.cpp:292-295): GPU `rdev` of server `rs`,
+// or the host when the server has no GPUs.
+inline int classify_link(const qvb_topology& t, uint32_t rs, uint32_t rdev, int64_t id,
+                         int* second) {
+  return classify_link_from(t, rs, t.gpus_per_server > 0 ? QVB_TIER_GPU : QVB_TIER_HOST, rdev, id,
+                            second);
 }
 
 // nominal_read_cost (placement.cpp:298-302): setup + 1 MiB / bandwidth.

@@ -169,6 +169,11 @@ _SIGNATURES = {
     "qvb_graph_phase_ms": (i32, [vp, P(C.c_double), P(C.c_uint32)]),
     "qvb_graph_in_rows": (i32, [vp, vp, u64, vp, vp, vp]),
     "qvb_graph_destroy": (i32, [vp]),
+    "qvb_graph_validate": (i32, [i32, u64, u64, vp, vp, vp]),
+    "qvb_build_csr": (i32, [i32, u64, vp, u64, vp, vp, vp]),
+    "qvb_transition_view": (i32, [i32, u64, u64, vp, vp, vp, vp, vp, P(i32), P(vp)]),
+    "qvb_classify_link": (i32, [P(Topology), u32, u32, u32, C.c_int64, P(i32), P(i32)]),
+    "qvb_fetch_cost": (i32, [P(Topology), u32, u32, u32, u64, vp, vp, vp, u64, vp, P(C.c_double)]),
     "qvb_access_prob": (i32, [vp, u32, vp, i32, vp]),
     "qvb_compute_access_prob_ie": (i32, [i32, u64, u64, vp, vp, vp, u32, vp, vp]),
     "qvb_compute_fap": (i32, [i32, u64, u64, vp, vp, vp, u32, vp, vp]),
@@ -191,6 +196,8 @@ _SIGNATURES = {
     "qvb_gather_planned": (i32, [vp, vp, u64, vp, vp]),
     "qvb_gather_host": (i32, [vp, vp, u64, vp, vp]),
     "qvb_store_check_error": (i32, [vp]),
+    "qvb_store_plan_reads": (i32, [vp, vp, u64, i32, u64, vp, vp, vp, P(u64), vp, vp]),
+    "qvb_plan_reads_device": (i32, [i32, vp, vp, u64, vp, u64, u64, vp, vp, vp, P(u64), vp, vp]),
     "qvb_request_ids_synthetic": (i32, [i32, u64, u64, u64, vp, u64, vp]),
     "qvb_sampler_create": (i32, [i32, u64, u64, vp, vp, vp, vp, P(vp)]),
     "qvb_sampler_synthetic": (i32, [i32, u64, u64, u64, i32, i32, vp, P(vp)]),
@@ -373,6 +380,47 @@ def synthetic_csr(n: int, e: int, seed: int = 7, weighted: bool = False,
     return ro, col[:e], w[:e]
 
 
+def transition_view(row_offsets, col, weights=None, device: int = 0, keep: bool = False):
+    """qv::transition_view (graph.cpp:292-318) on the device:
+    (row_sums, distinct_out, has_parallel_edges[, DeviceGraph]). keep=True
+    also returns the device graph the same upload built (for access_prob)."""
+    ro = np.ascontiguousarray(row_offsets, np.uint64)
+    c = np.ascontiguousarray(col, np.uint64)
+    w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+    n, e = len(ro) - 1, len(c)
+    rs = np.empty(max(n, 1), np.float64)
+    dist = np.empty(max(n, 1), np.uint64)
+    par = C.c_int(0)
+    h = C.c_void_p()
+    _check(_lib().qvb_transition_view(device, n, e, _ptr(ro), _ptr(c) if e else None, _ptr(w),
+                                      _ptr(rs), _ptr(dist), C.byref(par), C.byref(h) if keep else None))
+    out = (rs[:n], dist[:n], bool(par.value))
+    return out + (DeviceGraph(h.value),) if keep else out
+
+
+def graph_validate(row_offsets, col, weights=None, device: int = 0) -> None:
+    """qv::Graph::validate (graph.cpp:58-93) on the device."""
+    ro = np.ascontiguousarray(row_offsets, np.uint64)
+    c = np.ascontiguousarray(col, np.uint64)
+    w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+    _check(_lib().qvb_graph_validate(device, len(ro) - 1, len(c), _ptr(ro), _ptr(c) if len(c) else None,
+                                     _ptr(w)))
+
+
+def from_edges(n: int, src, dst, weights, device: int = 0):
+    """qv::Graph::from_edges (graph.cpp:16-56) on the device -> out-CSR."""
+    e = len(src)
+    edges = np.empty(max(e, 1), dtype=[("src", "<u8"), ("dst", "<u8"), ("w", "<f8")])
+    edges["src"][:e] = np.asarray(src, np.uint64)
+    edges["dst"][:e] = np.asarray(dst, np.uint64)
+    edges["w"][:e] = np.asarray(weights, np.float64)
+    ro = np.empty(n + 1, np.uint64)
+    col = np.empty(max(e, 1), np.uint64)
+    w = np.empty(max(e, 1), np.float64)
+    _check(_lib().qvb_build_csr(device, n, edges.ctypes.data, e, _ptr(ro), _ptr(col), _ptr(w)))
+    return ro, col[:e], w[:e]
+
+
 def in_adjacency(row_offsets, col, weights=None, device: int = 0):
     """qv::in_adjacency (graph.cpp:260-281) on the device -> host transpose."""
     ro = np.ascontiguousarray(row_offsets, np.uint64)
@@ -510,6 +558,29 @@ def plan_reads(location_ids, offsets, ids, page_size: int = 8, device: int = 0):
     return gl[:g].copy(), gc[:g].copy(), gt[:g].copy(), oo[:b].copy()
 
 
+def _plan_out(b: int, groups_cap: int):
+    m = max(b, 1)
+    g = max(1, min(m, groups_cap))
+    return (np.empty(g, np.int64), np.empty(g, np.uint64), np.empty(g, np.uint64),
+            np.empty(m, np.uint64), u64(0))
+
+
+def plan_reads_device(location_ids, offsets, ids, page_size: int = 8, device: int = 0, stream=None):
+    """qv::plan_reads over a lookup table already on the device (torch tensors
+    location_ids int64[n], offsets uint64/int64[n], ids [b]): no table upload."""
+    for t in (location_ids, offsets, ids):
+        if not t.is_cuda or not t.is_contiguous() or t.element_size() != 8:
+            raise ValidationError("table and ids must be contiguous 64-bit device tensors")
+    b = int(ids.numel())
+    gl, gc, gt, oo, ng = _plan_out(b, b)
+    _check(_lib().qvb_plan_reads_device(device, _ptr(location_ids), _ptr(offsets),
+                                        int(location_ids.numel()), _ptr(ids), b, page_size,
+                                        _ptr(gl), _ptr(gc), _ptr(gt), C.byref(ng), _ptr(oo),
+                                        _stream_ptr(stream)))
+    g = ng.value
+    return gl[:g], gc[:g], gt[:g], oo[:b]
+
+
 # ---- K5 feature store + gather ---------------------------------------------------
 class FeatureStore:
     """One reader GPU's view of the placed feature table (qvb_store).
@@ -571,6 +642,24 @@ class FeatureStore:
 
     def check_error(self) -> None:
         _check(_lib().qvb_store_check_error(self._h))
+
+    def plan_reads(self, ids, page_size: int = 8, stream=None):
+        """qv::plan_reads over this store's resident lookup table; ids are a
+        host array or a device tensor. Same flattened result as plan_reads."""
+        on_dev = hasattr(ids, "is_cuda") and ids.is_cuda
+        if on_dev:
+            if not ids.is_contiguous() or ids.element_size() != 8:
+                raise ValidationError("ids must be a contiguous 64-bit tensor")
+            req, b = ids, int(ids.numel())
+        else:
+            req = np.ascontiguousarray(ids, np.uint64)
+            b = len(req)
+        gl, gc, gt, oo, ng = _plan_out(b, self.info().location_count)
+        _check(_lib().qvb_store_plan_reads(self._h, _ptr(req) if b else None, b, int(on_dev), page_size,
+                                           _ptr(gl), _ptr(gc), _ptr(gt), C.byref(ng), _ptr(oo),
+                                           _stream_ptr(stream)))
+        g = ng.value
+        return gl[:g], gc[:g], gt[:g], oo[:b]
 
     def gather_host(self, ids, out=None, stream=None) -> np.ndarray:
         """End-to-end collect from host buffers (H2D ids, gather, D2H rows)."""
