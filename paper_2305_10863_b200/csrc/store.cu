@@ -537,6 +537,156 @@ __global__ void k_plan_keys_packed(const uint64_t* __restrict__ ids, uint64_t b,
   }
 }
 
+// ---- tier-isolated gather (requests bucketed by location class) -------------
+// The reference groups a batch by location before reading (plan_reads,
+// placement.cpp:363-379) and models each location's reads as concurrent
+// streams (fetch_cost, :388-402). Here: one pass sorts the requests into
+// three lists — local HBM, peer HBM (NVLink), host (PCIe) — and the copy
+// kernel's warps take 32-row groups from the lists through atomic cursors,
+// each warp starting on its own class, so PCIe rows never sit in the same
+// load round as HBM rows (a mixed round waits for its slowest row).
+constexpr int kClasses = 3;  // 0 local, 1 peer, 2 host
+
+struct ClassLists {
+  uint32_t* req[kClasses];             // request index
+  unsigned long long* src[kClasses];   // source row address
+  unsigned int* count;                 // [kClasses] list lengths
+  unsigned int* cursor;                // [kClasses] next 32-row group to take
+};
+
+__global__ void __launch_bounds__(256)
+    k_split_classes(const uint64_t* __restrict__ ids, uint64_t b, const uint64_t* __restrict__ lut,
+                    Bases bases, uint64_t stride, uint64_t n, int local_loc, int host_loc,
+                    ClassLists L, unsigned long long* err) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint64_t stride_all = (uint64_t)gridDim.x * blockDim.x;
+  // warp-uniform trip count: every lane reaches the ballots
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < b; i0 += stride_all) {
+    const uint64_t i = i0 + lane;
+    int cls = -1;
+    uint64_t src = 0;
+    if (i < b) {
+      const uint64_t f = __ldg(ids + i);
+      if (f >= n) {
+        atomicMin(err, (unsigned long long)i);
+      } else {
+        const uint64_t e = __ldg(lut + f);
+        const int loc = static_cast<int>(e >> kOffsetBits);
+        cls = loc == local_loc ? 0 : (loc == host_loc ? 2 : 1);
+        src = reinterpret_cast<uint64_t>(bases.p[loc]) + (e & kOffsetMask) * stride;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kClasses; ++c) {
+      const uint32_t m = __ballot_sync(0xffffffffu, cls == c);
+      if (!m) continue;
+      unsigned int base = 0;
+      if (lane == __ffs(m) - 1) base = atomicAdd(L.count + c, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+      if (cls == c) {
+        const unsigned int pos = base + __popc(m & lt);
+        L.req[c][pos] = static_cast<uint32_t>(i);
+        L.src[c][pos] = src;
+      }
+    }
+  }
+}
+
+template <int VEC, int kU>
+__global__ void __launch_bounds__(kGatherBlock, 4)
+    k_gather_classes(ClassLists L, uint32_t cpr, uint32_t row_bytes, char* __restrict__ out,
+                     int host_every) {
+  using V = Vec<VEC>;
+  const uint64_t pol = policy_evict_first();  // rows: a stream
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t q32 = 32 / cpr, r32 = 32 % cpr;
+  const uint32_t row0 = lane / cpr, k0 = lane - row0 * cpr;
+  // class order of this warp: one warp in `host_every` starts on the host
+  // list (enough PCIe reads in flight), the others on local then peer rows;
+  // a warp whose list runs dry moves on to the next class
+  int order[kClasses] = {0, 1, 2};
+  if (warp % host_every == 0) {
+    order[0] = 2;
+    order[1] = 0;
+    order[2] = 1;
+  }
+  unsigned int cnt[kClasses];
+#pragma unroll
+  for (int c = 0; c < kClasses; ++c) cnt[c] = __ldcg(L.count + c);
+  int oi = 0;
+  // next (class, group) for this warp, or class -1 when every list is done
+  auto take = [&](int& cls, unsigned int& g) {
+    cls = -1;
+    while (oi < kClasses) {
+      const int c = order[oi];
+      unsigned int t = 0;
+      if (lane == 0) t = cnt[c] ? atomicAdd(L.cursor + c, 1u) : 0xFFFFFFFFu;
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (cnt[c] && (uint64_t)t * 32 < cnt[c]) {
+        cls = c;
+        g = t;
+        return;
+      }
+      ++oi;
+    }
+  };
+  auto fetch = [&](int cls, unsigned int g, uint64_t& src, uint64_t& dst) {
+    src = 0;
+    dst = 0;
+    if (cls < 0) return;
+    const uint64_t j = (uint64_t)g * 32 + lane;
+    if (j < cnt[cls]) {
+      src = L.src[cls][j];
+      dst = reinterpret_cast<uint64_t>(out) + (uint64_t)L.req[cls][j] * row_bytes;
+    }
+  };
+  int cls;
+  unsigned int g;
+  take(cls, g);
+  uint64_t src, dst;
+  fetch(cls, g, src, dst);
+  while (cls >= 0) {
+    int ncls;
+    unsigned int ng;
+    take(ncls, ng);  // the next group's rows resolve while this one copies
+    uint64_t nsrc, ndst;
+    fetch(ncls, ng, nsrc, ndst);
+    const uint64_t left = cnt[cls] - (uint64_t)g * 32;
+    const uint32_t nr = static_cast<uint32_t>(left < 32 ? left : 32);
+    const uint32_t tot = nr * cpr;
+    uint32_t row = row0, k = k0;
+    for (uint32_t cb = 0; cb < tot; cb += 32 * kU) {  // warp-uniform trip count
+      typename V::T v[kU];
+      uint64_t d[kU];
+      bool ok[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t c = cb + lane + u * 32;
+        const uint32_t rr = row < 32 ? row : 31;
+        const uint64_t s = __shfl_sync(0xffffffffu, src, rr);
+        d[u] = __shfl_sync(0xffffffffu, dst, rr) + (uint64_t)k * VEC;
+        ok[u] = c < tot;
+        if (ok[u]) v[u] = V::load(reinterpret_cast<const char*>(s) + (uint64_t)k * VEC, pol);
+        row += q32;
+        k += r32;
+        if (k >= cpr) {
+          k -= cpr;
+          ++row;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (ok[u]) V::store(reinterpret_cast<char*>(d[u]), v[u], pol);
+    }
+    cls = ncls;
+    g = ng;
+    src = nsrc;
+    dst = ndst;
+  }
+}
+
 __global__ void k_fill_synthetic(const uint64_t* __restrict__ feat_of_row, uint64_t rows,
                                  uint32_t dim, uint64_t stride, char* __restrict__ shard) {
   const uint64_t total = rows * dim;
@@ -665,6 +815,16 @@ struct qvb_store {
     // overrides the request-count threshold.
     const char* sm = std::getenv("QVB_GATHER_SMALL");
     const uint64_t small_rows = sm ? std::strtoull(sm, nullptr, 10) : 49152ull;
+    // rows from more than this GPU's shard (peers over NVLink, the host tier
+    // over PCIe): bucket by location class first so the links do not share
+    // load rounds (QVB_GATHER_SPLIT=0 keeps the mixed row-group kernel)
+    const bool mixed = (used_mask & ~(1ull << reader)) != 0;
+    const char* split_e = std::getenv("QVB_GATHER_SPLIT");  // per call (tests flip it)
+    const int split_env = split_e ? std::atoi(split_e) : 1;
+    if (kind != 1 && b > small_rows && mixed && split_env && b < (1ull << 32) && (V == 16 || V == 4 || V == 8)) {
+      launch_split(ids, b, cpr, out, s, err);
+      return;
+    }
     if (kind != 1 && b > small_rows) {
       if (V == 16) launch_rows<16>(ids, b, cpr, out, s, err);
       else if (V == 8 && stride % 16 == 0) launch_rows_wide(ids, b, out, s, err);
@@ -680,6 +840,40 @@ struct qvb_store {
       else if (V == 8) launch_direct<8>(ids + r0, rows, cpr, o, r0, s, err);
       else launch_direct<4>(ids + r0, rows, cpr, o, r0, s, err);
     }
+  }
+
+  void launch_split(const uint64_t* ids, uint64_t b, uint32_t cpr, char* out, cudaStream_t s,
+                    unsigned long long* err) {
+    DevBuf<uint32_t> req(b * kClasses, s);
+    DevBuf<unsigned long long> srcs(b * kClasses, s);
+    DevBuf<unsigned int> ctr(2 * kClasses, s);
+    QVB_CUDA(cudaMemsetAsync(ctr.p, 0, 2 * kClasses * sizeof(unsigned int), s));
+    ClassLists L;
+    for (int c = 0; c < kClasses; ++c) {
+      L.req[c] = req.p + c * b;
+      L.src[c] = srcs.p + c * b;
+    }
+    L.count = ctr.p;
+    L.cursor = ctr.p + kClasses;
+    const unsigned sgrid = resident_grid_cached(k_split_classes, 256, 0);
+    k_split_classes<<<std::min<uint64_t>(sgrid, (b + 255) / 256), 256, 0, s>>>(
+        ids, b, lut, bases, stride, n, static_cast<int>(reader), nloc - 2, L, err);
+    QVB_LAUNCH_CHECK();
+    static const int host_every = [] {
+      const char* e = std::getenv("QVB_HOST_EVERY");
+      return e ? std::max(1, std::atoi(e)) : 8;
+    }();
+    const int V = vec();
+    if (V == 16) launch_classes<16>(L, cpr, out, host_every, s);
+    else if (V == 8) launch_classes<8>(L, cpr, out, host_every, s);
+    else launch_classes<4>(L, cpr, out, host_every, s);
+  }
+
+  template <int V>
+  void launch_classes(const ClassLists& L, uint32_t cpr, char* out, int host_every, cudaStream_t s) {
+    const unsigned grid = resident_grid_cached(k_gather_classes<V, 4>, kGatherBlock, 0);
+    k_gather_classes<V, 4><<<grid, kGatherBlock, 0, s>>>(L, cpr, row_bytes, out, host_every);
+    QVB_LAUNCH_CHECK();
   }
 
   static uint64_t work_blocks(uint64_t chunks) {

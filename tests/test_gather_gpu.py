@@ -197,3 +197,58 @@ def test_c2_gather_full_size(qvb, oracle):
     assert (got[sample] == x_rows[req[sample].astype(np.int64)]).all()
     assert (got == x_rows[req.astype(np.int64)]).all()
     st.close()
+
+
+@pytest.mark.parametrize("mix", ["host", "peer", "peer+host"])
+@pytest.mark.parametrize("dim", [128, 100, 33, 602])
+def test_tier_split_gather_bit_exact(qvb, oracle, mix, dim, monkeypatch):
+    """The location-bucketed gather (local / peer / host lists, warps taking
+    32-row groups per class) against the restatement, for every class mix,
+    row width and both device and host entry points; the mixed row-group
+    kernel (QVB_GATHER_SPLIT=0) gives the same bytes."""
+    import torch
+
+    monkeypatch.setenv("QVB_GATHER_SMALL", "0")
+    n = 12000
+    gpus = 1 if mix == "host" else 4
+    host = n if "host" in mix else 0
+    cap = n // 2 if mix == "host" else (n // gpus + 1 if mix == "peer" else n // (2 * gpus))
+    t, lo, ids = plan(qvb, n, gpus=gpus, cap=cap, host=host)
+    stores = [qvb.FeatureStore(lo, ids, dim, t, reader=r) for r in range(gpus)]
+    for r, st in enumerate(stores):
+        for p in range(gpus):
+            if p != r:
+                st.attach_local_peer(p, stores[p])
+    x = oracle.features(n, dim)
+    req = oracle.request_ids(11, 21, n, 70001)
+    exp = oracle.gather(x, req)
+    d_ids = torch.from_numpy(req.view(np.int64)).cuda()
+    for st in stores[:2]:
+        assert (st.gather_host(req) == exp).all()
+        out = torch.full((len(req), dim), -1.0, dtype=torch.float32, device="cuda")
+        st.gather(d_ids, out)
+        st.check_error()
+        assert (out.cpu().numpy() == exp).all()
+    monkeypatch.setenv("QVB_GATHER_SPLIT", "0")
+    assert (stores[-1].gather_host(req) == exp).all()
+    for st in stores:
+        st.close()
+
+
+def test_tier_split_gather_reports_bad_ids(qvb, oracle, monkeypatch):
+    import torch
+
+    monkeypatch.setenv("QVB_GATHER_SMALL", "0")
+    n, dim = 5000, 32
+    t, lo, ids = plan(qvb, n, cap=n // 3, host=n)
+    st = qvb.FeatureStore(lo, ids, dim, t, reader=0)
+    req = oracle.request_ids(11, 5, n, 60000)
+    req[33333] = n + 5
+    with pytest.raises(qvb.ValidationError, match=f"feature id {n + 5} outside"):
+        st.gather_host(req)
+    d = torch.from_numpy(req.view(np.int64)).cuda()
+    out = torch.empty((len(req), dim), dtype=torch.float32, device="cuda")
+    st.gather(d, out)
+    with pytest.raises(qvb.ValidationError, match="request 33333"):
+        st.check_error()
+    st.close()
