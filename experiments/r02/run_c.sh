@@ -5,6 +5,10 @@ OUT=gpurun_out; T=r02c; mkdir -p $OUT
 timeout 1500 python -m pytest -q -x tests/test_reference_tests_gpu.py tests/test_dropin_graph_gpu.py \
   tests/test_reads_resident_gpu.py tests/test_gather_gpu.py tests/test_cpp_dropin_gpu.py \
   tests/test_placement_gpu.py > $OUT/${T}_tests.log 2>&1; tail -3 $OUT/${T}_tests.log
+for tool in memcheck racecheck synccheck initcheck; do
+  timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python experiments/r02/sanitize.py > $OUT/${T}_sanitize_$tool.log 2>&1
+  echo "sanitizer $tool rc=$?"; tail -2 $OUT/${T}_sanitize_$tool.log
+done
 B="python bench.py --no-cpu-baseline --no-e2e --sample-seeds 0 --steps 10 --warmup 3 --clock-window 0.3"
 summ() { python -c "
 import json,sys

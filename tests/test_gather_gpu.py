@@ -214,7 +214,7 @@ def test_tier_split_gather_bit_exact(qvb, oracle, mix, dim, monkeypatch):
     host = n if "host" in mix else 0
     cap = n // 2 if mix == "host" else (n // gpus + 1 if mix == "peer" else n // (2 * gpus))
     t, lo, ids = plan(qvb, n, gpus=gpus, cap=cap, host=host)
-    stores = [qvb.FeatureStore(lo, ids, dim, t, reader=r) for r in range(gpus)]
+    stores = [qvb.FeatureStore(lo, ids, dim, t, reader=r, device=0) for r in range(gpus)]
     for r, st in enumerate(stores):
         for p in range(gpus):
             if p != r:

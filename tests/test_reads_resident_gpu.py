@@ -25,7 +25,7 @@ def test_store_plan_reads_matches_reference_plan(qvb, oracle, gpus, rep, host):
                       host=n if host is None else host + n)
     ot = otopo_from(t)
     for reader in sorted({0, gpus - 1}):
-        st = qvb.FeatureStore(lo, ids, 16, t, reader=reader)
+        st = qvb.FeatureStore(lo, ids, 16, t, reader=reader, device=0)
         loc, off = oracle.build_lookup_table(lo, ids, ot, 0, reader)
         for k, (b, page) in enumerate([(1, 8), (777, 1), (5000, 8), (65536, 3)]):
             req = oracle.request_ids(11, 40 + k, n, b)
