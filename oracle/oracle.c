@@ -242,6 +242,34 @@ void qvo_features_mt(uint64_t first, uint64_t count, uint32_t dim, float* x, int
   for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
 }
 
+/* out[i] = X[ids[i]] straight from the feature generator,
+ * without materialising X: the expected rows of a gather over a table too
+ * big for host RAM checks (C4: 56.8 GB). */
+typedef struct {
+  const uint64_t* ids;
+  uint32_t dim;
+  float* out;
+  uint64_t lo, hi;
+} rows_job;
+
+static void* rows_worker(void* arg) {
+  rows_job* j = (rows_job*)arg;
+  for (uint64_t i = j->lo; i < j->hi; ++i) qvo_features(j->ids[i], 1, j->dim, j->out + i * j->dim);
+  return NULL;
+}
+
+void qvo_feature_rows(const uint64_t* ids, uint64_t b, uint32_t dim, float* out, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  rows_job jobs[256];
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = (rows_job){ids, dim, out, b * t / threads, b * (t + 1) / threads};
+    pthread_create(&th[t], NULL, rows_worker, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+}
+
 /* Graph::validate (graph.cpp:58-93) */
 int qvo_validate(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col,
                  const double* w) {

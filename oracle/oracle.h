@@ -91,6 +91,7 @@ int qvo_plan_reads(const int64_t* location_ids, const uint64_t* offsets, uint64_
 
 /* Synthetic inputs of SURVEY §8(d). */
 void qvo_features(uint64_t first, uint64_t count, uint32_t dim, float* x);
+void qvo_feature_rows(const uint64_t* ids, uint64_t b, uint32_t dim, float* out, int threads);
 void qvo_features_mt(uint64_t first, uint64_t count, uint32_t dim, float* x, int threads);
 void qvo_request_ids(uint64_t seed, uint64_t batch, uint64_t n, uint64_t* ids, uint64_t b);
 /* Row gather restatement: out[i] = X[ids[i]] with `threads` pthreads. */

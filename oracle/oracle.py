@@ -114,6 +114,7 @@ class Oracle(_Lib):
         L.qvo_synthetic_graph_mt.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.c_int,
                                              C.c_int, u64p, u64p, f64p]
         L.qvo_features_mt.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, f32p, C.c_int]
+        L.qvo_feature_rows.argtypes = [u64p, C.c_uint64, C.c_uint32, f32p, C.c_int]
         L.qvo_build_csr.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, u64p, u64p, f64p]
         L.qvo_validate.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p]
         L.qvo_in_adjacency.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, u64p, u64p, f64p]
@@ -265,6 +266,13 @@ class Oracle(_Lib):
         else:
             self._lib.qvo_features(first, n, dim, x.reshape(-1))
         return x
+
+    def feature_rows(self, ids, dim: int, threads: int = 1):
+        """X[ids] from the generator, without the table."""
+        ids = np.ascontiguousarray(ids, np.uint64)
+        out = np.empty((max(len(ids), 1), dim), np.float32)
+        self._lib.qvo_feature_rows(_pad(ids, np.uint64), len(ids), dim, out.reshape(-1), threads)
+        return out[: len(ids)]
 
     def request_ids(self, seed: int, batch: int, n: int, b: int):
         ids = np.zeros(b, np.uint64)

@@ -10,7 +10,7 @@ import os
 import numpy as np
 import pytest
 
-from tests.util import CONFIGS, bits, derive_stream, fig8_edges, random_edges
+from tests.util import c4_reference_enabled, CONFIGS, bits, derive_stream, fig8_edges, random_edges
 
 pytestmark = pytest.mark.gpu
 
@@ -378,8 +378,8 @@ def test_c4_sampled_against_oracle(qvb, oracle):
     assert (bits(p3[nodes]) == bits(exp3)).all()
 
 
-@pytest.mark.skipif(os.environ.get("QVB_C4_REFERENCE") != "1",
-                    reason="opt-in: ~3 min and ~90 GB of host RAM (QVB_C4_REFERENCE=1)")
+@pytest.mark.skipif(not c4_reference_enabled(),
+                    reason="needs >= 150 GB host RAM (QVB_C4_REFERENCE=1 forces, =0 skips)")
 def test_c4_full_against_reference():
     """All 111M C4 nodes against the unmodified reference's own
     compute_access_prob_ie (oracle/_ref, 16 threads), from one host CSR."""

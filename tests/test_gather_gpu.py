@@ -5,6 +5,8 @@ restatement out[i] = X[ids[i]] (oracle.c qvo_gather) over the same synthetic
 features and request streams ("parity unpinned" for the bytes,
 pinned for the lookup table that routes them).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -251,4 +253,29 @@ def test_tier_split_gather_reports_bad_ids(qvb, oracle, monkeypatch):
     st.gather(d, out)
     with pytest.raises(qvb.ValidationError, match="request 33333"):
         st.check_error()
+    st.close()
+
+
+def test_c4_gather_full_size(qvb, oracle):
+    """C4 shape (111M x 128 fp32 = 56.8 GB in HBM) with a 1M-id batch: every
+    gathered row bit-identical to the generator's row (no host copy of the
+    table needed)."""
+    import torch
+
+    from tests.util import CONFIGS
+
+    c = CONFIGS["C4"]
+    n, dim, b = c["n"], 128, 1 << 20
+    t, lo, ids = plan(qvb, n)
+    st = qvb.FeatureStore(lo, ids, dim, t, reader=0)
+    d_ids = torch.empty(b, dtype=torch.int64, device="cuda")
+    qvb.request_ids_synthetic(11, 0, n, d_ids)
+    out = torch.empty((b, dim), dtype=torch.float32, device="cuda")
+    st.gather(d_ids, out)
+    st.check_error()
+    req = d_ids.cpu().numpy().view(np.uint64)
+    assert (req == oracle.request_ids(11, 0, n, b)).all()
+    exp = oracle.feature_rows(req, dim, threads=os.cpu_count() or 1)
+    assert (out.cpu().numpy() == exp).all()
+    assert (st.gather_host(req[:300_000]) == exp[:300_000]).all()
     st.close()

@@ -309,3 +309,9 @@ def test_threaded_generator_matches_sequential(oracle, n, e, weighted, transpose
         assert all((x.view(np.uint64) == y.view(np.uint64)).all() for x, y in zip(a, b))
     x = oracle.features(1000, 37, first=5)
     assert (x == oracle.features(1000, 37, first=5, threads=5)).all()
+
+
+def test_feature_rows_match_table(oracle):
+    x = oracle.features(3000, 41)
+    ids = oracle.request_ids(5, 1, 3000, 20000)
+    assert (oracle.feature_rows(ids, 41, threads=3) == x[ids.astype(np.int64)]).all()

@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 from oracle.oracle import topology_defaults
-from tests.util import CONFIGS, bits, derive_stream
+from tests.util import c4_reference_enabled, CONFIGS, bits, derive_stream
 
 pytestmark = pytest.mark.gpu
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
@@ -246,8 +246,8 @@ def test_c2_rank_and_lut_vs_oracle(qvb, oracle):
         assert (x == y).all()
 
 
-@pytest.mark.skipif(os.environ.get("QVB_C4_REFERENCE") != "1",
-                    reason="opt-in: ~2 min, C4-sized planner runs (QVB_C4_REFERENCE=1)")
+@pytest.mark.skipif(not c4_reference_enabled(),
+                    reason="needs >= 150 GB host RAM (QVB_C4_REFERENCE=1 forces, =0 skips)")
 def test_c4_full_placement_against_reference(qvb):
     """C4 at full size (111M features, 8 GPUs, capacity N/16): plan, lookup
     table and a 1M-id read plan equal the unmodified reference's own."""

@@ -6,6 +6,8 @@ random graphs below are the same graphs the reference's own tests draw
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 M64 = (1 << 64) - 1
@@ -76,3 +78,20 @@ CONFIGS = {
     "C3": dict(n=233_000, e=114_000_000, weighted=True, layers=3, dim=602),
     "C4": dict(n=111_000_000, e=1_600_000_000, weighted=False, layers=3, dim=128),
 }
+
+
+def host_ram_gb() -> float:
+    try:
+        return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 1e9
+    except (ValueError, OSError, AttributeError):
+        return 0.0
+
+
+def c4_reference_enabled() -> bool:
+    """C4-vs-unmodified-reference checks: on by default where the host has
+    the RAM (the B200 boxes: 196 GB); QVB_C4_REFERENCE=0 turns them off,
+    =1 forces them."""
+    v = os.environ.get("QVB_C4_REFERENCE")
+    if v is not None:
+        return v == "1"
+    return host_ram_gb() >= 150
