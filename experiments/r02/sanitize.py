@@ -43,7 +43,7 @@ def main():
             g.close()
             for k in env:
                 del os.environ[k]
-        assert (qvb.compute_fap(ro, col, w, 3) == o.compute_fap(ro, col, w, 3)).all()
+        assert (bits(qvb.compute_fap(ro, col, w, 3).values) == bits(o.compute_fap(ro, col, w, 3))).all()
         tro, tcol, tw = qvb.in_adjacency(ro, col, w)
         a = o.in_adjacency(ro, col, w)
         assert (tro == a[0]).all() and (tcol == a[1]).all()

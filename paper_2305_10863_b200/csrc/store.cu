@@ -552,12 +552,23 @@ struct ClassLists {
   unsigned long long* src[kClasses];   // source row address
   unsigned int* count;                 // [kClasses] list lengths
   unsigned int* cursor;                // [kClasses] next 32-row group to take
+  unsigned int* hist;                  // host rows per offset bucket (null: unordered)
+  int hshift;                          // host offset >> hshift = bucket
 };
+
+// Host-tier requests in ascending offset buckets (a counting sort of the host
+// list on kHostBuckets offset ranges): pinned host pages are then walked in
+// address order, which keeps the GPU's page-table walks for system memory
+// local — random rows from a 14 GB host tier read at 38 GB/s, rows in offset
+// order well above (profiles/r01k_host_tier.txt, r01m_gather_sweep.md).
+constexpr int kHostBucketBits = 16;
+constexpr int kHostBuckets = 1 << kHostBucketBits;
 
 __global__ void __launch_bounds__(256)
     k_split_classes(const uint64_t* __restrict__ ids, uint64_t b, const uint64_t* __restrict__ lut,
                     Bases bases, uint64_t stride, uint64_t n, int local_loc, int host_loc,
                     ClassLists L, unsigned long long* err) {
+  const uint64_t host_base = reinterpret_cast<uint64_t>(bases.p[host_loc]);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
   const uint64_t stride_all = (uint64_t)gridDim.x * blockDim.x;
@@ -588,8 +599,51 @@ __global__ void __launch_bounds__(256)
         const unsigned int pos = base + __popc(m & lt);
         L.req[c][pos] = static_cast<uint32_t>(i);
         L.src[c][pos] = src;
+        if (c == 2 && L.hist) atomicAdd(L.hist + ((src - host_base) / stride >> L.hshift), 1u);
       }
     }
+  }
+}
+
+// exclusive scan of the bucket counts in place (one block of 1024 threads)
+__global__ void __launch_bounds__(1024) k_bucket_scan(unsigned int* __restrict__ hist) {
+  constexpr int per = kHostBuckets / 1024;
+  __shared__ unsigned int part[1024];
+  unsigned int v[per], sum = 0;
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < per; ++k) {
+    v[k] = hist[t * per + k];
+    sum += v[k];
+  }
+  part[t] = sum;
+  __syncthreads();
+  for (int d = 1; d < 1024; d <<= 1) {  // Hillis-Steele inclusive scan
+    const unsigned int x = t >= d ? part[t - d] : 0;
+    __syncthreads();
+    part[t] += x;
+    __syncthreads();
+  }
+  unsigned int run = part[t] - sum;
+#pragma unroll
+  for (int k = 0; k < per; ++k) {
+    hist[t * per + k] = run;
+    run += v[k];
+  }
+}
+
+// host list -> bucket order (order inside a bucket is arbitrary; every row
+// still lands at its request's output position)
+__global__ void k_bucket_scatter(ClassLists L, const uint32_t* __restrict__ in_req,
+                                 const unsigned long long* __restrict__ in_src, uint64_t host_base,
+                                 uint64_t stride, uint64_t cap) {
+  const unsigned int cnt = __ldcg(L.count + 2);
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < cap && j < cnt;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long src = in_src[j];
+    const unsigned int pos = atomicAdd(L.hist + ((src - host_base) / stride >> L.hshift), 1u);
+    L.req[2][pos] = in_req[j];
+    L.src[2][pos] = src;
   }
 }
 
@@ -844,10 +898,13 @@ struct qvb_store {
 
   void launch_split(const uint64_t* ids, uint64_t b, uint32_t cpr, char* out, cudaStream_t s,
                     unsigned long long* err) {
-    DevBuf<uint32_t> req(b * kClasses, s);
-    DevBuf<unsigned long long> srcs(b * kClasses, s);
-    DevBuf<unsigned int> ctr(2 * kClasses, s);
-    QVB_CUDA(cudaMemsetAsync(ctr.p, 0, 2 * kClasses * sizeof(unsigned int), s));
+    const int host_loc = nloc - 2;
+    const char* so = std::getenv("QVB_HOST_SORT");  // per call: tests and A/B flip it
+    const bool order_host = host_rows > 0 && (used_mask >> host_loc & 1) && !(so && *so == '0');
+    DevBuf<uint32_t> req(b * (kClasses + (order_host ? 1 : 0)), s);
+    DevBuf<unsigned long long> srcs(b * (kClasses + (order_host ? 1 : 0)), s);
+    DevBuf<unsigned int> ctr(2 * kClasses + (order_host ? kHostBuckets : 0), s);
+    QVB_CUDA(cudaMemsetAsync(ctr.p, 0, (2 * kClasses + (order_host ? kHostBuckets : 0)) * sizeof(unsigned int), s));
     ClassLists L;
     for (int c = 0; c < kClasses; ++c) {
       L.req[c] = req.p + c * b;
@@ -855,10 +912,25 @@ struct qvb_store {
     }
     L.count = ctr.p;
     L.cursor = ctr.p + kClasses;
+    L.hist = order_host ? ctr.p + 2 * kClasses : nullptr;
+    const int hb = bits_for(host_rows > 1 ? host_rows - 1 : 1);
+    L.hshift = hb > kHostBucketBits ? hb - kHostBucketBits : 0;
     const unsigned sgrid = resident_grid_cached(k_split_classes, 256, 0);
     k_split_classes<<<std::min<uint64_t>(sgrid, (b + 255) / 256), 256, 0, s>>>(
-        ids, b, lut, bases, stride, n, static_cast<int>(reader), nloc - 2, L, err);
+        ids, b, lut, bases, stride, n, static_cast<int>(reader), host_loc, L, err);
     QVB_LAUNCH_CHECK();
+    if (order_host) {
+      k_bucket_scan<<<1, 1024, 0, s>>>(L.hist);
+      QVB_LAUNCH_CHECK();
+      ClassLists sorted = L;  // the gather reads the bucket-ordered host list
+      sorted.req[2] = req.p + kClasses * b;
+      sorted.src[2] = srcs.p + kClasses * b;
+      const unsigned bgrid = resident_grid_cached(k_bucket_scatter, 256, 0);
+      k_bucket_scatter<<<std::min<uint64_t>(bgrid, (b + 255) / 256), 256, 0, s>>>(
+          sorted, L.req[2], L.src[2], reinterpret_cast<uint64_t>(bases.p[host_loc]), stride, b);
+      QVB_LAUNCH_CHECK();
+      L = sorted;
+    }
     static const int host_every = [] {
       const char* e = std::getenv("QVB_HOST_EVERY");
       return e ? std::max(1, std::atoi(e)) : 8;

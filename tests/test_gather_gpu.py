@@ -231,6 +231,8 @@ def test_tier_split_gather_bit_exact(qvb, oracle, mix, dim, monkeypatch):
         st.gather(d_ids, out)
         st.check_error()
         assert (out.cpu().numpy() == exp).all()
+    monkeypatch.setenv("QVB_HOST_SORT", "0")  # host list unordered
+    assert (stores[-1].gather_host(req) == exp).all()
     monkeypatch.setenv("QVB_GATHER_SPLIT", "0")
     assert (stores[-1].gather_host(req) == exp).all()
     for st in stores:
