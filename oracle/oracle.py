@@ -316,6 +316,10 @@ class RefLib(_Lib):
                                           C.POINTER(C.c_int)]
         L.qvr_from_edges.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, u64p, u64p, f64p]
         L.qvr_validate.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p]
+        L.qvr_classify_link.argtypes = [C.POINTER(Topology), C.c_uint32, C.c_uint32, C.c_uint32,
+                                        C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.qvr_fetch_cost.argtypes = [C.POINTER(Topology), C.c_uint32, C.c_uint32, C.c_uint32,
+                                     C.c_uint64, i64p, u64p, u64p, C.c_uint64, f64p, dp]
         L.qvr_plan_placement.argtypes = [f64p, C.c_uint64, C.POINTER(Topology), u64p, i64p,
                                          C.c_uint64, C.POINTER(C.c_uint64), dp]
         L.qvr_build_lookup_table.argtypes = [u64p, i64p, C.c_uint64, C.POINTER(Topology),
@@ -379,6 +383,24 @@ class RefLib(_Lib):
         self._check(self._lib.qvr_row_sums(n, len(col), ro, _pad(col, np.uint64),
                                            _pad(w, np.float64), rs))
         return rs
+
+    def classify_link(self, topo: Topology, loc: int, rs: int = 0, rtier: int = 0, rdev: int = 0):
+        a, b = C.c_int(0), C.c_int(0)
+        self._check(self._lib.qvr_classify_link(C.byref(topo), rs, rtier, rdev, loc, C.byref(a),
+                                                C.byref(b)))
+        return a.value, (b.value if b.value >= 0 else None)
+
+    def fetch_cost(self, groups, topo: Topology, feature_bytes: int, rs: int = 0, rtier: int = 0,
+                   rdev: int = 0):
+        gl = np.ascontiguousarray(groups[0], np.int64)
+        gc = np.ascontiguousarray(groups[1], np.uint64)
+        gt = np.ascontiguousarray(groups[2], np.uint64)
+        per = np.zeros(max(len(gl), 1), np.float64)
+        tot = C.c_double(0)
+        self._check(self._lib.qvr_fetch_cost(C.byref(topo), rs, rtier, rdev, len(gl), _pad(gl, np.int64),
+                                             _pad(gc, np.uint64), _pad(gt, np.uint64), feature_bytes,
+                                             per, C.byref(tot)))
+        return tot.value, per[: len(gl)]
 
     def transition_view(self, ro, col, w):
         """transition_view(g): (row_sums, distinct_out, has_parallel_edges)."""

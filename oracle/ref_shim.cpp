@@ -216,6 +216,39 @@ int qvr_validate(uint64_t n, uint64_t e, const uint64_t* ro, const uint64_t* col
   return guard([&] { make_graph(n, e, ro, col, w).validate(); });
 }
 
+int qvr_classify_link(const qvb_topology* topo, uint32_t rs, uint32_t rtier, uint32_t rdev,
+                      int64_t id, int* first, int* second) {
+  return guard([&] {
+    qv::ClusterTopology t = make_topo(topo);
+    qv::DeviceRef r{rs, static_cast<qv::Tier>(rtier), rdev};
+    qv::LinkPath p = qv::classify_link(t, r, id);
+    *first = static_cast<int>(p.first);
+    *second = p.second ? static_cast<int>(*p.second) : -1;
+  });
+}
+
+/* fetch_cost over a flattened plan: the groups' offsets are only counted, so
+ * each group gets count zero offsets */
+int qvr_fetch_cost(const qvb_topology* topo, uint32_t rs, uint32_t rtier, uint32_t rdev, uint64_t groups,
+                   const int64_t* gl, const uint64_t* gc, const uint64_t* gt, uint64_t feature_bytes,
+                   double* per, double* total) {
+  return guard([&] {
+    qv::ClusterTopology t = make_topo(topo);
+    qv::ReadPlan plan;
+    plan.home_server = rs;
+    for (uint64_t g = 0; g < groups; ++g) {
+      qv::ReadPlan::LocationReads r;
+      r.location_id = gl[g];
+      r.offsets.assign(gc[g], 0);
+      r.page_transitions = gt[g];
+      plan.per_location.push_back(std::move(r));
+    }
+    qv::FetchCost c = qv::fetch_cost(plan, t, feature_bytes, qv::DeviceRef{rs, static_cast<qv::Tier>(rtier), rdev});
+    for (uint64_t g = 0; g < groups; ++g) per[g] = c.per_location_s[g].second;
+    *total = c.total_s;
+  });
+}
+
 int qvr_plan_placement(const double* v, uint64_t n, const qvb_topology* topo,
                        uint64_t* loc_offsets, int64_t* loc_ids, uint64_t cap, uint64_t* copies,
                        double* ms_out) {

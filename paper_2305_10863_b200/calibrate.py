@@ -78,31 +78,7 @@ def calibrated_topology(base: qvb.Topology | None = None, device: int = 0,
 def fetch_cost(groups, topo: qvb.Topology, feature_bytes: int, reader_device: int = 0,
                home_server: int = 0) -> float:
     """The reference's fetch_cost model (placement.cpp:382-404) over a flat
-    read plan: groups = (group_loc, group_count, group_transitions)."""
-    gl, gc, gt = groups
-    total = 0.0
-    stride = topo.gpus_per_server + 2
-    for loc, cnt, tr in zip(gl, gc, gt):
-        server, slot = divmod(int(loc), stride)
-        if server != home_server:
-            link, translated = (qvb.LINK_INFINIBAND if topo.infiniband else qvb.LINK_ETHERNET), True
-            if slot == topo.gpus_per_server + 1:
-                raise NotImplementedError("remote disk reads are outside the device store")
-        elif slot < topo.gpus_per_server:
-            gpn = topo.gpus_per_server // topo.numa_per_server
-            if slot == reader_device:
-                link, translated = qvb.LINK_LOCAL, False
-            elif reader_device // gpn == slot // gpn:
-                link = qvb.LINK_NVLINK if topo.nvlink_within_numa else qvb.LINK_PCIE
-                translated = link == qvb.LINK_PCIE
-            else:
-                link, translated = qvb.LINK_UPI, True
-        elif slot == topo.gpus_per_server:
-            link, translated = qvb.LINK_PCIE, True
-        else:
-            link, translated = qvb.LINK_DISK, False
-        lat = topo.link_latency_s[link] + feature_bytes * float(cnt) / topo.link_bandwidth_Bps[link]
-        if translated:
-            lat += topo.tlb_miss_penalty_s * float(tr)
-        total = max(total, lat)
-    return total
+    read plan groups = (group_loc, group_count, group_transitions), through
+    the library's qvb_fetch_cost."""
+    return qvb.fetch_cost(groups, topo, feature_bytes, reader_server=home_server,
+                          reader_device=reader_device)[0]

@@ -565,6 +565,29 @@ def _plan_out(b: int, groups_cap: int):
             np.empty(m, np.uint64), u64(0))
 
 
+def classify_link(topo: Topology, location_id: int, reader_server: int = 0,
+                  reader_tier: int = TIER_GPU, reader_device: int = 0):
+    """classify_link (placement.cpp:228-267) -> (first, second or None)."""
+    a, b = C.c_int(0), C.c_int(0)
+    _check(_lib().qvb_classify_link(C.byref(topo), reader_server, reader_tier, reader_device,
+                                    location_id, C.byref(a), C.byref(b)))
+    return a.value, (b.value if b.value >= 0 else None)
+
+
+def fetch_cost(groups, topo: Topology, feature_bytes: int, reader_server: int = 0,
+               reader_tier: int = TIER_GPU, reader_device: int = 0):
+    """fetch_cost (placement.cpp:382-404) over a flattened read plan
+    (group_loc, group_count, group_transitions) -> (total_s, per_location_s)."""
+    gl = np.ascontiguousarray(groups[0], np.int64)
+    gc = np.ascontiguousarray(groups[1], np.uint64)
+    gt = np.ascontiguousarray(groups[2], np.uint64)
+    per = np.zeros(max(len(gl), 1), np.float64)
+    tot = C.c_double(0)
+    _check(_lib().qvb_fetch_cost(C.byref(topo), reader_server, reader_tier, reader_device, len(gl),
+                                 _ptr(gl), _ptr(gc), _ptr(gt), feature_bytes, _ptr(per), C.byref(tot)))
+    return tot.value, per[: len(gl)]
+
+
 def plan_reads_device(location_ids, offsets, ids, page_size: int = 8, device: int = 0, stream=None):
     """qv::plan_reads over a lookup table already on the device (torch tensors
     location_ids int64[n], offsets uint64/int64[n], ids [b]): no table upload."""

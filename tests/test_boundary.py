@@ -83,3 +83,46 @@ def test_no_cpu_fallback(q):
         q.compute_access_prob_ie(np.array([0, 1, 1], np.uint64), np.array([1], np.uint64), None, 2)
     with pytest.raises(q.CudaError):
         q.device_count()
+
+
+def test_fetch_cost_and_classify_match_reference(q):
+    """The reference's cost model through the C-ABI (host arithmetic, runs on
+    CPU) against the unmodified reference (oracle/_ref) on random topologies,
+    every location, every reader tier, random flattened plans."""
+    from oracle.oracle import RefLib
+    from tests.util import derive_stream
+
+    if not RefLib.available():
+        pytest.skip("oracle/_ref not built")
+    ref = RefLib()
+    rng = derive_stream(191, 1)
+    for _ in range(40):
+        t = q.Topology.with_defaults(servers=1 + rng.below(3), numa_per_server=1 + rng.below(2))
+        t.gpus_per_server = t.numa_per_server * rng.below(4)
+        t.nvlink_within_numa = rng.below(2)
+        t.infiniband = rng.below(2)
+        for i in range(7):
+            t.link_latency_s[i] = rng.uniform() * 1e-5
+            t.link_bandwidth_Bps[i] = 1e9 + rng.uniform() * 1e12
+        t.tlb_miss_penalty_s = rng.uniform() * 1e-6
+        ot = ref.topology_defaults()
+        for f, _ in q.Topology._fields_:
+            if f.startswith("link_"):
+                for i in range(7):
+                    getattr(ot, f)[i] = getattr(t, f)[i]
+            else:
+                setattr(ot, f, getattr(t, f))
+        nloc = t.servers * (t.gpus_per_server + 2)
+        for rs in range(t.servers):
+            for rtier in (q.TIER_GPU, q.TIER_HOST):
+                rdev = rng.below(max(1, t.gpus_per_server))
+                for loc in range(nloc):
+                    assert q.classify_link(t, loc, rs, rtier, rdev) == ref.classify_link(ot, loc, rs, rtier, rdev)
+                k = 1 + rng.below(nloc)
+                groups = (list(range(nloc))[:k], [rng.below(5000) for _ in range(k)],
+                          [rng.below(300) for _ in range(k)])
+                a = q.fetch_cost(groups, t, 400, rs, rtier, rdev)
+                b = ref.fetch_cost(groups, ot, 400, rs, rtier, rdev)
+                assert a[0] == b[0] and (a[1] == b[1]).all()
+    with pytest.raises(q.ValidationError, match="unknown location id"):
+        q.fetch_cost(([99], [1], [1]), q.Topology.with_defaults(), 512)

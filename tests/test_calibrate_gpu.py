@@ -1,6 +1,8 @@
 """fetch_cost calibration: measured link specs are
 sane and the reference's own cost model, fed with them, predicts the real
-gather time of a mixed local/host batch within 2x."""
+gather time of a mixed local/host batch within 25% (the tier-isolated
+gather runs the local and host reads concurrently, which is the model's
+max-over-locations tail rule)."""
 import numpy as np
 import pytest
 
@@ -35,4 +37,4 @@ def test_calibrated_links_predict_gather(qvb):
     t.tlb_miss_penalty_s = 0.0  # zero-copy reads are not page-walk bound here
     predicted = calibrate.fetch_cost(plan[:3], t, dim * 4)
     store.close()
-    assert predicted / 2 < measured < predicted * 2, (predicted, measured)
+    assert 0.75 * predicted < measured < 1.25 * predicted, (predicted, measured)
