@@ -9,7 +9,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ga
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_codes -s 7 -c 7 -o $OUT/${T}_codes -f $B > $OUT/${T}_codes.log 2>&1; echo codes=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_products -s 1 -c 1 -o $OUT/${T}_products -f $B > $OUT/${T}_products.log 2>&1; echo products=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_first -s 1 -c 1 -o $OUT/${T}_first -f $B > $OUT/${T}_first.log 2>&1; echo first=$?
-PM=$(grep -ioE "^pcie__[a-z_.]*bytes[a-z_.]*" $OUT/r02d_ncu_metric_names.txt 2>/dev/null | head -4 | tr '\n' ',' | sed 's/,$//')
+ncu --query-metrics > $OUT/${T}_ncu_metrics_all.txt 2>&1
+PM=$(grep -oE "\bpcie__[a-z0-9_]*bytes[a-z0-9_]*" $OUT/${T}_ncu_metrics_all.txt | sort -u | head -6 | sed 's/$/.sum/' | tr '\n' ',' | sed 's/,$//')
 echo "pcie metrics: $PM"
-timeout 900 ncu --set full ${PM:+--metrics $PM} --clock-control none --import-source on -k regex:k_gather_classes -s 3 -c 1 -o $OUT/${T}_host25 -f $B --host-frac 0.25 > $OUT/${T}_host25.log 2>&1; echo host25=$?
+timeout 900 ncu --set full ${PM:+--metrics $PM,lts__t_sectors_aperture_sysmem.sum} --clock-control none --import-source on -k regex:k_gather_classes -s 3 -c 1 -o $OUT/${T}_host25 -f $B --host-frac 0.25 > $OUT/${T}_host25.log 2>&1; echo host25=$?
 ls -la $OUT/ | grep $T

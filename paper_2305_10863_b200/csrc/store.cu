@@ -561,7 +561,7 @@ struct ClassLists {
 // address order, which keeps the GPU's page-table walks for system memory
 // local — random rows from a 14 GB host tier read at 38 GB/s, rows in offset
 // order well above (profiles/r01k_host_tier.txt, r01m_gather_sweep.md).
-constexpr int kHostBucketBits = 16;
+constexpr int kHostBucketBits = 18;
 constexpr int kHostBuckets = 1 << kHostBucketBits;
 
 __global__ void __launch_bounds__(256)
@@ -605,17 +605,15 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// exclusive scan of the bucket counts in place (one block of 1024 threads)
+// exclusive scan of the bucket counts in place (one block of 1024 threads,
+// each owning kHostBuckets / 1024 consecutive buckets)
 __global__ void __launch_bounds__(1024) k_bucket_scan(unsigned int* __restrict__ hist) {
   constexpr int per = kHostBuckets / 1024;
   __shared__ unsigned int part[1024];
-  unsigned int v[per], sum = 0;
   const int t = threadIdx.x;
-#pragma unroll
-  for (int k = 0; k < per; ++k) {
-    v[k] = hist[t * per + k];
-    sum += v[k];
-  }
+  unsigned int* mine = hist + t * per;
+  unsigned int sum = 0;
+  for (int k = 0; k < per; ++k) sum += mine[k];
   part[t] = sum;
   __syncthreads();
   for (int d = 1; d < 1024; d <<= 1) {  // Hillis-Steele inclusive scan
@@ -625,10 +623,10 @@ __global__ void __launch_bounds__(1024) k_bucket_scan(unsigned int* __restrict__
     __syncthreads();
   }
   unsigned int run = part[t] - sum;
-#pragma unroll
   for (int k = 0; k < per; ++k) {
-    hist[t * per + k] = run;
-    run += v[k];
+    const unsigned int v = mine[k];
+    mine[k] = run;
+    run += v;
   }
 }
 
@@ -899,8 +897,14 @@ struct qvb_store {
   void launch_split(const uint64_t* ids, uint64_t b, uint32_t cpr, char* out, cudaStream_t s,
                     unsigned long long* err) {
     const int host_loc = nloc - 2;
+    // host requests in offset order once the host tier outgrows the GPU's
+    // reach over system-memory pages (random rows: 51 GB/s up to 2 GB, 38 GB/s
+    // at 14 GB, profiles/r01k_host_tier.txt; C4 at h=0.25: 4.76 -> 3.44 ms,
+    // C2's 0.3 GB tier: no gain, profiles/r02/r02d_host_order.md)
     const char* so = std::getenv("QVB_HOST_SORT");  // per call: tests and A/B flip it
-    const bool order_host = host_rows > 0 && (used_mask >> host_loc & 1) && !(so && *so == '0');
+    const bool big_tier = host_rows * stride >= (4ull << 30);
+    const bool order_host = host_rows > 0 && (used_mask >> host_loc & 1) &&
+                            (so ? *so == '1' : big_tier);
     DevBuf<uint32_t> req(b * (kClasses + (order_host ? 1 : 0)), s);
     DevBuf<unsigned long long> srcs(b * (kClasses + (order_host ? 1 : 0)), s);
     DevBuf<unsigned int> ctr(2 * kClasses + (order_host ? kHostBuckets : 0), s);

@@ -211,6 +211,7 @@ def test_tier_split_gather_bit_exact(qvb, oracle, mix, dim, monkeypatch):
     import torch
 
     monkeypatch.setenv("QVB_GATHER_SMALL", "0")
+    monkeypatch.setenv("QVB_HOST_SORT", "1")  # offset-bucketed host list (default only for big tiers)
     n = 12000
     gpus = 1 if mix == "host" else 4
     host = n if "host" in mix else 0
