@@ -395,6 +395,7 @@ def run_ours(args):
                "h2d_bytes_per_step": B * 8, "d2h_bytes_per_step": B * row_bytes,
                "note": "qvb_gather_host per step: H2D ids (pinned) + gather + D2H rows (pinned) "
                        "+ stream sync; wall clock, max over ranks"}
+    if not args.no_e2e and rank == 0:  # the P legs are per-rank replicas: rank 0 reports them
         # P(n,j) end to end: host out-CSR -> device -> in-CSR -> sweeps -> host P
         ro, col, w = qvb.synthetic_csr(n, e, 7, cfg["weighted"], False, device=local)
         tm = [0.0, 0.0, 0.0]
@@ -414,6 +415,24 @@ def run_ours(args):
             "d2h_bytes": n * 8,
             "note": "qvb_compute_access_prob_ie from a host qv::Graph-layout CSR (the reference "
                     "call, which rebuilds its transpose every call)"}
+        # the drop-in's call pattern compute_access_prob_ie(g, transition_view(g), L):
+        # one upload builds the view (row sums, distinct out-degrees) and the
+        # device graph the sweeps then run on
+        wv = w if cfg["weighted"] else None
+        t0 = time.perf_counter()
+        rs, dist_out, _par, vg = qvb.transition_view(ro, col, wv, device=local, keep=True)
+        t1 = time.perf_counter()
+        pv = vg.access_prob(layers)
+        t2 = time.perf_counter()
+        vg.close()
+        access_prob["e2e_dropin"] = {
+            "value": info.unique_edge_count * (layers - 1) / (t2 - t0), "unit": "edges/s",
+            "wall_s": t2 - t0, "transition_view_s": t1 - t0, "compute_access_prob_ie_s": t2 - t1,
+            "identical_to_device_call": bool((pv.view(np.uint64) == p_host.view(np.uint64)).all()),
+            "note": "qv::compute_access_prob_ie(g, qv::transition_view(g), L) from a host CSR: "
+                    "qvb_transition_view (upload, device row sums / distinct out-degrees, "
+                    "in-CSR kept) + qvb_access_prob on it, P copied to the host"}
+        del rs, dist_out, pv
     else:
         ro = col = w = None
 
