@@ -377,6 +377,11 @@ def run_ours(args):
              "nvlink": (B * row_bytes * f_p, NVLINK_GBS, "measured peer copy (B200_PROFILING.md)"),
              "pcie": (B * row_bytes * f_h, PCIE_GBS, "measured random-row PCIe reads, experiments/host_tier.cu")}
     bound = max(links, key=lambda k: links[k][0] / links[k][1])
+    # the store buckets batches that leave its own shard by location class
+    # (csrc/store.cu launch_split); batches <= 48K ids take the flat kernel
+    gather_kernel = ("k_gather" if B <= 49152 else
+                     "k_gather_classes" if (f_p > 0 or f_h > 0) and not args.planned else
+                     "k_gather_sorted" if args.planned else "k_gather_rows")
     alg, link_peak, link_src = links[bound]
     achieved = alg / (per_launch_ms / 1e3) / 1e9
 
@@ -470,7 +475,7 @@ def run_ours(args):
                               "so these timings are not a performance measurement"}
                if D.shared_gpu() and world > 1 else {}),
         },
-        "roofline": {"bound": bound, "kernel": "k_gather_rows", "achieved": achieved,
+        "roofline": {"bound": bound, "kernel": gather_kernel, "achieved": achieved,
                      "peak": link_peak, "unit": "GB/s", "frac": achieved / link_peak,
                      "traffic": None, "algorithmic_bytes_per_id": hbm_per_id,
                      "algorithmic_bytes_per_launch": alg,
@@ -487,7 +492,7 @@ def run_ours(args):
     # ncu dram bytes per launch (profiles/make_traffic.py), only from a capture
     # of exactly this line's workload key; null otherwise
     tr = load_traffic(traffic_key(args, world))
-    line["roofline"]["traffic"] = tr.get("k_gather_rows")
+    line["roofline"]["traffic"] = tr.get(gather_kernel)
     access_prob["roofline"]["traffic"] = tr.get(access_prob["roofline"]["kernel"])
     line["roofline"]["traffic_key"] = access_prob["roofline"]["traffic_key"] = traffic_key(args, world)
     store.close()
