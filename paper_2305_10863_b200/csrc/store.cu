@@ -208,6 +208,66 @@ __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
   }
 }
 
+// Row-group gather for rows of 512·m bytes (D = 128·m fp32): lane l owns the
+// 16-byte columns l, l+32, ... of every row, so a round of kU loads covers kU
+// whole rows with no per-chunk (row, offset) bookkeeping — a quarter of
+// k_gather_rows' registers per load in flight, so more rows are in flight per
+// SM. Same id -> entry -> row resolution, one and two groups ahead.
+template <int kU, int kMinBlocks>
+__global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
+    k_gather_rows512(const uint64_t* __restrict__ ids, uint64_t rows,
+                     const uint64_t* __restrict__ lut, Bases bases, uint64_t stride, uint32_t m,
+                     uint64_t n, char* __restrict__ out, unsigned long long* err, int lut_keep) {
+  using V = Vec<16>;
+  const uint64_t pol = policy_evict_first();  // rows: a stream
+  const uint64_t lpol = lut_keep ? policy_evict_last() : policy_evict_normal();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t groups = (rows + 31) / 32;
+  const uint64_t row_bytes = 512ull * m;
+  auto load_id = [&](uint64_t g) -> uint64_t {
+    const uint64_t r = g * 32 + lane;
+    return (g < groups && r < rows) ? __ldg(ids + r) : ~0ull;
+  };
+  auto resolve = [&](uint64_t g, uint64_t f) -> uint64_t {  // source row address or 0
+    const uint64_t r = g * 32 + lane;
+    if (g >= groups || r >= rows) return 0;
+    if (f >= n) {
+      atomicMin(err, (unsigned long long)r);
+      return 0;
+    }
+    const uint64_t e = ld_hint(lut + f, lpol);
+    return reinterpret_cast<uint64_t>(bases.p[e >> kOffsetBits]) + (e & kOffsetMask) * stride;
+  };
+  uint64_t g = warp;
+  uint64_t src = resolve(g, load_id(g));
+  uint64_t id_next = load_id(g + nwarps);
+  for (; g < groups; g += nwarps) {
+    const uint64_t src_next = resolve(g + nwarps, id_next);
+    id_next = load_id(g + 2 * nwarps);
+    const uint32_t nr = static_cast<uint32_t>(rows - g * 32 < 32 ? rows - g * 32 : 32);
+    char* dst0 = out + g * 32 * row_bytes + lane * 16;
+    for (uint32_t rc = 0; rc < nr * m; rc += kU) {  // (row, 512-byte column) pairs, warp-uniform
+      typename V::T v[kU];
+      uint32_t ok = 0;  // pairs of this round that were loaded (one bit each)
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t r = (rc + u) / m, c = (rc + u) - r * m;
+        const uint64_t sr = __shfl_sync(0xffffffffu, src, r & 31);
+        if (r < nr && sr) {
+          v[u] = V::load(reinterpret_cast<const char*>(sr) + c * 512 + lane * 16, pol);
+          ok |= 1u << u;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (ok >> u & 1) V::store(dst0 + (uint64_t)(rc + u) * 512, v[u], pol);
+    }
+    src = src_next;
+  }
+}
+
 // Rows that are 8-byte but not 16-byte multiples (e.g. 602 fp32 = 2408 B):
 // the shard stride is 64-byte aligned, so the source side still moves 16-byte
 // vectors; the destination rows are only 8-byte aligned, so every 16-byte
@@ -973,10 +1033,37 @@ struct qvb_store {
       const char* u = std::getenv("QVB_GATHER_U");
       return u ? std::atoi(u) : 0;
     }();
-    if (variant == 8) launch_rows_u<V, 8, 1>(ids, rows, cpr, o, s, err);
+    if (V == 16 && row_bytes % 512 == 0 && variant != 4 && variant != 2 && variant < 8) {
+      launch_rows512(ids, rows, o, s, err, variant);
+      return;
+    }
+    if (variant == 84) launch_rows_u<V, 8, 4>(ids, rows, cpr, o, s, err);
+    else if (variant == 46) launch_rows_u<V, 4, 6>(ids, rows, cpr, o, s, err);
+    else if (variant == 85) launch_rows_u<V, 8, 3>(ids, rows, cpr, o, s, err);
+    else if (variant == 8) launch_rows_u<V, 8, 1>(ids, rows, cpr, o, s, err);
     else if (variant == 4) launch_rows_u<V, 4, 4>(ids, rows, cpr, o, s, err);
     else if (variant == 2) launch_rows_u<V, 2, 6>(ids, rows, cpr, o, s, err);
     else launch_rows_u<V, 4, 4>(ids, rows, cpr, o, s, err);
+  }
+
+  void launch_rows512(const uint64_t* ids, uint64_t rows, char* o, cudaStream_t s,
+                      unsigned long long* err, int variant) {
+    const int lut_keep = lut_keep_flag();
+    const uint64_t warps_needed = (rows + 31) / 32;
+    const uint64_t blocks = (warps_needed + kGatherBlock / 32 - 1) / (kGatherBlock / 32);
+    const uint32_t m = row_bytes / 512;
+#define QVB_R512(U, MB)                                                                          \
+    do {                                                                                         \
+      const unsigned full = resident_grid_cached(k_gather_rows512<U, MB>, kGatherBlock, 0);      \
+      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(full, blocks));             \
+      k_gather_rows512<U, MB><<<grid, kGatherBlock, 0, s>>>(ids, rows, lut, bases, stride, m, n, o, \
+                                                            err, lut_keep);                      \
+    } while (0)
+    if (variant == 5) QVB_R512(6, 5);
+    else if (variant == 7) QVB_R512(16, 2);
+    else QVB_R512(8, 4);
+#undef QVB_R512
+    QVB_LAUNCH_CHECK();
   }
 
   void launch_cp(const uint64_t* ids, uint64_t rows, char* o, cudaStream_t s, unsigned long long* err) {
