@@ -208,15 +208,15 @@ __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
   }
 }
 
-// Row-group gather for rows of 512·m bytes (D = 128·m fp32): lane l owns the
-// 16-byte columns l, l+32, ... of every row, so a round of kU loads covers kU
-// whole rows with no per-chunk (row, offset) bookkeeping — a quarter of
-// k_gather_rows' registers per load in flight, so more rows are in flight per
-// SM. Same id -> entry -> row resolution, one and two groups ahead.
+// Row-group gather for 512-byte rows (D = 128 fp32): lane l owns the 16-byte
+// column l of every row, so a round of kU loads covers kU whole rows with no
+// per-chunk (row, offset) bookkeeping. Lookup entries are fetched two groups
+// ahead and ids three, so the dependent id -> entry -> row chain (the table
+// does not fit L2 at papers scale) stays off the copy's critical path.
 template <int kU, int kMinBlocks>
 __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
     k_gather_rows512(const uint64_t* __restrict__ ids, uint64_t rows,
-                     const uint64_t* __restrict__ lut, Bases bases, uint64_t stride, uint32_t m,
+                     const uint64_t* __restrict__ lut, Bases bases, uint64_t stride,
                      uint64_t n, char* __restrict__ out, unsigned long long* err, int lut_keep) {
   using V = Vec<16>;
   const uint64_t pol = policy_evict_first();  // rows: a stream
@@ -225,7 +225,6 @@ __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t groups = (rows + 31) / 32;
-  const uint64_t row_bytes = 512ull * m;
   auto load_id = [&](uint64_t g) -> uint64_t {
     const uint64_t r = g * 32 + lane;
     return (g < groups && r < rows) ? __ldg(ids + r) : ~0ull;
@@ -242,29 +241,30 @@ __global__ void __launch_bounds__(kGatherBlock, kMinBlocks)
   };
   uint64_t g = warp;
   uint64_t src = resolve(g, load_id(g));
-  uint64_t id_next = load_id(g + nwarps);
+  uint64_t src1 = resolve(g + nwarps, load_id(g + nwarps));
+  uint64_t id2 = load_id(g + 2 * nwarps);
   for (; g < groups; g += nwarps) {
-    const uint64_t src_next = resolve(g + nwarps, id_next);
-    id_next = load_id(g + 2 * nwarps);
+    const uint64_t src2 = resolve(g + 2 * nwarps, id2);  // two groups ahead
+    id2 = load_id(g + 3 * nwarps);                      // three groups ahead
     const uint32_t nr = static_cast<uint32_t>(rows - g * 32 < 32 ? rows - g * 32 : 32);
-    char* dst0 = out + g * 32 * row_bytes + lane * 16;
-    for (uint32_t rc = 0; rc < nr * m; rc += kU) {  // (row, 512-byte column) pairs, warp-uniform
+    char* dst0 = out + g * 32 * 512ull + lane * 16;
+    for (uint32_t r0 = 0; r0 < nr; r0 += kU) {  // warp-uniform
       typename V::T v[kU];
-      uint32_t ok = 0;  // pairs of this round that were loaded (one bit each)
+      uint32_t ok = 0;  // rows of this round that were loaded (one bit each)
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const uint32_t r = (rc + u) / m, c = (rc + u) - r * m;
-        const uint64_t sr = __shfl_sync(0xffffffffu, src, r & 31);
-        if (r < nr && sr) {
-          v[u] = V::load(reinterpret_cast<const char*>(sr) + c * 512 + lane * 16, pol);
+        const uint64_t sr = __shfl_sync(0xffffffffu, src, (r0 + u) & 31);
+        if (r0 + u < nr && sr) {
+          v[u] = V::load(reinterpret_cast<const char*>(sr) + lane * 16, pol);
           ok |= 1u << u;
         }
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u)
-        if (ok >> u & 1) V::store(dst0 + (uint64_t)(rc + u) * 512, v[u], pol);
+        if (ok >> u & 1) V::store(dst0 + (uint64_t)(r0 + u) * 512, v[u], pol);
     }
-    src = src_next;
+    src = src1;
+    src1 = src2;
   }
 }
 
@@ -705,7 +705,7 @@ __global__ void k_bucket_scatter(ClassLists L, const uint32_t* __restrict__ in_r
   }
 }
 
-template <int VEC, int kU>
+template <int VEC, int kU, bool kR512>
 __global__ void __launch_bounds__(kGatherBlock, 4)
     k_gather_classes(ClassLists L, uint32_t cpr, uint32_t row_bytes, char* __restrict__ out,
                      int host_every) {
@@ -767,6 +767,34 @@ __global__ void __launch_bounds__(kGatherBlock, 4)
     fetch(ncls, ng, nsrc, ndst);
     const uint64_t left = cnt[cls] - (uint64_t)g * 32;
     const uint32_t nr = static_cast<uint32_t>(left < 32 ? left : 32);
+    if (kR512) {  // rows of 512·m bytes: lane = 16-byte column (k_gather_rows512's loop)
+      const uint32_t m = row_bytes / 512;
+      for (uint32_t rc = 0; rc < nr * m; rc += kU) {
+        typename V::T v[kU];
+        uint32_t ok = 0;  // warp-uniform: which (row, column) pairs of the round exist
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const uint32_t r = (rc + u) / m, c = (rc + u) - r * m;
+          const uint64_t s = __shfl_sync(0xffffffffu, src, r & 31);
+          if (r < nr) {
+            v[u] = V::load(reinterpret_cast<const char*>(s) + c * 512 + lane * 16, pol);
+            ok |= 1u << u;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          if (!(ok >> u & 1)) continue;
+          const uint32_t r = (rc + u) / m, c = (rc + u) - r * m;
+          const uint64_t d = __shfl_sync(0xffffffffu, dst, r & 31) + c * 512 + lane * 16;
+          V::store(reinterpret_cast<char*>(d), v[u], pol);
+        }
+      }
+      cls = ncls;
+      g = ng;
+      src = nsrc;
+      dst = ndst;
+      continue;
+    }
     const uint32_t tot = nr * cpr;
     uint32_t row = row0, k = k0;
     for (uint32_t cb = 0; cb < tot; cb += 32 * kU) {  // warp-uniform trip count
@@ -1007,8 +1035,13 @@ struct qvb_store {
 
   template <int V>
   void launch_classes(const ClassLists& L, uint32_t cpr, char* out, int host_every, cudaStream_t s) {
-    const unsigned grid = resident_grid_cached(k_gather_classes<V, 4>, kGatherBlock, 0);
-    k_gather_classes<V, 4><<<grid, kGatherBlock, 0, s>>>(L, cpr, row_bytes, out, host_every);
+    if (V == 16 && row_bytes % 512 == 0) {
+      const unsigned grid = resident_grid_cached(k_gather_classes<16, 4, true>, kGatherBlock, 0);
+      k_gather_classes<16, 4, true><<<grid, kGatherBlock, 0, s>>>(L, cpr, row_bytes, out, host_every);
+    } else {
+      const unsigned grid = resident_grid_cached(k_gather_classes<V, 4, false>, kGatherBlock, 0);
+      k_gather_classes<V, 4, false><<<grid, kGatherBlock, 0, s>>>(L, cpr, row_bytes, out, host_every);
+    }
     QVB_LAUNCH_CHECK();
   }
 
@@ -1033,7 +1066,7 @@ struct qvb_store {
       const char* u = std::getenv("QVB_GATHER_U");
       return u ? std::atoi(u) : 0;
     }();
-    if (V == 16 && row_bytes % 512 == 0 && variant != 4 && variant != 2 && variant < 8) {
+    if (V == 16 && row_bytes == 512 && variant != 4 && variant != 2 && variant < 8) {
       launch_rows512(ids, rows, o, s, err, variant);
       return;
     }
@@ -1051,17 +1084,17 @@ struct qvb_store {
     const int lut_keep = lut_keep_flag();
     const uint64_t warps_needed = (rows + 31) / 32;
     const uint64_t blocks = (warps_needed + kGatherBlock / 32 - 1) / (kGatherBlock / 32);
-    const uint32_t m = row_bytes / 512;
 #define QVB_R512(U, MB)                                                                          \
     do {                                                                                         \
       const unsigned full = resident_grid_cached(k_gather_rows512<U, MB>, kGatherBlock, 0);      \
       const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(full, blocks));             \
-      k_gather_rows512<U, MB><<<grid, kGatherBlock, 0, s>>>(ids, rows, lut, bases, stride, m, n, o, \
+      k_gather_rows512<U, MB><<<grid, kGatherBlock, 0, s>>>(ids, rows, lut, bases, stride, n, o, \
                                                             err, lut_keep);                      \
     } while (0)
-    if (variant == 5) QVB_R512(6, 5);
+    if (variant == 5) QVB_R512(2, 6);
+    else if (variant == 6) QVB_R512(8, 4);
     else if (variant == 7) QVB_R512(16, 2);
-    else QVB_R512(8, 4);
+    else QVB_R512(4, 4);
 #undef QVB_R512
     QVB_LAUNCH_CHECK();
   }
