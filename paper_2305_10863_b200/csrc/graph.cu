@@ -23,6 +23,7 @@
 #include <cstring>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstdio>
 #include <memory>
 #include <mutex>
@@ -1218,17 +1219,12 @@ namespace qvb {
 // call pays for pinning them). Returns the first out-of-range column index
 // as (i << 2) | 1, or kNone.
 struct ColStage {
-  std::mutex mu;
   uint32_t* pinned = nullptr;  // threads * 2 slots of kChunk entries
   unsigned threads = 0;
   static constexpr uint64_t kChunk = 1ull << 21;
 };
-ColStage& col_stage() {
-  static ColStage c;
-  return c;
-}
 
-void ensure_pinned(ColStage& cs) {  // with cs.mu held
+void ensure_pinned(ColStage& cs) {  // by the lease holder only
   if (cs.pinned) return;
   const char* te = std::getenv("QVB_UPLOAD_THREADS");
   unsigned t = te ? static_cast<unsigned>(std::atoi(te)) : std::thread::hardware_concurrency();
@@ -1236,6 +1232,64 @@ void ensure_pinned(ColStage& cs) {  // with cs.mu held
   QVB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&cs.pinned),
                          cs.threads * 2 * ColStage::kChunk * sizeof(uint32_t), cudaHostAllocPortable));
 }
+
+// A small pool of staging sets (each threads x 2 pinned 8 MB slots): large
+// host<->device copies of different graphs, stores or threads proceed
+// concurrently, one set each; a caller waits only when QVB_STAGE_SETS (4)
+// copies are already in flight. Sets are pinned on first use and kept.
+class StagePool {
+ public:
+  static StagePool& get() {
+    static StagePool p;
+    return p;
+  }
+  ColStage* acquire() {
+    std::unique_lock<std::mutex> lock(mu_);
+    cv_.wait(lock, [&] { return !free_.empty() || all_.size() < max_; });
+    ColStage* cs;
+    if (!free_.empty()) {
+      cs = free_.back();
+      free_.pop_back();
+    } else {
+      all_.push_back(std::make_unique<ColStage>());
+      cs = all_.back().get();
+    }
+    return cs;
+  }
+  void release(ColStage* cs) {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      free_.push_back(cs);
+    }
+    cv_.notify_one();
+  }
+
+ private:
+  StagePool() {
+    const char* e = std::getenv("QVB_STAGE_SETS");
+    max_ = e ? std::max<size_t>(1, std::strtoull(e, nullptr, 10)) : 4;
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::vector<std::unique_ptr<ColStage>> all_;
+  std::vector<ColStage*> free_;
+  size_t max_ = 4;
+};
+
+struct StageLease {
+  ColStage* cs;
+  StageLease() : cs(StagePool::get().acquire()) {
+    try {
+      ensure_pinned(*cs);
+    } catch (...) {
+      StagePool::get().release(cs);
+      throw;
+    }
+  }
+  ~StageLease() { StagePool::get().release(cs); }
+  StageLease(const StageLease&) = delete;
+  StageLease& operator=(const StageLease&) = delete;
+};
 
 // Device -> pageable host copy through the same pinned slots: each thread
 // DMAs its chunks into its two slots (one in flight while it copies the
@@ -1249,9 +1303,8 @@ void copy_to_host(void* dst, const void* src, uint64_t bytes, cudaStream_t s) {
     QVB_CUDA(cudaStreamSynchronize(s));
     return;
   }
-  ColStage& cs = col_stage();
-  std::lock_guard<std::mutex> lock(cs.mu);
-  ensure_pinned(cs);
+  StageLease lease;  // one staging set for this copy; others may run concurrently
+  ColStage& cs = *lease.cs;
   const uint64_t nchunks = (bytes + kBytes - 1) / kBytes;
   const unsigned T = static_cast<unsigned>(std::min<uint64_t>(cs.threads, nchunks));
   cudaEvent_t start;
@@ -1304,9 +1357,8 @@ void copy_to_host(void* dst, const void* src, uint64_t bytes, cudaStream_t s) {
 unsigned long long upload_columns(const uint64_t* col, uint64_t e, uint64_t n, uint32_t* dcol,
                                   cudaStream_t s) {
   constexpr unsigned long long kNoBad = ~0ull;
-  ColStage& cs = col_stage();
-  std::lock_guard<std::mutex> lock(cs.mu);
-  ensure_pinned(cs);
+  StageLease lease;  // one staging set for this copy; others may run concurrently
+  ColStage& cs = *lease.cs;
   const uint64_t nchunks = (e + ColStage::kChunk - 1) / ColStage::kChunk;
   const unsigned T = static_cast<unsigned>(std::min<uint64_t>(cs.threads, nchunks));
   cudaEvent_t start;

@@ -396,3 +396,29 @@ def test_c4_full_against_reference():
     ref.set_threads(os.cpu_count() or 1)
     exp = ref.access_prob(ro, col, w, c["layers"], parallel=True)
     assert (bits(p) == bits(exp)).all()
+
+
+def test_concurrent_uploads_and_downloads(qvb, oracle):
+    """Several host threads upload graphs and copy P back at once (the staging
+    pool gives each large copy its own pinned set): every result exact."""
+    import threading
+
+    c = CONFIGS["C2"]
+    ro, col, w = oracle.synthetic_graph(c["n"], c["e"], 7, False, False, threads=8)
+    exp = oracle.access_prob(ro, col, w, 2)
+    res, errs = {}, []
+
+    def run(k):
+        try:
+            res[k] = qvb.compute_access_prob_ie(ro, col, None, 2).values
+        except Exception as ex:  # noqa: BLE001
+            errs.append(ex)
+
+    th = [threading.Thread(target=run, args=(k,)) for k in range(6)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for k in range(6):
+        assert (bits(res[k]) == bits(exp)).all()
