@@ -667,8 +667,8 @@ __global__ void __launch_bounds__(256)
 
 // exclusive scan of the bucket counts in place (one block of 1024 threads,
 // each owning kHostBuckets / 1024 consecutive buckets)
-__global__ void __launch_bounds__(1024) k_bucket_scan(unsigned int* __restrict__ hist) {
-  constexpr int per = kHostBuckets / 1024;
+__global__ void __launch_bounds__(1024) k_bucket_scan(unsigned int* __restrict__ hist, int buckets) {
+  const int per = buckets / 1024;
   __shared__ unsigned int part[1024];
   const int t = threadIdx.x;
   unsigned int* mine = hist + t * per;
@@ -995,8 +995,11 @@ struct qvb_store {
                             (so ? *so == '1' : big_tier);
     DevBuf<uint32_t> req(b * (kClasses + (order_host ? 1 : 0)), s);
     DevBuf<unsigned long long> srcs(b * (kClasses + (order_host ? 1 : 0)), s);
-    DevBuf<unsigned int> ctr(2 * kClasses + (order_host ? kHostBuckets : 0), s);
-    QVB_CUDA(cudaMemsetAsync(ctr.p, 0, (2 * kClasses + (order_host ? kHostBuckets : 0)) * sizeof(unsigned int), s));
+    const char* bb = std::getenv("QVB_HOST_BUCKET_BITS");  // A/B knob: 10..18
+    const int bbits = bb ? std::max(10, std::min(kHostBucketBits, std::atoi(bb))) : kHostBucketBits;
+    const int nbuckets = 1 << bbits;
+    DevBuf<unsigned int> ctr(2 * kClasses + (order_host ? nbuckets : 0), s);
+    QVB_CUDA(cudaMemsetAsync(ctr.p, 0, (2 * kClasses + (order_host ? nbuckets : 0)) * sizeof(unsigned int), s));
     ClassLists L;
     for (int c = 0; c < kClasses; ++c) {
       L.req[c] = req.p + c * b;
@@ -1006,13 +1009,13 @@ struct qvb_store {
     L.cursor = ctr.p + kClasses;
     L.hist = order_host ? ctr.p + 2 * kClasses : nullptr;
     const int hb = bits_for(host_rows > 1 ? host_rows - 1 : 1);
-    L.hshift = hb > kHostBucketBits ? hb - kHostBucketBits : 0;
+    L.hshift = hb > bbits ? hb - bbits : 0;
     const unsigned sgrid = resident_grid_cached(k_split_classes, 256, 0);
     k_split_classes<<<std::min<uint64_t>(sgrid, (b + 255) / 256), 256, 0, s>>>(
         ids, b, lut, bases, stride, n, static_cast<int>(reader), host_loc, L, err);
     QVB_LAUNCH_CHECK();
     if (order_host) {
-      k_bucket_scan<<<1, 1024, 0, s>>>(L.hist);
+      k_bucket_scan<<<1, 1024, 0, s>>>(L.hist, nbuckets);
       QVB_LAUNCH_CHECK();
       ClassLists sorted = L;  // the gather reads the bucket-ordered host list
       sorted.req[2] = req.p + kClasses * b;
@@ -1035,7 +1038,8 @@ struct qvb_store {
 
   template <int V>
   void launch_classes(const ClassLists& L, uint32_t cpr, char* out, int host_every, cudaStream_t s) {
-    if (V == 16 && row_bytes % 512 == 0) {
+    const char* r5 = std::getenv("QVB_CLASS_R512");  // A/B knob (default on)
+    if (V == 16 && row_bytes % 512 == 0 && !(r5 && *r5 == '0')) {
       const unsigned grid = resident_grid_cached(k_gather_classes<16, 4, true>, kGatherBlock, 0);
       k_gather_classes<16, 4, true><<<grid, kGatherBlock, 0, s>>>(L, cpr, row_bytes, out, host_every);
     } else {
