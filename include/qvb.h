@@ -208,6 +208,22 @@ int qvb_graph_destroy(qvb_graph* g);
  * on the host (out_on_device=0) or the device (1). layers >= 1. */
 int qvb_access_prob(qvb_graph* g, uint32_t layers, double* out, int out_on_device,
                     void* stream);
+/* Row-sharded P over `world` ranks (one exchange step per
+ * layer), each rank holding the same graph on its own device. Rank r
+ * computes nodes [r*chunk, min(n, (r+1)*chunk)), chunk = ceil(n/world/32)*32;
+ * after every sweep j the library calls exchange(ctx, j, p, codes,
+ * chunk, stream): p (double) and codes (uint32, NULL when the next sweep
+ * needs none) each hold world*chunk entries, this rank's chunk written; the
+ * callback must all-gather the chunks in place (e.g. ncclAllGather with
+ * sendbuff = p + rank*chunk) ordered on `stream`, and return 0. Per-node
+ * arithmetic is unchanged: the result is bit-identical to qvb_access_prob.
+ * Graphs whose layout does not split by node ranges compute every node on
+ * every rank without calling exchange; *sharded (nullable) reports which. */
+typedef int (*qvb_exchange_fn)(void* ctx, uint32_t layer, void* p, void* codes,
+                               uint64_t chunk_nodes, void* stream);
+int qvb_access_prob_sharded(qvb_graph* g, uint32_t layers, uint32_t rank, uint32_t world,
+                            qvb_exchange_fn exchange, void* ctx, double* out, int out_on_device,
+                            void* stream, int* sharded);
 /* The whole reference call from host CSR to host table:
  * qv::compute_access_prob_ie(g, transition_view(g), layers)
  * (metrics.hpp:53-54). Uploads, builds the in-CSR, runs the sweeps and copies

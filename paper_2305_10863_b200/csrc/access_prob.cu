@@ -505,7 +505,7 @@ __device__ __noinline__ double slice_product_exc(uint32_t len, const uint16_t* _
 // whole sectors; small graphs sort windows of 256 (less padding) and their
 // scattered stores merge in L2.
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    k_first(uint64_t S, uint64_t n, double base, uint32_t ncls, const double* __restrict__ cls_inv,
+    k_first(uint64_t s0, uint64_t S, uint64_t n, double base, uint32_t ncls, const double* __restrict__ cls_inv,
                   const uint32_t* __restrict__ perm, const uint64_t* __restrict__ sptr,
                   const uint16_t* __restrict__ cls, const uint64_t* __restrict__ xslot,
                   const double* __restrict__ xR, uint64_t nx, const double* __restrict__ inv,
@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   const int lane = threadIdx.x & 31;
   const uint64_t pol = policy_evict_first();
   const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
-  for (uint64_t sl = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); sl < S; sl += warps) {
+  for (uint64_t sl = s0 + (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); sl < S; sl += warps) {
     // node order (f1_ident): the slot names the node, no perm word to read
     const uint32_t v = perm ? (perm[sl * 32 + lane] & kNodeMask)
                             : (sl * 32 + lane < n ? static_cast<uint32_t>(sl * 32 + lane) : kNoNode);
@@ -908,7 +908,7 @@ __global__ void k_build_runs(int K, uint64_t S, const uint8_t* __restrict__ lenf
 }
 
 __global__ void __launch_bounds__(kPtWarps * 32)
-    k_products_tma(int K, uint64_t S, uint64_t n, const uint8_t* __restrict__ lenf,
+    k_products_tma(int K, uint64_t S, uint64_t s0, uint64_t s1, uint64_t n, const uint8_t* __restrict__ lenf,
                    const uint64_t* __restrict__ desc, const ulonglong2* __restrict__ runs,
                    const uint64_t* __restrict__ sbase, const uint32_t* __restrict__ ncode,
                    const uint32_t* __restrict__ ncol, const uint32_t* __restrict__ exc_src,
@@ -940,14 +940,14 @@ __global__ void __launch_bounds__(kPtWarps * 32)
   const uint32_t sent_reg = bufw - zw;
 
   auto load_desc = [&](uint64_t sl) -> uint64_t {
-    return (sl < S && lane < static_cast<uint32_t>(K)) ? ld_stream(desc + sl * K + lane, pol) : 0ull;
+    return (sl < s1 && lane < static_cast<uint32_t>(K)) ? ld_stream(desc + sl * K + lane, pol) : 0ull;
   };
   // Copies of a slice into buffer b: 0 nothing to copy, 1 in flight on
   // bars[b], 2 global path (too big for the buffer, or markers).
   auto issue = [&](uint64_t sl, uint64_t d, int b, uint32_t& maxt) -> uint32_t {
     const uint32_t hi0 = __shfl_sync(kFull, static_cast<uint32_t>(d >> 32), 0);
     maxt = (hi0 >> 22) & 0x1FF;
-    if (sl >= S) return 0;
+    if (sl >= s1) return 0;
     if ((hi0 & 0x80000000u) || mk) return 2;
     const uint32_t words = static_cast<uint32_t>(d & 0x7FF);
     const uint32_t total = __reduce_add_sync(kFull, words);
@@ -966,14 +966,14 @@ __global__ void __launch_bounds__(kPtWarps * 32)
     return 1;
   };
 
-  uint64_t sl = gw;
+  uint64_t sl = s0 + gw;  // this call's slices: [s0, s1) (a rank's node range when sharded)
   uint64_t d1 = load_desc(sl);
-  ulonglong2 rc = sl < S ? runs[sl * 32 + lane] : make_ulonglong2(0, 0);
+  ulonglong2 rc = sl < s1 ? runs[sl * 32 + lane] : make_ulonglong2(0, 0);
   uint32_t maxt_cur, maxt_nxt;
   uint32_t stat_cur = issue(sl, d1, 0, maxt_cur), stat_nxt;
   d1 = load_desc(sl + nw);
   uint32_t par = 0;  // expected parity per buffer
-  for (int i = 0; sl < S; ++i, sl += nw) {
+  for (int i = 0; sl < s1; ++i, sl += nw) {
     const int b = i & 1;
     const uint64_t v = sl * 32 + lane;
     const bool real = v < n;
@@ -985,7 +985,7 @@ __global__ void __launch_bounds__(kPtWarps * 32)
     // the next slice's copies go into the other buffer: its reads by the
     // previous iteration have completed (their values were consumed)
     stat_nxt = issue(sl + nw, d1, b ^ 1, maxt_nxt);
-    const ulonglong2 rn = sl + nw < S ? runs[(sl + nw) * 32 + lane] : make_ulonglong2(0, 0);
+    const ulonglong2 rn = sl + nw < s1 ? runs[(sl + nw) * 32 + lane] : make_ulonglong2(0, 0);
     d1 = load_desc(sl + 2 * nw);
 
     double miss = 1.0;  // metrics.cpp:152
@@ -1076,28 +1076,53 @@ struct PhaseTimer {
 
 }  // namespace
 
-const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, double* final_out) {
+const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, double* final_out,
+                              const Shard& sh) {
+  constexpr int kPtKMaxSh = kPtKMax;
   if (layers < 1) fail(QVB_ERR_VALIDATION, "access probability needs layers >= 1");
   const uint64_t n = g.n;
   const bool compact = g.layout == 0;
   const bool codes = g.nm && compact;                    // nm compact sweeps gather 4-byte codes
   const bool f1 = compact && g.ncls > 0 && layers >= 2;  // class-stream first sweep
   // entry N of every gathered vector is the padding operand: 0 (factor 1.0);
-  // set once when the buffer is made (sweeps write entries < N only)
+  // set once when the buffer is made (sweeps write entries < N only). P and
+  // code buffers carry kShardPad more zero entries: a sharded call's ranks
+  // own chunks of ceil(n / world / 32) * 32 nodes, world * chunk <= n + 32 world
   for (int i = 0; i < 2; ++i) {
     if (!g.p[i]) {
-      QVB_CUDA(cudaMalloc(&g.p[i], (n + 1) * sizeof(double)));
-      QVB_CUDA(cudaMemsetAsync(g.p[i] + n, 0, sizeof(double), s));
+      QVB_CUDA(cudaMalloc(&g.p[i], (n + 1 + kShardPad) * sizeof(double)));
+      QVB_CUDA(cudaMemsetAsync(g.p[i] + n, 0, (1 + kShardPad) * sizeof(double), s));
     }
     if (compact && !g.nm && !g.y[i]) {
       QVB_CUDA(cudaMalloc(&g.y[i], (n + 1) * sizeof(double)));
       QVB_CUDA(cudaMemsetAsync(g.y[i] + n, 0, sizeof(double), s));
     }
     if (codes && !g.kcode[i]) {
-      QVB_CUDA(cudaMalloc(&g.kcode[i], (n + 1) * sizeof(uint32_t)));
-      QVB_CUDA(cudaMemsetAsync(g.kcode[i] + n, 0, sizeof(uint32_t), s));
+      QVB_CUDA(cudaMalloc(&g.kcode[i], (n + 1 + kShardPad) * sizeof(uint32_t)));
+      QVB_CUDA(cudaMemsetAsync(g.kcode[i] + n, 0, (1 + kShardPad) * sizeof(uint32_t), s));
     }
   }
+  // Row-sharded sweeps: this rank computes the nodes of its
+  // chunk, then the exchange callback all-gathers P (and the codes the next
+  // sweep gathers) in place. Per-node arithmetic is unchanged, so the result
+  // is bit-identical to the single-GPU call. Layouts other than the
+  // node-major compact one with TMA products compute every node on every
+  // rank (no exchange needed).
+  bool sharded = false;
+  uint64_t chunk = n, s0 = 0, s1 = g.nm ? g.nm_S : 0;
+  if (sh.world > 1) {
+    if (sh.rank >= sh.world || !sh.fn) fail(QVB_ERR_VALIDATION, "bad shard (rank, world, exchange)");
+    chunk = ((n + sh.world - 1) / sh.world + 31) / 32 * 32;
+    if ((uint64_t)sh.world * chunk > n + 1 + kShardPad) fail(QVB_ERR_UNSUPPORTED, "too many ranks for the graph");
+    const int nseg_ = static_cast<int>(g.seg_slice.size()) - 1;
+    sharded = codes && (!f1 || g.f1_ident) && nseg_ <= kPtKMaxSh && g.long_threshold <= 256 &&
+              !std::getenv("QVB_PRODUCTS");
+    const uint64_t lo = std::min<uint64_t>(n, (uint64_t)sh.rank * chunk);
+    const uint64_t hi = std::min<uint64_t>(n, lo + chunk);
+    s0 = lo / 32;
+    s1 = (hi + 31) / 32;
+  }
+  g.last_sharded = sharded;
   if (codes && !g.nm_code) {  // +128: k_products reads whole 4-code groups past a run's end
     QVB_CUDA(cudaMalloc(&g.nm_code, (g.nm_cols + 128) * sizeof(uint32_t)));
     QVB_CUDA(cudaMalloc(&g.marked, sizeof(uint32_t)));
@@ -1126,9 +1151,17 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, dou
     const int cur = (j - 2) & 1, nxt = cur ^ 1;
     const bool first = j == 2;
     double* yout = (compact && !g.nm && j < layers) ? g.y[nxt] : nullptr;
-    // the last sweep writes straight into the caller's device buffer
-    double* const pout = (j == layers && final_out) ? final_out : g.p[nxt];
+    // the last sweep writes straight into the caller's device buffer (not
+    // when sharded: the exchange needs the padded buffer)
+    double* const pout = (j == layers && final_out && !sharded) ? final_out : g.p[nxt];
     uint32_t* kout = (codes && j < layers) ? g.kcode[nxt] : nullptr;
+    // after a sharded sweep: every rank's chunk of P_j (and of its codes,
+    // which the next sweep gathers) into every rank's buffers
+    auto exchange = [&]() {
+      if (!sharded) return;
+      const int rc = sh.fn(sh.ctx, j, pout, kout, chunk, s);
+      if (rc != 0) fail(QVB_ERR_GENERIC, "exchange callback failed at layer " + std::to_string(j));
+    };
 
     if (first && f1) {  // ---- first sweep over the class stream
       pt.begin(0);
@@ -1153,7 +1186,8 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, dou
                                     (g.f1_S + kWarpsPerBlock - 1) / kWarpsPerBlock);
         }
         const unsigned grid = g.f1_grid;
-        k_first<<<grid, kWarpsPerBlock * 32, smem, s>>>(g.f1_S, n, base, g.ncls, g.cls_inv,
+        k_first<<<grid, kWarpsPerBlock * 32, smem, s>>>(sharded ? s0 : 0, sharded ? s1 : g.f1_S, n, base,
+                                                        g.ncls, g.cls_inv,
                                                         g.f1_ident ? nullptr : g.f1_perm,
                                                         g.f1_sptr, g.f1_cls, g.f1_xslot, g.f1_xR,
                                                         g.f1_nx, g.inv, pout, yout, kout);
@@ -1161,6 +1195,7 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, dou
         ++launched;
       }
       pt.end(launched);
+      exchange();
       continue;
     }
 
@@ -1177,8 +1212,18 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, dou
       }
       // one launch per source segment: the CTAs in flight gather from one
       // L2-resident code segment
+      if (sharded && g.shard_key != (uint64_t)sh.world << 32 | sh.rank) {  // this rank's entries per pass
+        g.shard_e.assign(2 * nseg, 0);
+        for (int k = 0; k < nseg; ++k) {
+          QVB_CUDA(cudaMemcpy(&g.shard_e[2 * k], g.nm_sbase + (uint64_t)k * g.nm_S + s0, 8, cudaMemcpyDeviceToHost));
+          QVB_CUDA(cudaMemcpy(&g.shard_e[2 * k + 1], g.nm_sbase + (uint64_t)k * g.nm_S + s1, 8,
+                              cudaMemcpyDeviceToHost));
+        }
+        g.shard_key = (uint64_t)sh.world << 32 | sh.rank;
+      }
       for (int k = 0; k < nseg; ++k) {
-        const uint64_t e0 = g.nm_region[k], e1 = g.nm_region[k + 1];
+        const uint64_t e0 = sharded ? g.shard_e[2 * k] : g.nm_region[k];
+        const uint64_t e1 = sharded ? g.shard_e[2 * k + 1] : g.nm_region[k + 1];
         if (e1 <= e0) continue;
         if (!g.codes_grid) g.codes_grid = resident_grid(k_codes, 256, 0, ~0ull);
         const unsigned cg = static_cast<unsigned>(std::min<uint64_t>(g.codes_grid, (e1 - e0 + 2047) / 2048));
@@ -1223,7 +1268,7 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, dou
       if (g.prod_bufw && !old_products) {
         const size_t smem = (size_t)kPtWarps * pt_warp_bytes(g.prod_bufw);
         k_products_tma<<<g.prod_grid, kPtWarps * 32, smem, s>>>(
-            nseg, g.nm_S, n, g.nm_lenf, g.nm_desc, reinterpret_cast<const ulonglong2*>(g.nm_runs),
+            nseg, g.nm_S, sharded ? s0 : 0, sharded ? s1 : g.nm_S, n, g.nm_lenf, g.nm_desc, reinterpret_cast<const ulonglong2*>(g.nm_runs),
             g.nm_sbase, g.nm_code, g.nm_col, g.exc_src, g.exc_R, g.p[cur], g.inv, pout, kout,
             g.marked, g.prod_bufw, g.prod_zw);
       } else {
@@ -1234,6 +1279,7 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, dou
       }
       QVB_LAUNCH_CHECK();
       pt.end(1);
+      exchange();
       continue;
     }
 
@@ -1276,8 +1322,8 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, dou
     pt.end(launched);
   }
   QVB_CUDA(cudaEventRecord(g.ev[1], s));
-  if (final_out && layers == 1) {
-    QVB_CUDA(cudaMemcpyAsync(final_out, g.p[0], n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (final_out && (layers == 1 || sharded)) {
+    QVB_CUDA(cudaMemcpyAsync(final_out, g.p[(layers - 1) & 1], n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     return final_out;
   }
   return final_out ? final_out : g.p[(layers - 1) & 1];
@@ -1305,6 +1351,31 @@ extern "C" int qvb_access_prob(qvb_graph* g, uint32_t layers, double* out, int o
       QVB_CUDA(cudaEventRecord(g->done, s));
       copy_to_host(out, p, g->n * sizeof(double), s);
     }
+  });
+}
+
+extern "C" int qvb_access_prob_sharded(qvb_graph* g, uint32_t layers, uint32_t rank, uint32_t world,
+                                       qvb_exchange_fn exchange, void* ctx, double* out,
+                                       int out_on_device, void* stream, int* sharded) {
+  return guarded([&] {
+    if (!g || !out) fail(QVB_ERR_VALIDATION, "null argument");
+    if (layers < 1) fail(QVB_ERR_VALIDATION, "access probability needs layers >= 1");
+    if (world < 1 || rank >= world) fail(QVB_ERR_VALIDATION, "rank out of range");
+    if (world > 1 && !exchange) fail(QVB_ERR_VALIDATION, "a sharded call needs an exchange callback");
+    DeviceGuard dg(g->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lock(g->run_mu);
+    if (!g->done) QVB_CUDA(cudaEventCreateWithFlags(&g->done, cudaEventDisableTiming));
+    QVB_CUDA(cudaStreamWaitEvent(s, g->done, 0));
+    Shard sh;
+    sh.rank = rank;
+    sh.world = world;
+    sh.fn = exchange;
+    sh.ctx = ctx;
+    const double* p = run_access_prob(*g, layers, s, out_on_device ? out : nullptr, sh);
+    QVB_CUDA(cudaEventRecord(g->done, s));
+    if (!out_on_device) copy_to_host(out, p, g->n * sizeof(double), s);
+    if (sharded) *sharded = g->last_sharded ? 1 : 0;
   });
 }
 

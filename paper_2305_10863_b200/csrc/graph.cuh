@@ -133,6 +133,9 @@ struct qvb_graph {
   uint64_t bytes = 0;
   double build_ms = 0.0;
   cudaEvent_t ev[2] = {nullptr, nullptr};  // bracket the sweeps of the last run
+  bool last_sharded = false;                // the last run split its sweeps over ranks
+  uint64_t shard_key = ~0ull;               // (world << 32 | rank) of shard_e
+  std::vector<uint64_t> shard_e;            // per pass: this rank's nm_col entry range
   // per-phase brackets of the last run: (phase, start, end); phase 0 = first
   // sweep (class stream), 1 = code gather (k_codes), 2 = ordered products,
   // 3 = any other sweep kernel
@@ -230,9 +233,20 @@ void generate_out_csr(uint64_t n, uint64_t e, uint64_t seed, int weighted, int t
                       cudaStream_t s, DevBuf<uint64_t>& ro, DevBuf<uint32_t>& col,
                       DevBuf<double>& w, DevBuf<uint32_t>& ssrc);
 
+// Row-sharded P call (qvb_access_prob_sharded): rank of world, and the
+// caller's exchange (an in-place all-gather of each sweep's P and codes).
+struct Shard {
+  uint32_t rank = 0, world = 1;
+  qvb_exchange_fn fn = nullptr;
+  void* ctx = nullptr;
+};
+// zero entries past N in the P / code buffers: chunks of ceil(n/world/32)*32
+// nodes for up to 64 ranks
+constexpr uint64_t kShardPad = 32 * 64;
+
 // Runs layers-1 sweeps; returns the device buffer holding P_layers
 // (final_out, when given: the last sweep writes it directly).
 const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s,
-                              double* final_out = nullptr);
+                              double* final_out = nullptr, const Shard& sh = Shard{});
 
 }  // namespace qvb

@@ -613,6 +613,7 @@ struct ClassLists {
   unsigned int* count;                 // [kClasses] list lengths
   unsigned int* cursor;                // [kClasses] next 32-row group to take
   unsigned int* hist;                  // host rows per offset bucket (null: unordered)
+  unsigned long long* cur;             // bucket cursors: exclusive prefix of hist
   int hshift;                          // host offset >> hshift = bucket
 };
 
@@ -621,7 +622,7 @@ struct ClassLists {
 // address order, which keeps the GPU's page-table walks for system memory
 // local — random rows from a 14 GB host tier read at 38 GB/s, rows in offset
 // order well above (profiles/r01k_host_tier.txt, r01m_gather_sweep.md).
-constexpr int kHostBucketBits = 18;
+constexpr int kHostBucketBits = 18;  // upper bound of QVB_HOST_BUCKET_BITS
 constexpr int kHostBuckets = 1 << kHostBucketBits;
 
 __global__ void __launch_bounds__(256)
@@ -665,31 +666,6 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// exclusive scan of the bucket counts in place (one block of 1024 threads,
-// each owning kHostBuckets / 1024 consecutive buckets)
-__global__ void __launch_bounds__(1024) k_bucket_scan(unsigned int* __restrict__ hist, int buckets) {
-  const int per = buckets / 1024;
-  __shared__ unsigned int part[1024];
-  const int t = threadIdx.x;
-  unsigned int* mine = hist + t * per;
-  unsigned int sum = 0;
-  for (int k = 0; k < per; ++k) sum += mine[k];
-  part[t] = sum;
-  __syncthreads();
-  for (int d = 1; d < 1024; d <<= 1) {  // Hillis-Steele inclusive scan
-    const unsigned int x = t >= d ? part[t - d] : 0;
-    __syncthreads();
-    part[t] += x;
-    __syncthreads();
-  }
-  unsigned int run = part[t] - sum;
-  for (int k = 0; k < per; ++k) {
-    const unsigned int v = mine[k];
-    mine[k] = run;
-    run += v;
-  }
-}
-
 // host list -> bucket order (order inside a bucket is arbitrary; every row
 // still lands at its request's output position)
 __global__ void k_bucket_scatter(ClassLists L, const uint32_t* __restrict__ in_req,
@@ -699,7 +675,7 @@ __global__ void k_bucket_scatter(ClassLists L, const uint32_t* __restrict__ in_r
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < cap && j < cnt;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const unsigned long long src = in_src[j];
-    const unsigned int pos = atomicAdd(L.hist + ((src - host_base) / stride >> L.hshift), 1u);
+    const unsigned long long pos = atomicAdd(L.cur + ((src - host_base) / stride >> L.hshift), 1ull);
     L.req[2][pos] = in_req[j];
     L.src[2][pos] = src;
   }
@@ -996,7 +972,7 @@ struct qvb_store {
     DevBuf<uint32_t> req(b * (kClasses + (order_host ? 1 : 0)), s);
     DevBuf<unsigned long long> srcs(b * (kClasses + (order_host ? 1 : 0)), s);
     const char* bb = std::getenv("QVB_HOST_BUCKET_BITS");  // A/B knob: 10..18
-    const int bbits = bb ? std::max(10, std::min(kHostBucketBits, std::atoi(bb))) : kHostBucketBits;
+    const int bbits = bb ? std::max(10, std::min(kHostBucketBits, std::atoi(bb))) : 16;
     const int nbuckets = 1 << bbits;
     DevBuf<unsigned int> ctr(2 * kClasses + (order_host ? nbuckets : 0), s);
     QVB_CUDA(cudaMemsetAsync(ctr.p, 0, (2 * kClasses + (order_host ? nbuckets : 0)) * sizeof(unsigned int), s));
@@ -1008,6 +984,7 @@ struct qvb_store {
     L.count = ctr.p;
     L.cursor = ctr.p + kClasses;
     L.hist = order_host ? ctr.p + 2 * kClasses : nullptr;
+    L.cur = nullptr;
     const int hb = bits_for(host_rows > 1 ? host_rows - 1 : 1);
     L.hshift = hb > bbits ? hb - bbits : 0;
     const unsigned sgrid = resident_grid_cached(k_split_classes, 256, 0);
@@ -1015,8 +992,9 @@ struct qvb_store {
         ids, b, lut, bases, stride, n, static_cast<int>(reader), host_loc, L, err);
     QVB_LAUNCH_CHECK();
     if (order_host) {
-      k_bucket_scan<<<1, 1024, 0, s>>>(L.hist, nbuckets);
-      QVB_LAUNCH_CHECK();
+      DevBuf<unsigned long long> cur(nbuckets, s);  // bucket starts (device scan primitive)
+      exclusive_sum_u32_u64(L.hist, reinterpret_cast<uint64_t*>(cur.p), nbuckets, s);
+      L.cur = cur.p;
       ClassLists sorted = L;  // the gather reads the bucket-ordered host list
       sorted.req[2] = req.p + kClasses * b;
       sorted.src[2] = srcs.p + kClasses * b;

@@ -115,3 +115,47 @@ def build_store(qvb, loc_offsets, loc_ids, dim: int, topo, rank: int, local_rank
             store.attach_peer(peer, h)
     barrier()
     return store
+
+
+class _DevView:
+    """A device pointer as a torch tensor (``__cuda_array_interface__``)."""
+
+    def __init__(self, ptr: int, count: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3}
+
+
+def allgather_exchange(rank: int, world: int, device: int):
+    """The exchange step of the row-sharded P pass: after each
+    sweep, every rank's chunk of P_j (f64) and of the codes the next sweep
+    gathers (u32) is all-gathered IN PLACE into every rank's buffers — one
+    ncclAllGather per array over NVLink/NVSwitch, ordered on the library's
+    stream. With gloo (ranks sharing one GPU in tests) the chunks travel
+    through host memory."""
+
+    def exchange(layer, p_ptr, codes_ptr, chunk, stream_ptr):
+        ext = torch.cuda.ExternalStream(stream_ptr, device=device) if stream_ptr else \
+            torch.cuda.default_stream(device)
+        with torch.cuda.device(device), torch.cuda.stream(ext):
+            for ptr, ts in ((p_ptr, "<f8"), (codes_ptr, "<i4")):  # codes: u32 bits as i32
+                if not ptr:
+                    continue
+                whole = torch.as_tensor(_DevView(ptr, world * chunk, ts), device=f"cuda:{device}")
+                mine = whole[rank * chunk:(rank + 1) * chunk]
+                if dist.get_backend() == "nccl":
+                    dist.all_gather_into_tensor(whole, mine)
+                else:  # gloo: host staging (functional multi-rank tests on one GPU)
+                    host = mine.cpu()
+                    parts = [torch.empty_like(host) for _ in range(world)]
+                    dist.all_gather(parts, host)
+                    whole.copy_(torch.cat(parts).to(whole.device))
+
+    return exchange
+
+
+def sharded_access_prob(graph, layers: int, device: int, out=None, stream=None):
+    """P(n, layers) with the sweeps split over the ranks (one process per
+    GPU, each holding the graph): bit-identical to the single-GPU call."""
+    rank, world = (dist.get_rank(), dist.get_world_size()) if is_dist() else (0, 1)
+    return graph.access_prob_sharded(layers, rank, world, allgather_exchange(rank, world, device),
+                                     out=out, stream=stream)

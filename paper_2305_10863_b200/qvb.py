@@ -146,6 +146,8 @@ class SampleInfo(C.Structure):
 
 
 _LIB = None
+# qvb_exchange_fn: int (*)(void* ctx, uint32_t layer, void* p, void* codes, uint64_t chunk, void* stream)
+ExchangeFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
 vp = C.c_void_p
 u64 = C.c_uint64
 u32 = C.c_uint32
@@ -176,6 +178,7 @@ _SIGNATURES = {
     "qvb_fetch_cost": (i32, [P(Topology), u32, u32, u32, u64, vp, vp, vp, u64, vp, P(C.c_double)]),
     "qvb_access_prob": (i32, [vp, u32, vp, i32, vp]),
     "qvb_compute_access_prob_ie": (i32, [i32, u64, u64, vp, vp, vp, u32, vp, vp]),
+    "qvb_access_prob_sharded": (i32, [vp, u32, u32, u32, vp, vp, vp, i32, vp, P(i32)]),
     "qvb_compute_fap": (i32, [i32, u64, u64, vp, vp, vp, u32, vp, vp]),
     "qvb_rank_desc": (i32, [i32, vp, u64, vp, i32, vp]),
     "qvb_plan_placement": (i32, [i32, vp, u64, P(Topology), vp, vp, u64, P(u64)]),
@@ -322,6 +325,35 @@ class DeviceGraph:
         on_dev = 0 if isinstance(out, np.ndarray) else 1
         _check(_lib().qvb_access_prob(self._h, layers, _ptr(out), on_dev, _stream_ptr(stream)))
         return out
+
+    def access_prob_sharded(self, layers: int, rank: int, world: int, exchange, out=None,
+                            stream=None):
+        """Row-sharded P (qvb_access_prob_sharded): this rank computes its
+        node chunk of every sweep; ``exchange(layer, p_ptr, codes_ptr, chunk,
+        stream_ptr)`` must all-gather the chunks in place and return. Returns
+        (P for every node, whether the layout was actually split)."""
+        n = self.info().node_count
+        if out is None:
+            out = np.zeros(n, np.float64)
+        on_dev = 0 if isinstance(out, np.ndarray) else 1
+        err = []
+
+        def cb(_ctx, layer, p, codes, chunk, st):
+            try:
+                exchange(layer, p, codes, chunk, st)
+                return 0
+            except Exception as ex:  # noqa: BLE001 - reported by the library as a failure
+                err.append(ex)
+                return 1
+
+        fn = ExchangeFn(cb)
+        sh = C.c_int(0)
+        rc = _lib().qvb_access_prob_sharded(self._h, layers, rank, world, C.cast(fn, C.c_void_p), None,
+                                             _ptr(out), on_dev, _stream_ptr(stream), C.byref(sh))
+        if err:
+            raise err[0]
+        _check(rc)
+        return out, bool(sh.value)
 
     def last_sweep_ms(self) -> float:
         """Device time of the P sweeps of the last access_prob call."""

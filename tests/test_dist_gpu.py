@@ -79,3 +79,46 @@ def test_two_process_ipc_gather(replicate, host_frac):
         local, peer, host = fr
         assert peer > 0.2 and local > 0.2  # both shards really serve rows
         assert (host > 0.1) == (host_frac > 0)
+
+
+def _p_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank), QVB_SEG_MB="4", QVB_F1_WINDOW="32")
+    try:
+        import torch
+        import torch.distributed as dist
+
+        from paper_2305_10863_b200 import dist as D
+        from paper_2305_10863_b200 import qvb
+
+        D.init(backend="gloo")
+        torch.cuda.set_device(0)
+        n, e = 2_400_000, 62_000_000
+        g = qvb.DeviceGraph.synthetic(n, e, 7, False, False)
+        p, sharded = D.sharded_access_prob(g, 3, 0)
+        ref = g.access_prob(3)
+        g.close()
+        q.put((rank, "ok", bool((p.view(np.uint64) == ref.view(np.uint64)).all()) and sharded))
+        dist.destroy_process_group()
+    except Exception:  # noqa: BLE001
+        import traceback
+
+        q.put((rank, "fail", traceback.format_exc()))
+
+
+def test_two_process_sharded_access_prob():
+    """Two processes split the C2 sweeps by node chunks and all-gather P and
+    the codes over torch.distributed after every sweep (gloo through host
+    memory here, since both share the box's one GPU; NCCL in place on a
+    multi-GPU node): both end with the single-GPU answer bit for bit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, status, ok in res:
+        assert status == "ok" and ok is True, ok

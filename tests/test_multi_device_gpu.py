@@ -109,3 +109,41 @@ def test_nccl_ranks_ipc_gather():
 def test_device_count_reported(qvb):
     """Runs everywhere: the library sees the devices torch sees."""
     assert qvb.device_count() == torch.cuda.device_count()
+
+
+def _sharded_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank), QVB_SEG_MB="4", QVB_F1_WINDOW="32")
+    try:
+        import torch.distributed as dist
+
+        from paper_2305_10863_b200 import dist as D
+        from paper_2305_10863_b200 import qvb
+
+        D.init()  # NCCL, one process per device: in-place all-gathers over NVLink
+        g = qvb.DeviceGraph.synthetic(2_400_000, 62_000_000, 7, False, False, device=rank)
+        p, sharded = D.sharded_access_prob(g, 3, rank)
+        ref = g.access_prob(3)
+        g.close()
+        q.put((rank, "ok", bool((p.view(np.uint64) == ref.view(np.uint64)).all()) and sharded))
+        dist.destroy_process_group()
+    except Exception:  # noqa: BLE001
+        import traceback
+
+        q.put((rank, "fail", traceback.format_exc()))
+
+
+@needs2
+def test_nccl_sharded_access_prob():
+    world = min(_gpus(), 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, status, ok in res:
+        assert status == "ok" and ok is True, ok
