@@ -265,21 +265,33 @@ def run_ours(args):
     g = qvb.DeviceGraph.synthetic(n, e, 7, cfg["weighted"], False, device=local, stream=stream)
     info = g.info()
     p_dev = torch.empty(n, dtype=torch.float64, device=dev)
+    sharded = [False]
+
+    def p_call():
+        # N > 1: the sweeps split over the ranks by node chunks with one
+        # in-place all-gather of P (and codes) per layer
+        if world > 1 and not D.shared_gpu():
+            _, sharded[0] = D.sharded_access_prob(g, layers, local, out=p_dev, stream=stream)
+        else:
+            g.access_prob(layers, out=p_dev, stream=stream)
+
     for _ in range(args.warmup):
-        g.access_prob(layers, out=p_dev, stream=stream)
+        p_call()
     torch.cuda.synchronize(dev)
+    D.barrier()
     ap_call, ap_sweep, phases = [], [], []
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     for _ in range(args.steps):
         ev[0].record(stream)
-        g.access_prob(layers, out=p_dev, stream=stream)
+        p_call()
         ev[1].record(stream)
         ev[1].synchronize()
-        ap_call.append(ev[0].elapsed_time(ev[1]))
+        ap_call.append(D.max_over_ranks(ev[0].elapsed_time(ev[1])))
         ap_sweep.append(g.last_sweep_ms())
         phases.append(g.phase_ms())
     p_host = p_dev.cpu().numpy()
     access_prob = access_prob_line(cfg, info, layers, ap_call, ap_sweep, phases, pk)
+    access_prob["sharded_over_ranks"] = world if sharded[0] else 1
     g.close()
 
     # ---- K0 sampler: qv_bench's batch_sample (tools/bench.cpp:89-94) ----------
