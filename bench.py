@@ -292,6 +292,11 @@ def run_ours(args):
     p_host = p_dev.cpu().numpy()
     access_prob = access_prob_line(cfg, info, layers, ap_call, ap_sweep, phases, pk)
     access_prob["sharded_over_ranks"] = world if sharded[0] else 1
+    if sharded[0]:  # the roofline of the whole job: world GPUs' HBM
+        sm = access_prob["survey_model"]
+        sm["t_roof_ms"] /= world
+        sm["frac"] = sm["t_roof_ms"] / sm["ms"]
+        sm["note"] += f"; sweeps split over {world} GPUs: T_roof / {world}"
     g.close()
 
     # ---- K0 sampler: qv_bench's batch_sample (tools/bench.cpp:89-94) ----------

@@ -285,6 +285,32 @@ int main(int argc, char** argv) {
       ok &= std::memcmp(got.data() + r * dim, x.data() + ids[r] * dim, dim * 4) == 0;
     CHECK(ok);
     CHECK_THROWS_AS(store.gather(std::vector<NodeId>{n}), ValidationError, "outside lookup table");
+    // the per-batch read plan over the store's resident table == the table's
+    FeatureLookupTable table = build_lookup_table(plan, topo, 0);
+    for (uint64_t page : {1, 3, 8}) {
+      ReadPlan a = plan_reads(table, ids, page), b = plan_reads(store, ids, page);
+      bool same = a.per_location.size() == b.per_location.size();
+      for (size_t k = 0; same && k < a.per_location.size(); ++k)
+        same = a.per_location[k].location_id == b.per_location[k].location_id &&
+               a.per_location[k].offsets == b.per_location[k].offsets &&
+               a.per_location[k].page_transitions == b.per_location[k].page_transitions;
+      CHECK(same);
+    }
+    CHECK_THROWS_AS(plan_reads(store, std::vector<NodeId>{0, n}, 8), ValidationError, "outside lookup table");
+  }
+  {  // transition_view keeps the device graph; a view of another graph falls back to an upload
+    Graph g = random_graph(60, 400, true);
+    Graph h = random_graph(60, 400, false);
+    TransitionView tg = transition_view(g);
+    CHECK(tg.resident_for(g) && !tg.resident_for(h));
+    for (uint32_t L = 1; L <= 3; ++L) {
+      CHECK(same_bits(compute_access_prob_ie(g, tg, L).values, oracle_p(g, L)));
+      CHECK(same_bits(compute_access_prob_ie(h, tg, L).values, oracle_p(h, L)));
+    }
+    Graph g2 = g;  // a copy owns new arrays: no stale device graph is used for it
+    g2.edge_weights[0] *= 2.0;
+    CHECK(!tg.resident_for(g2));
+    CHECK(same_bits(compute_access_prob_ie(g2, transition_view(g2), 3).values, oracle_p(g2, 3)));
   }
 
   // --- sampler: test_sampler.cpp:15-150, vs the oracle restatement ------------
