@@ -1115,7 +1115,7 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, dou
     chunk = ((n + sh.world - 1) / sh.world + 31) / 32 * 32;
     if ((uint64_t)sh.world * chunk > n + 1 + kShardPad) fail(QVB_ERR_UNSUPPORTED, "too many ranks for the graph");
     const int nseg_ = static_cast<int>(g.seg_slice.size()) - 1;
-    sharded = codes && (!f1 || g.f1_ident) && nseg_ <= kPtKMaxSh && g.long_threshold <= 256 &&
+    sharded = layers >= 2 && codes && (!f1 || g.f1_ident) && nseg_ <= kPtKMaxSh && g.long_threshold <= 256 &&
               !std::getenv("QVB_PRODUCTS");
     const uint64_t lo = std::min<uint64_t>(n, (uint64_t)sh.rank * chunk);
     const uint64_t hi = std::min<uint64_t>(n, lo + chunk);
