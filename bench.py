@@ -270,7 +270,7 @@ def run_ours(args):
     def p_call():
         # N > 1: the sweeps split over the ranks by node chunks with one
         # in-place all-gather of P (and codes) per layer
-        if world > 1 and not D.shared_gpu():
+        if world > 1:  # (QVB_SHARE_GPU: gloo exchange through host memory, function only)
             _, sharded[0] = D.sharded_access_prob(g, layers, local, out=p_dev, stream=stream)
         else:
             g.access_prob(layers, out=p_dev, stream=stream)
