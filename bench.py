@@ -232,7 +232,7 @@ def access_prob_line(cfg, info, layers, ap_call, ap_sweep, phases, pk):
                   "exceptions": info.exception_count,
                   "layout": "weighted" if info.layout else "compact",
                   "first_sweep_classes": info.classes, "source_segments": nseg,
-                  "in_csr_build_ms": info.build_ms, "device_bytes": info.device_bytes},
+                  "in_csr_build_ms": info.build_ms, "in_csr_build_note": "device generator + in-CSR build, first build in the process (includes growing the stream-ordered memory pool; a warm build at C4 takes ~0.23 s, see access_prob.e2e)", "device_bytes": info.device_bytes},
         "roofline": roof,
         "kernels": kernels,
         "survey_model": {"bytes": survey_bytes, "t_roof_ms": t_roof, "ms": ap_ms,

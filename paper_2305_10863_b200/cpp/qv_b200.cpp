@@ -549,10 +549,43 @@ namespace {
 constexpr char kCsrMagic[6] = {'Q', 'V', 'C', 'S', 'R', '1'};
 constexpr char kTabMagic[6] = {'Q', 'V', 'T', 'A', 'B', '1'};
 
-template <typename T>
-void read_pod(std::ifstream& in, T* p, std::size_t n, const std::string& path, const char* what) {
-  in.read(reinterpret_cast<char*>(p), static_cast<std::streamsize>(sizeof(T) * n));
-  if (!in) throw ParseError(path + what);
+// Binary table files: a 6-byte magic, little-endian u64 header words, raw
+// payload arrays (QVCSR1 graph.cpp:197-258, QVTAB1 metrics.cpp:203-250).
+class BinFile {
+ public:
+  BinFile(const std::string& path, bool write) : path_(path), f_(std::fopen(path.c_str(), write ? "wb" : "rb")) {}
+  ~BinFile() {
+    if (f_) std::fclose(f_);
+  }
+  BinFile(const BinFile&) = delete;
+  BinFile& operator=(const BinFile&) = delete;
+  bool open() const { return f_ != nullptr; }
+  // reads count items; false when the file ends first
+  template <typename T>
+  bool get(T* dst, std::size_t count) {
+    return std::fread(dst, sizeof(T), count, f_) == count;
+  }
+  template <typename T>
+  bool put(const T* src, std::size_t count) {
+    return std::fwrite(src, sizeof(T), count, f_) == count;
+  }
+  bool close_ok() {
+    const bool ok = std::fflush(f_) == 0 && !std::ferror(f_);
+    std::fclose(f_);
+    f_ = nullptr;
+    return ok;
+  }
+
+ private:
+  std::string path_;
+  std::FILE* f_;
+};
+
+// Text exports: the whole file is formatted in memory and written once.
+void write_text_file(const std::string& path, const std::string& text, const char* kind) {
+  BinFile f(path, true);
+  if (!f.open()) throw Error(std::string("cannot write ") + kind + " file: " + path);
+  if (!f.put(text.data(), text.size()) || !f.close_ok()) throw Error("short write to " + path);
 }
 
 // The text edge-list format (graph.cpp:112-188 semantics): "src dst [w]"
@@ -632,75 +665,71 @@ void json_escape_free_write(std::ostringstream& o, int indent) {
 
 Graph load_graph(const std::string& path, GraphFormat format, bool remap_sparse_ids) {
   if (format == GraphFormat::edge_list_text) return load_edge_list(path, remap_sparse_ids);
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw ParseError("cannot open graph file: " + path);
+  BinFile f(path, false);
+  if (!f.open()) throw ParseError("cannot open graph file: " + path);
+  const std::string truncated = path + ": truncated csr-binary file";
   char magic[6];
-  read_pod(in, magic, 6, path, ": truncated csr-binary file");
+  if (!f.get(magic, 6)) throw ParseError(truncated);
   if (std::memcmp(magic, kCsrMagic, 6) != 0) throw ParseError(path + ": bad magic, not a QVCSR1 file");
+  std::uint64_t head[2];  // node count, edge count
+  if (!f.get(head, 2)) throw ParseError(truncated);
+  if (head[0] == 0) throw ValidationError("empty graph in " + path);
   Graph g;
-  read_pod(in, &g.node_count, 1, path, ": truncated csr-binary file");
-  read_pod(in, &g.edge_count, 1, path, ": truncated csr-binary file");
-  if (g.node_count == 0) throw ValidationError("empty graph in " + path);
-  g.row_offsets.resize(g.node_count + 1);
-  g.col_indices.resize(g.edge_count);
-  g.edge_weights.resize(g.edge_count);
-  read_pod(in, g.row_offsets.data(), g.row_offsets.size(), path, ": truncated csr-binary file");
-  read_pod(in, g.col_indices.data(), g.col_indices.size(), path, ": truncated csr-binary file");
-  read_pod(in, g.edge_weights.data(), g.edge_weights.size(), path, ": truncated csr-binary file");
-  g.validate();
+  g.node_count = head[0];
+  g.edge_count = head[1];
+  g.row_offsets.resize(head[0] + 1);
+  g.col_indices.resize(head[1]);
+  g.edge_weights.resize(head[1]);
+  const bool whole = f.get(g.row_offsets.data(), g.row_offsets.size()) &&
+                     f.get(g.col_indices.data(), g.col_indices.size()) &&
+                     f.get(g.edge_weights.data(), g.edge_weights.size());
+  if (!whole) throw ParseError(truncated);
+  g.validate();  // on the device
   return g;
 }
 
 void save_graph_csr(const Graph& g, const std::string& path) {
-  std::ofstream out(path, std::ios::binary | std::ios::trunc);
-  if (!out) throw Error("cannot write graph file: " + path);
-  out.write(kCsrMagic, 6);
-  out.write(reinterpret_cast<const char*>(&g.node_count), 8);
-  out.write(reinterpret_cast<const char*>(&g.edge_count), 8);
-  out.write(reinterpret_cast<const char*>(g.row_offsets.data()), g.row_offsets.size() * 8);
-  out.write(reinterpret_cast<const char*>(g.col_indices.data()), g.col_indices.size() * 8);
-  out.write(reinterpret_cast<const char*>(g.edge_weights.data()), g.edge_weights.size() * 8);
-  if (!out) throw Error("short write to " + path);
+  BinFile f(path, true);
+  if (!f.open()) throw Error("cannot write graph file: " + path);
+  const std::uint64_t head[2] = {g.node_count, g.edge_count};
+  const bool ok = f.put(kCsrMagic, 6) && f.put(head, 2) &&
+                  f.put(g.row_offsets.data(), g.row_offsets.size()) &&
+                  f.put(g.col_indices.data(), g.col_indices.size()) &&
+                  f.put(g.edge_weights.data(), g.edge_weights.size());
+  if (!ok || !f.close_ok()) throw Error("short write to " + path);
 }
 
 void save_table_binary(const std::string& path, std::span<const double> values, std::uint64_t k) {
-  std::ofstream out(path, std::ios::binary | std::ios::trunc);
-  if (!out) throw Error("cannot write table file: " + path);
-  const std::uint64_t n = values.size();
-  out.write(kTabMagic, 6);
-  out.write(reinterpret_cast<const char*>(&n), 8);
-  out.write(reinterpret_cast<const char*>(&k), 8);
-  out.write(reinterpret_cast<const char*>(values.data()), n * 8);
-  if (!out) throw Error("short write to " + path);
+  BinFile f(path, true);
+  if (!f.open()) throw Error("cannot write table file: " + path);
+  const std::uint64_t head[2] = {values.size(), k};
+  if (!(f.put(kTabMagic, 6) && f.put(head, 2) && f.put(values.data(), values.size())) || !f.close_ok())
+    throw Error("short write to " + path);
 }
 
 LoadedTable load_table_binary(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw ParseError("cannot open table file: " + path);
+  BinFile f(path, false);
+  if (!f.open()) throw ParseError("cannot open table file: " + path);
   char magic[6];
-  in.read(magic, 6);
-  if (!in || std::memcmp(magic, kTabMagic, 6) != 0) throw ParseError(path + ": bad magic, not a QVTAB1 file");
-  std::uint64_t n = 0;
+  if (!f.get(magic, 6) || std::memcmp(magic, kTabMagic, 6) != 0)
+    throw ParseError(path + ": bad magic, not a QVTAB1 file");
+  std::uint64_t head[2];  // value count, k
+  if (!f.get(head, 2)) throw ParseError(path + ": truncated table header");
   LoadedTable t;
-  in.read(reinterpret_cast<char*>(&n), 8);
-  in.read(reinterpret_cast<char*>(&t.k), 8);
-  if (!in) throw ParseError(path + ": truncated table header");
-  t.values.resize(n);
-  in.read(reinterpret_cast<char*>(t.values.data()), n * 8);
-  if (!in) throw ParseError(path + ": truncated table values");
+  t.k = head[1];
+  t.values.resize(head[0]);
+  if (!f.get(t.values.data(), t.values.size())) throw ParseError(path + ": truncated table values");
   return t;
 }
 
 void save_table_csv(const std::string& path, std::span<const double> values) {
-  std::ofstream out(path, std::ios::trunc);
-  if (!out) throw Error("cannot write csv file: " + path);
-  out << "node_id,value\n";
+  std::string text = "node_id,value\n";
   char buf[64];
   for (std::size_t i = 0; i < values.size(); ++i) {
-    std::snprintf(buf, sizeof buf, "%zu,%.17g\n", i, values[i]);
-    out << buf;
+    const int len = std::snprintf(buf, sizeof buf, "%zu,%.17g\n", i, values[i]);
+    text.append(buf, static_cast<std::size_t>(len));
   }
-  if (!out) throw Error("short write to " + path);
+  write_text_file(path, text, "csv");
 }
 
 std::string placement_to_json_text(const PlacementPlan& plan) {
@@ -735,14 +764,12 @@ std::string placement_to_json_text(const PlacementPlan& plan) {
 }
 
 void save_placement_csv(const PlacementPlan& plan, const std::string& path) {
-  std::ofstream out(path, std::ios::trunc);
-  if (!out) throw Error("cannot write csv file: " + path);
-  out << "feature_id,server,tier,device,replica\n";
+  std::string text = "feature_id,server,tier,device,replica\n";
   for (std::uint64_t f = 0; f < plan.feature_count; ++f)
     for (const Location& l : plan.locations[f])
-      out << f << ',' << l.server << ',' << tier_name(l.tier) << ',' << l.device << ','
-          << (l.replica ? 1 : 0) << '\n';
-  if (!out) throw Error("short write to " + path);
+      text += std::to_string(f) + ',' + std::to_string(l.server) + ',' + tier_name(l.tier) + ',' +
+              std::to_string(l.device) + ',' + (l.replica ? '1' : '0') + '\n';
+  write_text_file(path, text, "csv");
 }
 
 std::string lookup_to_json_text(const FeatureLookupTable& table) {
@@ -764,12 +791,11 @@ std::string lookup_to_json_text(const FeatureLookupTable& table) {
 }
 
 void save_lookup_csv(const FeatureLookupTable& table, const std::string& path) {
-  std::ofstream out(path, std::ios::trunc);
-  if (!out) throw Error("cannot write csv file: " + path);
-  out << "feature_id,location_id,offset\n";
+  std::string text = "feature_id,location_id,offset\n";
   for (std::size_t f = 0; f < table.location_ids.size(); ++f)
-    out << f << ',' << table.location_ids[f] << ',' << table.offsets[f] << '\n';
-  if (!out) throw Error("short write to " + path);
+    text += std::to_string(f) + ',' + std::to_string(table.location_ids[f]) + ',' +
+            std::to_string(table.offsets[f]) + '\n';
+  write_text_file(path, text, "csv");
 }
 
 // ---- feature store ----------------------------------------------------------------

@@ -282,3 +282,30 @@ def test_c4_gather_full_size(qvb, oracle):
     assert (out.cpu().numpy() == exp).all()
     assert (st.gather_host(req[:300_000]) == exp[:300_000]).all()
     st.close()
+
+
+@pytest.mark.parametrize("variant", ["9", "7", "2", "8"])
+def test_gather_kernel_variants_bit_exact(variant):
+    """The opt-in gather variants (QVB_GATHER_U, read once per process: run
+    in a child) return the same rows."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, torch\n"
+        "from oracle.oracle import Oracle\n"
+        "from paper_2305_10863_b200 import qvb\n"
+        "o = Oracle(); n, dim = 40000, 128\n"
+        "t = qvb.Topology.with_defaults(gpus_per_server=1, gpu_feature_capacity=n, host_feature_capacity=n)\n"
+        "lo, ids = qvb.plan_placement(np.random.default_rng(1).random(n), t)\n"
+        "st = qvb.FeatureStore(lo, ids, dim, t, reader=0)\n"
+        "req = o.request_ids(11, 3, n, 100003)\n"
+        "d = torch.from_numpy(req.view(np.int64)).cuda()\n"
+        "out = torch.empty((len(req), dim), dtype=torch.float32, device='cuda')\n"
+        "st.gather(d, out); st.check_error()\n"
+        "assert (out.cpu().numpy() == o.gather(o.features(n, dim), req)).all()\n"
+        "print('variant ok')\n")
+    env = dict(os.environ, QVB_GATHER_U=variant)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "variant ok" in r.stdout, r.stderr[-3000:]
