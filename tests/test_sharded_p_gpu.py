@@ -104,3 +104,17 @@ def test_sharded_world_one_is_the_plain_call(qvb):
     with pytest.raises(qvb.ValidationError):
         g.access_prob_sharded(3, 2, 2, lambda *a: None)
     g.close()
+
+
+def test_sharded_c4_full_size_bit_exact(qvb):
+    """Papers scale (C4: 111M nodes, 1.6B edges, its default node-major
+    layout): two ranks' sharded 3-layer pass equals the one-GPU pass on all
+    111M nodes."""
+    c = CONFIGS["C4"]
+    g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, False, False)
+    exp = g.access_prob(3)
+    g.close()
+    out, flags = run_threads(qvb, lambda: qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, False, False), 3, 2)
+    assert all(flags)
+    for r in range(2):
+        assert (bits(out[r]) == bits(exp)).all(), r
