@@ -48,7 +48,7 @@ CONFIGS = {
 }
 META_BYTES = 24  # 8 B id + 16 B reference-layout lookup row per request
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
-PCIE_GBS = 51.4  # measured: random 512-byte row reads of pinned host memory (profiles/r01k_host_tier.txt)
+PCIE_GBS = 56.9  # measured: 512-byte row reads of pinned host memory in offset order, the best PCIe read rate on the box (profiles/r02/r02o_host_vmm.txt; random rows: 51.3)
 
 
 def bench_config(args, cfg, world: int) -> dict:
@@ -392,7 +392,7 @@ def run_ours(args):
     hbm_per_id = META_BYTES + row_bytes * (1 + f_l + f_p)
     links = {"hbm": (B * hbm_per_id, pk["hbm_gbs"], pk["source"]),
              "nvlink": (B * row_bytes * f_p, NVLINK_GBS, "measured peer copy (B200_PROFILING.md)"),
-             "pcie": (B * row_bytes * f_h, PCIE_GBS, "measured random-row PCIe reads, experiments/host_tier.cu")}
+             "pcie": (B * row_bytes * f_h, PCIE_GBS, "measured offset-ordered row reads over PCIe, experiments/r02/host_vmm.cu")}
     bound = max(links, key=lambda k: links[k][0] / links[k][1])
     # the store buckets batches that leave its own shard by location class
     # (csrc/store.cu launch_split); batches <= 48K ids take the flat kernel

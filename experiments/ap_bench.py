@@ -19,13 +19,16 @@ for setting in sys.argv[2:] or [""]:
         k, v = kv.split("=")
         os.environ[k] = v
     out = g.access_prob(c["layers"])
-    ms = []
-    for _ in range(3):
+    ms, ph = [], []
+    for _ in range(5):
         g.access_prob(c["layers"], out=out)
         ms.append(g.last_sweep_ms())
+        ph.append(g.phase_ms())
     same = ref is None or bool((out.view(np.uint64) == ref.view(np.uint64)).all())
     ref = out.copy() if ref is None else ref
     print(f"{setting or 'default'}: sweeps_ms={min(ms):.3f} per_sweep={min(ms) / (c['layers'] - 1):.3f} "
           f"same_as_first={same}", flush=True)
+    best = ph[int(np.argmin(ms))]
+    print("   phases_ms", {k: (round(v, 3) if isinstance(v, float) else v) for k, v in best.items()}, flush=True)
     for kv in setting.split():
         os.environ.pop(kv.split("=")[0], None)

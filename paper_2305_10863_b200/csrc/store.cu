@@ -684,7 +684,7 @@ __global__ void k_bucket_scatter(ClassLists L, const uint32_t* __restrict__ in_r
 template <int VEC, int kU, bool kR512>
 __global__ void __launch_bounds__(kGatherBlock, 4)
     k_gather_classes(ClassLists L, uint32_t cpr, uint32_t row_bytes, char* __restrict__ out,
-                     int host_every) {
+                     int host_every, uint32_t host_group) {
   using V = Vec<VEC>;
   const uint64_t pol = policy_evict_first();  // rows: a stream
   const uint32_t lane = threadIdx.x & 31;
@@ -704,6 +704,12 @@ __global__ void __launch_bounds__(kGatherBlock, 4)
 #pragma unroll
   for (int c = 0; c < kClasses; ++c) cnt[c] = __ldcg(L.count + c);
   int oi = 0;
+  // rows per group: 32 for HBM / NVLink rows; host rows in groups of
+  // host_group, so the rows in flight across the GPU form one narrow window
+  // of the offset-ordered host list (with 32-row groups the ~4.7K resident
+  // warps spread their reads over half of a 262K-row list, and the GPU's
+  // page walks over system memory lose their locality)
+  auto gsz = [&](int c) -> uint32_t { return c == 2 ? host_group : 32u; };
   // next (class, group) for this warp, or class -1 when every list is done
   auto take = [&](int& cls, unsigned int& g) {
     cls = -1;
@@ -712,7 +718,7 @@ __global__ void __launch_bounds__(kGatherBlock, 4)
       unsigned int t = 0;
       if (lane == 0) t = cnt[c] ? atomicAdd(L.cursor + c, 1u) : 0xFFFFFFFFu;
       t = __shfl_sync(0xffffffffu, t, 0);
-      if (cnt[c] && (uint64_t)t * 32 < cnt[c]) {
+      if (cnt[c] && (uint64_t)t * gsz(c) < cnt[c]) {
         cls = c;
         g = t;
         return;
@@ -724,8 +730,8 @@ __global__ void __launch_bounds__(kGatherBlock, 4)
     src = 0;
     dst = 0;
     if (cls < 0) return;
-    const uint64_t j = (uint64_t)g * 32 + lane;
-    if (j < cnt[cls]) {
+    const uint64_t j = (uint64_t)g * gsz(cls) + lane;
+    if (lane < gsz(cls) && j < cnt[cls]) {
       src = L.src[cls][j];
       dst = reinterpret_cast<uint64_t>(out) + (uint64_t)L.req[cls][j] * row_bytes;
     }
@@ -741,8 +747,8 @@ __global__ void __launch_bounds__(kGatherBlock, 4)
     take(ncls, ng);  // the next group's rows resolve while this one copies
     uint64_t nsrc, ndst;
     fetch(ncls, ng, nsrc, ndst);
-    const uint64_t left = cnt[cls] - (uint64_t)g * 32;
-    const uint32_t nr = static_cast<uint32_t>(left < 32 ? left : 32);
+    const uint64_t left = cnt[cls] - (uint64_t)g * gsz(cls);
+    const uint32_t nr = static_cast<uint32_t>(left < gsz(cls) ? left : gsz(cls));
     if (kR512) {  // rows of 512·m bytes: lane = 16-byte column (k_gather_rows512's loop)
       const uint32_t m = row_bytes / 512;
       for (uint32_t rc = 0; rc < nr * m; rc += kU) {
@@ -1016,13 +1022,20 @@ struct qvb_store {
 
   template <int V>
   void launch_classes(const ClassLists& L, uint32_t cpr, char* out, int host_every, cudaStream_t s) {
+    // host rows per group: 2 when the host list is offset-ordered (C4 at
+    // h = 0.25: 3.73 ms with 32-row groups, 3.15 with 4, 2.80 with 2, 2.81 with
+    // 1 — gpurun_out/r02p_*), 32 for an unordered list (no locality to keep,
+    // fewer cursor atomics); QVB_HOST_GROUP (1..32) overrides
+    const char* hg = std::getenv("QVB_HOST_GROUP");
+    const uint32_t host_group =
+        hg ? static_cast<uint32_t>(std::max(1, std::min(32, std::atoi(hg)))) : (L.hist ? 2u : 32u);
     const char* r5 = std::getenv("QVB_CLASS_R512");  // A/B knob (default on)
     if (V == 16 && row_bytes % 512 == 0 && !(r5 && *r5 == '0')) {
       const unsigned grid = resident_grid_cached(k_gather_classes<16, 4, true>, kGatherBlock, 0);
-      k_gather_classes<16, 4, true><<<grid, kGatherBlock, 0, s>>>(L, cpr, row_bytes, out, host_every);
+      k_gather_classes<16, 4, true><<<grid, kGatherBlock, 0, s>>>(L, cpr, row_bytes, out, host_every, host_group);
     } else {
       const unsigned grid = resident_grid_cached(k_gather_classes<V, 4, false>, kGatherBlock, 0);
-      k_gather_classes<V, 4, false><<<grid, kGatherBlock, 0, s>>>(L, cpr, row_bytes, out, host_every);
+      k_gather_classes<V, 4, false><<<grid, kGatherBlock, 0, s>>>(L, cpr, row_bytes, out, host_every, host_group);
     }
     QVB_LAUNCH_CHECK();
   }
