@@ -625,17 +625,26 @@ struct ClassLists {
 constexpr int kHostBucketBits = 18;  // upper bound of QVB_HOST_BUCKET_BITS
 constexpr int kHostBuckets = 1 << kHostBucketBits;
 
-__global__ void __launch_bounds__(256)
+// One id per thread; list positions are reserved with ONE atomic per class
+// per block-iteration (warp ballots -> per-warp counts in shared memory ->
+// block prefix), not one per warp: 1M ids with per-warp atomics queued ~65K
+// atomics on the three list counters and took 0.11-0.13 ms (ncu, C4 h = 0.1),
+// a tenth of the whole gather.
+constexpr int kSplitBlock = 256;
+__global__ void __launch_bounds__(kSplitBlock)
     k_split_classes(const uint64_t* __restrict__ ids, uint64_t b, const uint64_t* __restrict__ lut,
                     Bases bases, uint64_t stride, uint64_t n, int local_loc, int host_loc,
                     ClassLists L, unsigned long long* err) {
+  constexpr int kWarps = kSplitBlock / 32;
+  __shared__ unsigned int wpre[kWarps][kClasses];  // per-warp counts -> exclusive block prefix
+  __shared__ unsigned int bbase[kClasses];         // the block's reserved list starts
   const uint64_t host_base = reinterpret_cast<uint64_t>(bases.p[host_loc]);
-  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
   const uint64_t stride_all = (uint64_t)gridDim.x * blockDim.x;
-  // warp-uniform trip count: every lane reaches the ballots
-  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < b; i0 += stride_all) {
-    const uint64_t i = i0 + lane;
+  // block-uniform trip count: every thread reaches the barriers
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x; i0 < b; i0 += stride_all) {
+    const uint64_t i = i0 + threadIdx.x;
     int cls = -1;
     uint64_t src = 0;
     if (i < b) {
@@ -649,20 +658,32 @@ __global__ void __launch_bounds__(256)
         src = reinterpret_cast<uint64_t>(bases.p[loc]) + (e & kOffsetMask) * stride;
       }
     }
+    unsigned int mine = 0;  // ballot of this lane's class
 #pragma unroll
     for (int c = 0; c < kClasses; ++c) {
-      const uint32_t m = __ballot_sync(0xffffffffu, cls == c);
-      if (!m) continue;
-      unsigned int base = 0;
-      if (lane == __ffs(m) - 1) base = atomicAdd(L.count + c, __popc(m));
-      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-      if (cls == c) {
-        const unsigned int pos = base + __popc(m & lt);
-        L.req[c][pos] = static_cast<uint32_t>(i);
-        L.src[c][pos] = src;
-        if (c == 2 && L.hist) atomicAdd(L.hist + ((src - host_base) / stride >> L.hshift), 1u);
-      }
+      const unsigned int m = __ballot_sync(0xffffffffu, cls == c);
+      if (cls == c) mine = m;
+      if (lane == 0) wpre[warp][c] = __popc(m);
     }
+    __syncthreads();
+    if (threadIdx.x < kClasses) {
+      const int c = threadIdx.x;
+      unsigned int run = 0;
+      for (int w = 0; w < kWarps; ++w) {
+        const unsigned int t = wpre[w][c];
+        wpre[w][c] = run;
+        run += t;
+      }
+      bbase[c] = run ? atomicAdd(L.count + c, run) : 0u;
+    }
+    __syncthreads();
+    if (cls >= 0) {
+      const unsigned int pos = bbase[cls] + wpre[warp][cls] + __popc(mine & lt);
+      L.req[cls][pos] = static_cast<uint32_t>(i);
+      L.src[cls][pos] = src;
+      if (cls == 2 && L.hist) atomicAdd(L.hist + ((src - host_base) / stride >> L.hshift), 1u);
+    }
+    __syncthreads();  // wpre / bbase are rewritten by the next iteration
   }
 }
 
@@ -993,8 +1014,8 @@ struct qvb_store {
     L.cur = nullptr;
     const int hb = bits_for(host_rows > 1 ? host_rows - 1 : 1);
     L.hshift = hb > bbits ? hb - bbits : 0;
-    const unsigned sgrid = resident_grid_cached(k_split_classes, 256, 0);
-    k_split_classes<<<std::min<uint64_t>(sgrid, (b + 255) / 256), 256, 0, s>>>(
+    const unsigned sgrid = resident_grid_cached(k_split_classes, kSplitBlock, 0);
+    k_split_classes<<<std::min<uint64_t>(sgrid, (b + kSplitBlock - 1) / kSplitBlock), kSplitBlock, 0, s>>>(
         ids, b, lut, bases, stride, n, static_cast<int>(reader), host_loc, L, err);
     QVB_LAUNCH_CHECK();
     if (order_host) {
@@ -1012,7 +1033,7 @@ struct qvb_store {
     }
     static const int host_every = [] {
       const char* e = std::getenv("QVB_HOST_EVERY");
-      return e ? std::max(1, std::atoi(e)) : 8;
+      return e ? std::max(1, std::atoi(e)) : 2;  // C4 h = 0.1: 1.198 ms with 8, 1.148 with 2 (r02t)
     }();
     const int V = vec();
     if (V == 16) launch_classes<16>(L, cpr, out, host_every, s);
