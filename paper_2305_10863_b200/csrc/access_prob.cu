@@ -1248,6 +1248,10 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, dou
         QVB_LAUNCH_CHECK();
         const unsigned most = read_scalar(mx.p, s);
         g.prod_bufw = std::min<uint32_t>(kPtMaxBufw, (most + g.prod_zw + 31) & ~31u);
+        if (const char* bw = std::getenv("QVB_PT_BUFW")) {  // tests: force a buffer size (slices beyond it take the global path)
+          const uint32_t w = static_cast<uint32_t>(std::atoi(bw)) & ~31u;
+          if (w >= g.prod_zw + 32 && w <= kPtMaxBufw) g.prod_bufw = w;
+        }
         QVB_CUDA(cudaMalloc(&g.nm_desc, g.nm_S * nseg * sizeof(uint64_t)));
         QVB_CUDA(cudaMalloc(&g.nm_runs, g.nm_S * 32 * 2 * sizeof(uint64_t)));
         g.bytes += g.nm_S * nseg * sizeof(uint64_t) + g.nm_S * 32 * 2 * sizeof(uint64_t);
@@ -1259,8 +1263,11 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, dou
         QVB_LAUNCH_CHECK();
         g.prod_big = read_scalar(big.p, s);
         const size_t smem = (size_t)kPtWarps * pt_warp_bytes(g.prod_bufw);
+        // always the largest buffer any graph can ask for: graphs built on
+        // other threads (or devices) set the same value, so none of them can
+        // leave the attribute below another graph's launch size
         QVB_CUDA(cudaFuncSetAttribute(k_products_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
+                                      static_cast<int>((size_t)kPtWarps * pt_warp_bytes(kPtMaxBufw))));
         g.prod_grid = resident_grid(k_products_tma, kPtWarps * 32, smem,
                                     (g.nm_S + kPtWarps - 1) / kPtWarps);
       }

@@ -248,6 +248,20 @@ def test_c2_node_major_segments_bit_exact(qvb, oracle, weighted, monkeypatch):
     g.close()
 
 
+@pytest.mark.parametrize("bufw", ["160", "928"])
+def test_products_small_staging_buffer(qvb, oracle, bufw, monkeypatch):
+    """k_products_tma with a staging buffer smaller than most slices
+    (QVB_PT_BUFW): slices that outgrow it take the global lock-step path,
+    the rest the staged one; C2 node-major segments stay bit-exact."""
+    c = CONFIGS["C2"]
+    monkeypatch.setenv("QVB_SEG_MB", "4")
+    monkeypatch.setenv("QVB_PT_BUFW", bufw)
+    ro, col, w = oracle.synthetic_graph(c["n"], c["e"], 7, False, False)
+    g = qvb.DeviceGraph.synthetic(c["n"], c["e"], 7, False, False)
+    assert (bits(g.access_prob(3)) == bits(oracle.access_prob(ro, col, w, 3))).all()
+    g.close()
+
+
 def test_c3_weighted_bit_exact(qvb, oracle):
     """C3 (Reddit-shaped, 233K nodes, 114M edges, 3-layer edge-weighted) at full size."""
     c = CONFIGS["C3"]
