@@ -395,8 +395,10 @@ def run_ours(args):
              "pcie": (B * row_bytes * f_h, PCIE_GBS, "measured offset-ordered row reads over PCIe, experiments/r02/host_vmm.cu")}
     bound = max(links, key=lambda k: links[k][0] / links[k][1])
     # the store buckets batches that leave its own shard by location class
-    # (csrc/store.cu launch_split); batches <= 48K ids take the flat kernel
-    gather_kernel = ("k_gather" if B <= 49152 else
+    # (csrc/store.cu launch_split); batches <= 48K ids (and, with a host tier,
+    # batches <= 256K ids expecting <= 16K host rows) take the flat kernel
+    flat = B <= 49152 or (f_h > 0 and B <= 262144 and B * f_h <= 16384)  # store.cu launch_gather
+    gather_kernel = ("k_gather" if flat else
                      "k_gather_classes" if (f_p > 0 or f_h > 0) and not args.planned else
                      "k_gather_sorted" if args.planned else "k_gather_rows")
     alg, link_peak, link_src = links[bound]

@@ -954,10 +954,19 @@ struct qvb_store {
     // pairs over every thread, one id -> entry -> row chain deep
     // (1K ids: 9.9 -> 7.5 us at 400-byte rows, 44.6 -> 7.6 us at 2408-byte
     // rows; ~40K ids: 11.4 -> 9.8 and 62.6 -> 52.0 us; at 64K ids the row-group
-    // kernel is ahead again — profiles/r01m_gather_sweep.md). QVB_GATHER_SMALL
-    // overrides the request-count threshold.
+    // kernel is ahead again — profiles/r01m_gather_sweep.md). With a host tier
+    // the flat kernel also stays ahead of the class split while the batch
+    // holds few host rows: the split's fixed cost (lookups, bucket scan,
+    // scatter) is not repaid on a short host list. C4: 64K ids 51 / 113 / 296
+    // us against 99-111 / 161-173 / 344-354 at h = 0.05 / 0.10 / 0.25; 256K
+    // ids at h = 0.05 206 against 216 us, at h = 0.10 445 against 414
+    // (profiles/r02/r02w_host_knobs.txt, r02x_host_knobs.txt). So batches up
+    // to 256K ids whose expected host rows (uniform ids: B x host share) are
+    // at most 16K take the flat kernel. QVB_GATHER_SMALL overrides the
+    // request-count threshold.
     const char* sm = std::getenv("QVB_GATHER_SMALL");
-    const uint64_t small_rows = sm ? std::strtoull(sm, nullptr, 10) : 49152ull;
+    uint64_t small_rows = sm ? std::strtoull(sm, nullptr, 10) : 49152ull;
+    if (!sm && host_used && b <= 262144 && b * host_rows <= 16384ull * n) small_rows = b;
     // rows from more than this GPU's shard (peers over NVLink, the host tier
     // over PCIe): bucket by location class first so the links do not share
     // load rounds (QVB_GATHER_SPLIT=0 keeps the mixed row-group kernel)
@@ -988,18 +997,25 @@ struct qvb_store {
   void launch_split(const uint64_t* ids, uint64_t b, uint32_t cpr, char* out, cudaStream_t s,
                     unsigned long long* err) {
     const int host_loc = nloc - 2;
-    // host requests in offset order once the host tier outgrows the GPU's
-    // reach over system-memory pages (random rows: 51 GB/s up to 2 GB, 38 GB/s
-    // at 14 GB, profiles/r01k_host_tier.txt; C4 at h=0.25: 4.76 -> 3.44 ms,
-    // C2's 0.3 GB tier: no gain, profiles/r02/r02d_host_order.md)
+    // host requests in offset order once the host tier outgrows the reach of
+    // the translation over system memory (random rows: 51 GB/s up to 2 GB,
+    // 41 at 8 GB, 38 at 14 GB; in offset order 52-57, profiles/r02/
+    // r02op_host_tier_and_lookup.md). C4 h = 0.05 (a 2.8 GB tier), 1M ids:
+    // 886 -> 658 us ordered (r02w_host_knobs.txt); C2's 0.3 GB tier: no gain
+    // (profiles/r02/r02d_host_order.md), so tiers below 1 GB stay unordered.
     const char* so = std::getenv("QVB_HOST_SORT");  // per call: tests and A/B flip it
-    const bool big_tier = host_rows * stride >= (4ull << 30);
+    const bool big_tier = host_rows * stride >= (1ull << 30);
     const bool order_host = host_rows > 0 && (used_mask >> host_loc & 1) &&
                             (so ? *so == '1' : big_tier);
     DevBuf<uint32_t> req(b * (kClasses + (order_host ? 1 : 0)), s);
     DevBuf<unsigned long long> srcs(b * (kClasses + (order_host ? 1 : 0)), s);
     const char* bb = std::getenv("QVB_HOST_BUCKET_BITS");  // A/B knob: 10..18
-    const int bbits = bb ? std::max(10, std::min(kHostBucketBits, std::atoi(bb))) : 16;
+    // buckets: ~64 requests of the batch per bucket, 2^10..2^16 (the bucket
+    // scan's cost follows the bucket count; 2^12 vs 2^16 at 64K-256K ids:
+    // -5..-12 us, equal at 1M, r02w_host_knobs.txt)
+    int lgb = 0;
+    while ((2ull << lgb) <= b) ++lgb;  // floor(log2 b)
+    const int bbits = bb ? std::max(10, std::min(kHostBucketBits, std::atoi(bb))) : std::max(10, std::min(16, lgb - 6));
     const int nbuckets = 1 << bbits;
     DevBuf<unsigned int> ctr(2 * kClasses + (order_host ? nbuckets : 0), s);
     QVB_CUDA(cudaMemsetAsync(ctr.p, 0, (2 * kClasses + (order_host ? nbuckets : 0)) * sizeof(unsigned int), s));
