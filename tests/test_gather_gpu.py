@@ -240,6 +240,36 @@ def test_tier_split_gather_bit_exact(qvb, oracle, mix, dim, monkeypatch):
         st.close()
 
 
+@pytest.mark.parametrize("b", [1000, 50000, 131072, 262144, 300000])
+@pytest.mark.parametrize("host_share", [0.05, 0.5])
+def test_default_dispatch_with_host_tier(qvb, oracle, b, host_share, monkeypatch):
+    """With a host tier the store picks the flat kernel or the class split by
+    batch size and expected host rows (<= 256K ids and <= 16K expected host
+    rows: flat), and small host groups over an offset-ordered host list (any
+    tier size here, QVB_HOST_SORT=1; the default orders tiers >= 1 GB). Every
+    choice returns the same bytes as X[ids]."""
+    import torch
+
+    for k in ("QVB_GATHER_SMALL", "QVB_HOST_SORT", "QVB_GATHER_SPLIT", "QVB_HOST_GROUP"):
+        monkeypatch.delenv(k, raising=False)
+    n, dim = 40000, 64
+    t, lo, ids = plan(qvb, n, cap=int(n * (1 - host_share)), host=n)
+    st = qvb.FeatureStore(lo, ids, dim, t, reader=0)
+    x = oracle.features(n, dim)
+    req = oracle.request_ids(11, 77, n, b)
+    exp = oracle.gather(x, req)
+    d = torch.from_numpy(req.view(np.int64)).cuda()
+    for sort in (None, "1"):
+        if sort:
+            monkeypatch.setenv("QVB_HOST_SORT", sort)
+        out = torch.full((b, dim), -1.0, dtype=torch.float32, device="cuda")
+        st.gather(d, out)
+        st.check_error()
+        assert (out.cpu().numpy() == exp).all()
+        assert (st.gather_host(req) == exp).all()
+    st.close()
+
+
 def test_tier_split_gather_reports_bad_ids(qvb, oracle, monkeypatch):
     import torch
 
