@@ -89,7 +89,7 @@ def main():
     assert all((a == b).all() for a, b in zip(st.plan_reads(req, 8), exp_plan))
     d_ids = torch.from_numpy(req.view(np.int64)).cuda()
     out = torch.empty((len(req), dim), dtype=torch.float32, device="cuda")
-    for env in ({}, {"QVB_GATHER_SPLIT": "0"}, {"QVB_GATHER_SMALL": "1000000"}):
+    for env in ({}, {"QVB_HOST_SORT": "1"}, {"QVB_GATHER_SPLIT": "0"}, {"QVB_GATHER_SMALL": "1000000"}):
         os.environ.update(env)
         st.gather(d_ids, out)
         torch.cuda.synchronize()
