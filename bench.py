@@ -48,6 +48,7 @@ CONFIGS = {
 }
 META_BYTES = 24  # 8 B id + 16 B reference-layout lookup row per request
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+D2H_GBS = 57.3  # measured: pinned 512 MB device->host copies (experiments/r02/pcie_copy.py, profiles/r02/r02ae_pcie_copy.txt)
 PCIE_GBS = 56.9  # measured: 512-byte row reads of pinned host memory in offset order, the best PCIe read rate on the box (profiles/r02/r02o_host_vmm.txt; random rows: 51.3)
 
 
@@ -417,6 +418,8 @@ def run_ours(args):
         e2e_s = D.max_over_ranks(time.perf_counter() - t0)
         e2e = {"value": payload / e2e_s / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": B * 8, "d2h_bytes_per_step": B * row_bytes,
+               # the rows leave over PCIe: the pinned D2H copy rate bounds the call
+               "d2h_ceiling_GBps": D2H_GBS, "frac_of_d2h_ceiling": payload / e2e_s / 1e9 / D2H_GBS,
                "note": "qvb_gather_host per step: H2D ids (pinned) + gather + D2H rows (pinned) "
                        "+ stream sync; wall clock, max over ranks"}
     if not args.no_e2e and rank == 0:  # the P legs are per-rank replicas: rank 0 reports them
