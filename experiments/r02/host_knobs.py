@@ -23,6 +23,13 @@ SETTINGS = {
     "sort_bits12": {"QVB_HOST_SORT": "1", "QVB_HOST_BUCKET_BITS": "12"},
     "flat": {"QVB_GATHER_SMALL": str(1 << 21)},
 }
+if "--more" in sys.argv:  # host-list knobs of the class split
+    SETTINGS.update({
+        "unsorted": {"QVB_HOST_SORT": "0"},
+        "group4": {"QVB_HOST_GROUP": "4"},
+        "group1": {"QVB_HOST_GROUP": "1"},
+        "mixed_rows": {"QVB_GATHER_SPLIT": "0"},
+    })
 
 
 def main():
@@ -41,13 +48,19 @@ def main():
     req = torch.empty((reps + 2, 1 << 20), dtype=torch.int64, device=dev)
     for k in range(reps + 2):
         qvb.request_ids_synthetic(11, k, n, req[k], device=0, stream=st)
+    if "--p-weighted" in sys.argv:  # ids drawn from the CDF of P (simulator.cpp:99-132)
+        cdf = np.cumsum(ph)
+        cdf /= cdf[-1]
+        rng = np.random.default_rng(5)
+        req = torch.from_numpy(np.searchsorted(cdf, rng.random((reps + 2, 1 << 20)), side="right")
+                               .clip(0, n - 1).astype(np.int64)).to(dev)
     out = torch.empty((1 << 20, dim), dtype=torch.float32, device=dev)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    for h in (0.05, 0.10, 0.25):
+    for h in ((0.05, 0.10) if "--p-weighted" in sys.argv else (0.05, 0.10, 0.25)):
         topo = D.topology_for(qvb, n, 1, 0.0, h)
         lo, ids = qvb.plan_placement(ph, topo, device=0)
         store = D.build_store(qvb, lo, ids, dim, topo, 0, 0)
-        for b in (1 << 16, 1 << 18, 1 << 20):
+        for b in ((1 << 18, 1 << 20) if "--p-weighted" in sys.argv else (1 << 16, 1 << 18, 1 << 20)):
             line = []
             for name, env in SETTINGS.items():
                 for k, v in env.items():

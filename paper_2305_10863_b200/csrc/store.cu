@@ -1059,13 +1059,15 @@ struct qvb_store {
 
   template <int V>
   void launch_classes(const ClassLists& L, uint32_t cpr, char* out, int host_every, cudaStream_t s) {
-    // host rows per group: 2 when the host list is offset-ordered (C4 at
-    // h = 0.25: 3.73 ms with 32-row groups, 3.15 with 4, 2.80 with 2, 2.81 with
-    // 1 — gpurun_out/r02p_*), 32 for an unordered list (no locality to keep,
+    // host rows per group: 1 when the host list is offset-ordered (C4 uniform
+    // ids at h = 0.25: 3.73 ms with 32-row groups, 3.15 with 4, 2.80 with 2,
+    // 2.81 with 1 — profiles/r02/r02op_*; P-weighted ids, whose host rows are
+    // sparser, at h = 0.05 / 0.10: 497 -> 443 us and 861 -> 831 us from 2 to 1,
+    // r02ag_host_knobs_pw.txt), 32 for an unordered list (no locality to keep,
     // fewer cursor atomics); QVB_HOST_GROUP (1..32) overrides
     const char* hg = std::getenv("QVB_HOST_GROUP");
     const uint32_t host_group =
-        hg ? static_cast<uint32_t>(std::max(1, std::min(32, std::atoi(hg)))) : (L.hist ? 2u : 32u);
+        hg ? static_cast<uint32_t>(std::max(1, std::min(32, std::atoi(hg)))) : (L.hist ? 1u : 32u);
     const char* r5 = std::getenv("QVB_CLASS_R512");  // A/B knob (default on)
     if (V == 16 && row_bytes % 512 == 0 && !(r5 && *r5 == '0')) {
       const unsigned grid = resident_grid_cached(k_gather_classes<16, 4, true>, kGatherBlock, 0);
