@@ -1042,6 +1042,127 @@ __global__ void __launch_bounds__(kPtWarps * 32)
   }
 }
 
+// ---- k_pass_fused: gathers and ordered products of one source segment -------
+// The decoupled sweep above writes every entry's code (nm_code) and reads it
+// back in k_products_tma: 8 bytes of HBM per edge on top of the L1-bound
+// gathers, and a second kernel whose issue-bound products do not overlap
+// them. Here one launch per pass k does both. Every warp is an independent
+// pipeline (no CTA barriers): it owns chunks of kFpSlices consecutive slices,
+// whose pass-k entries are contiguous in nm_col ([sbase(k,c0), sbase(k,c1))).
+// The warp gathers the chunk's codes (kFpU in flight per lane) into its own
+// shared-memory buffer at each entry's position, then, lane = node, multiplies
+// each lane's run in order into the running product carried between passes
+// in `state` (coalesced, 16 bytes per node and pass instead of 8 per edge); a
+// node's last pass finishes P. Passes run in source order and each run is
+// ascending: the reference's left-to-right product (metrics.cpp:152-168),
+// bit-identical. Lanes past their run read word 0 of the buffer's tail, a
+// zero code (factor 1.0, an exact identity). Chunks with an unrepresentable
+// factor (marker) or more entries than `cap` run the exact loop on nm_col
+// (both rare).
+constexpr int kFpWarps = 4;
+constexpr int kFpSlices = 4;            // slices per warp chunk
+constexpr uint32_t kFpBufw = 1024;      // words per warp buffer, the last one kept zero
+constexpr int kFpU = 8;                 // gathers in flight per lane
+constexpr size_t kFpSmem = (size_t)kFpWarps * kFpBufw * sizeof(uint32_t);
+
+__global__ void __launch_bounds__(kFpWarps * 32)
+    k_pass_fused(int k, uint64_t S, uint64_t s0, uint64_t s1, uint64_t n, const uint8_t* __restrict__ lenf,
+                 const uint64_t* __restrict__ sbase, const uint32_t* __restrict__ ncol,
+                 const uint32_t* __restrict__ kprev, const uint32_t* __restrict__ exc_src,
+                 const double* __restrict__ exc_R, const double* __restrict__ prev,
+                 const double* __restrict__ inv, double* __restrict__ state, double* __restrict__ out,
+                 uint32_t* __restrict__ kout, uint32_t cap) {
+  extern __shared__ __align__(16) uint32_t fbuf[];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t* const buf = fbuf + wid * kFpBufw;
+  const uint32_t zero = kFpBufw - 1;
+  if (lane == 0) buf[zero] = 0u;
+  __syncwarp();
+  const uint64_t pol = policy_evict_first();
+  const uint64_t nch = (s1 - s0 + kFpSlices - 1) / kFpSlices;
+  const uint64_t* const sb = sbase + (uint64_t)k * S;
+  const uint8_t* const lk = lenf + (uint64_t)k * S * 32;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t ch = gw; ch < nch; ch += nw) {
+    const uint64_t c0 = s0 + ch * kFpSlices, c1 = c0 + kFpSlices < s1 ? c0 + kFpSlices : s1;
+    // the lane's lens of every slice (one byte each), the chunk's bounds
+    uint32_t lfs = 0;
+#pragma unroll
+    for (int q = 0; q < kFpSlices; ++q)
+      if (c0 + q < c1) lfs |= ld_stream_u8(lk + (c0 + q) * 32 + lane, pol) << (8 * q);
+    const uint64_t e0 = ld_stream(sb + c0, pol), e1 = ld_stream(sb + c1, pol);
+    const uint32_t cnt = static_cast<uint32_t>(e1 - e0);
+    bool exact = e1 - e0 > cap;
+    if (!exact) {
+      uint32_t any = 0;
+      for (uint32_t i0 = lane; i0 < cnt; i0 += kFpU * 32) {
+        uint32_t c[kFpU], kc[kFpU];
+#pragma unroll
+        for (int u = 0; u < kFpU; ++u) {
+          const uint32_t i = i0 + u * 32;
+          c[u] = i < cnt ? ld_stream(ncol + e0 + i, pol) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kFpU; ++u) kc[u] = (c[u] & kExcFlag) ? kExcCode : __ldg(kprev + c[u]);
+#pragma unroll
+        for (int u = 0; u < kFpU; ++u) {
+          const uint32_t i = i0 + u * 32;
+          if (i < cnt) {
+            const uint32_t j = kc[u] < kExcCode ? kc[u] : code_of(c[u], kc[u], exc_src, exc_R, prev, inv, any);
+            buf[i] = 0u - j;
+          }
+        }
+      }
+      exact = __any_sync(kFull, any);
+      __syncwarp();
+    }
+    uint32_t pre = 0;  // entries of the chunk's earlier slices
+#pragma unroll
+    for (int q = 0; q < kFpSlices; ++q) {
+      const uint64_t sl = c0 + q;
+      if (sl >= c1) break;  // warp-uniform
+      const uint64_t v = sl * 32 + lane;
+      const uint32_t lf = (lfs >> (8 * q)) & 0xFF;
+      const uint32_t len = lf & kNmLen;
+      double m = (lf != 0 && !(lf & kNmFirst)) ? ld_stream(state + v, pol) : 1.0;
+      double pv = 0.0, iv = 0.0;
+      if ((lf & kNmLast) && v < n) {
+        pv = ld_stream(prev + v, pol);
+        if (kout) iv = ld_stream(inv + v, pol);
+      }
+      const uint32_t incl = warp_incl_scan(len);
+      const uint32_t total = __shfl_sync(kFull, incl, 31);
+      const uint32_t b0 = pre + incl - len;  // the lane's run, relative to e0
+      pre += total;
+      if (!exact) {
+        const uint32_t maxlen = __reduce_max_sync(kFull, len);
+        for (uint32_t t = 0; t < maxlen; ++t) {
+          const uint32_t L = buf[t < len ? b0 + t : zero];
+          m = __dmul_rn(m, low_to_factor(L));
+        }
+      } else {
+        for (uint32_t t = 0; t < len; ++t) {
+          const uint32_t c = ncol[e0 + b0 + t];
+          uint32_t any = 0;
+          const uint32_t j = code_of(c, (c & kExcFlag) ? kExcCode : __ldg(kprev + c), exc_src, exc_R, prev, inv, any);
+          m = __dmul_rn(m, j == kExcCode ? marker_factor(c, exc_src, exc_R, prev, inv) : low_to_factor(0u - j));
+        }
+      }
+      if (lf & kNmLast) {
+        if (v < n) {  // metrics.cpp:169: prev + (1 - prev) * (1 - miss_all)
+          const double P = __dadd_rn(pv, __dmul_rn(__dsub_rn(1.0, pv), __dsub_rn(1.0, m)));
+          st_stream(out + v, P, pol);
+          if (kout) st_stream(kout + v, y_code(__dmul_rn(P, iv)), pol);
+        }
+      } else if (len) {
+        st_stream(state + v, m, pol);
+      }
+    }
+    __syncwarp();  // the buffer is refilled by the next chunk
+  }
+}
+
 }  // namespace
 
 namespace {
@@ -1116,7 +1237,7 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, dou
     if ((uint64_t)sh.world * chunk > n + 1 + kShardPad) fail(QVB_ERR_UNSUPPORTED, "too many ranks for the graph");
     const int nseg_ = static_cast<int>(g.seg_slice.size()) - 1;
     sharded = layers >= 2 && codes && (!f1 || g.f1_ident) && nseg_ <= kPtKMaxSh && g.long_threshold <= 256 &&
-              !std::getenv("QVB_PRODUCTS");
+              (!std::getenv("QVB_PRODUCTS") || std::string(std::getenv("QVB_PRODUCTS")) == "fused");
     const uint64_t lo = std::min<uint64_t>(n, (uint64_t)sh.rank * chunk);
     const uint64_t hi = std::min<uint64_t>(n, lo + chunk);
     s0 = lo / 32;
@@ -1209,6 +1330,31 @@ const double* run_access_prob(qvb_graph& g, uint32_t layers, cudaStream_t s, dou
             pout, kout);
         QVB_LAUNCH_CHECK();
         ++launched;
+      }
+      const char* pm = std::getenv("QVB_PRODUCTS");  // "fused": fused passes (A/B)
+      const int products_mode = pm && std::string(pm) == "fused" ? 1 : 0;
+      if (products_mode == 1) {
+        // one fused pass per source segment (k_pass_fused): gathers and
+        // ordered products together, the running product in g.state
+        uint32_t fp_cap = kFpBufw - 1;  // tests: QVB_FP_CAP forces the exact path for larger chunks
+        if (const char* c = std::getenv("QVB_FP_CAP")) fp_cap = std::min<uint32_t>(kFpBufw - 1, std::atoi(c));
+        if (!g.fused_grid) {
+          QVB_CUDA(cudaFuncSetAttribute(k_pass_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kFpSmem)));
+          g.fused_grid = resident_grid(k_pass_fused, kFpWarps * 32, kFpSmem, ~0ull);
+        }
+        const uint64_t nch = (s1 - s0 + kFpSlices - 1) / kFpSlices;
+        const unsigned fg = static_cast<unsigned>(std::min<uint64_t>(g.fused_grid, nch ? nch : 1));
+        for (int k = 0; k < nseg; ++k) {
+          k_pass_fused<<<fg, kFpWarps * 32, kFpSmem, s>>>(k, g.nm_S, s0, s1, n, g.nm_lenf, g.nm_sbase, g.nm_col,
+                                                   g.kcode[cur], g.exc_src, g.exc_R, g.p[cur], g.inv,
+                                                   g.state, pout, kout, fp_cap);
+          QVB_LAUNCH_CHECK();
+          ++launched;
+        }
+        pt.end(launched);
+        exchange();
+        continue;
       }
       // one launch per source segment: the CTAs in flight gather from one
       // L2-resident code segment

@@ -212,6 +212,13 @@ __device__ __forceinline__ uint16_t ld_stream(const uint16_t* a, uint64_t pol) {
                : "l"(a), "l"(pol));
   return v;
 }
+__device__ __forceinline__ uint32_t ld_stream_u8(const uint8_t* a, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;"
+               : "=r"(v)
+               : "l"(a), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ void st_stream(uint32_t* a, uint32_t v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
 }

@@ -143,7 +143,7 @@ struct qvb_graph {
   std::vector<PhaseEv> phase_ev;
   size_t phase_used = 0;
   uint32_t launches = 0;  // kernels launched by the last run
-  unsigned f1_grid = 0, codes_grid = 0;  // resident grids, computed on first use
+  unsigned f1_grid = 0, codes_grid = 0, fused_grid = 0;  // resident grids, computed on first use
   // k_products_tma's static staging layout (access_prob.cu), built on first use
   uint64_t* nm_desc = nullptr;  // [S][K] bulk-copy descriptor per (slice, pass)
   uint64_t* nm_runs = nullptr;  // [N pad][2] per node: staged run of every pass
