@@ -1092,19 +1092,33 @@ __global__ void __launch_bounds__(kFpWarps * 32)
     for (int q = 0; q < kFpSlices; ++q)
       if (c0 + q < c1) lfs |= ld_stream_u8(lk + (c0 + q) * 32 + lane, pol) << (8 * q);
     const uint64_t e0 = ld_stream(sb + c0, pol), e1 = ld_stream(sb + c1, pol);
+    // every slice's running product and P(j-1) in flight under the gathers
+    double m[kFpSlices], pv[kFpSlices];
+#pragma unroll
+    for (int q = 0; q < kFpSlices; ++q) {
+      const uint32_t lf = (lfs >> (8 * q)) & 0xFF;
+      const uint64_t v = (c0 + q) * 32 + lane;
+      m[q] = (lf != 0 && !(lf & kNmFirst)) ? ld_stream(state + v, pol) : 1.0;
+      pv[q] = ((lf & kNmLast) && v < n) ? ld_stream(prev + v, pol) : 0.0;
+    }
     const uint32_t cnt = static_cast<uint32_t>(e1 - e0);
     bool exact = e1 - e0 > cap;
     if (!exact) {
       uint32_t any = 0;
       for (uint32_t i0 = lane; i0 < cnt; i0 += kFpU * 32) {
         uint32_t c[kFpU], kc[kFpU];
+        // all kFpU column loads, then all gathers (volatile: kept in this order)
 #pragma unroll
         for (int u = 0; u < kFpU; ++u) {
           const uint32_t i = i0 + u * 32;
-          c[u] = i < cnt ? ld_stream(ncol + e0 + i, pol) : 0u;
+          c[u] = i < cnt ? ld_stream(ncol + e0 + i, pol) : kExcFlag;
         }
 #pragma unroll
-        for (int u = 0; u < kFpU; ++u) kc[u] = (c[u] & kExcFlag) ? kExcCode : __ldg(kprev + c[u]);
+        for (int u = 0; u < kFpU; ++u) {
+          kc[u] = kExcCode;
+          if (!(c[u] & kExcFlag))
+            asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(kc[u]) : "l"(kprev + c[u]));
+        }
 #pragma unroll
         for (int u = 0; u < kFpU; ++u) {
           const uint32_t i = i0 + u * 32;
@@ -1125,38 +1139,33 @@ __global__ void __launch_bounds__(kFpWarps * 32)
       const uint64_t v = sl * 32 + lane;
       const uint32_t lf = (lfs >> (8 * q)) & 0xFF;
       const uint32_t len = lf & kNmLen;
-      double m = (lf != 0 && !(lf & kNmFirst)) ? ld_stream(state + v, pol) : 1.0;
-      double pv = 0.0, iv = 0.0;
-      if ((lf & kNmLast) && v < n) {
-        pv = ld_stream(prev + v, pol);
-        if (kout) iv = ld_stream(inv + v, pol);
-      }
       const uint32_t incl = warp_incl_scan(len);
       const uint32_t total = __shfl_sync(kFull, incl, 31);
       const uint32_t b0 = pre + incl - len;  // the lane's run, relative to e0
       pre += total;
+      double mq = m[q];
       if (!exact) {
         const uint32_t maxlen = __reduce_max_sync(kFull, len);
         for (uint32_t t = 0; t < maxlen; ++t) {
           const uint32_t L = buf[t < len ? b0 + t : zero];
-          m = __dmul_rn(m, low_to_factor(L));
+          mq = __dmul_rn(mq, low_to_factor(L));
         }
       } else {
         for (uint32_t t = 0; t < len; ++t) {
           const uint32_t c = ncol[e0 + b0 + t];
           uint32_t any = 0;
           const uint32_t j = code_of(c, (c & kExcFlag) ? kExcCode : __ldg(kprev + c), exc_src, exc_R, prev, inv, any);
-          m = __dmul_rn(m, j == kExcCode ? marker_factor(c, exc_src, exc_R, prev, inv) : low_to_factor(0u - j));
+          mq = __dmul_rn(mq, j == kExcCode ? marker_factor(c, exc_src, exc_R, prev, inv) : low_to_factor(0u - j));
         }
       }
       if (lf & kNmLast) {
         if (v < n) {  // metrics.cpp:169: prev + (1 - prev) * (1 - miss_all)
-          const double P = __dadd_rn(pv, __dmul_rn(__dsub_rn(1.0, pv), __dsub_rn(1.0, m)));
+          const double P = __dadd_rn(pv[q], __dmul_rn(__dsub_rn(1.0, pv[q]), __dsub_rn(1.0, mq)));
           st_stream(out + v, P, pol);
-          if (kout) st_stream(kout + v, y_code(__dmul_rn(P, iv)), pol);
+          if (kout) st_stream(kout + v, y_code(__dmul_rn(P, ld_stream(inv + v, pol))), pol);
         }
       } else if (len) {
-        st_stream(state + v, m, pol);
+        st_stream(state + v, mq, pol);
       }
     }
     __syncwarp();  // the buffer is refilled by the next chunk
